@@ -1,0 +1,173 @@
+/*
+ * snn_lif.h -- C ABI of the B200 (sm_100a) temporally fused LIF library
+ *              (libsnn_lif.so, built from paper_2408_00280_b200/csrc/).
+ *
+ * The method: "temporal fusion" (arXiv 2408.00280) -- every LIF layer
+ * runs all T time steps of its neurons inside ONE kernel launch, each neuron's state
+ * held in registers across the time loop ("assigns each neuron's computation to an
+ * individual GPU thread, amalgamating memory operations for each layer across all time
+ * steps within the GPU kernel"), forward (Eq. 1-2) and backward
+ * (Eq. 3) alike (Fig. 2 caption).  The paper's programming model
+ * (Listing 1) exposes fusedForwardLIF(x, args) /
+ * fusedBackwardLIF(grad_y, args); snn_lif_forward / snn_lif_backward are those two calls.
+ *
+ * ----------------------------------------------------------------------------------
+ * Conventions shared by every entry point
+ *
+ *  Layout.  Time-major, row-major [T, N] with row stride `ld` elements (ld >= N), i.e.
+ *  element (t, n) at t*ld + n (the paper's "memory alignment post-concatenation",
+ *  PAPER.md:217-218; Listing 1 caption: x "aggregates a tensor for all neurons i across
+ *  each time step t").  ld > N lets a caller pass a neuron-shard view
+ *  (column range) of a wider tensor.  [N] vectors are dense fp32.
+ *
+ *  Ownership.  Every data pointer is a DEVICE pointer owned by the caller (PyTorch
+ *  allocates).  The library never allocates, frees or synchronises; every call only
+ *  enqueues kernels on `stream` (a cudaStream_t passed as void*; NULL = legacy default
+ *  stream) and returns.  Outputs are valid once that stream's work completes.
+ *
+ *  Errors.  Arguments are validated synchronously, before anything is enqueued; a
+ *  non-OK status means nothing was launched.  A launch failure is reported as
+ *  SNN_ERR_CUDA (from cudaGetLastError); faults inside a kernel surface at the
+ *  caller's next synchronisation, as for any CUDA call.  snn_last_error_message()
+ *  returns a thread-local detail string for the last non-OK status of this thread.
+ *
+ *  Alignment.  Element alignment is mandatory (SNN_ERR_MISALIGNED otherwise).  The
+ *  128-bit vector fast path additionally needs 16-byte-aligned base pointers and
+ *  ld % (16 / sizeof(io element)) == 0; otherwise a scalar path runs (never an error).
+ *
+ *  Determinism.  Identical inputs and build give bitwise-identical outputs, and chained
+ *  segments (v_final -> v_init forward, grad_v_init -> grad_v_final backward) are
+ *  bitwise equal to one whole-axis call.  SAVE_H and
+ *  SAVE_RECOMPUTE produce bitwise-identical gradients.
+ *
+ *  Threading.  No global mutable state besides the thread-local error string; calls on
+ *  different streams may run concurrently.
+ */
+#ifndef SNN_LIF_H
+#define SNN_LIF_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SNN_LIF_ABI_VERSION 1
+
+typedef enum {
+    SNN_OK = 0,
+    SNN_ERR_INVALID_VALUE = 1,  /* a size, flag or hyper-parameter is out of range      */
+    SNN_ERR_NULL_POINTER = 2,   /* a required pointer is NULL                            */
+    SNN_ERR_MISALIGNED = 3,     /* a pointer is not aligned to its element size          */
+    SNN_ERR_UNSUPPORTED = 4,    /* a valid but unimplemented combination                 */
+    SNN_ERR_CUDA = 5,           /* the CUDA runtime reported an error at launch          */
+    SNN_ERR_NCCL = 6            /* reserved for the time-split transport                 */
+} snn_status;
+
+/* dtype of x, grad_spikes, grad_x (and of spikes when spike_fmt == SNN_SPK_IO).
+ * Arithmetic is always fp32: bf16 values are widened exactly on load and
+ * results rounded to nearest-even on store. */
+typedef enum { SNN_F32 = 0, SNN_BF16 = 1 } snn_dtype;
+
+/* Reset after a spike.  HARD: V = V_reset (Eq. 1's (1 - y) and V_rest*y terms,
+ * PAPER.md:165).  SOFT: V = H - V_th (BASELINE.json north_star; not in the paper). */
+typedef enum { SNN_RESET_HARD = 0, SNN_RESET_SOFT = 1 } snn_reset_mode;
+
+/* Surrogate derivative delta(u), u = H - V_th.
+ * SIGMOID: alpha e^{-alpha|u|} / (1 + e^{-alpha|u|})^2 (alpha = 4).
+ * ATAN:    (alpha/2) / (1 + (pi/2 alpha u)^2) (SpikingJelly convention). */
+typedef enum { SNN_SURR_SIGMOID = 0, SNN_SURR_ATAN = 1 } snn_surrogate;
+
+/* Spike output format (values are exactly 0 or 1):
+ *   U8   uint8  [T, ld]
+ *   BITS uint32 [T, ceil(N/32)] (dense rows; bit j of word w is neuron 32w + j;
+ *        bits of neurons >= N are 0)
+ *   IO   io dtype [T, ld] (fp32 or bf16 1.0/0.0 -- the form a following conv consumes) */
+typedef enum { SNN_SPK_U8 = 0, SNN_SPK_BITS = 1, SNN_SPK_IO = 2 } snn_spike_fmt;
+
+/* What the forward keeps for the backward (the paper never shows it: Listing 1 stores
+ * only args):
+ *   SAVE_H          fp32 pre-reset potential H[t, n] for every step;
+ *   SAVE_RECOMPUTE  fp32 post-reset V every SNN_LIF_CKPT_INTERVAL steps; the backward
+ *                   re-runs the forward charge from those checkpoints and x, bitwise;
+ *   SAVE_NONE       nothing (inference). */
+typedef enum { SNN_SAVE_H = 0, SNN_SAVE_RECOMPUTE = 1, SNN_SAVE_NONE = 2 } snn_save_mode;
+
+#define SNN_LIF_CKPT_INTERVAL 16
+
+/* Hyper-parameters (the paper's Eq. 1 and the north star's charge are one
+ * family).  With k = 1 - 1/tau and s = (decay_input ? 1/tau : 1):
+ *     H[t] = k V[t-1] + V_reset/tau + s X[t]       (charge; Eq. 1 at V_reset = 0, s = 1)
+ *     S[t] = (H[t] >= V_th)                         (fire, Eq. 2)
+ *     V[t] = HARD ? (S ? V_reset : H) : H - V_th S  (reset)
+ * Paper mode: tau = 1.25 (k_tau = 0.2), v_th = 0.3, v_reset = 0,
+ * HARD, decay_input = 0, detach_reset = 0, SIGMOID, alpha = 4. */
+typedef struct {
+    float tau;          /* >= 1 (finite).  k = 1 - 1/tau computed in fp32       */
+    float v_th;         /* > v_reset                                             */
+    float v_reset;      /* reset value, and V[-1] when v_init is NULL          */
+    int   reset_mode;   /* snn_reset_mode                                                     */
+    int   decay_input;  /* 1: H = V + (X - (V - V_reset))/tau (north star); 0: paper Eq. 1    */
+    int   detach_reset; /* 0: gradient flows through the reset (Eq. 3's -v delta term); 1: not */
+    int   surrogate;    /* snn_surrogate                                                      */
+    float alpha;        /* > 0 (finite)                                                       */
+} snn_lif_params;
+
+typedef struct {
+    int64_t T;          /* >= 1 time steps                                                    */
+    int64_t N;          /* >= 1 neurons                                                       */
+    int64_t ld;         /* >= N; row stride (elements) of x, spikes (U8/IO), grad_spikes, grad_x */
+    int     io_dtype;   /* snn_dtype                                                          */
+    int     spike_fmt;  /* snn_spike_fmt                                                      */
+    int     save_mode;  /* snn_save_mode                                                      */
+} snn_lif_shape;
+
+/* Bytes of the opaque `saved` buffer for (params, shape); 0 for SAVE_NONE or an invalid
+ * shape.  The buffer must be 16-byte aligned; its layout is private and valid only for
+ * the same (params, shape) pair and the same x / v_init. */
+size_t snn_lif_saved_bytes(const snn_lif_params* params, const snn_lif_shape* shape);
+
+/* Forward over all T steps in one launch (fusedForwardLIF; Eq. 1-2).
+ *   x        [T, ld] io dtype             input currents x_i^(t)               (read)
+ *   v_init   [N] fp32 or NULL -> v_reset   carry-in V[-1]          (read)
+ *   spikes   per shape->spike_fmt          S[t, n] = y_i^(t)                     (write)
+ *   saved    snn_lif_saved_bytes() bytes, NULL iff SAVE_NONE                    (write)
+ *   v_final  [N] fp32 or NULL              carry-out V[T-1], post-reset          (write)
+ * x must not alias any output. */
+snn_status snn_lif_forward(const snn_lif_params* params, const snn_lif_shape* shape,
+                           const void* x, const float* v_init, void* spikes, void* saved,
+                           float* v_final, void* stream);
+
+/* Backward (surrogate BPTT) over t = T-1..0 in one launch (fusedBackwardLIF,
+ * PAPER.md:302; Eq. 3):
+ *   gH[t] = gS[t] delta[t] + gV dV/dH[t];  grad_x[t] = s gH[t];  gV <- k gH[t]
+ * with dV/dH = HARD: (1 - S) + (V_reset - H) delta;  SOFT: 1 - V_th delta
+ * (the delta term dropped when detach_reset).
+ *   grad_spikes  [T, ld] io dtype   dL/dS[t] from the next layer (the paper's grad y)  (read)
+ *   x            [T, ld] io dtype   required iff SAVE_RECOMPUTE, else ignored (may be NULL)
+ *   v_init       [N] fp32 or NULL   the value given to the forward (RECOMPUTE only)
+ *   saved        the forward's saved buffer (same params/shape)                   (read)
+ *   grad_v_final [N] fp32 or NULL -> 0   dL/dV[T-1] from a later time segment      (read)
+ *   grad_x       [T, ld] io dtype   dL/dX[t]; must not alias any input            (write)
+ *   grad_v_init  [N] fp32 or NULL   dL/dV[-1], the carry to an earlier segment     (write)
+ * SAVE_NONE -> SNN_ERR_INVALID_VALUE. */
+snn_status snn_lif_backward(const snn_lif_params* params, const snn_lif_shape* shape,
+                            const void* grad_spikes, const void* x, const float* v_init,
+                            const void* saved, const float* grad_v_final, void* grad_x,
+                            float* grad_v_init, void* stream);
+
+/* Status name, e.g. "SNN_ERR_INVALID_VALUE" (static storage). */
+const char* snn_status_string(snn_status status);
+
+/* Detail for the last non-OK status returned on the calling thread ("" if none). */
+const char* snn_last_error_message(void);
+
+/* SNN_LIF_ABI_VERSION of the built library. */
+int snn_lif_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SNN_LIF_H */

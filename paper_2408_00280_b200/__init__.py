@@ -1,0 +1,13 @@
+"""B200-native (sm_100a) temporally fused LIF neurons -- arXiv 2408.00280.
+
+Product path: ``libsnn_lif.so`` (include/snn_lif.h C ABI, CUDA kernels in csrc/) and the
+thin Python layers over it (``lif`` functional API, ``autograd`` FusedLIF / LIFLayer,
+``dist`` multi-GPU sharding and time-split).  Importing this package loads the CUDA
+library and raises if it is missing: there is no CPU fallback.
+"""
+from . import _lib  # noqa: F401  (fails loudly when libsnn_lif.so is absent)
+from .lif import LIFForward, LIFParams, lif_backward, lif_forward, unpack_bits  # noqa: F401
+from .autograd import FusedLIF, LIFLayer  # noqa: F401
+
+__all__ = ["LIFParams", "LIFForward", "lif_forward", "lif_backward", "unpack_bits",
+           "FusedLIF", "LIFLayer"]

@@ -1,0 +1,99 @@
+"""ctypes binding of include/snn_lif.h (argument marshalling only).
+
+Loads the in-tree ``libsnn_lif.so``.  There is no fallback: if the library is missing or
+fails to load, importing this module raises, naming the fix (``__graft_entry__.build()``).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libsnn_lif.so")
+
+# enums (include/snn_lif.h)
+SNN_OK = 0
+STATUS_NAMES = {0: "SNN_OK", 1: "SNN_ERR_INVALID_VALUE", 2: "SNN_ERR_NULL_POINTER",
+                3: "SNN_ERR_MISALIGNED", 4: "SNN_ERR_UNSUPPORTED", 5: "SNN_ERR_CUDA",
+                6: "SNN_ERR_NCCL"}
+SNN_F32, SNN_BF16 = 0, 1
+SNN_RESET_HARD, SNN_RESET_SOFT = 0, 1
+SNN_SURR_SIGMOID, SNN_SURR_ATAN = 0, 1
+SNN_SPK_U8, SNN_SPK_BITS, SNN_SPK_IO = 0, 1, 2
+SNN_SAVE_H, SNN_SAVE_RECOMPUTE, SNN_SAVE_NONE = 0, 1, 2
+SNN_LIF_CKPT_INTERVAL = 16
+
+# Every symbol include/snn_lif.h declares (checked by tests/test_abi.py).
+EXPORTED_SYMBOLS = (
+    "snn_lif_saved_bytes", "snn_lif_forward", "snn_lif_backward", "snn_status_string",
+    "snn_last_error_message", "snn_lif_abi_version",
+)
+
+
+class snn_lif_params(ctypes.Structure):
+    _fields_ = [("tau", ctypes.c_float), ("v_th", ctypes.c_float), ("v_reset", ctypes.c_float),
+                ("reset_mode", ctypes.c_int), ("decay_input", ctypes.c_int),
+                ("detach_reset", ctypes.c_int), ("surrogate", ctypes.c_int),
+                ("alpha", ctypes.c_float)]
+
+
+class snn_lif_shape(ctypes.Structure):
+    _fields_ = [("T", ctypes.c_int64), ("N", ctypes.c_int64), ("ld", ctypes.c_int64),
+                ("io_dtype", ctypes.c_int), ("spike_fmt", ctypes.c_int),
+                ("save_mode", ctypes.c_int)]
+
+
+def _load() -> ctypes.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build the CUDA library first "
+                          "(python -c 'import __graft_entry__ as g; g.build()'); "
+                          "there is no CPU fallback")
+    lib = ctypes.CDLL(LIB_PATH)
+    P = ctypes.POINTER(snn_lif_params)
+    S = ctypes.POINTER(snn_lif_shape)
+    vp, fp = ctypes.c_void_p, ctypes.c_void_p
+    lib.snn_lif_saved_bytes.argtypes = [P, S]
+    lib.snn_lif_saved_bytes.restype = ctypes.c_size_t
+    lib.snn_lif_forward.argtypes = [P, S, vp, fp, vp, vp, fp, vp]
+    lib.snn_lif_forward.restype = ctypes.c_int
+    lib.snn_lif_backward.argtypes = [P, S, vp, vp, fp, vp, fp, vp, fp, vp]
+    lib.snn_lif_backward.restype = ctypes.c_int
+    lib.snn_status_string.argtypes = [ctypes.c_int]
+    lib.snn_status_string.restype = ctypes.c_char_p
+    lib.snn_last_error_message.argtypes = []
+    lib.snn_last_error_message.restype = ctypes.c_char_p
+    lib.snn_lif_abi_version.argtypes = []
+    lib.snn_lif_abi_version.restype = ctypes.c_int
+    return lib
+
+
+lib = _load()
+
+
+class SNNError(RuntimeError):
+    def __init__(self, status: int):
+        name = lib.snn_status_string(status).decode()
+        detail = lib.snn_last_error_message().decode()
+        super().__init__(f"{name}: {detail}")
+        self.status = status
+
+
+def check(status: int) -> None:
+    if status != SNN_OK:
+        raise SNNError(status)
+
+
+def snn_lif_saved_bytes(params: snn_lif_params, shape: snn_lif_shape) -> int:
+    return lib.snn_lif_saved_bytes(ctypes.byref(params), ctypes.byref(shape))
+
+
+def snn_lif_forward(params, shape, x, v_init, spikes, saved, v_final, stream) -> None:
+    """Raw entry point; pointer arguments are ints (device addresses) or None."""
+    check(lib.snn_lif_forward(ctypes.byref(params), ctypes.byref(shape), x, v_init, spikes,
+                              saved, v_final, stream))
+
+
+def snn_lif_backward(params, shape, grad_spikes, x, v_init, saved, grad_v_final, grad_x,
+                     grad_v_init, stream) -> None:
+    check(lib.snn_lif_backward(ctypes.byref(params), ctypes.byref(shape), grad_spikes, x, v_init,
+                               saved, grad_v_final, grad_x, grad_v_init, stream))

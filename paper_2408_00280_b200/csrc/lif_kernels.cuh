@@ -1,0 +1,302 @@
+// lif_kernels.cuh -- the temporally fused LIF forward / backward kernels (sm_100a).
+//
+// Temporal fusion: one thread owns VEC consecutive neurons for the
+// whole time axis; the membrane potential V (forward) or the carried gradient dL/dV
+// (backward) lives in registers across the T loop and each [T, N] tensor is streamed
+// exactly once, row by row, with 128-bit coalesced loads (a warp reads 32 x 16 B = 512 B
+// of one time row per instruction).  Memory-level parallelism comes from a PF-deep
+// register prefetch ring along T (loads do not depend on the recurrence, so rows t+1 ..
+// t+PF are in flight while row t is consumed).  No tensor cores: the op is elementwise-
+// recurrent and HBM-bound.
+#pragma once
+
+#include "lif_common.cuh"
+
+namespace snn {
+
+constexpr int kCkpt = 16;           // SNN_LIF_CKPT_INTERVAL
+constexpr int kBlock = 256;         // threads per CTA
+constexpr unsigned kFull = 0xffffffffu;
+
+enum { SPK_U8 = 0, SPK_BITS = 1, SPK_IO = 2 };
+enum { SAVE_H = 0, SAVE_RECOMPUTE = 1, SAVE_NONE = 2 };
+
+struct FwdArgs {
+    const void* x;        // [T, ld] IO
+    const float* v_init;  // [N] or null
+    void* spikes;         // per spike format
+    float* saved;         // SAVE_H: [T, ldh]; RECOMPUTE: [ceil(T/kCkpt), ldh]
+    float* v_final;       // [N] or null
+    int64_t T, N, ld, ldh, nwords;
+    LifConsts c;
+};
+
+struct BwdArgs {
+    const void* gS;             // [T, ld] IO
+    const void* x;              // [T, ld] IO (RECOMPUTE)
+    const float* saved;         // as FwdArgs::saved
+    const float* grad_v_final;  // [N] or null
+    void* gX;                   // [T, ld] IO
+    float* grad_v_init;         // [N] or null
+    int64_t T, N, ld, ldh;
+    LifConsts c;
+};
+
+// Pack VEC spike bits of this lane into the warp's uint32 words and store them
+// (SNN_SPK_BITS).  Lanes [w*L, (w+1)*L), L = 32/VEC, share word w of the warp.
+template <int VEC>
+__device__ __forceinline__ void store_spike_bits(uint32_t* row, int64_t g, unsigned bits,
+                                                 int64_t nwords) {
+    const int lane = threadIdx.x & 31;
+    uint32_t w;
+    if constexpr (VEC == 1) {
+        w = __ballot_sync(kFull, bits);
+    } else {
+        constexpr int L = 32 / VEC;
+        w = bits << ((lane % L) * VEC);
+#pragma unroll
+        for (int o = 1; o < L; o <<= 1) w |= __shfl_xor_sync(kFull, w, o);
+    }
+    constexpr int L = 32 / VEC;
+    if (lane % L == 0) {
+        const int64_t word = ((g - lane) * VEC) / 32 + lane / L;
+        if (word < nwords) __stcs(row + word, w);
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// Forward: Eq. 1-2 over t = 0..T-1.
+template <typename IO, int VEC, int SFMT, int SAVE, int PF>
+__global__ void __launch_bounds__(kBlock)
+lif_forward_kernel(const FwdArgs a) {
+    const int64_t g = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    const int64_t n0 = g * VEC;
+    const int nvalid = (int)max((int64_t)0, min((int64_t)VEC, a.N - n0));
+    // Lanes past N stay alive (their warp's shuffles need them) but touch no memory.
+    const IO* __restrict__ x = reinterpret_cast<const IO*>(a.x) + n0;
+    const LifConsts c = a.c;
+    const int64_t T = a.T, ld = a.ld;
+
+    float V[VEC];
+    if (a.v_init != nullptr && nvalid > 0) {
+        Pack<float, VEC> v0 = ld_group<float, VEC>(a.v_init + n0, nvalid);
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) V[i] = v0.v[i];
+    } else {
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) V[i] = c.v_reset;
+    }
+
+    Pack<IO, VEC> buf[PF];
+#pragma unroll
+    for (int j = 0; j < PF; ++j)
+        if (j < T) buf[j] = ld_group<IO, VEC>(x + (int64_t)j * ld, nvalid);
+
+    for (int64_t t0 = 0; t0 < T; t0 += PF) {
+#pragma unroll
+        for (int j = 0; j < PF; ++j) {
+            const int64_t t = t0 + j;
+            if (t < T) {
+                const Pack<IO, VEC> xv = buf[j];
+                if (t + PF < T)
+                    buf[j] = ld_group<IO, VEC>(x + (t + PF) * ld, nvalid);
+
+                if constexpr (SAVE == SAVE_RECOMPUTE) {
+                    if ((t % kCkpt) == 0 && nvalid > 0) {
+                        Pack<float, VEC> ck;
+#pragma unroll
+                        for (int i = 0; i < VEC; ++i) ck.v[i] = V[i];
+                        st_group<float, VEC>(a.saved + (t / kCkpt) * a.ldh + n0, ck, nvalid);
+                    }
+                }
+                Pack<float, VEC> hp;
+                unsigned bits = 0;
+#pragma unroll
+                for (int i = 0; i < VEC; ++i) {
+                    const float H = lif_charge(c, V[i], to_f32(xv.v[i]));
+                    const bool S = lif_fire(c, H);
+                    V[i] = lif_reset(c, H, S);
+                    hp.v[i] = H;
+                    bits |= (unsigned)S << i;
+                }
+                bits &= (nvalid >= VEC) ? ((VEC == 32) ? kFull : ((1u << VEC) - 1u)) : ((1u << nvalid) - 1u);
+                if constexpr (SAVE == SAVE_H) {
+                    if (nvalid > 0) st_group<float, VEC>(a.saved + t * a.ldh + n0, hp, nvalid);
+                }
+                if constexpr (SFMT == SPK_U8) {
+                    if (nvalid > 0) {
+                        Pack<uint8_t, VEC> sp;
+#pragma unroll
+                        for (int i = 0; i < VEC; ++i) sp.v[i] = (uint8_t)((bits >> i) & 1u);
+                        st_group<uint8_t, VEC>(reinterpret_cast<uint8_t*>(a.spikes) + t * ld + n0,
+                                               sp, nvalid);
+                    }
+                } else if constexpr (SFMT == SPK_IO) {
+                    if (nvalid > 0) {
+                        Pack<IO, VEC> sp;
+#pragma unroll
+                        for (int i = 0; i < VEC; ++i)
+                            sp.v[i] = from_f32<IO>(((bits >> i) & 1u) ? 1.0f : 0.0f);
+                        st_group<IO, VEC>(reinterpret_cast<IO*>(a.spikes) + t * ld + n0, sp, nvalid);
+                    }
+                } else {
+                    store_spike_bits<VEC>(reinterpret_cast<uint32_t*>(a.spikes) + t * a.nwords, g,
+                                          bits, a.nwords);
+                }
+            }
+        }
+    }
+    if (a.v_final != nullptr && nvalid > 0) {
+        Pack<float, VEC> vf;
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) vf.v[i] = V[i];
+        st_group<float, VEC>(a.v_final + n0, vf, nvalid);
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// Backward, SAVE_H: Eq. 3 over t = T-1..0 reading the saved H.
+template <typename IO, int VEC, int SURR, int PF>
+__global__ void __launch_bounds__(kBlock)
+lif_backward_saveh_kernel(const BwdArgs a) {
+    const int64_t g = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    const int64_t n0 = g * VEC;
+    const int nvalid = (int)max((int64_t)0, min((int64_t)VEC, a.N - n0));
+    if (nvalid == 0) return;  // no warp collectives in the backward
+    const IO* __restrict__ gs = reinterpret_cast<const IO*>(a.gS) + n0;
+    const float* __restrict__ hs = a.saved + n0;
+    IO* __restrict__ gx = reinterpret_cast<IO*>(a.gX) + n0;
+    const LifConsts c = a.c;
+    const int64_t T = a.T, ld = a.ld, ldh = a.ldh;
+
+    float gV[VEC];
+    if (a.grad_v_final != nullptr) {
+        Pack<float, VEC> g0 = ld_group<float, VEC>(a.grad_v_final + n0, nvalid);
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) gV[i] = g0.v[i];
+    } else {
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) gV[i] = 0.0f;
+    }
+
+    Pack<IO, VEC> gbuf[PF];
+    Pack<float, VEC> hbuf[PF];
+#pragma unroll
+    for (int j = 0; j < PF; ++j) {
+        const int64_t t = T - 1 - j;
+        if (t >= 0) {
+            gbuf[j] = ld_group<IO, VEC>(gs + t * ld, nvalid);
+            hbuf[j] = ld_group<float, VEC>(hs + t * ldh, nvalid);
+        }
+    }
+    for (int64_t t0 = T - 1; t0 >= 0; t0 -= PF) {
+#pragma unroll
+        for (int j = 0; j < PF; ++j) {
+            const int64_t t = t0 - j;
+            if (t >= 0) {
+                const Pack<IO, VEC> gv = gbuf[j];
+                const Pack<float, VEC> hv = hbuf[j];
+                if (t - PF >= 0) {
+                    gbuf[j] = ld_group<IO, VEC>(gs + (t - PF) * ld, nvalid);
+                    hbuf[j] = ld_group<float, VEC>(hs + (t - PF) * ldh, nvalid);
+                }
+                Pack<IO, VEC> out;
+#pragma unroll
+                for (int i = 0; i < VEC; ++i) {
+                    const float gH = lif_grad_step<SURR>(c, hv.v[i], to_f32(gv.v[i]), gV[i]);
+                    out.v[i] = from_f32<IO>(__fmul_rn(c.s, gH));
+                    gV[i] = __fmul_rn(c.k, gH);
+                }
+                st_group<IO, VEC>(gx + t * ld, out, nvalid);
+            }
+        }
+    }
+    if (a.grad_v_init != nullptr) {
+        Pack<float, VEC> gi;
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) gi.v[i] = gV[i];
+        st_group<float, VEC>(a.grad_v_init + n0, gi, nvalid);
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// Backward, SAVE_RECOMPUTE: per kCkpt-step chunk (last chunk first) reload the chunk's
+// entry V checkpoint, re-run the forward charge over the chunk from x (identical
+// instruction sequence -> bitwise-identical H), then walk the chunk backwards.  All
+// 2*kCkpt row loads of a chunk (x and gS) are issued before any is consumed.
+template <typename IO, int VEC, int SURR>
+__global__ void __launch_bounds__(kBlock)
+lif_backward_recompute_kernel(const BwdArgs a) {
+    const int64_t g = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    const int64_t n0 = g * VEC;
+    const int nvalid = (int)max((int64_t)0, min((int64_t)VEC, a.N - n0));
+    if (nvalid == 0) return;
+    const IO* __restrict__ gs = reinterpret_cast<const IO*>(a.gS) + n0;
+    const IO* __restrict__ xs = reinterpret_cast<const IO*>(a.x) + n0;
+    const float* __restrict__ ck = a.saved + n0;
+    IO* __restrict__ gx = reinterpret_cast<IO*>(a.gX) + n0;
+    const LifConsts c = a.c;
+    const int64_t T = a.T, ld = a.ld, ldh = a.ldh;
+
+    float gV[VEC];
+    if (a.grad_v_final != nullptr) {
+        Pack<float, VEC> g0 = ld_group<float, VEC>(a.grad_v_final + n0, nvalid);
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) gV[i] = g0.v[i];
+    } else {
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) gV[i] = 0.0f;
+    }
+
+    const int64_t nchunks = (T + kCkpt - 1) / kCkpt;
+    for (int64_t ch = nchunks - 1; ch >= 0; --ch) {
+        const int64_t t0 = ch * kCkpt;
+        const int len = (int)min((int64_t)kCkpt, T - t0);
+        const Pack<float, VEC> v0 = ld_group<float, VEC>(ck + ch * ldh, nvalid);
+        Pack<IO, VEC> xb[kCkpt];
+        Pack<IO, VEC> gb[kCkpt];
+#pragma unroll
+        for (int j = 0; j < kCkpt; ++j)
+            if (j < len) xb[j] = ld_group<IO, VEC>(xs + (t0 + j) * ld, nvalid);
+#pragma unroll
+        for (int j = 0; j < kCkpt; ++j)
+            if (j < len) gb[j] = ld_group<IO, VEC>(gs + (t0 + j) * ld, nvalid);
+
+        float h[kCkpt][VEC];
+        float V[VEC];
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) V[i] = v0.v[i];
+#pragma unroll
+        for (int j = 0; j < kCkpt; ++j) {
+            if (j < len) {
+#pragma unroll
+                for (int i = 0; i < VEC; ++i) {
+                    const float H = lif_charge(c, V[i], to_f32(xb[j].v[i]));
+                    V[i] = lif_reset(c, H, lif_fire(c, H));
+                    h[j][i] = H;
+                }
+            }
+        }
+#pragma unroll
+        for (int j = kCkpt - 1; j >= 0; --j) {
+            if (j < len) {
+                Pack<IO, VEC> out;
+#pragma unroll
+                for (int i = 0; i < VEC; ++i) {
+                    const float gH = lif_grad_step<SURR>(c, h[j][i], to_f32(gb[j].v[i]), gV[i]);
+                    out.v[i] = from_f32<IO>(__fmul_rn(c.s, gH));
+                    gV[i] = __fmul_rn(c.k, gH);
+                }
+                st_group<IO, VEC>(gx + (t0 + j) * ld, out, nvalid);
+            }
+        }
+    }
+    if (a.grad_v_init != nullptr) {
+        Pack<float, VEC> gi;
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) gi.v[i] = gV[i];
+        st_group<float, VEC>(a.grad_v_init + n0, gi, nvalid);
+    }
+}
+
+}  // namespace snn

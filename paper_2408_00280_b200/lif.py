@@ -1,0 +1,186 @@
+"""Functional torch-facing API over the C ABI (marshalling only; every step of the LIF
+path runs in the CUDA kernels of libsnn_lif.so).
+
+    lif_forward(x, params, ...)   -> LIFForward(spikes, saved, v_final, ...)
+    lif_backward(grad_spikes, fwd, ...) -> (grad_x, grad_v_init)
+
+``x`` is a CUDA tensor [T, N] (fp32 or bf16) whose rows may be strided (``x.stride(1)``
+must be 1; ``ld = x.stride(0)``), so a neuron-shard column view of a wider tensor is
+passed without a copy.  Kernels are enqueued on ``torch.cuda.current_stream()``.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, replace
+from typing import Optional
+
+import torch
+
+from . import _lib
+
+_SPIKE_FMTS = {"u8": _lib.SNN_SPK_U8, "bits": _lib.SNN_SPK_BITS, "io": _lib.SNN_SPK_IO}
+_SAVE_MODES = {"h": _lib.SNN_SAVE_H, "recompute": _lib.SNN_SAVE_RECOMPUTE, "none": _lib.SNN_SAVE_NONE}
+_DTYPES = {torch.float32: _lib.SNN_F32, torch.bfloat16: _lib.SNN_BF16}
+
+
+@dataclass(frozen=True)
+class LIFParams:
+    """LIF hyper-parameters (include/snn_lif.h ``snn_lif_params``).
+
+    Defaults are the paper's: k_tau = 0.2 (tau = 1.25), V_th = 0.3,
+    V_rest = 0, hard reset, input not decayed (Eq. 1), gradient through the reset (Eq. 3),
+    sigmoid surrogate with alpha = 4."""
+    tau: float = 1.25
+    v_th: float = 0.3
+    v_reset: float = 0.0
+    reset: str = "hard"          # "hard" | "soft"
+    decay_input: bool = False    # True: H = V + (X - (V - V_reset))/tau (north star)
+    detach_reset: bool = False
+    surrogate: str = "sigmoid"   # "sigmoid" | "atan"
+    alpha: float = 4.0
+
+    @staticmethod
+    def paper() -> "LIFParams":
+        return LIFParams()
+
+    @staticmethod
+    def north_star(**kw) -> "LIFParams":
+        """BASELINE.json configs[0]: tau=2, V_th=1, V_reset=0, hard, sigmoid, decay_input."""
+        return replace(LIFParams(tau=2.0, v_th=1.0, v_reset=0.0, decay_input=True), **kw)
+
+    def to_c(self) -> _lib.snn_lif_params:
+        return _lib.snn_lif_params(
+            float(self.tau), float(self.v_th), float(self.v_reset),
+            {"hard": _lib.SNN_RESET_HARD, "soft": _lib.SNN_RESET_SOFT}[self.reset],
+            int(bool(self.decay_input)), int(bool(self.detach_reset)),
+            {"sigmoid": _lib.SNN_SURR_SIGMOID, "atan": _lib.SNN_SURR_ATAN}[self.surrogate],
+            float(self.alpha))
+
+
+@dataclass
+class LIFForward:
+    """Result of lif_forward: spikes plus what the backward needs."""
+    spikes: torch.Tensor
+    saved: Optional[torch.Tensor]
+    v_final: Optional[torch.Tensor]
+    x: torch.Tensor
+    v_init: Optional[torch.Tensor]
+    params: LIFParams
+    shape: _lib.snn_lif_shape
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else t.data_ptr()
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _check_2d(name: str, t: torch.Tensor) -> None:
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU path exists)")
+    if t.dim() != 2 or (t.size(1) > 1 and t.stride(1) != 1):
+        raise ValueError(f"{name} must be [T, N] with unit column stride, got {tuple(t.shape)} "
+                         f"strides {t.stride()}")
+
+
+def _vec(name, t, N, device):
+    if t is None:
+        return None
+    if not (t.is_cuda and t.dtype == torch.float32 and t.numel() == N and t.is_contiguous()):
+        raise ValueError(f"{name} must be a contiguous fp32 CUDA tensor of {N} elements")
+    return t
+
+
+def make_shape(x: torch.Tensor, spike_fmt: str, save_mode: str) -> _lib.snn_lif_shape:
+    T, N = x.shape
+    ld = x.stride(0) if T > 1 else N
+    return _lib.snn_lif_shape(T, N, max(ld, N), _DTYPES[x.dtype], _SPIKE_FMTS[spike_fmt],
+                              _SAVE_MODES[save_mode])
+
+
+def saved_bytes(params: LIFParams, shape: _lib.snn_lif_shape) -> int:
+    return _lib.snn_lif_saved_bytes(params.to_c(), shape)
+
+
+def alloc_spikes(x: torch.Tensor, spike_fmt: str) -> torch.Tensor:
+    T, N = x.shape
+    if spike_fmt == "u8":
+        return torch.empty((T, N), dtype=torch.uint8, device=x.device)
+    if spike_fmt == "bits":
+        return torch.empty((T, (N + 31) // 32), dtype=torch.int32, device=x.device)
+    return torch.empty((T, N), dtype=x.dtype, device=x.device)
+
+
+def lif_forward(x: torch.Tensor, params: LIFParams = LIFParams(), *,
+                v_init: Optional[torch.Tensor] = None, spike_fmt: str = "u8",
+                save_mode: str = "recompute", return_v_final: bool = True,
+                spikes: Optional[torch.Tensor] = None, saved: Optional[torch.Tensor] = None,
+                v_final: Optional[torch.Tensor] = None) -> LIFForward:
+    """Eq. 1-2 over all T steps in one kernel launch (fusedForwardLIF).
+
+    spike_fmt: "u8" ([T, N] uint8), "bits" ([T, ceil(N/32)] int32 words, bit j of word w =
+    neuron 32w+j) or "io" (x's dtype, 0/1).  save_mode: "recompute" (V checkpoints every
+    16 steps), "h" (fp32 H every step) or "none" (inference).  Preallocated outputs may
+    be passed (spikes must then have row stride ld for u8/io)."""
+    _check_2d("x", x)
+    if x.dtype not in _DTYPES:
+        raise ValueError(f"x dtype {x.dtype} unsupported (fp32 / bf16)")
+    T, N = x.shape
+    shape = make_shape(x, spike_fmt, save_mode)
+    cp = params.to_c()
+    v_init = _vec("v_init", v_init, N, x.device)
+    if spikes is None:
+        spikes = alloc_spikes(x, spike_fmt)
+        if spike_fmt != "bits" and shape.ld != N:
+            # keep the caller's ld for views: allocate [T, ld] and view its first N columns
+            spikes = torch.empty((T, shape.ld), dtype=spikes.dtype, device=x.device)[:, :N]
+    nbytes = _lib.snn_lif_saved_bytes(cp, shape)
+    if save_mode != "none" and saved is None:
+        saved = torch.empty(nbytes // 4, dtype=torch.float32, device=x.device)
+    if return_v_final and v_final is None:
+        v_final = torch.empty(N, dtype=torch.float32, device=x.device)
+    _lib.snn_lif_forward(cp, shape, _ptr(x), _ptr(v_init), _ptr(spikes),
+                         _ptr(saved) if save_mode != "none" else None, _ptr(v_final), _stream())
+    return LIFForward(spikes, saved if save_mode != "none" else None, v_final, x, v_init,
+                      params, shape)
+
+
+def lif_backward(grad_spikes: torch.Tensor, fwd: LIFForward, *,
+                 grad_v_final: Optional[torch.Tensor] = None, return_grad_v_init: bool = True,
+                 grad_x: Optional[torch.Tensor] = None):
+    """Eq. 3 over t = T-1..0 in one kernel launch (fusedBackwardLIF).
+    Returns (grad_x [T, N] in x's dtype, grad_v_init [N] fp32 or None)."""
+    _check_2d("grad_spikes", grad_spikes)
+    x = fwd.x
+    T, N = x.shape
+    if tuple(grad_spikes.shape) != (T, N) or grad_spikes.dtype != x.dtype:
+        raise ValueError("grad_spikes must match x in shape and dtype")
+    if fwd.saved is None:
+        raise ValueError("forward ran with save_mode='none'; nothing to differentiate")
+    ld = fwd.shape.ld
+    if T > 1 and grad_spikes.stride(0) != ld:
+        grad_spikes = grad_spikes.contiguous() if ld == N else _restride(grad_spikes, ld)
+    if grad_x is None:
+        grad_x = torch.empty((T, ld), dtype=x.dtype, device=x.device)[:, :N]
+    grad_v_final = _vec("grad_v_final", grad_v_final, N, x.device)
+    grad_v_init = torch.empty(N, dtype=torch.float32, device=x.device) if return_grad_v_init else None
+    _lib.snn_lif_backward(fwd.params.to_c(), fwd.shape, _ptr(grad_spikes), _ptr(x),
+                          _ptr(fwd.v_init), _ptr(fwd.saved), _ptr(grad_v_final), _ptr(grad_x),
+                          _ptr(grad_v_init), _stream())
+    return grad_x, grad_v_init
+
+
+def _restride(t: torch.Tensor, ld: int) -> torch.Tensor:
+    T, N = t.shape
+    out = torch.empty((T, ld), dtype=t.dtype, device=t.device)[:, :N]
+    out.copy_(t)
+    return out
+
+
+def unpack_bits(words: torch.Tensor, N: int) -> torch.Tensor:
+    """[T, ceil(N/32)] int32 spike words -> [T, N] uint8 (a view helper for tests/users)."""
+    T, W = words.shape
+    shifts = torch.arange(32, device=words.device, dtype=torch.int32)
+    bits = (words.unsqueeze(-1) >> shifts) & 1
+    return bits.reshape(T, W * 32)[:, :N].to(torch.uint8)

@@ -1,0 +1,158 @@
+"""GPU-vs-oracle comparison protocol.
+
+Test infrastructure: imported by tests/, __graft_entry__.smoke() and bench.py's parity
+leg.  Runs the CUDA path through the product API and the oracle on the SAME seeded
+inputs (generated on the host by snn_synth; never copied back from the CUDA path), then
+compares:
+
+* spikes: exact, except a column whose first disagreement falls where the oracle has
+  |H - V_th| < tie_eps (1e-5, BASELINE.json north_star).  Such a column is
+  "tie-diverged": its later steps and its whole gradient column (the reverse recursion
+  makes every earlier gX depend on the diverged tail) are excluded and counted.
+* values (H, v_final, grad_x, grad_v_init): |gpu - oracle| <= rtol |oracle| + atol with
+  rtol = 1e-5 (fp32) / 1e-2 (bf16 outputs); atol = rtol * max(1, |V_th|, |V_reset|) for
+  potentials and rtol * max|oracle gradient| of the column for gradients (the surrogate
+  underflows smoothly, so a purely relative test on 1e-30-sized gradients is meaningless).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+import oracle
+import snn_synth
+
+TIE_EPS = 1e-5
+
+
+def oracle_params(p, smoothed=False) -> "oracle.OracleParams":
+    """The oracle reads the same float32 hyper-parameters the kernel received (R9)."""
+    f = lambda v: float(np.float32(v))
+    return oracle.OracleParams(tau=f(p.tau), v_th=f(p.v_th), v_reset=f(p.v_reset),
+                               soft_reset=(p.reset == "soft"), decay_input=bool(p.decay_input),
+                               detach_reset=bool(p.detach_reset), surrogate=p.surrogate,
+                               alpha=f(p.alpha), smoothed=smoothed)
+
+
+@dataclass
+class ParityReport:
+    ok: bool = True
+    tie_cols: int = 0
+    n_cols: int = 0
+    max_err: dict = field(default_factory=dict)
+    failures: list = field(default_factory=list)
+
+    def fail(self, msg):
+        self.ok = False
+        if len(self.failures) < 20:
+            self.failures.append(msg)
+
+    def __str__(self):
+        return (f"ok={self.ok} tie_cols={self.tie_cols}/{self.n_cols} max_err={self.max_err} "
+                f"failures={self.failures[:5]}")
+
+
+def _as_np(t):
+    if isinstance(t, torch.Tensor):
+        return t.detach().float().cpu().numpy().astype(np.float64)
+    return np.asarray(t, dtype=np.float64)
+
+
+def compare(params, ref_fwd, ref_gX, ref_gvi, S_gpu, gX_gpu, *, H_gpu=None, vf_gpu=None,
+            gvi_gpu=None, io_bf16=False, col_ids=None) -> ParityReport:
+    """ref_*: oracle outputs (float64 numpy, [T, n]); *_gpu: same-shaped GPU outputs."""
+    rep = ParityReport()
+    S_o, H_o = ref_fwd["S"], ref_fwd["H"]
+    T, n = S_o.shape
+    rep.n_cols = n
+    S_g = _as_np(S_gpu)
+    v_th = float(np.float32(params.v_th))
+    mism = S_g != S_o
+    bad_col = mism.any(axis=0)
+    diverged = np.zeros(n, dtype=bool)
+    first = np.full(n, T)
+    for c in np.nonzero(bad_col)[0]:
+        t0 = int(np.argmax(mism[:, c]))
+        first[c] = t0
+        if abs(H_o[t0, c] - v_th) < TIE_EPS:
+            diverged[c] = True
+        else:
+            cid = c if col_ids is None else int(col_ids[c])
+            rep.fail(f"spike mismatch at (t={t0}, n={cid}): oracle S={S_o[t0, c]} H={H_o[t0, c]!r} "
+                     f"gpu S={S_g[t0, c]}")
+    rep.tie_cols = int(diverged.sum())
+    keep = ~diverged
+
+    pot_rtol = 1e-5
+    pot_atol = 1e-5 * max(1.0, abs(v_th), abs(float(params.v_reset)))
+
+    def chk(name, got, ref, rtol, atol, mask=None):
+        got = _as_np(got)
+        err = np.abs(got - ref)
+        lim = rtol * np.abs(ref) + atol
+        both_nan = np.isnan(got) & np.isnan(ref)
+        bad = (err > lim) & ~both_nan
+        if mask is not None:
+            bad &= mask
+        e = np.where(np.isfinite(err) & (mask if mask is not None else True), err, 0.0)
+        rep.max_err[name] = float(e.max()) if e.size else 0.0
+        if bad.any():
+            idx = np.argwhere(bad)[0]
+            rep.fail(f"{name} mismatch at {tuple(int(i) for i in idx)}: gpu={got[tuple(idx)]!r} "
+                     f"oracle={ref[tuple(idx)]!r}")
+
+    if H_gpu is not None:
+        tmask = np.arange(T)[:, None] < np.where(diverged, first, T)[None, :]
+        chk("H", H_gpu, H_o, pot_rtol, pot_atol, tmask)
+    if vf_gpu is not None:
+        chk("v_final", vf_gpu, ref_fwd["v_final"], pot_rtol, pot_atol, keep)
+    if gX_gpu is not None:
+        g_rtol = 1e-2 if io_bf16 else 1e-5
+        colmax = np.abs(ref_gX).max(axis=0, initial=0.0)
+        if ref_gvi is not None:
+            colmax = np.maximum(colmax, np.abs(ref_gvi))
+        atol = g_rtol * np.maximum(colmax, 1e-30)[None, :]
+        chk("grad_x", gX_gpu, ref_gX, g_rtol, atol, np.broadcast_to(keep[None, :], ref_gX.shape))
+        if gvi_gpu is not None and ref_gvi is not None:
+            chk("grad_v_init", gvi_gpu, ref_gvi, 1e-5, 1e-5 * np.maximum(colmax, 1e-30), keep)
+    return rep
+
+
+def run_gpu_and_oracle(params, T, N, *, dtype=torch.float32, spike_fmt="u8", save_mode="recompute",
+                       seed_x=1234, seed_g=4321, x_mean=0.0, x_std=1.0, with_v_init=False,
+                       with_grad_v_final=False, ld=None, device="cuda"):
+    """Full-tensor parity case: host-generated inputs, GPU run, oracle run, compare."""
+    import paper_2408_00280_b200 as snn
+    ld = N if ld is None else ld
+    X = snn_synth.normal_tensor(seed_x, T, N, mean=x_mean, std=x_std, dtype=dtype)
+    G = snn_synth.normal_tensor(seed_g, T, N, dtype=dtype)
+    v0 = (snn_synth.normal_tensor(seed_x + 1, 1, N, std=0.5)[0] if with_v_init else None)
+    gvf = (snn_synth.normal_tensor(seed_g + 1, 1, N)[0] if with_grad_v_final else None)
+
+    xd_full = torch.zeros((T, ld), dtype=dtype, device=device)
+    xd_full[:, :N] = X.to(device)
+    xd = xd_full[:, :N]
+    gd_full = torch.zeros((T, ld), dtype=dtype, device=device)
+    gd_full[:, :N] = G.to(device)
+    gd = gd_full[:, :N]
+    fwd = snn.lif_forward(xd, params, v_init=None if v0 is None else v0.to(device),
+                          spike_fmt=spike_fmt, save_mode=save_mode)
+    gX, gvi = snn.lif_backward(gd, fwd, grad_v_final=None if gvf is None else gvf.to(device))
+    torch.cuda.synchronize()
+    S = fwd.spikes
+    if spike_fmt == "bits":
+        S = snn.unpack_bits(S, N)
+    H_gpu = None
+    if save_mode == "h":
+        ldh = (N + 15) // 16 * 16
+        H_gpu = fwd.saved.view(T, ldh)[:, :N]
+
+    op = oracle_params(params)
+    ref = oracle.forward(op, X.double().numpy(), v_init=None if v0 is None else v0.double().numpy())
+    rgX, rgvi = oracle.backward(op, G.double().numpy(), ref["H"],
+                                grad_v_final=None if gvf is None else gvf.double().numpy())
+    rep = compare(params, ref, rgX, rgvi, S, gX, H_gpu=H_gpu, vf_gpu=fwd.v_final, gvi_gpu=gvi,
+                  io_bf16=(dtype == torch.bfloat16))
+    return rep, dict(fwd=fwd, gX=gX, gvi=gvi, S=S, X=X, G=G)

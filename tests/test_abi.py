@@ -1,0 +1,95 @@
+"""The C-ABI library loads and exports every symbol include/snn_lif.h declares; host-side
+validation (which runs before any launch) rejects bad arguments.  No GPU needed: every
+call here returns an error status before touching the device."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from conftest import ROOT
+
+HEADER = os.path.join(ROOT, "include", "snn_lif.h")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(snn_\w+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    import __graft_entry__
+    __graft_entry__._build_module().build()
+    from paper_2408_00280_b200 import _lib
+    return _lib
+
+
+def test_every_declared_symbol_is_exported(lib):
+    decl = declared_functions()
+    assert decl, "no declarations parsed"
+    for name in decl:
+        assert hasattr(lib.lib, name), f"{name} declared in snn_lif.h but not exported"
+    assert sorted(lib.EXPORTED_SYMBOLS) == decl
+
+
+def test_abi_version_and_status_strings(lib):
+    assert lib.lib.snn_lif_abi_version() == 1
+    assert lib.lib.snn_status_string(0) == b"SNN_OK"
+    assert lib.lib.snn_status_string(3) == b"SNN_ERR_MISALIGNED"
+
+
+def _p(lib, **kw):
+    d = dict(tau=1.25, v_th=0.3, v_reset=0.0, reset_mode=0, decay_input=0, detach_reset=0,
+             surrogate=0, alpha=4.0)
+    d.update(kw)
+    return lib.snn_lif_params(**d)
+
+
+def _s(lib, **kw):
+    d = dict(T=8, N=1024, ld=1024, io_dtype=0, spike_fmt=0, save_mode=1)
+    d.update(kw)
+    return lib.snn_lif_shape(**d)
+
+
+def test_saved_bytes(lib):
+    # RECOMPUTE: ceil(T/16) rows of round_up(N, 16) floats; SAVE_H: T rows; NONE: 0
+    assert lib.snn_lif_saved_bytes(_p(lib), _s(lib, T=40, N=1000, ld=1000)) == 3 * 1008 * 4
+    assert lib.snn_lif_saved_bytes(_p(lib), _s(lib, T=40, N=1000, ld=1000, save_mode=0)) == 40 * 1008 * 4
+    assert lib.snn_lif_saved_bytes(_p(lib), _s(lib, save_mode=2)) == 0
+    assert lib.snn_lif_saved_bytes(_p(lib, tau=0.5), _s(lib)) == 0
+
+
+@pytest.mark.parametrize("pkw,skw,code", [
+    (dict(tau=0.9), {}, 1), (dict(tau=float("nan")), {}, 1), (dict(v_th=0.0), {}, 1),
+    (dict(alpha=0.0), {}, 1), (dict(reset_mode=2), {}, 1), (dict(surrogate=7), {}, 1),
+    (dict(decay_input=2), {}, 1),
+    ({}, dict(T=0), 1), ({}, dict(N=0), 1), ({}, dict(ld=10), 1), ({}, dict(io_dtype=5), 1),
+    ({}, dict(spike_fmt=3), 1), ({}, dict(save_mode=9), 1),
+    ({}, dict(T=1 << 40, N=1 << 30, ld=1 << 30), 1),
+])
+def test_forward_validation(lib, pkw, skw, code):
+    st = lib.lib.snn_lif_forward(ctypes.byref(_p(lib, **pkw)), ctypes.byref(_s(lib, **skw)),
+                                 16, None, 16, 16, None, None)
+    assert st == code
+    assert lib.lib.snn_last_error_message()
+
+
+def test_null_and_misaligned_pointers(lib):
+    P, S = ctypes.byref(_p(lib)), ctypes.byref(_s(lib))
+    assert lib.lib.snn_lif_forward(P, S, None, None, 16, 16, None, None) == 2
+    assert lib.lib.snn_lif_forward(P, S, 16, None, None, 16, None, None) == 2
+    assert lib.lib.snn_lif_forward(P, S, 16, None, 16, None, None, None) == 2   # saved needed
+    assert lib.lib.snn_lif_forward(P, S, 18, None, 16, 16, None, None) == 3     # x not 4-aligned
+    assert lib.lib.snn_lif_forward(P, S, 16, None, 16, 24, None, None) == 3     # saved not 16-aligned
+    # backward
+    assert lib.lib.snn_lif_backward(P, S, None, 16, None, 16, None, 16, None, None) == 2
+    assert lib.lib.snn_lif_backward(P, S, 16, None, None, 16, None, 16, None, None) == 2  # x for RECOMPUTE
+    Sn = ctypes.byref(_s(lib, save_mode=2))
+    assert lib.lib.snn_lif_backward(P, Sn, 16, 16, None, 16, None, 16, None, None) == 1
+
+
+def test_python_errors_are_loud(lib):
+    err = lib.SNNError(1)
+    assert "SNN_ERR_INVALID_VALUE" in str(err)

@@ -1,0 +1,207 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 oracle, element by element,
+on seeded inputs.  Plus GPU-vs-GPU bitwise invariants."""
+import itertools
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2408_00280_b200 as snn  # noqa: E402  (raises if libsnn_lif.so is missing)
+import oracle  # noqa: E402
+import snn_synth  # noqa: E402
+from parity import compare, oracle_params, run_gpu_and_oracle  # noqa: E402
+
+LIFParams = snn.LIFParams
+PAPER = LIFParams.paper()
+CFG0 = LIFParams.north_star()
+
+
+def assert_ok(rep):
+    assert rep.ok, str(rep)
+
+
+# ------------------------------------------------------------------ BASELINE configs[0]
+
+@pytest.mark.parametrize("save_mode", ["recompute", "h"])
+@pytest.mark.parametrize("spike_fmt", ["u8", "bits", "io"])
+def test_cfg0_n1024_t8(save_mode, spike_fmt):
+    """BASELINE.json configs[0]: N=1024, T=8, fp32, tau=2, V_th=1, hard, sigmoid;
+    X ~ N(1, 1) (DESIGN.md input recipe)."""
+    rep, _ = run_gpu_and_oracle(CFG0, 8, 1024, spike_fmt=spike_fmt, save_mode=save_mode, x_mean=1.0)
+    assert_ok(rep)
+    assert rep.tie_cols == 0
+
+
+# ------------------------------------------------------------------ shapes / ragged tails
+
+SHAPES = [(1, 1), (1, 37), (2, 3), (7, 31), (15, 32), (16, 33), (17, 129), (33, 1000),
+          (40, 4097), (64, 2051)]
+
+
+@pytest.mark.parametrize("T,N", SHAPES)
+@pytest.mark.parametrize("save_mode", ["recompute", "h"])
+def test_paper_params_shapes(T, N, save_mode):
+    rep, _ = run_gpu_and_oracle(PAPER, T, N, save_mode=save_mode, with_v_init=True,
+                                with_grad_v_final=True)
+    assert_ok(rep)
+
+
+FLAGS = list(itertools.product(["hard", "soft"], [False, True], [False, True], ["sigmoid", "atan"]))
+
+
+@pytest.mark.parametrize("reset,decay_input,detach,surr", FLAGS)
+def test_all_flag_combinations(reset, decay_input, detach, surr):
+    p = LIFParams(tau=1.7, v_th=0.8, v_reset=0.1, reset=reset, decay_input=decay_input,
+                  detach_reset=detach, surrogate=surr, alpha=2.0 if surr == "atan" else 4.0)
+    rep, _ = run_gpu_and_oracle(p, 37, 2500, x_mean=0.7, save_mode="recompute", with_v_init=True,
+                                with_grad_v_final=True)
+    assert_ok(rep)
+    rep, _ = run_gpu_and_oracle(p, 21, 777, x_mean=0.7, save_mode="h")
+    assert_ok(rep)
+
+
+@pytest.mark.parametrize("spike_fmt", ["u8", "bits", "io"])
+@pytest.mark.parametrize("save_mode", ["recompute", "h"])
+@pytest.mark.parametrize("N", [8, 1000, 4103])
+def test_bf16_io(spike_fmt, save_mode, N):
+    rep, _ = run_gpu_and_oracle(PAPER, 19, N, dtype=torch.bfloat16, spike_fmt=spike_fmt,
+                                save_mode=save_mode, with_v_init=True, with_grad_v_final=True)
+    assert_ok(rep)
+
+
+@pytest.mark.parametrize("ld_extra", [1, 3, 64])
+def test_strided_rows_scalar_and_vector_paths(ld_extra):
+    """ld > N (column views); ld % 4 != 0 forces the scalar path."""
+    rep, _ = run_gpu_and_oracle(PAPER, 23, 1500, ld=1500 + ld_extra, with_v_init=True)
+    assert_ok(rep)
+    rep, _ = run_gpu_and_oracle(PAPER, 23, 1500, ld=1500 + ld_extra, dtype=torch.bfloat16)
+    assert_ok(rep)
+
+
+def test_long_horizon_t1024():
+    rep, _ = run_gpu_and_oracle(PAPER, 1024, 3000, save_mode="recompute")
+    assert_ok(rep)
+
+
+def test_nan_propagates_like_oracle():
+    T, N = 5, 64
+    X = snn_synth.normal_tensor(3, T, N)
+    X[2, 5] = float("nan")
+    fwd = snn.lif_forward(X.cuda(), PAPER, save_mode="h")
+    torch.cuda.synchronize()
+    ref = oracle.forward(oracle_params(PAPER), X.double().numpy())
+    S = fwd.spikes.cpu().numpy()
+    assert S[2, 5] == 0 and (S == ref["S"]).all()
+    assert np.isnan(fwd.v_final[5].item())
+
+
+# ------------------------------------------------------------------ GPU-vs-GPU bitwise
+
+def _run(params, X, G, spike_fmt="u8", save_mode="recompute", v0=None, gvf=None):
+    fwd = snn.lif_forward(X, params, v_init=v0, spike_fmt=spike_fmt, save_mode=save_mode)
+    gX, gvi = snn.lif_backward(G, fwd, grad_v_final=gvf)
+    return fwd, gX, gvi
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_saveh_equals_recompute_and_formats_agree_bitwise(dtype):
+    T, N = 77, 5003
+    X = snn_synth.normal_tensor(11, T, N, dtype=dtype).cuda()
+    G = snn_synth.normal_tensor(12, T, N, dtype=dtype).cuda()
+    f1, g1, v1 = _run(PAPER, X, G, "u8", "recompute")
+    f2, g2, v2 = _run(PAPER, X, G, "bits", "h")
+    f3, g3, v3 = _run(PAPER, X, G, "io", "recompute")
+    torch.cuda.synchronize()
+    assert torch.equal(g1, g2) and torch.equal(v1, v2) and torch.equal(g1, g3)
+    assert torch.equal(f1.v_final, f2.v_final)
+    assert torch.equal(snn.unpack_bits(f2.spikes, N), f1.spikes)
+    assert torch.equal(f3.spikes.to(torch.uint8), f1.spikes)
+
+
+@pytest.mark.parametrize("cuts", [[1], [16], [5, 37], [3, 19, 50, 51]])
+def test_segmented_equals_whole_bitwise(cuts):
+    """chained segments (v_final -> v_init, grad_v_init -> grad_v_final) are
+    bitwise equal to the whole axis -- the property the time-split relies on."""
+    T, N = 64, 3001
+    p = LIFParams(tau=1.6, v_th=0.8, v_reset=0.1, decay_input=True)
+    X = snn_synth.normal_tensor(21, T, N, mean=0.8).cuda()
+    G = snn_synth.normal_tensor(22, T, N).cuda()
+    fw, gw, vw = _run(p, X, G)
+    b = [0] + cuts + [T]
+    v = None; fwds = []
+    for a, c in zip(b[:-1], b[1:]):
+        f = snn.lif_forward(X[a:c], p, v_init=v)
+        v = f.v_final; fwds.append(f)
+    g = None; gxs = []
+    for (a, c), f in reversed(list(zip(zip(b[:-1], b[1:]), fwds))):
+        gx, g = snn.lif_backward(G[a:c], f, grad_v_final=g)
+        gxs.insert(0, gx)
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat([f.spikes for f in fwds]), fw.spikes)
+    assert torch.equal(v, fw.v_final)
+    assert torch.equal(torch.cat(gxs), gw) and torch.equal(g, vw)
+
+
+def test_neuron_shard_views_equal_whole_bitwise():
+    """Column-range views (ld > N) of one tensor == the whole run (P11, 8(e).1)."""
+    T, N = 50, 8192
+    X = snn_synth.normal_tensor(31, T, N).cuda()
+    G = snn_synth.normal_tensor(32, T, N).cuda()
+    fw, gw, vw = _run(PAPER, X, G)
+    for a, c in [(0, 4096), (4096, 8192), (1024, 1028), (100, 3333)]:
+        f, g, v = _run(PAPER, X[:, a:c], G[:, a:c])
+        torch.cuda.synchronize()
+        assert torch.equal(f.spikes, fw.spikes[:, a:c])
+        assert torch.equal(g, gw[:, a:c]) and torch.equal(v, vw[a:c])
+
+
+def test_device_generator_matches_host_generator():
+    d = snn_synth.normal_tensor(1234, 16, 5000, device="cuda").cpu()
+    h = snn_synth.normal_tensor(1234, 16, 5000)
+    assert torch.equal(d, h)
+
+
+# ------------------------------------------------------------------ full size, sampled
+
+def test_cfg1_full_size_sampled_columns():
+    """BASELINE.json configs[1] at its largest T (N=2^20, T=512), in bench.py's launch
+    configuration, checked on 4096 sampled columns regenerated on the host (P11)."""
+    T, N = 512, 1 << 20
+    X = snn_synth.normal_tensor(1234, T, N, device="cuda")
+    G = snn_synth.normal_tensor(4321, T, N, device="cuda")
+    fwd, gX, gvi = _run(PAPER, X, G)
+    torch.cuda.synchronize()
+    cols = np.sort(np.random.default_rng(0).choice(N, 4096, replace=False))
+    ci = torch.as_tensor(cols, device="cuda")
+    Xh = snn_synth.normal_columns(1234, T, N, cols)
+    Gh = snn_synth.normal_columns(4321, T, N, cols)
+    op = oracle_params(PAPER)
+    ref = oracle.forward(op, Xh.double().numpy())
+    rgX, rgvi = oracle.backward(op, Gh.double().numpy(), ref["H"])
+    rep = compare(PAPER, ref, rgX, rgvi, fwd.spikes[:, ci].cpu(), gX[:, ci].cpu(),
+                  vf_gpu=fwd.v_final[ci].cpu(), gvi_gpu=gvi[ci].cpu(), col_ids=cols)
+    assert_ok(rep)
+
+
+# ------------------------------------------------------------------ fault injection
+
+def test_fault_injection_perturbed_k_fails_parity():
+    """a kernel whose k is off by 1e-3 relative must fail parity, naming
+    the first bad element -- the comparator is not vacuous."""
+    T, N = 32, 512
+    p_bad = LIFParams(tau=1.25 * (1 + 1e-3))
+    X = snn_synth.normal_tensor(1234, T, N)
+    G = snn_synth.normal_tensor(4321, T, N)
+    fwd, gX, gvi = _run(p_bad, X.cuda(), G.cuda())
+    torch.cuda.synchronize()
+    op = oracle_params(PAPER)
+    ref = oracle.forward(op, X.double().numpy())
+    rgX, rgvi = oracle.backward(op, G.double().numpy(), ref["H"])
+    rep = compare(PAPER, ref, rgX, rgvi, fwd.spikes.cpu(), gX.cpu(), vf_gpu=fwd.v_final.cpu(),
+                  gvi_gpu=gvi.cpu())
+    assert not rep.ok and rep.failures
