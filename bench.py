@@ -1,0 +1,402 @@
+#!/usr/bin/env python
+"""Benchmark of the temporally fused LIF path (arXiv 2408.00280) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload cfg1|cfg2|cfg4] [--T 512]
+
+One "step" = one fused forward + one fused backward over one batch of synthetic input
+(every row of SURVEY 8(a) A1-A9).  Default workload: BASELINE.json configs[1] at its
+largest T (N = 2^20 neurons, T = 512, fp32 currents, u8 spikes, RECOMPUTE save mode,
+the paper's LIF constants PAPER.md:428-441).  Under torchrun each rank runs the same
+per-GPU workload on its own neuron shard (weak scaling, no data-path collective: the
+neurons are independent); the time is the max over ranks.
+
+Rank 0 prints ONE JSON line (metric / value / roofline / cpu_baseline / e2e / clocks ...).
+DESIGN.md "Measurement" documents every field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fused LIF fwd+bwd neuron-steps/sec and HBM GB/s vs peak at 1/2/4/8 B200"
+UNIT = "neuron-steps/s"
+
+# VGG-11 CIFAR LIF layer shapes (C, H, W) -- BASELINE.json configs[2], SURVEY 8(d).2
+VGG11_LAYERS = [(64, 32, 32), (128, 16, 16), (256, 8, 8), (256, 8, 8), (512, 4, 4), (512, 4, 4),
+                (512, 2, 2), (512, 2, 2)]
+# Spiking-ResNet18 LIF layers on 2x128x128 DVS frames -- BASELINE.json configs[4]
+RESNET18_DVS_LAYERS = ([(64, 64, 64)] + [(64, 32, 32)] * 4 + [(128, 16, 16)] * 4 +
+                       [(256, 8, 8)] * 4 + [(512, 4, 4)] * 4)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=["cfg1", "cfg2", "cfg4"], default="cfg1")
+    ap.add_argument("--T", type=int, default=512, help="cfg1 time steps (8/32/128/512)")
+    ap.add_argument("--save-mode", choices=["recompute", "h"], default="recompute")
+    ap.add_argument("--spike-fmt", choices=["u8", "bits", "io"], default="u8")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0,
+                    help="target CPU time of the oracle baseline sample")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- workloads
+
+def layer_list(args, world):
+    """[(name, T, N_per_rank, dtype)] processed by one step on one rank."""
+    import torch
+    if args.workload == "cfg1":
+        return [("cfg1", args.T, 1 << 20, torch.float32)]
+    if args.workload == "cfg2":
+        B, T = 128, 16
+        return [(f"vgg11_l{i}", T, B * c * h * w, torch.bfloat16)
+                for i, (c, h, w) in enumerate(VGG11_LAYERS)]
+    B, T = 32, 64   # global batch 256 = 32 per rank on 8 ranks (weak scaling)
+    return [(f"r18dvs_l{i}", T, B * c * h * w, torch.float32)
+            for i, (c, h, w) in enumerate(RESNET18_DVS_LAYERS)]
+
+
+def bytes_per_neuron_step(dtype_bytes, spike_fmt, save_mode, T):
+    """Algorithmic HBM bytes per neuron-step."""
+    spk = {"u8": 1.0, "bits": 1.0 / 8.0, "io": float(dtype_bytes)}[spike_fmt]
+    if save_mode == "recompute":
+        ck = 4.0 * math.ceil(T / 16) / T          # fp32 V checkpoint every 16 steps
+        fwd = dtype_bytes + spk + ck               # read X, write S, write ckpt
+        bwd = 3 * dtype_bytes + ck                 # read gS, read X, write gX, read ckpt
+    else:
+        fwd = dtype_bytes + spk + 4.0              # read X, write S, write H (fp32)
+        bwd = 2 * dtype_bytes + 4.0                # read gS, read H, write gX
+    return fwd, bwd
+
+
+# ----------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """Samples SM clock + throttle reasons through NVML while the timed region runs."""
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover
+            self._nv = None
+            self.error = str(e)
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self._nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._nv is not None:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        s = sorted(self.samples)
+        return {"sm_mhz": s[len(s) // 2], "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(s)}
+
+
+# ----------------------------------------------------------------------------- helpers
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic(workload_key):
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu capture
+    (profiles/ncu_traffic.json, written from `ncu --set full`), or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(workload_key)
+    except Exception:
+        return None
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+def oracle_sample(layers, seconds, spike_seed=(1234, 4321)):
+    """Time the fp64 C oracle (as it stands, 1 thread) on a bounded column sample of the
+    workload: the first layer's T, sampled neuron columns regenerated on the host."""
+    import numpy as np
+    import oracle
+    import snn_synth
+
+    name, T, N, dtype = max(layers, key=lambda l: l[1] * l[2])
+    f32 = lambda v: float(np.float32(v))   # the fp32 constants the kernels receive (R9)
+    op = oracle.OracleParams(tau=f32(1.25), v_th=f32(0.3), v_reset=0.0, alpha=4.0)
+    cols = 256
+    total_t, total_ns = 0.0, 0
+    while True:
+        idx = np.arange(cols) * max(1, N // cols)
+        X = snn_synth.normal_columns(spike_seed[0], T, N, idx, dtype=dtype).double().numpy()
+        G = snn_synth.normal_columns(spike_seed[1], T, N, idx, dtype=dtype).double().numpy()
+        t0 = time.perf_counter()
+        ref = oracle.forward(op, X)
+        oracle.backward(op, G, ref["H"])
+        dt = time.perf_counter() - t0
+        total_t += dt
+        total_ns += T * cols
+        if total_t >= seconds or cols >= N:
+            break
+        cols = min(N, int(cols * max(2.0, min(8.0, seconds / max(dt, 1e-3) / 2))))
+    return {"value": total_ns / total_t, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{name}: T={T}, up to {cols} of {N} neuron columns (stride-sampled), "
+                      f"fwd+bwd, fp64 C oracle single-threaded, {total_t:.1f} s total"}
+
+
+# ----------------------------------------------------------------------------- arms
+
+def run_reference(args):
+    """--impl reference: the oracle as it stands on the host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import torch  # noqa: F401
+    world = int(os.environ.get("WORLD_SIZE", args.gpus))
+    layers = layer_list(args, world)
+    per_step = max(1.0, 60.0 / max(1, args.steps + args.warmup))
+    for _ in range(args.warmup):
+        oracle_sample(layers, min(per_step, 2.0))
+    vals = [oracle_sample(layers, per_step) for _ in range(args.steps)]
+    v = sum(x["value"] for x in vals) / len(vals)
+    cb = dict(vals[-1]); cb["value"] = v
+    name, T, N, dtype = layers[0]
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": args.workload, "T": T, "N": N},
+            "cpu_baseline": cb,
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2408_00280_b200 as snn
+    import snn_synth
+    from paper_2408_00280_b200 import lif as L
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    params = snn.LIFParams.paper()
+    layers = layer_list(args, world)
+
+    # ---- inputs, resident in HBM before the timed region (rank's neuron shard) -----
+    bufs = []
+    for name, T, N, dtype in layers:
+        X = snn_synth.normal_tensor(1234, T, N, n_global=N * world, n_offset=N * rank,
+                                    device=dev, dtype=dtype)
+        G = snn_synth.normal_tensor(4321, T, N, n_global=N * world, n_offset=N * rank,
+                                    device=dev, dtype=dtype)
+        shape = L.make_shape(X, args.spike_fmt, args.save_mode)
+        saved = torch.empty(L.saved_bytes(params, shape) // 4, dtype=torch.float32, device=dev)
+        spikes = L.alloc_spikes(X, args.spike_fmt)
+        gX = torch.empty_like(X)
+        bufs.append(dict(name=name, T=T, N=N, X=X, G=G, saved=saved, spikes=spikes, gX=gX))
+    torch.cuda.synchronize(dev)
+
+    ev = lambda: torch.cuda.Event(enable_timing=True)
+    kern = {"fwd": [], "bwd": []}
+
+    def step(record):
+        for b in bufs:
+            if record:
+                e0, e1, e2 = ev(), ev(), ev()
+                e0.record(stream)
+            f = snn.lif_forward(b["X"], params, spike_fmt=args.spike_fmt, save_mode=args.save_mode,
+                                spikes=b["spikes"], saved=b["saved"], return_v_final=False)
+            if record:
+                e1.record(stream)
+            snn.lif_backward(b["G"], f, grad_x=b["gX"], return_grad_v_init=False)
+            if record:
+                e2.record(stream)
+                kern["fwd"].append((e0, e1)); kern["bwd"].append((e1, e2))
+
+    for _ in range(max(3, args.warmup)):
+        step(False)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(dev.index) as clk:
+        t0, t1 = ev(), ev()
+        t0.record(stream)
+        for _ in range(args.steps):
+            step(True)
+        t1.record(stream)
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    ms = t0.elapsed_time(t1)
+    if world > 1:
+        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    ns_rank = sum(b["T"] * b["N"] for b in bufs)
+    total_ns = ns_rank * world * args.steps
+    value = total_ns / (ms / 1e3)
+
+    # ---- roofline of the dominant kernel -----------------------------------------
+    fwd_ms = sum(a.elapsed_time(b) for a, b in kern["fwd"]) / args.steps
+    bwd_ms = sum(a.elapsed_time(b) for a, b in kern["bwd"]) / args.steps
+    name0, T0, N0, dt0 = bufs[0]["name"], bufs[0]["T"], bufs[0]["N"], layers[0][3]
+    esz = torch.tensor([], dtype=dt0).element_size()
+    bpf, bpb = 0.0, 0.0
+    for b in bufs:
+        f_, b_ = bytes_per_neuron_step(esz, args.spike_fmt, args.save_mode, b["T"])
+        bpf += f_ * b["T"] * b["N"]; bpb += b_ * b["T"] * b["N"]
+    dom = "bwd" if bwd_ms >= fwd_ms else "fwd"
+    dom_ms = bwd_ms if dom == "bwd" else fwd_ms
+    dom_bytes = bpb if dom == "bwd" else bpf
+    nlaunch = len(bufs)
+    peak, peak_kind = measured_peak()
+    achieved = dom_bytes / (dom_ms / 1e3) / 1e9
+    key = f"{args.workload}_T{T0}_{args.save_mode}_{args.spike_fmt}_{dom}"
+    traffic = ncu_traffic(key)
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": traffic,
+            "kernel": f"lif_{'backward_recompute' if (dom == 'bwd' and args.save_mode == 'recompute') else ('backward_saveh' if dom == 'bwd' else 'forward')}_kernel",
+            "peak_kind": peak_kind, "algorithmic_bytes_per_launch": dom_bytes / nlaunch,
+            "fwd_ms": round(fwd_ms, 4), "bwd_ms": round(bwd_ms, 4),
+            "fwd_GBps": round(bpf / (fwd_ms / 1e3) / 1e9, 1),
+            "bwd_GBps": round(bpb / (bwd_ms / 1e3) / 1e9, 1),
+            "step_GBps": round((bpf + bpb) * args.steps / (ms / 1e3) / 1e9, 1)}
+
+    # ---- e2e: same metric through the public API with pinned host buffers -------------
+    e2e = None
+    if not args.no_e2e:
+        hb = []
+        for b in bufs:
+            hb.append(dict(X=b["X"].cpu().pin_memory(), G=b["G"].cpu().pin_memory(),
+                           S=torch.empty(b["spikes"].shape, dtype=b["spikes"].dtype).pin_memory(),
+                           gX=torch.empty(b["gX"].shape, dtype=b["gX"].dtype).pin_memory()))
+        h2d = sum(h["X"].numel() * h["X"].element_size() + h["G"].numel() * h["G"].element_size() for h in hb)
+        d2h = sum(h["S"].numel() * h["S"].element_size() + h["gX"].numel() * h["gX"].element_size() for h in hb)
+
+        def e2e_step():
+            for h in hb:
+                x = h["X"].to(dev, non_blocking=True)
+                g = h["G"].to(dev, non_blocking=True)
+                f = snn.lif_forward(x, params, spike_fmt=args.spike_fmt, save_mode=args.save_mode,
+                                    return_v_final=False)
+                gx, _ = snn.lif_backward(g, f, return_grad_v_init=False)
+                h["S"].copy_(f.spikes, non_blocking=True)
+                h["gX"].copy_(gx, non_blocking=True)
+
+        e2e_step(); torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        a, b_ = ev(), ev()
+        a.record(stream)
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        b_.record(stream)
+        torch.cuda.synchronize(dev)
+        ems = a.elapsed_time(b_)
+        if world > 1:
+            tt = torch.tensor([ems], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ems = float(tt.item())
+        e2e = {"value": ns_rank * world * args.e2e_steps / (ems / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
+               "ms_per_step": round(ems / args.e2e_steps, 3)}
+        del hb
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = oracle_sample(layers, args.cpu_seconds)
+
+    if rank == 0:
+        cfg = {"workload": {"cfg1": f"BASELINE configs[1]: single LIF layer N=2^20, T={args.T}",
+                            "cfg2": "BASELINE configs[2]: VGG-11 CIFAR LIF layers, B=128, T=16, bf16",
+                            "cfg4": "BASELINE configs[4]: Spiking-ResNet18 DVS LIF layers, B=256 global, T=64"}[args.workload],
+               "N_per_gpu": sum(b["N"] for b in bufs), "T": sorted({b["T"] for b in bufs}),
+               "layers": len(bufs), "params": "paper (tau=1.25 k=0.2, V_th=0.3, V_rest=0, hard, sigmoid a=4)",
+               "spike_fmt": args.spike_fmt, "save_mode": args.save_mode,
+               "l2": "no flush: per-step inputs (X, gS) exceed the 126 MB L2" if ns_rank * esz > 256e6
+                     else "inputs smaller than L2 (cfg2/4 small layers): L2-resident share reported",
+               "parallelism": f"neuron-shard x{world} (weak)"}
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms / args.steps,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "bf16" if dt0 == torch.bfloat16 else "f32", "data": "synthetic",
+                "config": cfg, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": 2 * nlaunch * args.steps, "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

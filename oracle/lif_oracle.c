@@ -150,6 +150,8 @@ void lif_oracle_forward(const lif_oracle_params* p, int64_t T, int64_t N,
  *   grad_v_final[N] or NULL -> 0: dL/dV[T-1] from a later time segment
  *   gX          [T, N]  dL/dX[t]
  *   grad_v_init [N] or NULL: dL/dV[-1] (carry-out to an earlier segment)
+ *   delta_out / dvdh_out [T, N] or NULL: the per-step delta and dV/dH (exposed so the
+ *                       parity comparator can bound rounding error; no other use)
  *
  * Derivation: with k = 1 - 1/tau and s = dH/dX = (decay_input ? 1/tau : 1),
  *   dH[t+1]/dV[t] = k in both charge forms;
@@ -164,7 +166,9 @@ void lif_oracle_backward(const lif_oracle_params* p, int64_t T, int64_t N,
                          const double* gS, const double* H,
                          const double* grad_v_final,
                          double* gX, double* grad_v_init,
-                         double* gV_work /* [N] scratch owned by the caller */)
+                         double* gV_work /* [N] scratch owned by the caller */,
+                         double* delta_out /* [T, N] or NULL: delta[t, n] */,
+                         double* dvdh_out  /* [T, N] or NULL: dV/dH[t, n] */)
 {
     const double k = 1.0 - 1.0 / p->tau;
     const double s = p->decay_input ? 1.0 / p->tau : 1.0;
@@ -183,6 +187,8 @@ void lif_oracle_backward(const lif_oracle_params* p, int64_t T, int64_t N,
             else
                 dVdH = (1.0 - S) + (p->detach_reset ? 0.0 : (p->v_reset - h) * delta);
             double gH = gS[t * N + n] * delta + gV[n] * dVdH;
+            if (delta_out) delta_out[t * N + n] = delta;
+            if (dvdh_out) dvdh_out[t * N + n] = dVdH;
             gX[t * N + n] = s * gH;
             gV[n] = k * gH;
         }

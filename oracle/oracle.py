@@ -84,7 +84,7 @@ def _load():
                                            dp, dp, dp, dp, dp]
         lib.lif_oracle_forward.restype = None
         lib.lif_oracle_backward.argtypes = [P, ctypes.c_int64, ctypes.c_int64, dp, dp, dp,
-                                            dp, dp, dp]
+                                            dp, dp, dp, dp, dp]
         lib.lif_oracle_backward.restype = None
         _lib = lib
     return _lib
@@ -128,8 +128,9 @@ def forward(p: OracleParams, x, v_init=None):
     return {"S": S, "H": H, "V": V, "v_final": vf}
 
 
-def backward(p: OracleParams, gS, H, grad_v_final=None):
-    """Backward over t = T-1..0.  Returns (gX [T, N], grad_v_init [N])."""
+def backward(p: OracleParams, gS, H, grad_v_final=None, return_terms=False):
+    """Backward over t = T-1..0.  Returns (gX [T, N], grad_v_init [N]) and, with
+    return_terms, also {"delta": [T, N], "dVdH": [T, N]} (for error bounds)."""
     gS = _f64(gS); H = _f64(H)
     if gS.ndim == 1:
         gS = gS[:, None]; H = H[:, None]
@@ -137,7 +138,11 @@ def backward(p: OracleParams, gS, H, grad_v_final=None):
     assert H.shape == (T, N)
     gvf = None if grad_v_final is None else _f64(grad_v_final).reshape(N)
     gX = np.empty((T, N)); gvi = np.empty(N); work = np.empty(N)
+    d = np.empty((T, N)) if return_terms else None
+    dv = np.empty((T, N)) if return_terms else None
     c = p._c()
     _load().lif_oracle_backward(ctypes.byref(c), T, N, _dp(gS), _dp(H), _dp(gvf), _dp(gX),
-                                _dp(gvi), _dp(work))
+                                _dp(gvi), _dp(work), _dp(d), _dp(dv))
+    if return_terms:
+        return gX, gvi, {"delta": d, "dVdH": dv}
     return gX, gvi

@@ -151,6 +151,10 @@ def lif_backward(grad_spikes: torch.Tensor, fwd: LIFForward, *,
                  grad_x: Optional[torch.Tensor] = None):
     """Eq. 3 over t = T-1..0 in one kernel launch (fusedBackwardLIF).
     Returns (grad_x [T, N] in x's dtype, grad_v_init [N] fp32 or None)."""
+    if not grad_spikes.is_cuda:
+        raise ValueError("grad_spikes must be a CUDA tensor (no CPU path exists)")
+    if grad_spikes.dim() == 2 and grad_spikes.size(1) > 1 and grad_spikes.stride(1) != 1:
+        grad_spikes = grad_spikes.contiguous()   # e.g. the expanded ones of y.sum().backward()
     _check_2d("grad_spikes", grad_spikes)
     x = fwd.x
     T, N = x.shape

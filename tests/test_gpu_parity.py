@@ -14,7 +14,7 @@ if not torch.cuda.is_available():
 import paper_2408_00280_b200 as snn  # noqa: E402  (raises if libsnn_lif.so is missing)
 import oracle  # noqa: E402
 import snn_synth  # noqa: E402
-from parity import compare, oracle_params, run_gpu_and_oracle  # noqa: E402
+from parity import compare, oracle_params, oracle_run, run_gpu_and_oracle  # noqa: E402
 
 LIFParams = snn.LIFParams
 PAPER = LIFParams.paper()
@@ -180,10 +180,8 @@ def test_cfg1_full_size_sampled_columns():
     ci = torch.as_tensor(cols, device="cuda")
     Xh = snn_synth.normal_columns(1234, T, N, cols)
     Gh = snn_synth.normal_columns(4321, T, N, cols)
-    op = oracle_params(PAPER)
-    ref = oracle.forward(op, Xh.double().numpy())
-    rgX, rgvi = oracle.backward(op, Gh.double().numpy(), ref["H"])
-    rep = compare(PAPER, ref, rgX, rgvi, fwd.spikes[:, ci].cpu(), gX[:, ci].cpu(),
+    ref = oracle_run(PAPER, Xh, Gh)
+    rep = compare(PAPER, ref, ref["gX"], ref["gvi"], fwd.spikes[:, ci].cpu(), gX[:, ci].cpu(),
                   vf_gpu=fwd.v_final[ci].cpu(), gvi_gpu=gvi[ci].cpu(), col_ids=cols)
     assert_ok(rep)
 
@@ -199,9 +197,7 @@ def test_fault_injection_perturbed_k_fails_parity():
     G = snn_synth.normal_tensor(4321, T, N)
     fwd, gX, gvi = _run(p_bad, X.cuda(), G.cuda())
     torch.cuda.synchronize()
-    op = oracle_params(PAPER)
-    ref = oracle.forward(op, X.double().numpy())
-    rgX, rgvi = oracle.backward(op, G.double().numpy(), ref["H"])
-    rep = compare(PAPER, ref, rgX, rgvi, fwd.spikes.cpu(), gX.cpu(), vf_gpu=fwd.v_final.cpu(),
+    ref = oracle_run(PAPER, X, G)
+    rep = compare(PAPER, ref, ref["gX"], ref["gvi"], fwd.spikes.cpu(), gX.cpu(), vf_gpu=fwd.v_final.cpu(),
                   gvi_gpu=gvi.cpu())
     assert not rep.ok and rep.failures
