@@ -1,0 +1,45 @@
+// fwd_generic.cu -- launcher of the generic forward kernels (lif_kernels.cuh): one thread
+// per VEC-neuron group with a register prefetch ring along T.  Used when the TMA path's
+// alignment requirements do not hold.
+#include "internal.h"
+
+namespace snn_host {
+
+namespace {
+constexpr int kFwdPF = 8;  // rows in flight per thread
+
+template <typename IO, int VEC>
+snn_status go(const snn_lif_shape* s, const snn::FwdArgs& a, bool soft, cudaStream_t st) {
+    const int64_t groups = (s->N + VEC - 1) / VEC;
+    const dim3 grid((unsigned)((groups + snn::kBlock - 1) / snn::kBlock));
+    auto launch = [&](auto sfmt, auto save, auto sft) {
+        snn::lif_forward_kernel<IO, VEC, decltype(sfmt)::value, decltype(save)::value,
+                                (bool)decltype(sft)::value, kFwdPF><<<grid, snn::kBlock, 0, st>>>(a);
+    };
+    auto by_soft = [&](auto sfmt, auto save) {
+        if (soft) launch(sfmt, save, IC<1>{}); else launch(sfmt, save, IC<0>{});
+    };
+    auto by_save = [&](auto sfmt) {
+        switch (s->save_mode) {
+            case SNN_SAVE_H: by_soft(sfmt, IC<snn::SAVE_H>{}); break;
+            case SNN_SAVE_RECOMPUTE: by_soft(sfmt, IC<snn::SAVE_RECOMPUTE>{}); break;
+            default: by_soft(sfmt, IC<snn::SAVE_NONE>{}); break;
+        }
+    };
+    switch (s->spike_fmt) {
+        case SNN_SPK_U8: by_save(IC<snn::SPK_U8>{}); break;
+        case SNN_SPK_BITS: by_save(IC<snn::SPK_BITS>{}); break;
+        default: by_save(IC<snn::SPK_IO>{}); break;
+    }
+    return launch_status("lif_forward_kernel");
+}
+}  // namespace
+
+snn_status launch_forward_generic(const snn_lif_shape* s, const snn::FwdArgs& a, bool soft, bool vec,
+                                  cudaStream_t st) {
+    if (s->io_dtype == SNN_BF16)
+        return vec ? go<__nv_bfloat16, 8>(s, a, soft, st) : go<__nv_bfloat16, 1>(s, a, soft, st);
+    return vec ? go<float, 4>(s, a, soft, st) : go<float, 1>(s, a, soft, st);
+}
+
+}  // namespace snn_host

@@ -1,0 +1,72 @@
+// internal.h -- host-side glue shared by the translation units of libsnn_lif.so
+// (not part of the public ABI; include/snn_lif.h is).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <type_traits>
+
+#include "../../include/snn_lif.h"
+#include "lif_kernels.cuh"
+
+namespace snn_host {
+
+// Thread-local error detail (snn_last_error_message) + status.
+snn_status fail(snn_status st, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+snn_status launch_status(const char* what);
+
+int num_sms();
+
+// 2-D tensor map over a row-major [outer, inner] tensor (row stride ld elements);
+// box = box_inner x box_outer elements; out-of-range elements read as zero.
+bool encode_2d(CUtensorMap* m, const void* base, size_t esz, int64_t inner, int64_t outer,
+               int64_t ld, int box_inner, int box_outer);
+bool tma_available();
+
+template <int V> using IC = std::integral_constant<int, V>;
+
+// Opt the kernel into its dynamic shared memory and return resident CTAs per SM.
+template <typename Kernel>
+int prepare(Kernel k, int threads, int smem) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, threads, smem) != cudaSuccess || occ < 1)
+        occ = 1;
+    return occ;
+}
+
+// Resident CTAs per SM of kernel `k` (cudaFuncSetAttribute + occupancy query), cached per
+// (device, kernel) -- the attribute must be set once per kernel, not per signature.
+int cached_occupancy(const void* k, int threads, int smem, int (*prep)(const void*, int, int));
+
+// Persistent launch: grid = min(tiles, SMs x resident CTAs); the kernel walks tiles
+// round-robin.
+template <typename Kernel, typename... Args>
+snn_status launch_persistent(Kernel k, int threads, int smem, int64_t ntiles, cudaStream_t st,
+                             const char* what, const Args&... args) {
+    const int occ = cached_occupancy(
+        reinterpret_cast<const void*>(k), threads, smem, [](const void* kk, int t, int sm) {
+            return prepare(reinterpret_cast<Kernel>(const_cast<void*>(kk)), t, sm);
+        });
+    const int64_t grid = std::min<int64_t>(ntiles, (int64_t)num_sms() * occ);
+    k<<<(unsigned)grid, threads, smem, st>>>(args..., ntiles);
+    return launch_status(what);
+}
+
+// ---- launchers (one translation unit each, compiled in parallel) -------------------
+// Generic path: any alignment; `vec` selects the 128-bit vector variant.
+snn_status launch_forward_generic(const snn_lif_shape* s, const snn::FwdArgs& a, bool soft, bool vec,
+                                  cudaStream_t st);
+snn_status launch_backward_generic(const snn_lif_shape* s, const snn::BwdArgs& a, int mode, bool vec,
+                                   cudaStream_t st);
+// TMA path: 16-byte-aligned pointers and rows, N % tma_vec_*(io) == 0.
+snn_status launch_forward_tma_f32(const snn_lif_shape* s, const snn::FwdArgs& a, bool soft, cudaStream_t st);
+snn_status launch_forward_tma_bf16(const snn_lif_shape* s, const snn::FwdArgs& a, bool soft, cudaStream_t st);
+snn_status launch_backward_tma_f32(const snn_lif_shape* s, const snn::BwdArgs& a, int mode, cudaStream_t st);
+snn_status launch_backward_tma_bf16(const snn_lif_shape* s, const snn::BwdArgs& a, int mode, cudaStream_t st);
+int tma_vec_forward(int io_dtype);
+int tma_vec_backward(int io_dtype);
+
+}  // namespace snn_host

@@ -1,0 +1,96 @@
+// launch_tma.cuh -- host launchers of the persistent TMA kernels (lif_tma.cuh), templated
+// on the io dtype; instantiated by fwd_tma_{f32,bf16}.cu and bwd_tma_{f32,bf16}.cu.
+#pragma once
+
+#include "internal.h"
+#include "lif_tma.cuh"
+
+namespace snn_host {
+
+// Tile configurations: VEC neurons per consumer lane x NCONS
+// consumer threads = W-neuron tile; R rows per stage; S stages in the smem ring.
+template <typename IO> struct TmaCfg;
+template <> struct TmaCfg<float> {
+    static constexpr int FV = 4, FN = 128, FR = 8, FS = 6;   // forward: 16 KB stages, 2 CTAs/SM
+    static constexpr int RV = 1, RN = 512, RS = 3;           // backward RECOMPUTE: 66 KB chunks
+    static constexpr int HV = 1, HN = 512, HR = 8, HS = 6;   // backward SAVE_H: 32 KB stages
+};
+template <> struct TmaCfg<__nv_bfloat16> {
+    static constexpr int FV = 8, FN = 128, FR = 8, FS = 6;
+    static constexpr int RV = 2, RN = 256, RS = 3;           // 34 KB chunks, 2 CTAs/SM
+    static constexpr int HV = 2, HN = 512, HR = 8, HS = 4;
+};
+
+template <typename IO>
+snn_status launch_forward_tma(const snn_lif_shape* s, const snn::FwdArgs& a, bool soft,
+                              cudaStream_t st) {
+    using C = TmaCfg<IO>;
+    using Cfg = snn::FwdTma<IO, C::FV, C::FN, C::FR, C::FS>;
+    CUtensorMap tmx;
+    if (!encode_2d(&tmx, a.x, sizeof(IO), s->N, s->T, s->ld, Cfg::BW, C::FR))
+        return fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled failed for x");
+    const int64_t ntiles = (s->N + Cfg::W - 1) / Cfg::W;
+    auto go = [&](auto sfmt, auto save, auto sft) {
+        auto k = snn::lif_forward_tma_kernel<IO, C::FV, decltype(sfmt)::value, decltype(save)::value,
+                                             (bool)decltype(sft)::value, C::FN, C::FR, C::FS>;
+        return launch_persistent(k, Cfg::THREADS, Cfg::SMEM, ntiles, st, "lif_forward_tma_kernel",
+                                 tmx, a);
+    };
+    auto by_soft = [&](auto sfmt, auto save) {
+        return soft ? go(sfmt, save, IC<1>{}) : go(sfmt, save, IC<0>{});
+    };
+    auto by_save = [&](auto sfmt) {
+        switch (s->save_mode) {
+            case SNN_SAVE_H: return by_soft(sfmt, IC<snn::SAVE_H>{});
+            case SNN_SAVE_RECOMPUTE: return by_soft(sfmt, IC<snn::SAVE_RECOMPUTE>{});
+            default: return by_soft(sfmt, IC<snn::SAVE_NONE>{});
+        }
+    };
+    switch (s->spike_fmt) {
+        case SNN_SPK_U8: return by_save(IC<snn::SPK_U8>{});
+        case SNN_SPK_BITS: return by_save(IC<snn::SPK_BITS>{});
+        default: return by_save(IC<snn::SPK_IO>{});
+    }
+}
+
+template <typename IO, int MODE>
+snn_status launch_backward_tma_mode(const snn_lif_shape* s, const snn::BwdArgs& a, cudaStream_t st) {
+    using C = TmaCfg<IO>;
+    if (s->save_mode == SNN_SAVE_H) {
+        using Cfg = snn::BwdHTma<IO, C::HV, C::HN, C::HR, C::HS>;
+        CUtensorMap tmh, tmg;
+        if (!encode_2d(&tmh, a.saved, 4, s->N, s->T, a.ldh, Cfg::BW, C::HR) ||
+            !encode_2d(&tmg, a.gS, sizeof(IO), s->N, s->T, s->ld, Cfg::BW, C::HR))
+            return fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled failed (SAVE_H backward)");
+        auto k = snn::lif_backward_saveh_tma_kernel<IO, C::HV, MODE, C::HN, C::HR, C::HS>;
+        return launch_persistent(k, Cfg::THREADS, Cfg::SMEM, (s->N + Cfg::W - 1) / Cfg::W, st,
+                                 "lif_backward_saveh_tma_kernel", tmh, tmg, a);
+    }
+    using Cfg = snn::BwdRecTma<IO, C::RV, C::RN, C::RS>;
+    const int64_t nch = (s->T + snn::kCkpt - 1) / snn::kCkpt;
+    CUtensorMap tmx, tmg, tmck;
+    if (!encode_2d(&tmx, a.x, sizeof(IO), s->N, s->T, s->ld, Cfg::BW, snn::kCkpt) ||
+        !encode_2d(&tmg, a.gS, sizeof(IO), s->N, s->T, s->ld, Cfg::BW, snn::kCkpt) ||
+        !encode_2d(&tmck, a.saved, 4, s->N, nch, a.ldh, Cfg::BW, 1))
+        return fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled failed (RECOMPUTE backward)");
+    auto k = snn::lif_backward_recompute_tma_kernel<IO, C::RV, MODE, C::RN, C::RS>;
+    return launch_persistent(k, Cfg::THREADS, Cfg::SMEM, (s->N + Cfg::W - 1) / Cfg::W, st,
+                             "lif_backward_recompute_tma_kernel", tmx, tmg, tmck, a);
+}
+
+template <typename IO>
+snn_status launch_backward_tma(const snn_lif_shape* s, const snn::BwdArgs& a, int mode,
+                               cudaStream_t st) {
+    switch (mode & 7) {
+        case 0: return launch_backward_tma_mode<IO, 0>(s, a, st);
+        case 1: return launch_backward_tma_mode<IO, 1>(s, a, st);
+        case 2: return launch_backward_tma_mode<IO, 2>(s, a, st);
+        case 3: return launch_backward_tma_mode<IO, 3>(s, a, st);
+        case 4: return launch_backward_tma_mode<IO, 4>(s, a, st);
+        case 5: return launch_backward_tma_mode<IO, 5>(s, a, st);
+        case 6: return launch_backward_tma_mode<IO, 6>(s, a, st);
+        default: return launch_backward_tma_mode<IO, 7>(s, a, st);
+    }
+}
+
+}  // namespace snn_host

@@ -1,7 +1,7 @@
-// lif_common.cuh -- device-side building blocks of the fused LIF kernels (sm_100a).
-//
-// Shared by lif_forward.cuh and lif_backward.cuh only.  Nothing here is shared with
-// oracle/ (the oracle is an independent fp64 C program).
+// lif_common.cuh -- device-side building blocks of the fused LIF kernels (sm_100a):
+// the per-step LIF arithmetic (one definition used by every kernel, so all paths round
+// identically) and vector I/O helpers.  Nothing here is shared with oracle/ (the oracle is
+// an independent fp64 C program).
 #pragma once
 
 #include <cuda_bf16.h>
@@ -11,67 +11,99 @@
 namespace snn {
 
 // ------------------------------------------------------------------------------------
-// Per-launch constants (computed once on the host in fp32 -- SURVEY R9).
+// Per-launch constants, computed once on the host in fp32.
 struct LifConsts {
-    float k;        // 1 - 1/tau
-    float s;        // dH/dX: 1/tau if decay_input else 1
-    float c0;       // V_reset / tau: the constant of the charge
-    float v_th;     // V_th
-    float v_reset;  // V_reset
-    float alpha;    // surrogate sharpness
-    float atan_c;   // pi/2 * alpha (arctan surrogate)
-    int   soft;     // soft reset
-    int   detach;   // detach_reset
+    float k;          // 1 - 1/tau
+    float s;          // dH/dX: 1/tau if decay_input else 1
+    float c0;         // V_reset / tau: the constant of the charge
+    float v_th;       // V_th
+    float v_reset;    // V_reset
+    float alpha;      // surrogate sharpness
+    float ex2_scale;  // -alpha * log2(e): e^{-alpha|u|} = 2^{|u| ex2_scale}
+    float atan_c;     // pi/2 * alpha (arctan surrogate)
+    float half_alpha; // alpha / 2   (arctan surrogate numerator)
 };
 
-// ------------------------------------------------------------------------------------
-// The per-step LIF arithmetic.  Written with explicit _rn intrinsics so the forward
-// kernel and the RECOMPUTE backward (which re-runs the charge) execute the identical
-// rounding sequence -> bitwise-identical H, S, V.
+// Keep the constants in registers: without this ptxas re-reads them from the constant
+// bank (LDC) inside the unrolled time loop, several instructions per neuron-step.
+__device__ __forceinline__ void pin(LifConsts& c) {
+    asm volatile("" : "+f"(c.k), "+f"(c.s), "+f"(c.c0), "+f"(c.v_th), "+f"(c.v_reset));
+    asm volatile("" : "+f"(c.alpha), "+f"(c.ex2_scale), "+f"(c.atan_c), "+f"(c.half_alpha));
+}
 
-// Charge (Eq. 1 / north-star form): H = k V + (s X + c0).
+// Compile-time variant of the backward: bit 0 surrogate (0 sigmoid, 1 arctan), bit 1 soft
+// reset, bit 2 detach_reset.  Branch-free inner loops.
+template <int MODE>
+struct Mode {
+    static constexpr int SURR = MODE & 1;
+    static constexpr bool SOFT = (MODE & 2) != 0;
+    static constexpr bool DETACH = (MODE & 4) != 0;
+};
+
+__device__ __forceinline__ float ex2_approx(float x) {  // MUFU.EX2, ftz
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rcp_approx(float x) {  // MUFU.RCP, ftz
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// ------------------------------------------------------------------------------------
+// The per-step LIF arithmetic (explicit _rn intrinsics: no compiler contraction choices,
+// so the forward kernel and the RECOMPUTE backward, which re-runs the charge, produce
+// bitwise-identical H, S, V -- DESIGN.md "Determinism").
+
+// Charge (Eq. 1 / north-star form, SURVEY 0.1): H = k V + (s X + c0).
 __device__ __forceinline__ float lif_charge(const LifConsts& c, float V, float X) {
     return __fmaf_rn(c.k, V, __fmaf_rn(c.s, X, c.c0));
 }
-// Fire (Eq. 2): S = [H - V_th >= 0], evaluated as H >= V_th.  NaN -> 0.
+// Fire (Eq. 2): S = [H - V_th >= 0], evaluated as H >= V_th.
+// NaN H -> no spike.
 __device__ __forceinline__ bool lif_fire(const LifConsts& c, float H) { return H >= c.v_th; }
-// Reset: hard V = S ? V_reset : H (Eq. 1's (1-y), V_rest y);  soft V = H - V_th S.
+// Reset: hard V = S ? V_reset : H (Eq. 1's (1 - y) and V_rest y terms);
+// soft V = H - V_th S (BASELINE.json north_star).
+template <bool SOFT>
 __device__ __forceinline__ float lif_reset(const LifConsts& c, float H, bool S) {
-    return S ? (c.soft ? __fsub_rn(H, c.v_th) : c.v_reset) : H;
+    if constexpr (SOFT) return S ? __fsub_rn(H, c.v_th) : H;
+    else return S ? c.v_reset : H;
 }
 
 // Surrogate derivative delta(u), u = H - V_th.
+// Sigmoid in the |u| form: e = 2^{|u| ex2_scale} =
+// e^{-alpha|u|} in [0, 1], so (1+e)^2 is in [1, 4] and the MUFU approximations are safe
+// (ex2.approx / rcp.approx, ~2 ulp; e flushes to 0 only where delta < 1e-38).
+// Arctan: (alpha/2) / (1 + (pi/2 alpha u)^2), denominator >= 1.
+// Relative error ~1e-6, inside the parity bound (tests/parity.py).
 template <int SURR>
-__device__ __forceinline__ float lif_surrogate(const LifConsts& c, float u);
-
-// Sigmoid, in the |u| form: e = exp(-alpha|u|) in (0, 1].
-template <>
-__device__ __forceinline__ float lif_surrogate<0>(const LifConsts& c, float u) {
-    const float e = expf(-c.alpha * fabsf(u));
-    const float q = __fadd_rn(1.0f, e);
-    return __fdiv_rn(__fmul_rn(c.alpha, e), __fmul_rn(q, q));
-}
-// Arctan: (alpha/2) / (1 + (pi/2 alpha u)^2).
-template <>
-__device__ __forceinline__ float lif_surrogate<1>(const LifConsts& c, float u) {
-    const float z = __fmul_rn(c.atan_c, u);
-    return __fdiv_rn(__fmul_rn(0.5f, c.alpha), __fmaf_rn(z, z, 1.0f));
-}
-
-// One reverse step of Eq. 3 (SURVEY 8(c).2):
-//   gH = gS delta + gV dV/dH,  dV/dH = hard: (1-S) + (V_reset - H) delta ; soft: 1 - V_th delta
-// returns gH; caller writes gX = s gH and carries gV = k gH.
-template <int SURR>
-__device__ __forceinline__ float lif_grad_step(const LifConsts& c, float H, float gS, float gV) {
-    const float u = __fsub_rn(H, c.v_th);
-    const float d = lif_surrogate<SURR>(c, u);
-    const bool S = lif_fire(c, H);
-    float dVdH;
-    if (c.soft) {
-        dVdH = c.detach ? 1.0f : __fmaf_rn(-c.v_th, d, 1.0f);
+__device__ __forceinline__ float lif_surrogate(const LifConsts& c, float u) {
+    if constexpr (SURR == 0) {
+        const float e = ex2_approx(__fmul_rn(fabsf(u), c.ex2_scale));
+        const float q = __fadd_rn(1.0f, e);
+        return __fmul_rn(__fmul_rn(c.alpha, e), rcp_approx(__fmul_rn(q, q)));
     } else {
-        const float base = S ? 0.0f : 1.0f;
-        dVdH = c.detach ? base : __fmaf_rn(__fsub_rn(c.v_reset, H), d, base);
+        const float z = __fmul_rn(c.atan_c, u);
+        return __fmul_rn(c.half_alpha, rcp_approx(__fmaf_rn(z, z, 1.0f)));
+    }
+}
+
+// One reverse step of Eq. 3 (PAPER.md:184-189; SURVEY 8(c).2):
+//   gH = gS delta + gV dV/dH,
+//   dV/dH = hard: (1 - S) + (V_reset - H) delta ; soft: 1 - V_th delta (delta term dropped
+//   when detach_reset).  Returns gH; the caller writes gX = s gH, gV <- k gH.
+template <int MODE>
+__device__ __forceinline__ float lif_grad_step(const LifConsts& c, float H, float gS, float gV) {
+    using M = Mode<MODE>;
+    const float u = __fsub_rn(H, c.v_th);
+    const float d = lif_surrogate<M::SURR>(c, u);
+    float dVdH;
+    if constexpr (M::SOFT) {
+        dVdH = M::DETACH ? 1.0f : __fmaf_rn(-c.v_th, d, 1.0f);
+    } else {
+        const float base = lif_fire(c, H) ? 0.0f : 1.0f;
+        dVdH = M::DETACH ? base : __fmaf_rn(__fsub_rn(c.v_reset, H), d, base);
     }
     return __fmaf_rn(gS, d, __fmul_rn(gV, dVdH));
 }
@@ -92,8 +124,7 @@ template <> __device__ __forceinline__ __nv_bfloat16 from_f32<__nv_bfloat16>(flo
     return __float2bfloat16_rn(v);
 }
 
-// Streaming loads: read once, never re-read by this kernel -> evict-first in L2 (.cs)
-// and no L1 allocation.
+// Streaming loads: read once, never re-read by this kernel -> evict-first in L2 (.cs).
 template <typename T, int VEC>
 __device__ __forceinline__ Pack<T, VEC> ld_stream(const T* p) {
     Pack<T, VEC> r;
@@ -119,6 +150,7 @@ __device__ __forceinline__ Pack<T, VEC> ld_stream(const T* p) {
     return r;
 }
 
+// Streaming stores (.cs: evict-first; the outputs are consumed by a later kernel).
 template <typename T, int VEC>
 __device__ __forceinline__ void st_stream(T* p, const Pack<T, VEC>& r) {
     if constexpr (sizeof(Pack<T, VEC>) == 32) {

@@ -1,12 +1,10 @@
-// lif_kernels.cuh -- the temporally fused LIF forward / backward kernels (sm_100a).
+// lif_kernels.cuh -- per-step helpers shared by every fused LIF kernel, and the GENERIC
+// kernels (one thread per VEC-neuron group, register prefetch along T) used when the TMA
+// path's alignment requirements do not hold (odd ld, unaligned views, tiny N).
 //
-// Temporal fusion: one thread owns VEC consecutive neurons for the
-// whole time axis; the membrane potential V (forward) or the carried gradient dL/dV
-// (backward) lives in registers across the T loop and each [T, N] tensor is streamed
-// exactly once, row by row, with 128-bit coalesced loads (a warp reads 32 x 16 B = 512 B
-// of one time row per instruction).  Memory-level parallelism comes from a PF-deep
-// register prefetch ring along T (loads do not depend on the recurrence, so rows t+1 ..
-// t+PF are in flight while row t is consumed).  No tensor cores: the op is elementwise-
+// Temporal fusion: a thread owns its neurons for the whole time axis;
+// V (forward) or the carried dL/dV (backward) lives in registers across the T loop and
+// each [T, N] tensor is streamed exactly once.  No tensor cores: the op is elementwise-
 // recurrent and HBM-bound.
 #pragma once
 
@@ -15,7 +13,7 @@
 namespace snn {
 
 constexpr int kCkpt = 16;           // SNN_LIF_CKPT_INTERVAL
-constexpr int kBlock = 256;         // threads per CTA
+constexpr int kBlock = 256;         // threads per CTA (generic kernels)
 constexpr unsigned kFull = 0xffffffffu;
 
 enum { SPK_U8 = 0, SPK_BITS = 1, SPK_IO = 2 };
@@ -42,31 +40,99 @@ struct BwdArgs {
     LifConsts c;
 };
 
+// ------------------------------------------------------------------------------------
+// Forward step helpers.
+
+// Eq. 1-2 + reset for this thread's VEC neurons: updates V, returns H in `hp` and the
+// spike bits (bit i = neuron i of the group).
+template <bool SOFT, typename IO, int VEC>
+__device__ __forceinline__ unsigned fwd_compute(const LifConsts& c, float (&V)[VEC],
+                                                const Pack<IO, VEC>& xv, Pack<float, VEC>& hp) {
+    unsigned bits = 0;
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) {
+        const float H = lif_charge(c, V[i], to_f32(xv.v[i]));
+        const bool S = lif_fire(c, H);
+        V[i] = lif_reset<SOFT>(c, H, S);
+        hp.v[i] = H;
+        bits |= (unsigned)S << i;
+    }
+    return bits;
+}
+
 // Pack VEC spike bits of this lane into the warp's uint32 words and store them
-// (SNN_SPK_BITS).  Lanes [w*L, (w+1)*L), L = 32/VEC, share word w of the warp.
+// (SNN_SPK_BITS).  Lanes [w*L, (w+1)*L), L = 32/VEC, share word w of the warp; the warp's
+// first neuron must be a multiple of 32 (group index g = warp-aligned).
 template <int VEC>
 __device__ __forceinline__ void store_spike_bits(uint32_t* row, int64_t g, unsigned bits,
                                                  int64_t nwords) {
+    constexpr int L = 32 / VEC;
     const int lane = threadIdx.x & 31;
     uint32_t w;
     if constexpr (VEC == 1) {
         w = __ballot_sync(kFull, bits);
     } else {
-        constexpr int L = 32 / VEC;
         w = bits << ((lane % L) * VEC);
 #pragma unroll
         for (int o = 1; o < L; o <<= 1) w |= __shfl_xor_sync(kFull, w, o);
     }
-    constexpr int L = 32 / VEC;
     if (lane % L == 0) {
         const int64_t word = ((g - lane) * VEC) / 32 + lane / L;
         if (word < nwords) __stcs(row + word, w);
     }
 }
 
+// Store one time row's spikes.  `row` = spikes + t*ld (U8/IO) or words + t*nwords (BITS).
+// Every lane of the warp must call this (BITS uses warp shuffles).
+template <typename IO, int VEC, int SFMT>
+__device__ __forceinline__ void store_spikes(void* row, int64_t g, int64_t n0, unsigned bits,
+                                             int nvalid, int64_t nwords) {
+    bits &= (nvalid >= VEC) ? ((VEC == 32) ? kFull : ((1u << VEC) - 1u)) : ((1u << nvalid) - 1u);
+    if constexpr (SFMT == SPK_U8) {
+        if (nvalid > 0) {
+            Pack<uint8_t, VEC> sp;
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) sp.v[i] = (uint8_t)((bits >> i) & 1u);
+            st_group<uint8_t, VEC>(reinterpret_cast<uint8_t*>(row) + n0, sp, nvalid);
+        }
+    } else if constexpr (SFMT == SPK_IO) {
+        if (nvalid > 0) {
+            Pack<IO, VEC> sp;
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) sp.v[i] = from_f32<IO>(((bits >> i) & 1u) ? 1.0f : 0.0f);
+            st_group<IO, VEC>(reinterpret_cast<IO*>(row) + n0, sp, nvalid);
+        }
+    } else {
+        store_spike_bits<VEC>(reinterpret_cast<uint32_t*>(row), g, bits, nwords);
+    }
+}
+
+// Byte stride between consecutive spike rows.
+template <typename IO, int SFMT>
+__device__ __forceinline__ int64_t spike_row_bytes(const FwdArgs& a) {
+    if constexpr (SFMT == SPK_U8) return a.ld;
+    else if constexpr (SFMT == SPK_IO) return a.ld * (int64_t)sizeof(IO);
+    else return a.nwords * 4;
+}
+
+// One reverse step of Eq. 3 for this thread's VEC neurons: returns gX[t] (io dtype) and
+// carries gV <- k gH.
+template <typename IO, int VEC, int MODE>
+__device__ __forceinline__ Pack<IO, VEC> bwd_step(const LifConsts& c, float (&gV)[VEC],
+                                                  const float (&h)[VEC], const Pack<IO, VEC>& gs) {
+    Pack<IO, VEC> out;
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) {
+        const float gH = lif_grad_step<MODE>(c, h[i], to_f32(gs.v[i]), gV[i]);
+        out.v[i] = from_f32<IO>(__fmul_rn(c.s, gH));
+        gV[i] = __fmul_rn(c.k, gH);
+    }
+    return out;
+}
+
 // ------------------------------------------------------------------------------------
-// Forward: Eq. 1-2 over t = 0..T-1.
-template <typename IO, int VEC, int SFMT, int SAVE, int PF>
+// Generic forward: PF-deep register prefetch ring along T.
+template <typename IO, int VEC, int SFMT, int SAVE, bool SOFT, int PF>
 __global__ void __launch_bounds__(kBlock)
 lif_forward_kernel(const FwdArgs a) {
     const int64_t g = (int64_t)blockIdx.x * kBlock + threadIdx.x;
@@ -74,7 +140,8 @@ lif_forward_kernel(const FwdArgs a) {
     const int nvalid = (int)max((int64_t)0, min((int64_t)VEC, a.N - n0));
     // Lanes past N stay alive (their warp's shuffles need them) but touch no memory.
     const IO* __restrict__ x = reinterpret_cast<const IO*>(a.x) + n0;
-    const LifConsts c = a.c;
+    LifConsts c = a.c;
+    pin(c);
     const int64_t T = a.T, ld = a.ld;
 
     float V[VEC];
@@ -92,15 +159,15 @@ lif_forward_kernel(const FwdArgs a) {
     for (int j = 0; j < PF; ++j)
         if (j < T) buf[j] = ld_group<IO, VEC>(x + (int64_t)j * ld, nvalid);
 
+    unsigned char* spk_row = reinterpret_cast<unsigned char*>(a.spikes);
+    const int64_t spk_step = spike_row_bytes<IO, SFMT>(a);
     for (int64_t t0 = 0; t0 < T; t0 += PF) {
 #pragma unroll
         for (int j = 0; j < PF; ++j) {
             const int64_t t = t0 + j;
             if (t < T) {
                 const Pack<IO, VEC> xv = buf[j];
-                if (t + PF < T)
-                    buf[j] = ld_group<IO, VEC>(x + (t + PF) * ld, nvalid);
-
+                if (t + PF < T) buf[j] = ld_group<IO, VEC>(x + (t + PF) * ld, nvalid);
                 if constexpr (SAVE == SAVE_RECOMPUTE) {
                     if ((t % kCkpt) == 0 && nvalid > 0) {
                         Pack<float, VEC> ck;
@@ -110,39 +177,12 @@ lif_forward_kernel(const FwdArgs a) {
                     }
                 }
                 Pack<float, VEC> hp;
-                unsigned bits = 0;
-#pragma unroll
-                for (int i = 0; i < VEC; ++i) {
-                    const float H = lif_charge(c, V[i], to_f32(xv.v[i]));
-                    const bool S = lif_fire(c, H);
-                    V[i] = lif_reset(c, H, S);
-                    hp.v[i] = H;
-                    bits |= (unsigned)S << i;
-                }
-                bits &= (nvalid >= VEC) ? ((VEC == 32) ? kFull : ((1u << VEC) - 1u)) : ((1u << nvalid) - 1u);
+                const unsigned bits = fwd_compute<SOFT>(c, V, xv, hp);
                 if constexpr (SAVE == SAVE_H) {
                     if (nvalid > 0) st_group<float, VEC>(a.saved + t * a.ldh + n0, hp, nvalid);
                 }
-                if constexpr (SFMT == SPK_U8) {
-                    if (nvalid > 0) {
-                        Pack<uint8_t, VEC> sp;
-#pragma unroll
-                        for (int i = 0; i < VEC; ++i) sp.v[i] = (uint8_t)((bits >> i) & 1u);
-                        st_group<uint8_t, VEC>(reinterpret_cast<uint8_t*>(a.spikes) + t * ld + n0,
-                                               sp, nvalid);
-                    }
-                } else if constexpr (SFMT == SPK_IO) {
-                    if (nvalid > 0) {
-                        Pack<IO, VEC> sp;
-#pragma unroll
-                        for (int i = 0; i < VEC; ++i)
-                            sp.v[i] = from_f32<IO>(((bits >> i) & 1u) ? 1.0f : 0.0f);
-                        st_group<IO, VEC>(reinterpret_cast<IO*>(a.spikes) + t * ld + n0, sp, nvalid);
-                    }
-                } else {
-                    store_spike_bits<VEC>(reinterpret_cast<uint32_t*>(a.spikes) + t * a.nwords, g,
-                                          bits, a.nwords);
-                }
+                store_spikes<IO, VEC, SFMT>(spk_row, g, n0, bits, nvalid, a.nwords);
+                spk_row += spk_step;
             }
         }
     }
@@ -155,8 +195,8 @@ lif_forward_kernel(const FwdArgs a) {
 }
 
 // ------------------------------------------------------------------------------------
-// Backward, SAVE_H: Eq. 3 over t = T-1..0 reading the saved H.
-template <typename IO, int VEC, int SURR, int PF>
+// Generic backward, SAVE_H: Eq. 3 over t = T-1..0 reading the saved H.
+template <typename IO, int VEC, int MODE, int PF>
 __global__ void __launch_bounds__(kBlock)
 lif_backward_saveh_kernel(const BwdArgs a) {
     const int64_t g = (int64_t)blockIdx.x * kBlock + threadIdx.x;
@@ -166,7 +206,8 @@ lif_backward_saveh_kernel(const BwdArgs a) {
     const IO* __restrict__ gs = reinterpret_cast<const IO*>(a.gS) + n0;
     const float* __restrict__ hs = a.saved + n0;
     IO* __restrict__ gx = reinterpret_cast<IO*>(a.gX) + n0;
-    const LifConsts c = a.c;
+    LifConsts c = a.c;
+    pin(c);
     const int64_t T = a.T, ld = a.ld, ldh = a.ldh;
 
     float gV[VEC];
@@ -200,14 +241,7 @@ lif_backward_saveh_kernel(const BwdArgs a) {
                     gbuf[j] = ld_group<IO, VEC>(gs + (t - PF) * ld, nvalid);
                     hbuf[j] = ld_group<float, VEC>(hs + (t - PF) * ldh, nvalid);
                 }
-                Pack<IO, VEC> out;
-#pragma unroll
-                for (int i = 0; i < VEC; ++i) {
-                    const float gH = lif_grad_step<SURR>(c, hv.v[i], to_f32(gv.v[i]), gV[i]);
-                    out.v[i] = from_f32<IO>(__fmul_rn(c.s, gH));
-                    gV[i] = __fmul_rn(c.k, gH);
-                }
-                st_group<IO, VEC>(gx + t * ld, out, nvalid);
+                st_group<IO, VEC>(gx + t * ld, bwd_step<IO, VEC, MODE>(c, gV, hv.v, gv), nvalid);
             }
         }
     }
@@ -220,11 +254,10 @@ lif_backward_saveh_kernel(const BwdArgs a) {
 }
 
 // ------------------------------------------------------------------------------------
-// Backward, SAVE_RECOMPUTE: per kCkpt-step chunk (last chunk first) reload the chunk's
-// entry V checkpoint, re-run the forward charge over the chunk from x (identical
-// instruction sequence -> bitwise-identical H), then walk the chunk backwards.  All
-// 2*kCkpt row loads of a chunk (x and gS) are issued before any is consumed.
-template <typename IO, int VEC, int SURR>
+// Generic backward, SAVE_RECOMPUTE: per kCkpt-step chunk (last chunk first) reload the
+// chunk's entry V checkpoint, re-run the forward charge over the chunk from x (identical
+// instruction sequence -> bitwise-identical H), then walk the chunk backwards.
+template <typename IO, int VEC, int MODE>
 __global__ void __launch_bounds__(kBlock)
 lif_backward_recompute_kernel(const BwdArgs a) {
     const int64_t g = (int64_t)blockIdx.x * kBlock + threadIdx.x;
@@ -235,7 +268,8 @@ lif_backward_recompute_kernel(const BwdArgs a) {
     const IO* __restrict__ xs = reinterpret_cast<const IO*>(a.x) + n0;
     const float* __restrict__ ck = a.saved + n0;
     IO* __restrict__ gx = reinterpret_cast<IO*>(a.gX) + n0;
-    const LifConsts c = a.c;
+    LifConsts c = a.c;
+    pin(c);
     const int64_t T = a.T, ld = a.ld, ldh = a.ldh;
 
     float gV[VEC];
@@ -272,23 +306,16 @@ lif_backward_recompute_kernel(const BwdArgs a) {
 #pragma unroll
                 for (int i = 0; i < VEC; ++i) {
                     const float H = lif_charge(c, V[i], to_f32(xb[j].v[i]));
-                    V[i] = lif_reset(c, H, lif_fire(c, H));
+                    V[i] = lif_reset<Mode<MODE>::SOFT>(c, H, lif_fire(c, H));
                     h[j][i] = H;
                 }
             }
         }
 #pragma unroll
         for (int j = kCkpt - 1; j >= 0; --j) {
-            if (j < len) {
-                Pack<IO, VEC> out;
-#pragma unroll
-                for (int i = 0; i < VEC; ++i) {
-                    const float gH = lif_grad_step<SURR>(c, h[j][i], to_f32(gb[j].v[i]), gV[i]);
-                    out.v[i] = from_f32<IO>(__fmul_rn(c.s, gH));
-                    gV[i] = __fmul_rn(c.k, gH);
-                }
-                st_group<IO, VEC>(gx + (t0 + j) * ld, out, nvalid);
-            }
+            if (j < len)
+                st_group<IO, VEC>(gx + (t0 + j) * ld, bwd_step<IO, VEC, MODE>(c, gV, h[j], gb[j]),
+                                  nvalid);
         }
     }
     if (a.grad_v_init != nullptr) {

@@ -1,0 +1,437 @@
+// lif_tma.cuh -- persistent, warp-specialised fused LIF kernels for sm_100a, fed by the
+// Tensor Memory Accelerator.
+//
+// Why this shape:
+//  * The path is HBM-bound (a few flops per byte), so what matters is keeping enough
+//    bytes in flight per SM (Little's law: ~6.5 TB/s x ~1-2 us ~= 50-100 KB per SM)
+//    independently of how many registers the recurrence needs.  One producer lane issues
+//    2-D TMA tile loads (cp.async.bulk.tensor.2d -> UTMALDG; box = up to 256 neurons x R
+//    time rows, 4-16 KB per instruction) into a shared-memory ring; completion is counted
+//    in bytes on an mbarrier.  The ring size, not the register file, sets the bytes in
+//    flight, and the TMA engine (not the LSU) does the address generation.
+//  * Grids are persistent (1-2 CTAs per SM) and walk W-neuron tiles round-robin: every
+//    consumer thread still owns its neurons for the whole time axis (temporal fusion,
+//    PAPER.md:220-222), but the machine is filled in one wave and the tail is one tile,
+//    instead of the partial last wave of a one-thread-per-neuron grid.
+//  * Consumer warps read their neurons from the ring (conflict-free 4-16 B per lane), run
+//    the recurrence in registers and store outputs straight to HBM with coalesced
+//    streaming stores, then release the ring slot (one mbarrier arrive per warp).
+//  * Ragged T (not a multiple of the row block) and a ragged last tile are handled by the
+//    TMA's zero fill; consumers do not store past T / N.  Host guarantees N % VEC == 0.
+//
+// Smem layout of one tensor's row-block: NB boxes of [rows][BW] (BW = min(W, 256)).
+#pragma once
+
+#include <cuda.h>
+
+#include "lif_async.cuh"
+#include "lif_kernels.cuh"
+
+namespace snn {
+
+template <int S>
+struct Barriers {
+    uint64_t full[S];
+    uint64_t empty[S];
+};
+
+constexpr int kAlignSlack = 1024;
+
+// Dynamic smem, re-based to 1024 B (TMA destinations must be >=128 B aligned).
+__device__ __forceinline__ unsigned char* smem_base() {
+    extern __shared__ __align__(1024) unsigned char dyn_smem[];
+    const uint32_t a = smem_u32(dyn_smem);
+    return dyn_smem + ((1024u - (a & 1023u)) & 1023u);
+}
+
+template <int S>
+__device__ __forceinline__ void init_barriers(Barriers<S>* b, uint32_t consumer_warps) {
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&b->full[s], 1);
+            mbar_init(&b->empty[s], consumer_warps);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+}
+
+// Element offset of neuron nt (VEC-aligned, < W) at row r of a [NB][ROWS][BW] region.
+template <int VEC, int BW, int ROWS>
+__device__ __forceinline__ int box_off(int nt, int r) {
+    return ((nt / BW) * ROWS + r) * BW + (nt % BW);
+}
+
+// ------------------------------------------------------------------------------------
+// Forward.  Stage = R time rows of a W-neuron tile.  Warp 0 lane 0 = producer;
+// warps 1..NCONS/32 = consumers, each lane owning VEC neurons.
+template <typename IO, int VEC, int NCONS, int R, int S>
+struct FwdTma {
+    static constexpr int W = NCONS * VEC;
+    static constexpr int BW = W < 256 ? W : 256;
+    static constexpr int NB = W / BW;
+    static constexpr int BOX_BYTES = BW * R * (int)sizeof(IO);
+    static constexpr int STAGE_BYTES = NB * BOX_BYTES;
+    static constexpr int SMEM = S * STAGE_BYTES + (int)sizeof(Barriers<S>) + kAlignSlack;
+    static constexpr int THREADS = NCONS + 32;
+    static_assert(W % BW == 0 && BW % VEC == 0, "tile geometry");
+};
+
+template <typename IO, int VEC, int SFMT, int SAVE, bool SOFT, int NCONS, int R, int S>
+__global__ void __launch_bounds__(NCONS + 32)
+lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const FwdArgs a, const int64_t ntiles) {
+    using Cfg = FwdTma<IO, VEC, NCONS, R, S>;
+    constexpr int W = Cfg::W, BW = Cfg::BW, NB = Cfg::NB;
+    unsigned char* smem = smem_base();
+    auto* bar = reinterpret_cast<Barriers<S>*>(smem + S * Cfg::STAGE_BYTES);
+    init_barriers<S>(bar, NCONS / 32);
+
+    const int64_t T = a.T, N = a.N;
+    const int64_t nrb = (T + R - 1) / R;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (warp == 0) {  // ---------------- producer
+        if (lane == 0) {
+            tma_prefetch_desc(&tmx);
+            const uint64_t pol = policy_evict_first();
+            uint32_t k = 0;
+            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                for (int64_t rb = 0; rb < nrb; ++rb, ++k) {
+                    const int s = k % S;
+                    unsigned char* stg = smem + s * Cfg::STAGE_BYTES;
+                    mbar_wait(&bar->empty[s], ((k / S) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&bar->full[s], Cfg::STAGE_BYTES);
+#pragma unroll
+                    for (int b = 0; b < NB; ++b)
+                        tma_load_2d(stg + b * Cfg::BOX_BYTES, &tmx, (int)(tile * W + b * BW),
+                                    (int)(rb * R), &bar->full[s], pol);
+                }
+            }
+        }
+        return;
+    }
+
+    // ---------------- consumers
+    LifConsts c = a.c;
+    pin(c);
+    const int ct = threadIdx.x - 32;
+    const int xoff = box_off<VEC, BW, R>(ct * VEC, 0);
+    const int64_t spk_step = spike_row_bytes<IO, SFMT>(a);
+    uint32_t k = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t g = tile * NCONS + ct;
+        const int64_t n0 = g * VEC;
+        const int nvalid = n0 < N ? VEC : 0;
+        float V[VEC];
+        if (a.v_init != nullptr && nvalid > 0) {
+            const Pack<float, VEC> v0 = ld_stream<float, VEC>(a.v_init + n0);
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) V[i] = v0.v[i];
+        } else {
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) V[i] = c.v_reset;
+        }
+        unsigned char* spk_row = reinterpret_cast<unsigned char*>(a.spikes);
+        float* h_row = a.saved + n0;   // SAVE_H: advanced one row per step
+        for (int64_t rb = 0; rb < nrb; ++rb, ++k) {
+            const int rows = (int)min((int64_t)R, T - rb * R);
+            const int s = k % S;
+            const IO* xs = reinterpret_cast<const IO*>(smem + s * Cfg::STAGE_BYTES) + xoff;
+            mbar_wait(&bar->full[s], (k / S) & 1);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                if (r < rows) {
+                    const Pack<IO, VEC> xv = *reinterpret_cast<const Pack<IO, VEC>*>(xs + r * BW);
+                    if constexpr (SAVE == SAVE_RECOMPUTE) {
+                        // checkpoint the V entering step t when t % kCkpt == 0
+                        const int64_t t = rb * R + r;
+                        if ((t % kCkpt) == 0 && nvalid > 0) {
+                            Pack<float, VEC> ck;
+#pragma unroll
+                            for (int i = 0; i < VEC; ++i) ck.v[i] = V[i];
+                            st_stream<float, VEC>(h_row + (t / kCkpt) * a.ldh, ck);
+                        }
+                    }
+                    Pack<float, VEC> hp;
+                    const unsigned bits = fwd_compute<SOFT>(c, V, xv, hp);
+                    if constexpr (SAVE == SAVE_H) {
+                        if (nvalid > 0) st_stream<float, VEC>(h_row, hp);
+                        h_row += a.ldh;
+                    }
+                    store_spikes<IO, VEC, SFMT>(spk_row, g, n0, bits, nvalid, a.nwords);
+                    spk_row += spk_step;
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar->empty[s]);
+        }
+        if (a.v_final != nullptr && nvalid > 0) {
+            Pack<float, VEC> vf;
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) vf.v[i] = V[i];
+            st_stream<float, VEC>(a.v_final + n0, vf);
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// Backward, RECOMPUTE.  Stage = one kCkpt-step chunk of the tile: x rows, gS rows and the
+// chunk's entry-V checkpoint row.  Chunks of a tile are streamed last-first.
+template <typename IO, int VEC, int NCONS, int S>
+struct BwdRecTma {
+    static constexpr int W = NCONS * VEC;
+    static constexpr int BW = W < 256 ? W : 256;
+    static constexpr int NB = W / BW;
+    static constexpr int BOX_BYTES = BW * kCkpt * (int)sizeof(IO);
+    static constexpr int CK_BOX_BYTES = BW * 4;
+    static constexpr int X_OFF = 0;
+    static constexpr int G_OFF = NB * BOX_BYTES;
+    static constexpr int CK_OFF = 2 * NB * BOX_BYTES;
+    static constexpr int STAGE_BYTES = 2 * NB * BOX_BYTES + NB * CK_BOX_BYTES;
+    static constexpr int SMEM = S * STAGE_BYTES + (int)sizeof(Barriers<S>) + kAlignSlack;
+    static constexpr int THREADS = NCONS + 32;
+    static_assert(W % BW == 0 && BW % VEC == 0 && STAGE_BYTES % 128 == 0, "tile geometry");
+};
+
+// Reverse walk over rows [0, ROWS) of one chunk (compile-time ROWS for the common full
+// chunk: no per-step guards).  h = recomputed H; gsm = gS rows in smem; gxp = gX row of
+// the chunk's LAST row, walked backwards by ld.
+template <typename IO, int VEC, int MODE, int BW, int ROWS_MAX>
+__device__ __forceinline__ void bwd_chunk(const LifConsts& c, float (&gV)[VEC],
+                                          const float (&h)[ROWS_MAX][VEC], const IO* gsm,
+                                          IO* gxp, int64_t ld, int rows, bool valid) {
+#pragma unroll
+    for (int j = ROWS_MAX - 1; j >= 0; --j) {
+        if (j < rows) {
+            const Pack<IO, VEC> gv = *reinterpret_cast<const Pack<IO, VEC>*>(gsm + j * BW);
+            const Pack<IO, VEC> out = bwd_step<IO, VEC, MODE>(c, gV, h[j], gv);
+            if (valid) st_stream<IO, VEC>(gxp, out);
+            gxp -= ld;
+        }
+    }
+}
+
+template <typename IO, int VEC, int MODE, int NCONS, int S>
+__global__ void __launch_bounds__(NCONS + 32)
+lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
+                                  const __grid_constant__ CUtensorMap tmg,
+                                  const __grid_constant__ CUtensorMap tmck, const BwdArgs a,
+                                  const int64_t ntiles) {
+    using Cfg = BwdRecTma<IO, VEC, NCONS, S>;
+    constexpr int W = Cfg::W, BW = Cfg::BW, NB = Cfg::NB;
+    unsigned char* smem = smem_base();
+    auto* bar = reinterpret_cast<Barriers<S>*>(smem + S * Cfg::STAGE_BYTES);
+    init_barriers<S>(bar, NCONS / 32);
+
+    const int64_t T = a.T, N = a.N, ld = a.ld;
+    const int64_t nch = (T + kCkpt - 1) / kCkpt;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (warp == 0) {  // ---------------- producer
+        if (lane == 0) {
+            tma_prefetch_desc(&tmx); tma_prefetch_desc(&tmg); tma_prefetch_desc(&tmck);
+            const uint64_t pol = policy_evict_first();
+            uint32_t k = 0;
+            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                for (int64_t ch = nch - 1; ch >= 0; --ch, ++k) {
+                    const int s = k % S;
+                    unsigned char* stg = smem + s * Cfg::STAGE_BYTES;
+                    mbar_wait(&bar->empty[s], ((k / S) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&bar->full[s], Cfg::STAGE_BYTES);
+#pragma unroll
+                    for (int b = 0; b < NB; ++b) {
+                        const int c0 = (int)(tile * W + b * BW);
+                        tma_load_2d(stg + Cfg::CK_OFF + b * Cfg::CK_BOX_BYTES, &tmck, c0, (int)ch,
+                                    &bar->full[s], pol);
+                        tma_load_2d(stg + Cfg::X_OFF + b * Cfg::BOX_BYTES, &tmx, c0, (int)(ch * kCkpt),
+                                    &bar->full[s], pol);
+                        tma_load_2d(stg + Cfg::G_OFF + b * Cfg::BOX_BYTES, &tmg, c0, (int)(ch * kCkpt),
+                                    &bar->full[s], pol);
+                    }
+                }
+            }
+        }
+        return;
+    }
+
+    // ---------------- consumers
+    LifConsts c = a.c;
+    pin(c);
+    const int ct = threadIdx.x - 32;
+    const int nt = ct * VEC;
+    const int roff = box_off<VEC, BW, kCkpt>(nt, 0);
+    const int ckoff = box_off<VEC, BW, 1>(nt, 0);
+    IO* gx = reinterpret_cast<IO*>(a.gX);
+    uint32_t k = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t n0 = tile * W + nt;
+        const bool valid = n0 < N;   // N % VEC == 0 on this path
+        float gV[VEC];
+        if (a.grad_v_final != nullptr && valid) {
+            const Pack<float, VEC> g0 = ld_stream<float, VEC>(a.grad_v_final + n0);
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) gV[i] = g0.v[i];
+        } else {
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) gV[i] = 0.0f;
+        }
+        for (int64_t ch = nch - 1; ch >= 0; --ch, ++k) {
+            const int64_t t0 = ch * kCkpt;
+            const int rows = (int)min((int64_t)kCkpt, T - t0);
+            const int s = k % S;
+            const unsigned char* stg = smem + s * Cfg::STAGE_BYTES;
+            const IO* xs = reinterpret_cast<const IO*>(stg + Cfg::X_OFF) + roff;
+            const IO* gsm = reinterpret_cast<const IO*>(stg + Cfg::G_OFF) + roff;
+            mbar_wait(&bar->full[s], (k / S) & 1);
+            const Pack<float, VEC> v0 =
+                *reinterpret_cast<const Pack<float, VEC>*>(reinterpret_cast<const float*>(stg + Cfg::CK_OFF) + ckoff);
+            float V[VEC];
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) V[i] = v0.v[i];
+            float h[kCkpt][VEC];
+            IO* gxp = gx + (t0 + rows - 1) * ld + n0;
+            if (rows == kCkpt) {
+#pragma unroll
+                for (int j = 0; j < kCkpt; ++j) {
+                    const Pack<IO, VEC> xv = *reinterpret_cast<const Pack<IO, VEC>*>(xs + j * BW);
+#pragma unroll
+                    for (int i = 0; i < VEC; ++i) {
+                        const float H = lif_charge(c, V[i], to_f32(xv.v[i]));
+                        V[i] = lif_reset<Mode<MODE>::SOFT>(c, H, lif_fire(c, H));
+                        h[j][i] = H;
+                    }
+                }
+                bwd_chunk<IO, VEC, MODE, BW, kCkpt>(c, gV, h, gsm, gxp, ld, kCkpt, valid);
+            } else {
+#pragma unroll
+                for (int j = 0; j < kCkpt; ++j) {
+                    if (j < rows) {
+                        const Pack<IO, VEC> xv = *reinterpret_cast<const Pack<IO, VEC>*>(xs + j * BW);
+#pragma unroll
+                        for (int i = 0; i < VEC; ++i) {
+                            const float H = lif_charge(c, V[i], to_f32(xv.v[i]));
+                            V[i] = lif_reset<Mode<MODE>::SOFT>(c, H, lif_fire(c, H));
+                            h[j][i] = H;
+                        }
+                    }
+                }
+                bwd_chunk<IO, VEC, MODE, BW, kCkpt>(c, gV, h, gsm, gxp, ld, rows, valid);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar->empty[s]);
+        }
+        if (a.grad_v_init != nullptr && valid) {
+            Pack<float, VEC> gi;
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) gi.v[i] = gV[i];
+            st_stream<float, VEC>(a.grad_v_init + n0, gi);
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// Backward, SAVE_H.  Stage = R time rows of H (fp32) and gS; row blocks streamed last-first.
+template <typename IO, int VEC, int NCONS, int R, int S>
+struct BwdHTma {
+    static constexpr int W = NCONS * VEC;
+    static constexpr int BW = W < 256 ? W : 256;
+    static constexpr int NB = W / BW;
+    static constexpr int HBOX = BW * R * 4;
+    static constexpr int GBOX = BW * R * (int)sizeof(IO);
+    static constexpr int G_OFF = NB * HBOX;
+    static constexpr int STAGE_BYTES = NB * (HBOX + GBOX);
+    static constexpr int SMEM = S * STAGE_BYTES + (int)sizeof(Barriers<S>) + kAlignSlack;
+    static constexpr int THREADS = NCONS + 32;
+    static_assert(W % BW == 0 && BW % VEC == 0 && STAGE_BYTES % 128 == 0, "tile geometry");
+};
+
+template <typename IO, int VEC, int MODE, int NCONS, int R, int S>
+__global__ void __launch_bounds__(NCONS + 32)
+lif_backward_saveh_tma_kernel(const __grid_constant__ CUtensorMap tmh,
+                              const __grid_constant__ CUtensorMap tmg, const BwdArgs a,
+                              const int64_t ntiles) {
+    using Cfg = BwdHTma<IO, VEC, NCONS, R, S>;
+    constexpr int W = Cfg::W, BW = Cfg::BW, NB = Cfg::NB;
+    unsigned char* smem = smem_base();
+    auto* bar = reinterpret_cast<Barriers<S>*>(smem + S * Cfg::STAGE_BYTES);
+    init_barriers<S>(bar, NCONS / 32);
+
+    const int64_t T = a.T, N = a.N, ld = a.ld;
+    const int64_t nrb = (T + R - 1) / R;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            tma_prefetch_desc(&tmh); tma_prefetch_desc(&tmg);
+            const uint64_t pol = policy_evict_first();
+            uint32_t k = 0;
+            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                for (int64_t rb = nrb - 1; rb >= 0; --rb, ++k) {
+                    const int s = k % S;
+                    unsigned char* stg = smem + s * Cfg::STAGE_BYTES;
+                    mbar_wait(&bar->empty[s], ((k / S) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&bar->full[s], Cfg::STAGE_BYTES);
+#pragma unroll
+                    for (int b = 0; b < NB; ++b) {
+                        const int c0 = (int)(tile * W + b * BW);
+                        tma_load_2d(stg + b * Cfg::HBOX, &tmh, c0, (int)(rb * R), &bar->full[s], pol);
+                        tma_load_2d(stg + Cfg::G_OFF + b * Cfg::GBOX, &tmg, c0, (int)(rb * R),
+                                    &bar->full[s], pol);
+                    }
+                }
+            }
+        }
+        return;
+    }
+
+    LifConsts c = a.c;
+    pin(c);
+    const int ct = threadIdx.x - 32;
+    const int nt = ct * VEC;
+    const int roff = box_off<VEC, BW, R>(nt, 0);
+    IO* gx = reinterpret_cast<IO*>(a.gX);
+    uint32_t k = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t n0 = tile * W + nt;
+        const bool valid = n0 < N;
+        float gV[VEC];
+        if (a.grad_v_final != nullptr && valid) {
+            const Pack<float, VEC> g0 = ld_stream<float, VEC>(a.grad_v_final + n0);
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) gV[i] = g0.v[i];
+        } else {
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) gV[i] = 0.0f;
+        }
+        for (int64_t rb = nrb - 1; rb >= 0; --rb, ++k) {
+            const int rows = (int)min((int64_t)R, T - rb * R);
+            const int s = k % S;
+            const unsigned char* stg = smem + s * Cfg::STAGE_BYTES;
+            const float* hs = reinterpret_cast<const float*>(stg) + roff;
+            const IO* gsm = reinterpret_cast<const IO*>(stg + Cfg::G_OFF) + roff;
+            IO* gxp = gx + (rb * R + rows - 1) * ld + n0;
+            mbar_wait(&bar->full[s], (k / S) & 1);
+#pragma unroll
+            for (int r = R - 1; r >= 0; --r) {
+                if (r < rows) {
+                    const Pack<float, VEC> hv = *reinterpret_cast<const Pack<float, VEC>*>(hs + r * BW);
+                    const Pack<IO, VEC> gv = *reinterpret_cast<const Pack<IO, VEC>*>(gsm + r * BW);
+                    const Pack<IO, VEC> out = bwd_step<IO, VEC, MODE>(c, gV, hv.v, gv);
+                    if (valid) st_stream<IO, VEC>(gxp, out);
+                    gxp -= ld;
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar->empty[s]);
+        }
+        if (a.grad_v_init != nullptr && valid) {
+            Pack<float, VEC> gi;
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) gi.v[i] = gV[i];
+            st_stream<float, VEC>(a.grad_v_init + n0, gi);
+        }
+    }
+}
+
+}  // namespace snn

@@ -1,20 +1,24 @@
-// snn_lif_api.cu -- the C ABI of include/snn_lif.h: argument validation, variant
-// selection and kernel launch.  The library never allocates, frees or synchronises.
+// snn_lif_api.cu -- the C ABI of include/snn_lif.h: argument validation, constants,
+// variant selection.  Kernel launches live in fwd_*/bwd_* translation units.
+// The library never allocates, frees or synchronises.
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
-#include <type_traits>
+#include <initializer_list>
+#include <map>
+#include <mutex>
 #include <utility>
 
-#include "../../include/snn_lif.h"
-#include "lif_kernels.cuh"
+#include "internal.h"
+
+namespace snn_host {
 
 namespace {
-
 thread_local char g_err[512] = "";
+}
 
-snn_status fail(snn_status st, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
 snn_status fail(snn_status st, const char* fmt, ...) {
     va_list ap;
     va_start(ap, fmt);
@@ -23,11 +27,84 @@ snn_status fail(snn_status st, const char* fmt, ...) {
     return st;
 }
 
+snn_status launch_status(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(SNN_ERR_CUDA, "%s launch failed: %s", what, cudaGetErrorString(e));
+    return SNN_OK;
+}
+
+int num_sms() {
+    int dev = 0, n = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 148;
+    return n;
+}
+
+// ---- tensor maps (TMA descriptors), encoded per call on the host --------------------
+
+namespace {
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    return fn;
+}
+}  // namespace
+
+bool tma_available() { return encode_fn() != nullptr; }
+
+bool encode_2d(CUtensorMap* m, const void* base, size_t esz, int64_t inner, int64_t outer,
+               int64_t ld, int box_inner, int box_outer) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return false;
+    const CUtensorMapDataType dt = esz == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                            : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+    const cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+    const cuuint64_t strides[1] = {(cuuint64_t)(ld * (int64_t)esz)};
+    const cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
+    const cuuint32_t estr[2] = {1, 1};
+    return fn(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int cached_occupancy(const void* k, int threads, int smem, int (*prep)(const void*, int, int)) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, int> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find({dev, k});
+    if (it != cache.end()) return it->second;
+    const int occ = prep(k, threads, smem);
+    cache[{dev, k}] = occ;
+    return occ;
+}
+
+int tma_vec_forward(int io_dtype) { return io_dtype == SNN_BF16 ? 8 : 4; }
+int tma_vec_backward(int io_dtype) { return io_dtype == SNN_BF16 ? 2 : 1; }
+
+}  // namespace snn_host
+
+using namespace snn_host;
+
+namespace {
+
 constexpr int64_t kLdhAlign = 16;  // saved-row stride alignment (elements)
 
 int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
-
 bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+size_t io_size(int dt) { return dt == SNN_BF16 ? 2 : 4; }
 
 snn_status check_params(const snn_lif_params* p) {
     if (!p) return fail(SNN_ERR_NULL_POINTER, "params is NULL");
@@ -49,14 +126,13 @@ snn_status check_params(const snn_lif_params* p) {
 
 snn_status check_shape(const snn_lif_shape* s) {
     if (!s) return fail(SNN_ERR_NULL_POINTER, "shape is NULL");
-    if (s->T < 1 || s->N < 1) return fail(SNN_ERR_INVALID_VALUE, "T=%lld N=%lld must be >= 1",
-                                          (long long)s->T, (long long)s->N);
-    if (s->ld < s->N) return fail(SNN_ERR_INVALID_VALUE, "ld=%lld < N=%lld", (long long)s->ld,
-                                  (long long)s->N);
+    if (s->T < 1 || s->N < 1)
+        return fail(SNN_ERR_INVALID_VALUE, "T=%lld N=%lld must be >= 1", (long long)s->T, (long long)s->N);
+    if (s->ld < s->N)
+        return fail(SNN_ERR_INVALID_VALUE, "ld=%lld < N=%lld", (long long)s->ld, (long long)s->N);
     // T*ld (and T*ldh of the saved buffer) must fit in int64 byte offsets.
     const int64_t big = s->ld > s->N + kLdhAlign ? s->ld : s->N + kLdhAlign;
-    if (s->T > (INT64_MAX / 8) / big)
-        return fail(SNN_ERR_INVALID_VALUE, "dimension overflow: T*ld too large");
+    if (s->T > (INT64_MAX / 8) / big) return fail(SNN_ERR_INVALID_VALUE, "dimension overflow: T*ld too large");
     if (s->io_dtype != SNN_F32 && s->io_dtype != SNN_BF16)
         return fail(SNN_ERR_INVALID_VALUE, "io_dtype %d", s->io_dtype);
     if (s->spike_fmt < SNN_SPK_U8 || s->spike_fmt > SNN_SPK_IO)
@@ -75,10 +151,15 @@ snn::LifConsts make_consts(const snn_lif_params* p) {
     c.v_th = p->v_th;
     c.v_reset = p->v_reset;
     c.alpha = p->alpha;
-    c.atan_c = 1.57079632679489662f * p->alpha;
-    c.soft = p->reset_mode == SNN_RESET_SOFT;
-    c.detach = p->detach_reset;
+    c.ex2_scale = -p->alpha * 1.44269504088896341f;   // -alpha log2(e)
+    c.atan_c = 1.57079632679489662f * p->alpha;        // pi/2 alpha
+    c.half_alpha = 0.5f * p->alpha;
     return c;
+}
+
+int mode_of(const snn_lif_params* p) {
+    return (p->surrogate == SNN_SURR_ATAN ? 1 : 0) | (p->reset_mode == SNN_RESET_SOFT ? 2 : 0) |
+           (p->detach_reset ? 4 : 0);
 }
 
 int64_t saved_ld(const snn_lif_shape* s) { return round_up(s->N, kLdhAlign); }
@@ -89,58 +170,18 @@ int64_t saved_rows(const snn_lif_shape* s) {
     return 0;
 }
 
-size_t io_size(int dt) { return dt == SNN_BF16 ? 2 : 4; }
-
-snn_status launch_status(const char* what) {
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess)
-        return fail(SNN_ERR_CUDA, "%s launch failed: %s", what, cudaGetErrorString(e));
-    return SNN_OK;
-}
-
-template <int V> using IC = std::integral_constant<int, V>;
-
-// Forward prefetch depth along T (rows in flight per thread).
-constexpr int kFwdPF = 8;
-constexpr int kBwdPF = 8;
-
-template <typename IO, int VEC>
-snn_status launch_forward(const snn_lif_shape* s, const snn::FwdArgs& a, cudaStream_t st) {
-    const int64_t groups = (s->N + VEC - 1) / VEC;
-    const dim3 grid((unsigned)((groups + snn::kBlock - 1) / snn::kBlock));
-    auto go = [&](auto sfmt, auto save) {
-        snn::lif_forward_kernel<IO, VEC, decltype(sfmt)::value, decltype(save)::value, kFwdPF>
-            <<<grid, snn::kBlock, 0, st>>>(a);
-    };
-    auto by_save = [&](auto sfmt) {
-        switch (s->save_mode) {
-            case SNN_SAVE_H: go(sfmt, IC<snn::SAVE_H>{}); break;
-            case SNN_SAVE_RECOMPUTE: go(sfmt, IC<snn::SAVE_RECOMPUTE>{}); break;
-            default: go(sfmt, IC<snn::SAVE_NONE>{}); break;
-        }
-    };
-    switch (s->spike_fmt) {
-        case SNN_SPK_U8: by_save(IC<snn::SPK_U8>{}); break;
-        case SNN_SPK_BITS: by_save(IC<snn::SPK_BITS>{}); break;
-        default: by_save(IC<snn::SPK_IO>{}); break;
-    }
-    return launch_status("lif_forward_kernel");
-}
-
-template <typename IO, int VEC>
-snn_status launch_backward(const snn_lif_shape* s, int surrogate, const snn::BwdArgs& a,
-                           cudaStream_t st) {
-    const int64_t groups = (s->N + VEC - 1) / VEC;
-    const dim3 grid((unsigned)((groups + snn::kBlock - 1) / snn::kBlock));
-    auto go = [&](auto surr) {
-        constexpr int SURR = decltype(surr)::value;
-        if (s->save_mode == SNN_SAVE_H)
-            snn::lif_backward_saveh_kernel<IO, VEC, SURR, kBwdPF><<<grid, snn::kBlock, 0, st>>>(a);
-        else
-            snn::lif_backward_recompute_kernel<IO, VEC, SURR><<<grid, snn::kBlock, 0, st>>>(a);
-    };
-    if (surrogate == SNN_SURR_SIGMOID) go(IC<0>{}); else go(IC<1>{});
-    return launch_status("lif_backward_kernel");
+// TMA path: 16-byte-aligned base pointers, rows a multiple of 16 B (tensor-map strides),
+// N a multiple of the kernel's lane group, int32 coordinates.  SNN_LIF_NO_TMA=1 forces the
+// generic kernels (used by tests to cover both paths).
+bool tma_ok(const snn_lif_shape* s, int vec, std::initializer_list<const void*> ptrs) {
+    const char* e = std::getenv("SNN_LIF_NO_TMA");
+    if ((e && e[0] == '1') || !tma_available()) return false;
+    const int64_t q = 16 / (int64_t)io_size(s->io_dtype);
+    if (s->ld % q != 0 || s->N % vec != 0) return false;
+    if (s->N > INT32_MAX || s->T > INT32_MAX) return false;
+    for (const void* p : ptrs)
+        if (p && !aligned(p, 16)) return false;
+    return true;
 }
 
 }  // namespace
@@ -184,8 +225,7 @@ snn_status snn_lif_forward(const snn_lif_params* p, const snn_lif_shape* s, cons
     const size_t ssz = s->spike_fmt == SNN_SPK_U8 ? 1 : s->spike_fmt == SNN_SPK_BITS ? 4 : esz;
     if (!aligned(x, esz) || !aligned(spikes, ssz) || (v_init && !aligned(v_init, 4)) ||
         (v_final && !aligned(v_final, 4)) || (saved && s->save_mode != SNN_SAVE_NONE && !aligned(saved, 16)))
-        return fail(SNN_ERR_MISALIGNED, "a pointer is not aligned to its element size "
-                                        "(saved needs 16 B)");
+        return fail(SNN_ERR_MISALIGNED, "a pointer is not aligned to its element size (saved needs 16 B)");
 
     snn::FwdArgs a;
     a.x = x; a.v_init = v_init; a.spikes = spikes;
@@ -193,17 +233,17 @@ snn_status snn_lif_forward(const snn_lif_params* p, const snn_lif_shape* s, cons
     a.v_final = v_final;
     a.T = s->T; a.N = s->N; a.ld = s->ld; a.ldh = saved_ld(s); a.nwords = (s->N + 31) / 32;
     a.c = make_consts(p);
+    const bool soft = p->reset_mode == SNN_RESET_SOFT;
     cudaStream_t cs = static_cast<cudaStream_t>(stream);
 
+    if (tma_ok(s, tma_vec_forward(s->io_dtype), {x, v_init, v_final, a.saved, spikes}))
+        return s->io_dtype == SNN_BF16 ? launch_forward_tma_bf16(s, a, soft, cs)
+                                       : launch_forward_tma_f32(s, a, soft, cs);
     const int vec = s->io_dtype == SNN_BF16 ? 8 : 4;
     bool fast = (s->ld % vec) == 0 && aligned(x, 16) && (!v_init || aligned(v_init, 16)) &&
                 (!v_final || aligned(v_final, 16));
     if (s->spike_fmt == SNN_SPK_U8 || s->spike_fmt == SNN_SPK_IO) fast = fast && aligned(spikes, 16);
-    if (s->io_dtype == SNN_BF16) {
-        return fast ? launch_forward<__nv_bfloat16, 8>(s, a, cs)
-                    : launch_forward<__nv_bfloat16, 1>(s, a, cs);
-    }
-    return fast ? launch_forward<float, 4>(s, a, cs) : launch_forward<float, 1>(s, a, cs);
+    return launch_forward_generic(s, a, soft, fast, cs);
 }
 
 snn_status snn_lif_backward(const snn_lif_params* p, const snn_lif_shape* s,
@@ -225,8 +265,7 @@ snn_status snn_lif_backward(const snn_lif_params* p, const snn_lif_shape* s,
     if (!aligned(grad_spikes, esz) || !aligned(grad_x, esz) || (x && !aligned(x, esz)) ||
         !aligned(saved, 16) || (grad_v_final && !aligned(grad_v_final, 4)) ||
         (grad_v_init && !aligned(grad_v_init, 4)))
-        return fail(SNN_ERR_MISALIGNED, "a pointer is not aligned to its element size "
-                                        "(saved needs 16 B)");
+        return fail(SNN_ERR_MISALIGNED, "a pointer is not aligned to its element size (saved needs 16 B)");
     (void)v_init;  // the RECOMPUTE checkpoints already hold V[-1]
 
     snn::BwdArgs a;
@@ -234,22 +273,20 @@ snn_status snn_lif_backward(const snn_lif_params* p, const snn_lif_shape* s,
     a.grad_v_final = grad_v_final; a.gX = grad_x; a.grad_v_init = grad_v_init;
     a.T = s->T; a.N = s->N; a.ld = s->ld; a.ldh = saved_ld(s);
     a.c = make_consts(p);
+    const int mode = mode_of(p);
     cudaStream_t cs = static_cast<cudaStream_t>(stream);
 
-    // Backward threads own 8 bytes of io per row (2 fp32 / 4 bf16 neurons): the reverse
-    // walk keeps 2 x kCkpt rows of x and gS in registers, so a narrower group keeps
-    // occupancy up.
+    if (tma_ok(s, tma_vec_backward(s->io_dtype),
+               {grad_spikes, grad_x, s->save_mode == SNN_SAVE_RECOMPUTE ? x : nullptr, saved,
+                grad_v_final, grad_v_init}))
+        return s->io_dtype == SNN_BF16 ? launch_backward_tma_bf16(s, a, mode, cs)
+                                       : launch_backward_tma_f32(s, a, mode, cs);
     const int vec = s->io_dtype == SNN_BF16 ? 4 : 2;
     const bool fast = (s->ld % vec) == 0 && aligned(grad_spikes, 16) && aligned(grad_x, 16) &&
                       (!x || s->save_mode != SNN_SAVE_RECOMPUTE || aligned(x, 16)) &&
                       (!grad_v_final || aligned(grad_v_final, 16)) &&
                       (!grad_v_init || aligned(grad_v_init, 16));
-    if (s->io_dtype == SNN_BF16) {
-        return fast ? launch_backward<__nv_bfloat16, 4>(s, p->surrogate, a, cs)
-                    : launch_backward<__nv_bfloat16, 1>(s, p->surrogate, a, cs);
-    }
-    return fast ? launch_backward<float, 2>(s, p->surrogate, a, cs)
-                : launch_backward<float, 1>(s, p->surrogate, a, cs);
+    return launch_backward_generic(s, a, mode, fast, cs);
 }
 
 }  // extern "C"

@@ -201,3 +201,43 @@ def test_fault_injection_perturbed_k_fails_parity():
     rep = compare(PAPER, ref, ref["gX"], ref["gvi"], fwd.spikes.cpu(), gX.cpu(), vf_gpu=fwd.v_final.cpu(),
                   gvi_gpu=gvi.cpu())
     assert not rep.ok and rep.failures
+
+
+# ------------------------------------------------------------------ both kernel paths
+
+@pytest.mark.parametrize("T,N", [(17, 516), (33, 1028), (16, 4096), (100, 12296)])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("save_mode", ["recompute", "h"])
+def test_tma_edges_ragged_tiles_and_rows(T, N, dtype, save_mode):
+    """TMA path with a partial last tile (zero-filled boxes) and T not a multiple of the
+    row block / checkpoint interval."""
+    rep, _ = run_gpu_and_oracle(PAPER, T, N, dtype=dtype, save_mode=save_mode, with_v_init=True,
+                                with_grad_v_final=True, spike_fmt="bits")
+    assert_ok(rep)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("mode", range(8))
+def test_generic_and_tma_paths_agree_bitwise(monkeypatch, dtype, mode):
+    """SNN_LIF_NO_TMA=1 forces the generic kernels; both paths share the per-step
+    arithmetic (lif_common.cuh), so every output must be bitwise identical."""
+    p = LIFParams(tau=1.5, v_th=0.6, v_reset=-0.1, surrogate=("atan" if mode & 1 else "sigmoid"),
+                  reset=("soft" if mode & 2 else "hard"), detach_reset=bool(mode & 4),
+                  decay_input=bool(mode & 1))
+    T, N = 45, 3072
+    X = snn_synth.normal_tensor(41, T, N, dtype=dtype).cuda()
+    G = snn_synth.normal_tensor(42, T, N, dtype=dtype).cuda()
+    v0 = snn_synth.normal_tensor(43, 1, N)[0].cuda()
+    outs = []
+    for no_tma in ("0", "1"):
+        monkeypatch.setenv("SNN_LIF_NO_TMA", no_tma)
+        for sm in ("recompute", "h"):
+            f, g, v = _run(p, X, G, "bits", sm, v0=v0, gvf=v0)
+            torch.cuda.synchronize()
+            outs.append((f.spikes.clone(), f.v_final.clone(), g.clone(), v.clone()))
+    for o in outs[1:]:
+        for a, b in zip(outs[0], o):
+            assert torch.equal(a, b)
+    monkeypatch.delenv("SNN_LIF_NO_TMA")
+    rep, _ = run_gpu_and_oracle(p, T, N, dtype=dtype, with_v_init=True, with_grad_v_final=True)
+    assert_ok(rep)
