@@ -44,8 +44,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["cfg1", "cfg2", "cfg4"], default="cfg1")
-    ap.add_argument("--T", type=int, default=512, help="cfg1 time steps (8/32/128/512)")
+    ap.add_argument("--workload", choices=["cfg1", "cfg2", "cfg3", "cfg4"], default="cfg1")
+    ap.add_argument("--T", type=int, default=None, help="time steps (cfg1: 512, cfg3: 1024)")
+    ap.add_argument("--sweep", action="store_true",
+                    help="cfg1: also time T in {8,32,128,512} (L2 flushed before every launch)")
+    ap.add_argument("--chunks", type=int, default=32, help="cfg3 neuron chunks of the wavefront")
     ap.add_argument("--save-mode", choices=["recompute", "h"], default="recompute")
     ap.add_argument("--spike-fmt", choices=["u8", "bits", "io"], default="u8")
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -53,7 +56,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
                     help="target CPU time of the oracle baseline sample")
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.T is None:
+        a.T = 1024 if a.workload == "cfg3" else 512
+    return a
 
 
 # ----------------------------------------------------------------------------- workloads
@@ -63,6 +69,8 @@ def layer_list(args, world):
     import torch
     if args.workload == "cfg1":
         return [("cfg1", args.T, 1 << 20, torch.float32)]
+    if args.workload == "cfg3":
+        return [("cfg3", args.T, 1 << 22, torch.float32)]
     if args.workload == "cfg2":
         B, T = 128, 16
         return [(f"vgg11_l{i}", T, B * c * h * w, torch.bfloat16)
@@ -197,6 +205,136 @@ def oracle_sample(layers, seconds, spike_seed=(1234, 4321)):
     return {"value": total_ns / total_t, "unit": UNIT, "cores": 1, "kind": "oracle",
             "sample": f"{name}: T={T}, up to {cols} of {N} neuron columns (stride-sampled), "
                       f"fwd+bwd, fp64 C oracle single-threaded, {total_t:.1f} s total"}
+
+
+# ----------------------------------------------------------------------------- cfg1 sweep
+
+def run_sweep(args, params, dev, stream):
+    """BASELINE configs[1]: N = 2^20, T in {8, 32, 128, 512}.  Each fwd / bwd launch is
+    timed alone with CUDA events; an L2 flush (a 512 MiB memset, outside the events)
+    precedes every launch so small-T working sets are not served from the 126 MB L2."""
+    import torch
+    import paper_2408_00280_b200 as snn
+    import snn_synth
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    out = []
+    for T in (8, 32, 128, 512):
+        N = 1 << 20
+        X = snn_synth.normal_tensor(1234, T, N, device=dev)
+        G = snn_synth.normal_tensor(4321, T, N, device=dev)
+        tf, tb = [], []
+        for it in range(max(3, args.warmup) + 20):
+            flush.zero_()
+            e0, e1, e2, e3 = (torch.cuda.Event(enable_timing=True) for _ in range(4))
+            e0.record(stream)
+            f = snn.lif_forward(X, params, spike_fmt=args.spike_fmt, save_mode=args.save_mode,
+                                return_v_final=False)
+            e1.record(stream)
+            flush.zero_()
+            e2.record(stream)
+            snn.lif_backward(G, f, return_grad_v_init=False)
+            e3.record(stream)
+            torch.cuda.synchronize(dev)
+            if it >= max(3, args.warmup):
+                tf.append(e0.elapsed_time(e1)); tb.append(e2.elapsed_time(e3))
+        tf.sort(); tb.sort()
+        mf, mb = tf[len(tf) // 2], tb[len(tb) // 2]
+        bf, bb = bytes_per_neuron_step(4, args.spike_fmt, args.save_mode, T)
+        ns = N * T
+        out.append({"T": T, "fwd_ms": round(mf, 4), "bwd_ms": round(mb, 4),
+                    "neuron_steps_per_s": ns / ((mf + mb) / 1e3),
+                    "fwd_GBps": round(bf * ns / (mf / 1e3) / 1e9, 1),
+                    "bwd_GBps": round(bb * ns / (mb / 1e3) / 1e9, 1),
+                    "fwdbwd_GBps": round((bf + bb) * ns / ((mf + mb) / 1e3) / 1e9, 1)})
+        del X, G, f
+    return out
+
+
+# ----------------------------------------------------------------------------- cfg3 time split
+
+def run_tsplit(args):
+    """BASELINE configs[3]: N = 2^22, T = 1024, the paper's time-segment split over the
+    ranks: rank d owns partition_time(T, k)[d]; the boundary V (forward)
+    and dL/dV (backward) go to the neighbour rank with NCCL send/recv, M neuron chunks
+    form a wavefront (paper_2408_00280_b200/dist.py).  Strong scaling: the total work is
+    fixed.  Also measures T_c (one [N] fp32 boundary hop) and reports Eq. 5's mu."""
+    import torch
+    import torch.distributed as dist
+    import paper_2408_00280_b200 as snn
+    import snn_synth
+    from paper_2408_00280_b200 import dist as D
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    params = snn.LIFParams.paper()
+    T, N = args.T, 1 << 22
+    a, b = D.partition_time(T, world)[rank]
+    X = snn_synth.normal_tensor(1234, b - a, N, t_offset=a, device=dev)
+    G = snn_synth.normal_tensor(4321, b - a, N, t_offset=a, device=dev)
+    ts = D.TimeSplitLIF(rank, world, D.NcclTransport(), n_chunks=args.chunks if world > 1 else 1)
+    fwd_fn, bwd_fn = D.lif_segment_fns(params, spike_fmt=args.spike_fmt, save_mode=args.save_mode)
+
+    def step():
+        spikes, state, vf = ts.forward(X, fwd_fn)
+        ts.backward(G, state, bwd_fn)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    with ClockSampler(dev.index) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1)
+    # T_c: one boundary hop of [N] fp32 (rank 0 -> 1), median of 20
+    tc_ms = None
+    if world > 1:
+        buf = torch.empty(N, dtype=torch.float32, device=dev)
+        times = []
+        for _ in range(23):
+            dist.barrier()
+            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c0.record(stream)
+            if rank == 0:
+                dist.send(buf, 1)
+            elif rank == 1:
+                dist.recv(buf, 0)
+            c1.record(stream)
+            torch.cuda.synchronize(dev)
+            times.append(c0.elapsed_time(c1))
+        tc_ms = sorted(times[3:])[len(times[3:]) // 2]
+        tt = torch.tensor([ms, tc_ms if rank == 1 else 0.0], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms, tc_ms = float(tt[0].item()), float(tt[1].item())
+    value = N * T * args.steps / (ms / 1e3)
+    if rank == 0:
+        t_seg = ms / args.steps
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": max(3, args.warmup), "ms_per_step": t_seg, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": f"BASELINE configs[3]: N=2^22, T={T}, time-segment split k={world}",
+                           "chunks": ts.n_chunks, "spike_fmt": args.spike_fmt, "save_mode": args.save_mode,
+                           "parallelism": f"time-split k={world}",
+                           "l2": "no flush: per-rank inputs exceed the 126 MB L2"},
+                "tsplit": {"k": world, "T_c_ms": tc_ms,
+                           "pipeline_efficiency": D.pipeline_efficiency(ts.n_chunks, world),
+                           "mu_model_eq5": (D.speedup_mu(world * t_seg, tc_ms, world) if tc_ms else 1.0),
+                           "k_opt_eq5": (D.optimal_k(world * t_seg, tc_ms) if tc_ms else None)},
+                "gpu_launches": 2 * ts.n_chunks * args.steps, "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 # ----------------------------------------------------------------------------- arms
@@ -365,6 +503,10 @@ def run_ours(args):
                "ms_per_step": round(ems / args.e2e_steps, 3)}
         del hb
 
+    sweep = None
+    if args.sweep and args.workload == "cfg1" and rank == 0:
+        sweep = run_sweep(args, params, dev, stream)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = oracle_sample(layers, args.cpu_seconds)
@@ -385,6 +527,8 @@ def run_ours(args):
                 "dtype": "bf16" if dt0 == torch.bfloat16 else "f32", "data": "synthetic",
                 "config": cfg, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": 2 * nlaunch * args.steps, "clocks": clk.summary()}
+        if sweep is not None:
+            line["sweep"] = sweep
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -394,6 +538,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload == "cfg3":
+        run_tsplit(args)
     else:
         run_ours(args)
 

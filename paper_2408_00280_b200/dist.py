@@ -1,0 +1,225 @@
+"""Multi-GPU partitioning of the fused LIF path.
+
+Two ways the path shards on one 8xB200 box:
+
+1. Neuron / batch sharding (``shard_range``): every neuron's recurrence is autonomous
+   (PAPER.md:191-193), so rank r owns a contiguous neuron range and there is no
+   collective on the data path -- bench.py's weak-scaling runs and BASELINE configs[4].
+2. The paper's time-segment split (``TimeSplitLIF``; Fig. 1(b)):
+   rank d owns time steps [t_d, t_{d+1}) of every neuron (``partition_time``, the SPEC
+   remainder rule).  Forward: receive the post-reset V of the previous
+   segment, run the fused forward on the local segment, send the final V to d+1.
+   Backward: receive dL/dV from d+1, run the fused backward, send grad_v_init to d-1.
+   The payload is the [N] fp32 boundary state.  To give the k ranks
+   concurrent work on one layer the neurons are cut into M chunks processed
+   in the same order on every rank: rank d starts chunk m as soon as chunk m's boundary
+   arrives, a wavefront whose fill costs (k-1)/(M+k-1).
+
+Segmented execution is bitwise equal to the whole axis (the kernels carry exactly the
+state a whole run keeps in registers, tests/test_gpu_parity.py), so the
+time split is bitwise equal to k = 1.
+
+The host orchestration is transport-agnostic: ``NcclTransport`` moves device tensors
+with torch.distributed point-to-point ops (NCCL over NVLink on the GPU box);
+``HostTransport`` stages through pinned host memory with gloo, which lets the same
+protocol be tested with several processes on one GPU or on CPU (tests/test_dist.py).
+The per-segment compute is a callable, so the CPU tests can drive the protocol with the
+oracle; the product path passes the CUDA kernels (``lif_segment_forward`` / backward).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Callable, List, Optional, Sequence, Tuple
+
+import torch
+import torch.distributed as dist
+
+
+# ----------------------------------------------------------------------------- partitions
+
+def partition_time(T: int, k: int) -> List[Tuple[int, int]]:
+    """k contiguous near-equal segments of [0, T); the first T mod k get one extra step
+    (SURVEY R17).  Raises for k < 1 or k > T."""
+    if k < 1 or k > T:
+        raise ValueError(f"need 1 <= k <= T (k={k}, T={T})")
+    q, r = divmod(T, k)
+    out, t = [], 0
+    for d in range(k):
+        n = q + (1 if d < r else 0)
+        out.append((t, t + n))
+        t += n
+    return out
+
+
+def shard_range(N: int, world: int, rank: int, align: int = 1) -> Tuple[int, int]:
+    """Contiguous neuron range of `rank` (boundaries multiples of `align` except the end)."""
+    if not 0 <= rank < world:
+        raise ValueError("rank out of range")
+    units = -(-N // align)
+    q, r = divmod(units, world)
+    lo = rank * q + min(rank, r)
+    hi = lo + q + (1 if rank < r else 0)
+    return min(N, lo * align), min(N, hi * align)
+
+
+def neuron_chunks(N: int, M: int, align: int = 512) -> List[Tuple[int, int]]:
+    """M contiguous neuron chunks (boundaries on `align`, the TMA tile width)."""
+    M = max(1, min(M, -(-N // align)))
+    return [shard_range(N, M, m, align) for m in range(M)]
+
+
+# ----------------------------------------------------------------------------- Eq. 4-5
+
+def speedup_mu(Ts: float, Tc: float, k: int) -> float:
+    """Eq. 5: mu = k T_s / (k (k-1) T_c + T_s)."""
+    return k * Ts / (k * (k - 1) * Tc + Ts)
+
+
+def optimal_k(Ts: float, Tc: float) -> float:
+    """Continuous optimum of Eq. 5, k = sqrt(T_s / T_c)."""
+    return math.sqrt(Ts / Tc)
+
+
+def model_curve(ratios: Sequence[float], k_max: int):
+    """Fig. 4: rows (ratio, k, mu) with T_c = 1, T_s = ratio."""
+    return [(r, k, speedup_mu(r, 1.0, k)) for r in ratios for k in range(1, k_max + 1)]
+
+
+def pipeline_efficiency(M: int, k: int) -> float:
+    """Wavefront efficiency of M neuron chunks over k time segments."""
+    return M / (M + k - 1)
+
+
+# ----------------------------------------------------------------------------- transports
+
+class NcclTransport:
+    """Device tensors over torch.distributed P2P (NCCL on NVLink / NVSwitch)."""
+
+    def __init__(self, group=None):
+        self.group = group
+
+    def isend(self, t: torch.Tensor, dst: int):
+        return dist.isend(t, dst, group=self.group)
+
+    def irecv(self, t: torch.Tensor, src: int):
+        return dist.irecv(t, src, group=self.group)
+
+
+class HostTransport:
+    """Stages through host memory with a CPU-capable backend (gloo).  Used by the tests
+    to run the protocol with several processes on one GPU or on CPU; not a hot path."""
+
+    def __init__(self, group=None):
+        self.group = group
+
+    class _Req:
+        def __init__(self, work, dev_t=None, host_t=None):
+            self.work, self.dev_t, self.host_t = work, dev_t, host_t
+
+        def wait(self):
+            self.work.wait()
+            if self.dev_t is not None:
+                self.dev_t.copy_(self.host_t)
+
+    def isend(self, t: torch.Tensor, dst: int):
+        h = t.detach().to("cpu").contiguous()
+        return self._Req(dist.isend(h, dst, group=self.group))
+
+    def irecv(self, t: torch.Tensor, src: int):
+        if t.is_cuda:
+            h = torch.empty(t.shape, dtype=t.dtype)
+            return self._Req(dist.irecv(h, src, group=self.group), t, h)
+        return self._Req(dist.irecv(t, src, group=self.group))
+
+
+# ----------------------------------------------------------------------------- time split
+
+@dataclass
+class SegmentState:
+    """What one rank keeps between its forward and backward: per-chunk forward contexts."""
+    ctxs: list
+    chunks: List[Tuple[int, int]]
+
+
+class TimeSplitLIF:
+    """The paper's time-segment pipeline for one LIF layer.
+
+    ``rank`` (0..k-1) owns time segment ``partition_time(T, k)[rank]``; ranks are ordered
+    like time.  ``fwd_fn(x_chunk, v_in) -> (ctx, spikes_chunk, v_out)`` and
+    ``bwd_fn(g_chunk, ctx, g_in) -> (gx_chunk, g_out)`` run one segment of one neuron
+    chunk (the product passes the fused CUDA kernels, see ``lif_segment_fns``).
+    Messages per chunk per direction: exactly one per segment boundary, i.e.
+    (k-1) per chunk per layer in total.
+    """
+
+    def __init__(self, rank: int, k: int, transport, n_chunks: int = 32, align: int = 512):
+        self.rank, self.k, self.t = rank, k, transport
+        self.n_chunks, self.align = n_chunks, align
+        self.messages_sent = 0
+
+    def forward(self, x_local: torch.Tensor, fwd_fn: Callable, *, v_init: Optional[torch.Tensor] = None):
+        """x_local: [T_d, N] (this rank's time segment).  Returns (spikes_local, state,
+        v_final) -- v_final is the layer's final V on the last rank, else None."""
+        T_d, N = x_local.shape
+        chunks = neuron_chunks(N, self.n_chunks, self.align)
+        dev = x_local.device
+        prev, nxt = self.rank - 1, self.rank + 1
+        ctxs, spikes, sends, v_last = [], [], [], []
+        for (a, b) in chunks:
+            if prev >= 0:
+                v_in = torch.empty(b - a, dtype=torch.float32, device=dev)
+                self.t.irecv(v_in, prev).wait()
+            else:
+                v_in = None if v_init is None else v_init[a:b].contiguous()
+            ctx, spk, v_out = fwd_fn(x_local[:, a:b], v_in)
+            ctxs.append(ctx)
+            spikes.append(spk)
+            if nxt < self.k:
+                sends.append(self.t.isend(v_out, nxt))
+                self.messages_sent += 1
+            else:
+                v_last.append(v_out)
+        for s in sends:
+            s.wait()
+        v_final = torch.cat(v_last) if v_last else None
+        return spikes, SegmentState(ctxs, chunks), v_final
+
+    def backward(self, g_local: torch.Tensor, state: SegmentState, bwd_fn: Callable, *,
+                 grad_v_final: Optional[torch.Tensor] = None):
+        """g_local: [T_d, N] dL/dS of this segment.  Returns (gx chunks, grad_v_init) --
+        grad_v_init is the layer's dL/dV[-1] on rank 0, else None."""
+        dev = g_local.device
+        prev, nxt = self.rank - 1, self.rank + 1
+        gxs, sends, g_first = [], [], []
+        for (a, b), ctx in zip(state.chunks, state.ctxs):
+            if nxt < self.k:
+                g_in = torch.empty(b - a, dtype=torch.float32, device=dev)
+                self.t.irecv(g_in, nxt).wait()
+            else:
+                g_in = None if grad_v_final is None else grad_v_final[a:b].contiguous()
+            gx, g_out = bwd_fn(g_local[:, a:b], ctx, g_in)
+            gxs.append(gx)
+            if prev >= 0:
+                sends.append(self.t.isend(g_out, prev))
+                self.messages_sent += 1
+            else:
+                g_first.append(g_out)
+        for s in sends:
+            s.wait()
+        return gxs, (torch.cat(g_first) if g_first else None)
+
+
+def lif_segment_fns(params, *, spike_fmt: str = "u8", save_mode: str = "recompute"):
+    """(fwd_fn, bwd_fn) running one segment of one neuron chunk through the fused CUDA
+    kernels (C ABI) -- the product compute of TimeSplitLIF."""
+    from .lif import lif_backward, lif_forward
+
+    def fwd_fn(x_chunk, v_in):
+        f = lif_forward(x_chunk, params, v_init=v_in, spike_fmt=spike_fmt, save_mode=save_mode)
+        return f, f.spikes, f.v_final
+
+    def bwd_fn(g_chunk, ctx, g_in):
+        return lif_backward(g_chunk, ctx, grad_v_final=g_in)
+
+    return fwd_fn, bwd_fn

@@ -1,0 +1,76 @@
+"""Time-segment split with the CUDA kernels: k processes share cuda:0 and exchange the
+boundary V / dV through HostTransport (gloo); the result must be BITWISE equal to one
+whole-axis run (segmented execution carries exactly the register state)."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, T, N, n_chunks, dtype, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    import paper_2408_00280_b200 as snn
+    from paper_2408_00280_b200 import dist as D
+    import snn_synth
+    p = snn.LIFParams.paper()
+    a, b = D.partition_time(T, world)[rank]
+    X = snn_synth.normal_tensor(1234, b - a, N, t_offset=a, dtype=dtype, device="cuda")
+    G = snn_synth.normal_tensor(4321, b - a, N, t_offset=a, dtype=dtype, device="cuda")
+    ts = D.TimeSplitLIF(rank, world, D.HostTransport(), n_chunks=n_chunks)
+    fwd_fn, bwd_fn = D.lif_segment_fns(p)
+    spikes, state, v_final = ts.forward(X, fwd_fn)
+    gxs, gvi = ts.backward(G, state, bwd_fn)
+    torch.cuda.synchronize()
+    objs = [None] * world
+    dist.all_gather_object(objs, (a, b, torch.cat(spikes, 1).cpu(), torch.cat(gxs, 1).cpu(),
+                                  None if v_final is None else v_final.cpu(),
+                                  None if gvi is None else gvi.cpu()))
+    if rank == 0:
+        out.put(objs)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n_chunks,dtype", [(2, 4, torch.float32), (4, 3, torch.float32),
+                                                  (3, 2, torch.bfloat16)])
+def test_time_split_bitwise_equals_whole_axis(world, n_chunks, dtype):
+    import paper_2408_00280_b200 as snn
+    import snn_synth
+    T, N = 70, 4096
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    ps = [ctx.Process(target=_worker, args=(r, world, port, T, N, n_chunks, dtype, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    objs = sorted(q.get(timeout=300), key=lambda o: o[0])
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    X = snn_synth.normal_tensor(1234, T, N, dtype=dtype, device="cuda")
+    G = snn_synth.normal_tensor(4321, T, N, dtype=dtype, device="cuda")
+    f = snn.lif_forward(X, snn.LIFParams.paper())
+    gx, gvi = snn.lif_backward(G, f)
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat([o[2] for o in objs], 0), f.spikes.cpu())
+    assert torch.equal(torch.cat([o[3] for o in objs], 0), gx.cpu())
+    assert torch.equal(objs[-1][4], f.v_final.cpu())
+    assert torch.equal(objs[0][5], gvi.cpu())
