@@ -148,6 +148,22 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(s)}
 
 
+def workload_config(args, world, layers):
+    names = {"cfg1": f"BASELINE configs[1]: single LIF layer N=2^20, T={args.T}",
+             "cfg2": "BASELINE configs[2]: VGG-11 CIFAR LIF layers, B=128, T=16, bf16",
+             "cfg3": f"BASELINE configs[3]: N=2^22, T={args.T}, time-segment split k={world}",
+             "cfg4": "BASELINE configs[4]: Spiking-ResNet18 DVS LIF layers, B=256 global, T=64"}
+    ns_rank = sum(T * N for _, T, N, _ in layers)
+    return {"workload": names[args.workload], "N_per_gpu": sum(N for _, _, N, _ in layers),
+            "T": sorted({T for _, T, _, _ in layers}), "layers": len(layers),
+            "params": "paper (tau=1.25 k=0.2, V_th=0.3, V_rest=0, hard, sigmoid a=4)",
+            "spike_fmt": args.spike_fmt, "save_mode": args.save_mode,
+            "l2": ("no flush: per-step inputs (X, gS) exceed the 126 MB L2" if ns_rank * 2 > 256e6
+                   else "inputs smaller than L2"),
+            "parallelism": (f"time-split k={world}" if args.workload == "cfg3"
+                            else f"neuron-shard x{world} (weak)")}
+
+
 # ----------------------------------------------------------------------------- helpers
 
 def measured_peak():
@@ -177,34 +193,41 @@ def cpu_cores():
         return os.cpu_count()
 
 
-def oracle_sample(layers, seconds, spike_seed=(1234, 4321)):
-    """Time the fp64 C oracle (as it stands, 1 thread) on a bounded column sample of the
-    workload: the first layer's T, sampled neuron columns regenerated on the host."""
-    import numpy as np
-    import oracle
-    import snn_synth
+class OracleSample:
+    """The fp64 C oracle (as it stands, 1 thread) on a bounded column sample of the
+    workload's largest layer: `cols` stride-sampled neuron columns over all T steps,
+    regenerated on the host by snn_synth (never copied from the GPU)."""
 
-    name, T, N, dtype = max(layers, key=lambda l: l[1] * l[2])
-    f32 = lambda v: float(np.float32(v))   # the fp32 constants the kernels receive (R9)
-    op = oracle.OracleParams(tau=f32(1.25), v_th=f32(0.3), v_reset=0.0, alpha=4.0)  # PAPER.md:428-441
-    cols = 256
-    total_t, total_ns = 0.0, 0
-    while True:
+    def __init__(self, layers, cols=8192, seeds=(1234, 4321)):
+        import numpy as np
+        import oracle
+        import snn_synth
+        self.oracle = oracle
+        name, T, N, dtype = max(layers, key=lambda l: l[1] * l[2])
+        cols = min(cols, N)
         idx = np.arange(cols) * max(1, N // cols)
-        X = snn_synth.normal_columns(spike_seed[0], T, N, idx, dtype=dtype).double().numpy()
-        G = snn_synth.normal_columns(spike_seed[1], T, N, idx, dtype=dtype).double().numpy()
-        t0 = time.perf_counter()
-        ref = oracle.forward(op, X)
-        oracle.backward(op, G, ref["H"])
-        dt = time.perf_counter() - t0
-        total_t += dt
-        total_ns += T * cols
-        if total_t >= seconds or cols >= N:
-            break
-        cols = min(N, int(cols * max(2.0, min(8.0, seconds / max(dt, 1e-3) / 2))))
-    return {"value": total_ns / total_t, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{name}: T={T}, up to {cols} of {N} neuron columns (stride-sampled), "
-                      f"fwd+bwd, fp64 C oracle single-threaded, {total_t:.1f} s total"}
+        self.X = snn_synth.normal_columns(seeds[0], T, N, idx, dtype=dtype).double().numpy()
+        self.G = snn_synth.normal_columns(seeds[1], T, N, idx, dtype=dtype).double().numpy()
+        f32 = lambda v: float(np.float32(v))   # the fp32 constants the kernels receive (R9)
+        self.op = oracle.OracleParams(tau=f32(1.25), v_th=f32(0.3), v_reset=0.0, alpha=4.0)  # P:428-441
+        self.desc = f"{name}: T={T}, {cols} of {N} neuron columns (stride-sampled)"
+        self.ns = T * cols
+
+    def run(self, seconds):
+        """Repeat fwd+bwd passes over the sample for ~`seconds`; returns neuron-steps/s."""
+        total_t, total_ns = 0.0, 0
+        while total_t < seconds or total_ns == 0:
+            t0 = time.perf_counter()
+            ref = self.oracle.forward(self.op, self.X)
+            self.oracle.backward(self.op, self.G, ref["H"])
+            total_t += time.perf_counter() - t0
+            total_ns += self.ns
+        return total_ns / total_t, total_t
+
+    def baseline(self, seconds):
+        v, t = self.run(seconds)
+        return {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                "sample": f"{self.desc}, fwd+bwd, fp64 C oracle single-threaded, {t:.1f} s"}
 
 
 # ----------------------------------------------------------------------------- cfg1 sweep
@@ -347,17 +370,24 @@ def run_reference(args):
     import torch  # noqa: F401
     world = int(os.environ.get("WORLD_SIZE", args.gpus))
     layers = layer_list(args, world)
-    per_step = max(1.0, 60.0 / max(1, args.steps + args.warmup))
+    smp = OracleSample(layers, cols=2048)
+    per_step = min(2.0, max(0.2, 90.0 / max(1, args.steps + args.warmup)))
     for _ in range(args.warmup):
-        oracle_sample(layers, min(per_step, 2.0))
-    vals = [oracle_sample(layers, per_step) for _ in range(args.steps)]
-    v = sum(x["value"] for x in vals) / len(vals)
-    cb = dict(vals[-1]); cb["value"] = v
-    name, T, N, dtype = layers[0]
+        smp.run(per_step)
+    t_tot = 0.0
+    vals = []
+    for _ in range(args.steps):
+        v_, t_ = smp.run(per_step)
+        vals.append(v_); t_tot += t_
+    v = sum(vals) / len(vals)
+    cb = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+          "sample": f"{smp.desc} per step, fwd+bwd, fp64 C oracle single-threaded, "
+                    f"{args.steps} steps of ~{per_step:.1f} s"}
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": args.workload, "T": T, "N": N},
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_tot / args.steps,
+            "higher_is_better": True, "scaling": "strong" if args.workload == "cfg3" else "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(args, world, layers),
             "cpu_baseline": cb,
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -509,18 +539,10 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = oracle_sample(layers, args.cpu_seconds)
+        cpu = OracleSample(layers).baseline(args.cpu_seconds)
 
     if rank == 0:
-        cfg = {"workload": {"cfg1": f"BASELINE configs[1]: single LIF layer N=2^20, T={args.T}",
-                            "cfg2": "BASELINE configs[2]: VGG-11 CIFAR LIF layers, B=128, T=16, bf16",
-                            "cfg4": "BASELINE configs[4]: Spiking-ResNet18 DVS LIF layers, B=256 global, T=64"}[args.workload],
-               "N_per_gpu": sum(b["N"] for b in bufs), "T": sorted({b["T"] for b in bufs}),
-               "layers": len(bufs), "params": "paper (tau=1.25 k=0.2, V_th=0.3, V_rest=0, hard, sigmoid a=4)",
-               "spike_fmt": args.spike_fmt, "save_mode": args.save_mode,
-               "l2": "no flush: per-step inputs (X, gS) exceed the 126 MB L2" if ns_rank * esz > 256e6
-                     else "inputs smaller than L2 (cfg2/4 small layers): L2-resident share reported",
-               "parallelism": f"neuron-shard x{world} (weak)"}
+        cfg = workload_config(args, world, layers)
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms / args.steps,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
