@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--spike-fmt", choices=["u8", "bits", "io"], default="u8")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="launch the timed steps eagerly instead of as one captured CUDA graph")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
                     help="target CPU time of the oracle baseline sample")
@@ -245,21 +247,35 @@ def run_sweep(args, params, dev, stream):
         N = 1 << 20
         X = snn_synth.normal_tensor(1234, T, N, device=dev)
         G = snn_synth.normal_tensor(4321, T, N, device=dev)
-        tf, tb = [], []
-        for it in range(max(3, args.warmup) + 20):
+        f = snn.lif_forward(X, params, spike_fmt=args.spike_fmt, save_mode=args.save_mode,
+                            return_v_final=False)
+        gx, _ = snn.lif_backward(G, f, return_grad_v_init=False)
+        evs = []
+
+        def one(record):
             flush.zero_()
-            e0, e1, e2, e3 = (torch.cuda.Event(enable_timing=True) for _ in range(4))
-            e0.record(stream)
-            f = snn.lif_forward(X, params, spike_fmt=args.spike_fmt, save_mode=args.save_mode,
-                                return_v_final=False)
-            e1.record(stream)
+            e = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(4)] if record else None
+            if record: e[0].record()
+            snn.lif_forward(X, params, spike_fmt=args.spike_fmt, save_mode=args.save_mode,
+                            spikes=f.spikes, saved=f.saved, return_v_final=False)
+            if record: e[1].record()
             flush.zero_()
-            e2.record(stream)
-            snn.lif_backward(G, f, return_grad_v_init=False)
-            e3.record(stream)
-            torch.cuda.synchronize(dev)
-            if it >= max(3, args.warmup):
-                tf.append(e0.elapsed_time(e1)); tb.append(e2.elapsed_time(e3))
+            if record: e[2].record()
+            snn.lif_backward(G, f, grad_x=gx, return_grad_v_init=False)
+            if record:
+                e[3].record(); evs.append(e)
+
+        for _ in range(max(3, args.warmup)):
+            one(False)
+        torch.cuda.synchronize(dev)
+        g = torch.cuda.CUDAGraph()      # launched as one graph: no host gaps inside the events
+        with torch.cuda.graph(g):
+            for _ in range(20):
+                one(True)
+        g.replay()
+        torch.cuda.synchronize(dev)
+        tf = [e[0].elapsed_time(e[1]) for e in evs]
+        tb = [e[2].elapsed_time(e[3]) for e in evs]
         tf.sort(); tb.sort()
         mf, mb = tf[len(tf) // 2], tb[len(tb) // 2]
         bf, bb = bytes_per_neuron_step(4, args.spike_fmt, args.save_mode, T)
@@ -269,7 +285,7 @@ def run_sweep(args, params, dev, stream):
                     "fwd_GBps": round(bf * ns / (mf / 1e3) / 1e9, 1),
                     "bwd_GBps": round(bb * ns / (mb / 1e3) / 1e9, 1),
                     "fwdbwd_GBps": round((bf + bb) * ns / ((mf + mb) / 1e3) / 1e9, 1)})
-        del X, G, f
+        del X, G, f, gx, g
     return out
 
 
@@ -426,34 +442,51 @@ def run_ours(args):
         bufs.append(dict(name=name, T=T, N=N, X=X, G=G, saved=saved, spikes=spikes, gX=gX))
     torch.cuda.synchronize(dev)
 
-    ev = lambda: torch.cuda.Event(enable_timing=True)
+    # external=True: when captured into a CUDA graph the record becomes a real event-record
+    # node whose timestamps can be read after the replay.
+    ev = lambda: torch.cuda.Event(enable_timing=True, external=True)
     kern = {"fwd": [], "bwd": []}
 
     def step(record):
+        st = torch.cuda.current_stream(dev)   # the capture stream while building the graph
         for b in bufs:
             if record:
                 e0, e1, e2 = ev(), ev(), ev()
-                e0.record(stream)
+                e0.record(st)
             f = snn.lif_forward(b["X"], params, spike_fmt=args.spike_fmt, save_mode=args.save_mode,
                                 spikes=b["spikes"], saved=b["saved"], return_v_final=False)
             if record:
-                e1.record(stream)
+                e1.record(st)
             snn.lif_backward(b["G"], f, grad_x=b["gX"], return_grad_v_init=False)
             if record:
-                e2.record(stream)
+                e2.record(st)
                 kern["fwd"].append((e0, e1)); kern["bwd"].append((e1, e2))
 
     for _ in range(max(3, args.warmup)):
         step(False)
     torch.cuda.synchronize(dev)
+    graph = None
+    if not args.no_graph:
+        # The K timed steps (with their per-kernel events) are captured into ONE CUDA graph
+        # and launched once: the same kernels and bytes, without per-launch host overhead
+        # (ctypes + tensor-map encode ~20 us/call), which would otherwise gap small layers.
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            for _ in range(args.steps):
+                step(True)
+        graph.replay()            # warm the graph once (its events are overwritten below)
+        torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
     with ClockSampler(dev.index) as clk:
         t0, t1 = ev(), ev()
         t0.record(stream)
-        for _ in range(args.steps):
-            step(True)
+        if graph is not None:
+            graph.replay()
+        else:
+            for _ in range(args.steps):
+                step(True)
         t1.record(stream)
         torch.cuda.synchronize(dev)
     if world > 1:

@@ -41,17 +41,18 @@ int prepare(Kernel k, int threads, int smem) {
 // (device, kernel) -- the attribute must be set once per kernel, not per signature.
 int cached_occupancy(const void* k, int threads, int smem, int (*prep)(const void*, int, int));
 
-// Persistent launch: grid = min(tiles, SMs x resident CTAs); the kernel walks tiles
-// round-robin.
+// Tile launch: one CTA per tile; resident CTAs steal the tiles of pending CTAs through
+// cluster launch control (lif_tma.cuh), so the grid behaves persistently.  Short tiles
+// (few ring stages: small T) keep up to 4 steal requests in flight.
 template <typename Kernel, typename... Args>
-snn_status launch_persistent(Kernel k, int threads, int smem, int64_t ntiles, cudaStream_t st,
-                             const char* what, const Args&... args) {
-    const int occ = cached_occupancy(
-        reinterpret_cast<const void*>(k), threads, smem, [](const void* kk, int t, int sm) {
-            return prepare(reinterpret_cast<Kernel>(const_cast<void*>(kk)), t, sm);
-        });
-    const int64_t grid = std::min<int64_t>(ntiles, (int64_t)num_sms() * occ);
-    k<<<(unsigned)grid, threads, smem, st>>>(args..., ntiles);
+snn_status launch_tiles(Kernel k, int threads, int smem, int64_t ntiles, int64_t stages_per_tile,
+                        cudaStream_t st, const char* what, const Args&... args) {
+    cached_occupancy(reinterpret_cast<const void*>(k), threads, smem, [](const void* kk, int t, int sm) {
+        return prepare(reinterpret_cast<Kernel>(const_cast<void*>(kk)), t, sm);
+    });
+    if (ntiles > INT32_MAX) return fail(SNN_ERR_INVALID_VALUE, "too many tiles");
+    const int depth = (int)std::max<int64_t>(1, std::min<int64_t>(4, (8 + stages_per_tile - 1) / stages_per_tile));
+    k<<<(unsigned)ntiles, threads, smem, st>>>(args..., depth);
     return launch_status(what);
 }
 

@@ -12,8 +12,8 @@ namespace snn_host {
 template <typename IO> struct TmaCfg;
 template <> struct TmaCfg<float> {
     static constexpr int FV = 4, FN = 128, FR = 8, FS = 6;   // forward: 16 KB stages, 2 CTAs/SM
-    static constexpr int RV = 1, RN = 512, RS = 3;           // backward RECOMPUTE: 66 KB chunks
-    static constexpr int HV = 1, HN = 512, HR = 8, HS = 6;   // backward SAVE_H: 32 KB stages
+    static constexpr int RV = 2, RN = 256, RS = 3;           // backward RECOMPUTE: 66 KB chunks, FFMA2 pairs
+    static constexpr int HV = 2, HN = 256, HR = 8, HS = 6;   // backward SAVE_H: 32 KB stages
 };
 template <> struct TmaCfg<__nv_bfloat16> {
     static constexpr int FV = 8, FN = 128, FR = 8, FS = 6;
@@ -33,8 +33,8 @@ snn_status launch_forward_tma(const snn_lif_shape* s, const snn::FwdArgs& a, boo
     auto go = [&](auto sfmt, auto save, auto sft) {
         auto k = snn::lif_forward_tma_kernel<IO, C::FV, decltype(sfmt)::value, decltype(save)::value,
                                              (bool)decltype(sft)::value, C::FN, C::FR, C::FS>;
-        return launch_persistent(k, Cfg::THREADS, Cfg::SMEM, ntiles, st, "lif_forward_tma_kernel",
-                                 tmx, a);
+        return launch_tiles(k, Cfg::THREADS, Cfg::SMEM, ntiles, (s->T + C::FR - 1) / C::FR, st,
+                            "lif_forward_tma_kernel", tmx, a);
     };
     auto by_soft = [&](auto sfmt, auto save) {
         return soft ? go(sfmt, save, IC<1>{}) : go(sfmt, save, IC<0>{});
@@ -63,8 +63,8 @@ snn_status launch_backward_tma_mode(const snn_lif_shape* s, const snn::BwdArgs& 
             !encode_2d(&tmg, a.gS, sizeof(IO), s->N, s->T, s->ld, Cfg::BW, C::HR))
             return fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled failed (SAVE_H backward)");
         auto k = snn::lif_backward_saveh_tma_kernel<IO, C::HV, MODE, C::HN, C::HR, C::HS>;
-        return launch_persistent(k, Cfg::THREADS, Cfg::SMEM, (s->N + Cfg::W - 1) / Cfg::W, st,
-                                 "lif_backward_saveh_tma_kernel", tmh, tmg, a);
+        return launch_tiles(k, Cfg::THREADS, Cfg::SMEM, (s->N + Cfg::W - 1) / Cfg::W,
+                            (s->T + C::HR - 1) / C::HR, st, "lif_backward_saveh_tma_kernel", tmh, tmg, a);
     }
     using Cfg = snn::BwdRecTma<IO, C::RV, C::RN, C::RS>;
     const int64_t nch = (s->T + snn::kCkpt - 1) / snn::kCkpt;
@@ -74,8 +74,8 @@ snn_status launch_backward_tma_mode(const snn_lif_shape* s, const snn::BwdArgs& 
         !encode_2d(&tmck, a.saved, 4, s->N, nch, a.ldh, Cfg::BW, 1))
         return fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled failed (RECOMPUTE backward)");
     auto k = snn::lif_backward_recompute_tma_kernel<IO, C::RV, MODE, C::RN, C::RS>;
-    return launch_persistent(k, Cfg::THREADS, Cfg::SMEM, (s->N + Cfg::W - 1) / Cfg::W, st,
-                             "lif_backward_recompute_tma_kernel", tmx, tmg, tmck, a);
+    return launch_tiles(k, Cfg::THREADS, Cfg::SMEM, (s->N + Cfg::W - 1) / Cfg::W, nch, st,
+                        "lif_backward_recompute_tma_kernel", tmx, tmg, tmck, a);
 }
 
 template <typename IO>

@@ -84,4 +84,46 @@ __device__ __forceinline__ void tma_prefetch_desc(const void* tmap) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
 }
 
+// ---- cluster launch control (sm_100): hardware work stealing ------------------------
+// The grid has one CTA per tile.  A running CTA that finishes a tile asks the hardware to
+// cancel a CTA that has not started yet and takes over its tile (its blockIdx.x); when no
+// CTA is pending the request fails and the CTA drains.  Fast SMs therefore take more
+// tiles, which balances per-SM speed differences without a global atomic counter.
+struct ClcSlot {
+    uint4 resp;      // 16-byte try_cancel response (written by the async proxy)
+    uint64_t bar;    // completion barrier (16 transaction bytes)
+};
+
+__device__ __forceinline__ void clc_init(ClcSlot* c) { mbar_init(&c->bar, 1); }
+
+// Issue an asynchronous steal request (one thread).  Its answer is read with
+// clc_next_tile; issuing early hides the round trip behind the current tile.
+__device__ __forceinline__ void clc_request(ClcSlot* c) {
+    mbar_arrive_expect_tx(&c->bar, 16);
+    asm volatile(
+        "clusterlaunchcontrol.try_cancel.async.shared::cta.mbarrier::complete_tx::bytes.b128 [%0], [%1];"
+        ::"r"(smem_u32(&c->resp)), "r"(smem_u32(&c->bar))
+        : "memory");
+}
+
+// Waits for the outstanding request: the stolen tile (blockIdx.x of the cancelled CTA)
+// or -1 when no CTA was pending.  One thread only.  The proxy fence orders this generic
+// read of the response before the async write of the slot's next request.
+__device__ __forceinline__ int clc_next_tile(ClcSlot* c, uint32_t& phase) {
+    mbar_wait(&c->bar, phase);
+    phase ^= 1u;
+    uint32_t ok, x;
+    asm volatile(
+        "{\n\t.reg .b128 r;\n\t.reg .pred p;\n\t"
+        "ld.shared.b128 r, [%2];\n\t"
+        "clusterlaunchcontrol.query_cancel.is_canceled.pred.b128 p, r;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t"
+        "@p clusterlaunchcontrol.query_cancel.get_first_ctaid::x.b32.b128 %1, r;\n\t}"
+        : "=r"(ok), "=r"(x)
+        : "r"(smem_u32(&c->resp))
+        : "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    return ok ? (int)x : -1;
+}
+
 }  // namespace snn

@@ -109,6 +109,90 @@ __device__ __forceinline__ float lif_grad_step(const LifConsts& c, float H, floa
 }
 
 // ------------------------------------------------------------------------------------
+// Paired fp32 arithmetic (sm_100 FFMA2 / FMUL2 / FADD2: two IEEE fp32 operations per
+// instruction).  Each lane of a pair is rounded exactly like the scalar _rn intrinsic, so
+// the paired and scalar paths are bitwise identical; pairs halve the FMA-pipe instruction
+// count of the backward, which otherwise is issue-bound for bf16 io.
+struct F2 {
+    uint64_t v;
+};
+__device__ __forceinline__ F2 f2(float a, float b) {
+    F2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r.v) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ F2 f2(float a) { return f2(a, a); }
+__device__ __forceinline__ float lo(F2 a) {
+    float x, y;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(x), "=f"(y) : "l"(a.v));
+    (void)y;
+    return x;
+}
+__device__ __forceinline__ float hi(F2 a) {
+    float x, y;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(x), "=f"(y) : "l"(a.v));
+    (void)x;
+    return y;
+}
+__device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) {
+    F2 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(a.v), "l"(b.v), "l"(c.v));
+    return r;
+}
+__device__ __forceinline__ F2 mul2(F2 a, F2 b) {
+    F2 r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+    return r;
+}
+__device__ __forceinline__ F2 add2(F2 a, F2 b) {
+    F2 r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+    return r;
+}
+__device__ __forceinline__ F2 sub2(F2 a, F2 b) {
+    F2 r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+    return r;
+}
+
+// Charge for two neurons: H = k V + (s X + c0)   (same roundings as lif_charge).
+__device__ __forceinline__ F2 lif_charge2(const LifConsts& c, F2 V, F2 X) {
+    return fma2(f2(c.k), V, fma2(f2(c.s), X, f2(c.c0)));
+}
+
+// Surrogate for two neurons (same roundings as lif_surrogate, lane by lane).
+template <int SURR>
+__device__ __forceinline__ F2 lif_surrogate2(const LifConsts& c, F2 u) {
+    if constexpr (SURR == 0) {
+        const F2 t = mul2(f2(fabsf(lo(u)), fabsf(hi(u))), f2(c.ex2_scale));
+        const F2 e = f2(ex2_approx(lo(t)), ex2_approx(hi(t)));
+        const F2 q = add2(f2(1.0f), e);
+        const F2 q2 = mul2(q, q);
+        return mul2(mul2(f2(c.alpha), e), f2(rcp_approx(lo(q2)), rcp_approx(hi(q2))));
+    } else {
+        const F2 z = mul2(f2(c.atan_c), u);
+        const F2 d = fma2(z, z, f2(1.0f));
+        return mul2(f2(c.half_alpha), f2(rcp_approx(lo(d)), rcp_approx(hi(d))));
+    }
+}
+
+// One reverse step of Eq. 3 for two neurons (same roundings as lif_grad_step).
+template <int MODE>
+__device__ __forceinline__ F2 lif_grad_step2(const LifConsts& c, F2 H, F2 gS, F2 gV) {
+    using M = Mode<MODE>;
+    const F2 u = sub2(H, f2(c.v_th));
+    const F2 d = lif_surrogate2<M::SURR>(c, u);
+    F2 dVdH;
+    if constexpr (M::SOFT) {
+        dVdH = M::DETACH ? f2(1.0f) : fma2(f2(-c.v_th), d, f2(1.0f));
+    } else {
+        const F2 base = f2(lif_fire(c, lo(H)) ? 0.0f : 1.0f, lif_fire(c, hi(H)) ? 0.0f : 1.0f);
+        dVdH = M::DETACH ? base : fma2(sub2(f2(c.v_reset), H), d, base);
+    }
+    return fma2(gS, d, mul2(gV, dVdH));
+}
+
+// ------------------------------------------------------------------------------------
 // Vector I/O: VEC consecutive elements of type T as one (up to 128-bit) transaction.
 
 template <typename T, int VEC>

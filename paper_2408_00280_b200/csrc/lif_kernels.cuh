@@ -49,15 +49,51 @@ template <bool SOFT, typename IO, int VEC>
 __device__ __forceinline__ unsigned fwd_compute(const LifConsts& c, float (&V)[VEC],
                                                 const Pack<IO, VEC>& xv, Pack<float, VEC>& hp) {
     unsigned bits = 0;
+    if constexpr (VEC % 2 == 0) {   // paired FFMA2 charge, same roundings as the scalar path
 #pragma unroll
-    for (int i = 0; i < VEC; ++i) {
-        const float H = lif_charge(c, V[i], to_f32(xv.v[i]));
-        const bool S = lif_fire(c, H);
-        V[i] = lif_reset<SOFT>(c, H, S);
-        hp.v[i] = H;
-        bits |= (unsigned)S << i;
+        for (int i = 0; i < VEC; i += 2) {
+            const F2 H2 = lif_charge2(c, f2(V[i], V[i + 1]), f2(to_f32(xv.v[i]), to_f32(xv.v[i + 1])));
+            const float Ha = lo(H2), Hb = hi(H2);
+            const bool Sa = lif_fire(c, Ha), Sb = lif_fire(c, Hb);
+            V[i] = lif_reset<SOFT>(c, Ha, Sa);
+            V[i + 1] = lif_reset<SOFT>(c, Hb, Sb);
+            hp.v[i] = Ha;
+            hp.v[i + 1] = Hb;
+            bits |= ((unsigned)Sa << i) | ((unsigned)Sb << (i + 1));
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) {
+            const float H = lif_charge(c, V[i], to_f32(xv.v[i]));
+            const bool S = lif_fire(c, H);
+            V[i] = lif_reset<SOFT>(c, H, S);
+            hp.v[i] = H;
+            bits |= (unsigned)S << i;
+        }
     }
     return bits;
+}
+
+// Re-run the charge / fire / reset (no outputs) -- the RECOMPUTE backward's forward pass.
+template <bool SOFT, typename IO, int VEC>
+__device__ __forceinline__ void fwd_recompute_step(const LifConsts& c, float (&V)[VEC],
+                                                   const Pack<IO, VEC>& xv, float (&h)[VEC]) {
+    if constexpr (VEC % 2 == 0) {
+#pragma unroll
+        for (int i = 0; i < VEC; i += 2) {
+            const F2 H2 = lif_charge2(c, f2(V[i], V[i + 1]), f2(to_f32(xv.v[i]), to_f32(xv.v[i + 1])));
+            h[i] = lo(H2);
+            h[i + 1] = hi(H2);
+            V[i] = lif_reset<SOFT>(c, h[i], lif_fire(c, h[i]));
+            V[i + 1] = lif_reset<SOFT>(c, h[i + 1], lif_fire(c, h[i + 1]));
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) {
+            h[i] = lif_charge(c, V[i], to_f32(xv.v[i]));
+            V[i] = lif_reset<SOFT>(c, h[i], lif_fire(c, h[i]));
+        }
+    }
 }
 
 // Pack VEC spike bits of this lane into the warp's uint32 words and store them
@@ -121,11 +157,26 @@ template <typename IO, int VEC, int MODE>
 __device__ __forceinline__ Pack<IO, VEC> bwd_step(const LifConsts& c, float (&gV)[VEC],
                                                   const float (&h)[VEC], const Pack<IO, VEC>& gs) {
     Pack<IO, VEC> out;
+    if constexpr (VEC % 2 == 0) {   // paired FFMA2/FMUL2/FADD2, same roundings as scalar
 #pragma unroll
-    for (int i = 0; i < VEC; ++i) {
-        const float gH = lif_grad_step<MODE>(c, h[i], to_f32(gs.v[i]), gV[i]);
-        out.v[i] = from_f32<IO>(__fmul_rn(c.s, gH));
-        gV[i] = __fmul_rn(c.k, gH);
+        for (int i = 0; i < VEC; i += 2) {
+            const F2 gH = lif_grad_step2<MODE>(c, f2(h[i], h[i + 1]),
+                                               f2(to_f32(gs.v[i]), to_f32(gs.v[i + 1])),
+                                               f2(gV[i], gV[i + 1]));
+            const F2 gx = mul2(f2(c.s), gH);
+            const F2 gv = mul2(f2(c.k), gH);
+            out.v[i] = from_f32<IO>(lo(gx));
+            out.v[i + 1] = from_f32<IO>(hi(gx));
+            gV[i] = lo(gv);
+            gV[i + 1] = hi(gv);
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) {
+            const float gH = lif_grad_step<MODE>(c, h[i], to_f32(gs.v[i]), gV[i]);
+            out.v[i] = from_f32<IO>(__fmul_rn(c.s, gH));
+            gV[i] = __fmul_rn(c.k, gH);
+        }
     }
     return out;
 }
@@ -302,14 +353,7 @@ lif_backward_recompute_kernel(const BwdArgs a) {
         for (int i = 0; i < VEC; ++i) V[i] = v0.v[i];
 #pragma unroll
         for (int j = 0; j < kCkpt; ++j) {
-            if (j < len) {
-#pragma unroll
-                for (int i = 0; i < VEC; ++i) {
-                    const float H = lif_charge(c, V[i], to_f32(xb[j].v[i]));
-                    V[i] = lif_reset<Mode<MODE>::SOFT>(c, H, lif_fire(c, H));
-                    h[j][i] = H;
-                }
-            }
+            if (j < len) fwd_recompute_step<Mode<MODE>::SOFT>(c, V, xb[j], h[j]);
         }
 #pragma unroll
         for (int j = kCkpt - 1; j >= 0; --j) {

@@ -9,10 +9,11 @@
 //    time rows, 4-16 KB per instruction) into a shared-memory ring; completion is counted
 //    in bytes on an mbarrier.  The ring size, not the register file, sets the bytes in
 //    flight, and the TMA engine (not the LSU) does the address generation.
-//  * Grids are persistent (1-2 CTAs per SM) and walk W-neuron tiles round-robin: every
-//    consumer thread still owns its neurons for the whole time axis (temporal fusion,
-//    PAPER.md:220-222), but the machine is filled in one wave and the tail is one tile,
-//    instead of the partial last wave of a one-thread-per-neuron grid.
+//  * One CTA per W-neuron tile, made persistent by cluster launch control: a resident CTA
+//    that finishes a tile cancels a not-yet-started CTA and takes its tile (hardware work
+//    stealing, clusterlaunchcontrol.try_cancel).  Every consumer thread still owns its
+//    neurons for the whole time axis (temporal fusion); the machine is
+//    filled in one wave, faster SMs take more tiles, and the tail is < one tile.
 //  * Consumer warps read their neurons from the ring (conflict-free 4-16 B per lane), run
 //    the recurrence in registers and store outputs straight to HBM with coalesced
 //    streaming stores, then release the ring slot (one mbarrier arrive per warp).
@@ -24,16 +25,23 @@
 
 #include <cuda.h>
 
+#include <type_traits>
+
 #include "lif_async.cuh"
 #include "lif_kernels.cuh"
 
 namespace snn {
 
+// Shared-memory control block of a ring with S stages.
 template <int S>
 struct Barriers {
-    uint64_t full[S];
-    uint64_t empty[S];
+    uint64_t full[S];    // producer -> consumers: stage landed (TMA bytes counted)
+    uint64_t empty[S];   // consumers -> producer: stage released (one arrive per warp)
+    int tile[S];         // tile index the stage belongs to; -1 = no more work
+    ClcSlot clc[4];      // cluster-launch-control response slots (work stealing)
 };
+
+constexpr int kMaxClc = 4;
 
 constexpr int kAlignSlack = 1024;
 
@@ -52,9 +60,57 @@ __device__ __forceinline__ void init_barriers(Barriers<S>* b, uint32_t consumer_
             mbar_init(&b->full[s], 1);
             mbar_init(&b->empty[s], consumer_warps);
         }
+        for (int i = 0; i < kMaxClc; ++i) clc_init(&b->clc[i]);
         fence_mbar_init();
     }
     __syncthreads();
+}
+
+// Producer skeleton shared by the kernels.  The CTA processes its own tile (blockIdx.x)
+// first, then tiles of pending CTAs it cancels through cluster launch control.  Up to
+// `depth` (1..kMaxClc) steal requests are kept in flight, so with short tiles (few ring
+// stages, e.g. T = 8) the next tiles are known before the current one is issued; with
+// long tiles depth = 1 avoids hoarding work near the end.  Each tile is `nstages` ring
+// stages; `issue(stage_ptr, tile, j, bar)` issues the TMA loads of stage j.  Ends with a
+// tile = -1 sentinel stage; every outstanding request is drained before returning (its
+// response is an async smem write) and a late success is still processed.
+template <int S, int STAGE_BYTES, typename Issue>
+__device__ __forceinline__ void produce(unsigned char* smem, Barriers<S>* bar, int64_t nstages,
+                                        int depth, Issue issue) {
+    uint32_t k = 0;
+    uint32_t phase[kMaxClc] = {0, 0, 0, 0};
+    int issued = 0, consumed = 0;
+    bool stop = false;
+    for (int i = 0; i < depth; ++i, ++issued) clc_request(&bar->clc[i]);
+    int tile = (int)blockIdx.x;
+    while (true) {
+        for (int64_t j = 0; j < nstages; ++j, ++k) {
+            const int s = k % S;
+            mbar_wait(&bar->empty[s], ((k / S) & 1) ^ 1);
+            bar->tile[s] = tile;
+            mbar_arrive_expect_tx(&bar->full[s], STAGE_BYTES);
+            issue(smem + s * STAGE_BYTES, tile, j, &bar->full[s]);
+        }
+        tile = -1;
+        while (consumed < issued) {
+            const int i = consumed % depth;
+            const int r = clc_next_tile(&bar->clc[i], phase[i]);
+            ++consumed;
+            if (r >= 0) {
+                tile = r;
+                if (!stop) { clc_request(&bar->clc[i]); ++issued; }
+                break;
+            }
+            stop = true;   // no CTA pending: issue no more requests, drain the rest
+        }
+        if (tile < 0) {
+            const int s = k % S;
+            mbar_wait(&bar->empty[s], ((k / S) & 1) ^ 1);
+            bar->tile[s] = -1;
+            mbar_arrive(&bar->full[s]);
+            return;
+        }
+    }
 }
 
 // Element offset of neuron nt (VEC-aligned, < W) at row r of a [NB][ROWS][BW] region.
@@ -80,7 +136,7 @@ struct FwdTma {
 
 template <typename IO, int VEC, int SFMT, int SAVE, bool SOFT, int NCONS, int R, int S>
 __global__ void __launch_bounds__(NCONS + 32)
-lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const FwdArgs a, const int64_t ntiles) {
+lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const FwdArgs a, const int clc_depth) {
     using Cfg = FwdTma<IO, VEC, NCONS, R, S>;
     constexpr int W = Cfg::W, BW = Cfg::BW, NB = Cfg::NB;
     unsigned char* smem = smem_base();
@@ -95,19 +151,11 @@ lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const FwdArgs a,
         if (lane == 0) {
             tma_prefetch_desc(&tmx);
             const uint64_t pol = policy_evict_first();
-            uint32_t k = 0;
-            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-                for (int64_t rb = 0; rb < nrb; ++rb, ++k) {
-                    const int s = k % S;
-                    unsigned char* stg = smem + s * Cfg::STAGE_BYTES;
-                    mbar_wait(&bar->empty[s], ((k / S) & 1) ^ 1);
-                    mbar_arrive_expect_tx(&bar->full[s], Cfg::STAGE_BYTES);
+            produce<S, Cfg::STAGE_BYTES>(smem, bar, nrb, clc_depth, [&](unsigned char* stg, int tile, int64_t rb, uint64_t* fb) {
 #pragma unroll
-                    for (int b = 0; b < NB; ++b)
-                        tma_load_2d(stg + b * Cfg::BOX_BYTES, &tmx, (int)(tile * W + b * BW),
-                                    (int)(rb * R), &bar->full[s], pol);
-                }
-            }
+                for (int b = 0; b < NB; ++b)
+                    tma_load_2d(stg + b * Cfg::BOX_BYTES, &tmx, tile * W + b * BW, (int)(rb * R), fb, pol);
+            });
         }
         return;
     }
@@ -119,10 +167,15 @@ lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const FwdArgs a,
     const int xoff = box_off<VEC, BW, R>(ct * VEC, 0);
     const int64_t spk_step = spike_row_bytes<IO, SFMT>(a);
     uint32_t k = 0;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int64_t g = tile * NCONS + ct;
+    while (true) {
+        int s = k % S;
+        mbar_wait(&bar->full[s], (k / S) & 1);
+        const int tile = bar->tile[s];
+        if (tile < 0) break;
+        const int64_t g = (int64_t)tile * NCONS + ct;
         const int64_t n0 = g * VEC;
         const int nvalid = n0 < N ? VEC : 0;
+        const bool tile_full = (int64_t)(tile + 1) * W <= N;   // uniform across the CTA
         float V[VEC];
         if (a.v_init != nullptr && nvalid > 0) {
             const Pack<float, VEC> v0 = ld_stream<float, VEC>(a.v_init + n0);
@@ -135,18 +188,23 @@ lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const FwdArgs a,
         unsigned char* spk_row = reinterpret_cast<unsigned char*>(a.spikes);
         float* h_row = a.saved + n0;   // SAVE_H: advanced one row per step
         for (int64_t rb = 0; rb < nrb; ++rb, ++k) {
+            if (rb > 0) {
+                s = k % S;
+                mbar_wait(&bar->full[s], (k / S) & 1);
+            }
             const int rows = (int)min((int64_t)R, T - rb * R);
-            const int s = k % S;
             const IO* xs = reinterpret_cast<const IO*>(smem + s * Cfg::STAGE_BYTES) + xoff;
-            mbar_wait(&bar->full[s], (k / S) & 1);
+            auto rowloop = [&](auto full) {
+            constexpr bool F = decltype(full)::value;
+            const int nv = F ? VEC : nvalid;
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-                if (r < rows) {
+                if (F || r < rows) {
                     const Pack<IO, VEC> xv = *reinterpret_cast<const Pack<IO, VEC>*>(xs + r * BW);
                     if constexpr (SAVE == SAVE_RECOMPUTE) {
                         // checkpoint the V entering step t when t % kCkpt == 0
                         const int64_t t = rb * R + r;
-                        if ((t % kCkpt) == 0 && nvalid > 0) {
+                        if ((t % kCkpt) == 0 && nv > 0) {
                             Pack<float, VEC> ck;
 #pragma unroll
                             for (int i = 0; i < VEC; ++i) ck.v[i] = V[i];
@@ -156,13 +214,15 @@ lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const FwdArgs a,
                     Pack<float, VEC> hp;
                     const unsigned bits = fwd_compute<SOFT>(c, V, xv, hp);
                     if constexpr (SAVE == SAVE_H) {
-                        if (nvalid > 0) st_stream<float, VEC>(h_row, hp);
+                        if (nv > 0) st_stream<float, VEC>(h_row, hp);
                         h_row += a.ldh;
                     }
-                    store_spikes<IO, VEC, SFMT>(spk_row, g, n0, bits, nvalid, a.nwords);
+                    store_spikes<IO, VEC, SFMT>(spk_row, g, n0, bits, nv, a.nwords);
                     spk_row += spk_step;
                 }
             }
+            };
+            if (rows == R && tile_full) rowloop(std::true_type{}); else rowloop(std::false_type{});
             __syncwarp();
             if (lane == 0) mbar_arrive(&bar->empty[s]);
         }
@@ -194,9 +254,8 @@ struct BwdRecTma {
     static_assert(W % BW == 0 && BW % VEC == 0 && STAGE_BYTES % 128 == 0, "tile geometry");
 };
 
-// Reverse walk over rows [0, ROWS) of one chunk (compile-time ROWS for the common full
-// chunk: no per-step guards).  h = recomputed H; gsm = gS rows in smem; gxp = gX row of
-// the chunk's LAST row, walked backwards by ld.
+// Reverse walk over rows [0, rows) of one chunk.  h = recomputed H; gsm = gS rows in smem;
+// gxp = gX row of the chunk's LAST row, walked backwards by ld.
 template <typename IO, int VEC, int MODE, int BW, int ROWS_MAX>
 __device__ __forceinline__ void bwd_chunk(const LifConsts& c, float (&gV)[VEC],
                                           const float (&h)[ROWS_MAX][VEC], const IO* gsm,
@@ -212,12 +271,24 @@ __device__ __forceinline__ void bwd_chunk(const LifConsts& c, float (&gV)[VEC],
     }
 }
 
+template <typename IO, int VEC, int MODE, int BW>
+__device__ __forceinline__ void recompute_chunk(const LifConsts& c, float (&V)[VEC],
+                                                float (&h)[kCkpt][VEC], const IO* xs, int rows) {
+#pragma unroll
+    for (int j = 0; j < kCkpt; ++j) {
+        if (j < rows) {
+            const Pack<IO, VEC> xv = *reinterpret_cast<const Pack<IO, VEC>*>(xs + j * BW);
+            fwd_recompute_step<Mode<MODE>::SOFT>(c, V, xv, h[j]);
+        }
+    }
+}
+
 template <typename IO, int VEC, int MODE, int NCONS, int S>
 __global__ void __launch_bounds__(NCONS + 32)
 lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
                                   const __grid_constant__ CUtensorMap tmg,
                                   const __grid_constant__ CUtensorMap tmck, const BwdArgs a,
-                                  const int64_t ntiles) {
+                                  const int clc_depth) {
     using Cfg = BwdRecTma<IO, VEC, NCONS, S>;
     constexpr int W = Cfg::W, BW = Cfg::BW, NB = Cfg::NB;
     unsigned char* smem = smem_base();
@@ -228,29 +299,20 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
     const int64_t nch = (T + kCkpt - 1) / kCkpt;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-    if (warp == 0) {  // ---------------- producer
+    if (warp == 0) {  // ---------------- producer: chunks of a tile, last first
         if (lane == 0) {
             tma_prefetch_desc(&tmx); tma_prefetch_desc(&tmg); tma_prefetch_desc(&tmck);
             const uint64_t pol = policy_evict_first();
-            uint32_t k = 0;
-            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-                for (int64_t ch = nch - 1; ch >= 0; --ch, ++k) {
-                    const int s = k % S;
-                    unsigned char* stg = smem + s * Cfg::STAGE_BYTES;
-                    mbar_wait(&bar->empty[s], ((k / S) & 1) ^ 1);
-                    mbar_arrive_expect_tx(&bar->full[s], Cfg::STAGE_BYTES);
+            produce<S, Cfg::STAGE_BYTES>(smem, bar, nch, clc_depth, [&](unsigned char* stg, int tile, int64_t j, uint64_t* fb) {
+                const int ch = (int)(nch - 1 - j);
 #pragma unroll
-                    for (int b = 0; b < NB; ++b) {
-                        const int c0 = (int)(tile * W + b * BW);
-                        tma_load_2d(stg + Cfg::CK_OFF + b * Cfg::CK_BOX_BYTES, &tmck, c0, (int)ch,
-                                    &bar->full[s], pol);
-                        tma_load_2d(stg + Cfg::X_OFF + b * Cfg::BOX_BYTES, &tmx, c0, (int)(ch * kCkpt),
-                                    &bar->full[s], pol);
-                        tma_load_2d(stg + Cfg::G_OFF + b * Cfg::BOX_BYTES, &tmg, c0, (int)(ch * kCkpt),
-                                    &bar->full[s], pol);
-                    }
+                for (int b = 0; b < NB; ++b) {
+                    const int c0 = tile * W + b * BW;
+                    tma_load_2d(stg + Cfg::CK_OFF + b * Cfg::CK_BOX_BYTES, &tmck, c0, ch, fb, pol);
+                    tma_load_2d(stg + Cfg::X_OFF + b * Cfg::BOX_BYTES, &tmx, c0, ch * kCkpt, fb, pol);
+                    tma_load_2d(stg + Cfg::G_OFF + b * Cfg::BOX_BYTES, &tmg, c0, ch * kCkpt, fb, pol);
                 }
-            }
+            });
         }
         return;
     }
@@ -264,9 +326,14 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
     const int ckoff = box_off<VEC, BW, 1>(nt, 0);
     IO* gx = reinterpret_cast<IO*>(a.gX);
     uint32_t k = 0;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int64_t n0 = tile * W + nt;
+    while (true) {
+        int s = k % S;
+        mbar_wait(&bar->full[s], (k / S) & 1);
+        const int tile = bar->tile[s];
+        if (tile < 0) break;
+        const int64_t n0 = (int64_t)tile * W + nt;
         const bool valid = n0 < N;   // N % VEC == 0 on this path
+        const bool tile_full = (int64_t)(tile + 1) * W <= N;   // uniform across the CTA
         float gV[VEC];
         if (a.grad_v_final != nullptr && valid) {
             const Pack<float, VEC> g0 = ld_stream<float, VEC>(a.grad_v_final + n0);
@@ -277,13 +344,15 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
             for (int i = 0; i < VEC; ++i) gV[i] = 0.0f;
         }
         for (int64_t ch = nch - 1; ch >= 0; --ch, ++k) {
+            if (ch < nch - 1) {
+                s = k % S;
+                mbar_wait(&bar->full[s], (k / S) & 1);
+            }
             const int64_t t0 = ch * kCkpt;
             const int rows = (int)min((int64_t)kCkpt, T - t0);
-            const int s = k % S;
             const unsigned char* stg = smem + s * Cfg::STAGE_BYTES;
             const IO* xs = reinterpret_cast<const IO*>(stg + Cfg::X_OFF) + roff;
             const IO* gsm = reinterpret_cast<const IO*>(stg + Cfg::G_OFF) + roff;
-            mbar_wait(&bar->full[s], (k / S) & 1);
             const Pack<float, VEC> v0 =
                 *reinterpret_cast<const Pack<float, VEC>*>(reinterpret_cast<const float*>(stg + Cfg::CK_OFF) + ckoff);
             float V[VEC];
@@ -291,31 +360,11 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
             for (int i = 0; i < VEC; ++i) V[i] = v0.v[i];
             float h[kCkpt][VEC];
             IO* gxp = gx + (t0 + rows - 1) * ld + n0;
-            if (rows == kCkpt) {
-#pragma unroll
-                for (int j = 0; j < kCkpt; ++j) {
-                    const Pack<IO, VEC> xv = *reinterpret_cast<const Pack<IO, VEC>*>(xs + j * BW);
-#pragma unroll
-                    for (int i = 0; i < VEC; ++i) {
-                        const float H = lif_charge(c, V[i], to_f32(xv.v[i]));
-                        V[i] = lif_reset<Mode<MODE>::SOFT>(c, H, lif_fire(c, H));
-                        h[j][i] = H;
-                    }
-                }
-                bwd_chunk<IO, VEC, MODE, BW, kCkpt>(c, gV, h, gsm, gxp, ld, kCkpt, valid);
+            if (rows == kCkpt && tile_full) {   // full chunk of a full tile: guard-free code
+                recompute_chunk<IO, VEC, MODE, BW>(c, V, h, xs, kCkpt);
+                bwd_chunk<IO, VEC, MODE, BW, kCkpt>(c, gV, h, gsm, gxp, ld, kCkpt, true);
             } else {
-#pragma unroll
-                for (int j = 0; j < kCkpt; ++j) {
-                    if (j < rows) {
-                        const Pack<IO, VEC> xv = *reinterpret_cast<const Pack<IO, VEC>*>(xs + j * BW);
-#pragma unroll
-                        for (int i = 0; i < VEC; ++i) {
-                            const float H = lif_charge(c, V[i], to_f32(xv.v[i]));
-                            V[i] = lif_reset<Mode<MODE>::SOFT>(c, H, lif_fire(c, H));
-                            h[j][i] = H;
-                        }
-                    }
-                }
+                recompute_chunk<IO, VEC, MODE, BW>(c, V, h, xs, rows);
                 bwd_chunk<IO, VEC, MODE, BW, kCkpt>(c, gV, h, gsm, gxp, ld, rows, valid);
             }
             __syncwarp();
@@ -350,7 +399,7 @@ template <typename IO, int VEC, int MODE, int NCONS, int R, int S>
 __global__ void __launch_bounds__(NCONS + 32)
 lif_backward_saveh_tma_kernel(const __grid_constant__ CUtensorMap tmh,
                               const __grid_constant__ CUtensorMap tmg, const BwdArgs a,
-                              const int64_t ntiles) {
+                              const int clc_depth) {
     using Cfg = BwdHTma<IO, VEC, NCONS, R, S>;
     constexpr int W = Cfg::W, BW = Cfg::BW, NB = Cfg::NB;
     unsigned char* smem = smem_base();
@@ -365,22 +414,15 @@ lif_backward_saveh_tma_kernel(const __grid_constant__ CUtensorMap tmh,
         if (lane == 0) {
             tma_prefetch_desc(&tmh); tma_prefetch_desc(&tmg);
             const uint64_t pol = policy_evict_first();
-            uint32_t k = 0;
-            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-                for (int64_t rb = nrb - 1; rb >= 0; --rb, ++k) {
-                    const int s = k % S;
-                    unsigned char* stg = smem + s * Cfg::STAGE_BYTES;
-                    mbar_wait(&bar->empty[s], ((k / S) & 1) ^ 1);
-                    mbar_arrive_expect_tx(&bar->full[s], Cfg::STAGE_BYTES);
+            produce<S, Cfg::STAGE_BYTES>(smem, bar, nrb, clc_depth, [&](unsigned char* stg, int tile, int64_t j, uint64_t* fb) {
+                const int rb = (int)(nrb - 1 - j);
 #pragma unroll
-                    for (int b = 0; b < NB; ++b) {
-                        const int c0 = (int)(tile * W + b * BW);
-                        tma_load_2d(stg + b * Cfg::HBOX, &tmh, c0, (int)(rb * R), &bar->full[s], pol);
-                        tma_load_2d(stg + Cfg::G_OFF + b * Cfg::GBOX, &tmg, c0, (int)(rb * R),
-                                    &bar->full[s], pol);
-                    }
+                for (int b = 0; b < NB; ++b) {
+                    const int c0 = tile * W + b * BW;
+                    tma_load_2d(stg + b * Cfg::HBOX, &tmh, c0, rb * R, fb, pol);
+                    tma_load_2d(stg + Cfg::G_OFF + b * Cfg::GBOX, &tmg, c0, rb * R, fb, pol);
                 }
-            }
+            });
         }
         return;
     }
@@ -392,9 +434,14 @@ lif_backward_saveh_tma_kernel(const __grid_constant__ CUtensorMap tmh,
     const int roff = box_off<VEC, BW, R>(nt, 0);
     IO* gx = reinterpret_cast<IO*>(a.gX);
     uint32_t k = 0;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int64_t n0 = tile * W + nt;
+    while (true) {
+        int s = k % S;
+        mbar_wait(&bar->full[s], (k / S) & 1);
+        const int tile = bar->tile[s];
+        if (tile < 0) break;
+        const int64_t n0 = (int64_t)tile * W + nt;
         const bool valid = n0 < N;
+        const bool tile_full = (int64_t)(tile + 1) * W <= N;   // uniform across the CTA
         float gV[VEC];
         if (a.grad_v_final != nullptr && valid) {
             const Pack<float, VEC> g0 = ld_stream<float, VEC>(a.grad_v_final + n0);
@@ -405,23 +452,28 @@ lif_backward_saveh_tma_kernel(const __grid_constant__ CUtensorMap tmh,
             for (int i = 0; i < VEC; ++i) gV[i] = 0.0f;
         }
         for (int64_t rb = nrb - 1; rb >= 0; --rb, ++k) {
+            if (rb < nrb - 1) {
+                s = k % S;
+                mbar_wait(&bar->full[s], (k / S) & 1);
+            }
             const int rows = (int)min((int64_t)R, T - rb * R);
-            const int s = k % S;
             const unsigned char* stg = smem + s * Cfg::STAGE_BYTES;
             const float* hs = reinterpret_cast<const float*>(stg) + roff;
             const IO* gsm = reinterpret_cast<const IO*>(stg + Cfg::G_OFF) + roff;
             IO* gxp = gx + (rb * R + rows - 1) * ld + n0;
-            mbar_wait(&bar->full[s], (k / S) & 1);
+            auto walk = [&](auto full) {
 #pragma unroll
-            for (int r = R - 1; r >= 0; --r) {
-                if (r < rows) {
-                    const Pack<float, VEC> hv = *reinterpret_cast<const Pack<float, VEC>*>(hs + r * BW);
-                    const Pack<IO, VEC> gv = *reinterpret_cast<const Pack<IO, VEC>*>(gsm + r * BW);
-                    const Pack<IO, VEC> out = bwd_step<IO, VEC, MODE>(c, gV, hv.v, gv);
-                    if (valid) st_stream<IO, VEC>(gxp, out);
-                    gxp -= ld;
+                for (int r = R - 1; r >= 0; --r) {
+                    if (decltype(full)::value || r < rows) {
+                        const Pack<float, VEC> hv = *reinterpret_cast<const Pack<float, VEC>*>(hs + r * BW);
+                        const Pack<IO, VEC> gv = *reinterpret_cast<const Pack<IO, VEC>*>(gsm + r * BW);
+                        const Pack<IO, VEC> out = bwd_step<IO, VEC, MODE>(c, gV, hv.v, gv);
+                        if (decltype(full)::value || valid) st_stream<IO, VEC>(gxp, out);
+                        gxp -= ld;
+                    }
                 }
-            }
+            };
+            if (rows == R && tile_full) walk(std::true_type{}); else walk(std::false_type{});
             __syncwarp();
             if (lane == 0) mbar_arrive(&bar->empty[s]);
         }

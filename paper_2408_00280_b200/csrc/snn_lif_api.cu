@@ -92,7 +92,7 @@ int cached_occupancy(const void* k, int threads, int smem, int (*prep)(const voi
 }
 
 int tma_vec_forward(int io_dtype) { return io_dtype == SNN_BF16 ? 8 : 4; }
-int tma_vec_backward(int io_dtype) { return io_dtype == SNN_BF16 ? 2 : 1; }
+int tma_vec_backward(int io_dtype) { return 2; }
 
 }  // namespace snn_host
 
