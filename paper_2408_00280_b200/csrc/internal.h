@@ -52,7 +52,18 @@ snn_status launch_tiles(Kernel k, int threads, int smem, int64_t ntiles, int64_t
     });
     if (ntiles > INT32_MAX) return fail(SNN_ERR_INVALID_VALUE, "too many tiles");
     const int depth = (int)std::max<int64_t>(1, std::min<int64_t>(4, (8 + stages_per_tile - 1) / stages_per_tile));
-    k<<<(unsigned)ntiles, threads, smem, st>>>(args..., depth);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)ntiles);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL (lif_async.cuh)
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, k, args..., depth);
+    if (e != cudaSuccess) return fail(SNN_ERR_CUDA, "%s launch failed: %s", what, cudaGetErrorString(e));
     return launch_status(what);
 }
 

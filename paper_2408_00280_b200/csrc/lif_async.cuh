@@ -84,6 +84,17 @@ __device__ __forceinline__ void tma_prefetch_desc(const void* tmap) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
 }
 
+// ---- programmatic dependent launch ---------------------------------------------------
+// Kernels are launched with cudaLaunchAttributeProgrammaticStreamSerialization: a kernel
+// may start (barrier init, descriptor prefetch) while its predecessor drains, and blocks
+// in pdl_wait() -- before touching global memory -- until the predecessor has completed
+// and flushed.  A CTA calls pdl_trigger() once no tile is left to steal, so the successor
+// fills SMs freed during this kernel's tail.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ---- cluster launch control (sm_100): hardware work stealing ------------------------
 // The grid has one CTA per tile.  A running CTA that finishes a tile asks the hardware to
 // cancel a CTA that has not started yet and takes over its tile (its blockIdx.x); when no

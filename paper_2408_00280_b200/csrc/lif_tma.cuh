@@ -104,6 +104,7 @@ __device__ __forceinline__ void produce(unsigned char* smem, Barriers<S>* bar, i
             stop = true;   // no CTA pending: issue no more requests, drain the rest
         }
         if (tile < 0) {
+            pdl_trigger();   // nothing left to steal: let the next kernel start filling SMs
             const int s = k % S;
             mbar_wait(&bar->empty[s], ((k / S) & 1) ^ 1);
             bar->tile[s] = -1;
@@ -142,6 +143,7 @@ lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const FwdArgs a,
     unsigned char* smem = smem_base();
     auto* bar = reinterpret_cast<Barriers<S>*>(smem + S * Cfg::STAGE_BYTES);
     init_barriers<S>(bar, NCONS / 32);
+    pdl_wait();   // predecessor complete before any global-memory access
 
     const int64_t T = a.T, N = a.N;
     const int64_t nrb = (T + R - 1) / R;
@@ -294,6 +296,7 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
     unsigned char* smem = smem_base();
     auto* bar = reinterpret_cast<Barriers<S>*>(smem + S * Cfg::STAGE_BYTES);
     init_barriers<S>(bar, NCONS / 32);
+    pdl_wait();   // predecessor complete before any global-memory access
 
     const int64_t T = a.T, N = a.N, ld = a.ld;
     const int64_t nch = (T + kCkpt - 1) / kCkpt;
@@ -405,6 +408,7 @@ lif_backward_saveh_tma_kernel(const __grid_constant__ CUtensorMap tmh,
     unsigned char* smem = smem_base();
     auto* bar = reinterpret_cast<Barriers<S>*>(smem + S * Cfg::STAGE_BYTES);
     init_barriers<S>(bar, NCONS / 32);
+    pdl_wait();   // predecessor complete before any global-memory access
 
     const int64_t T = a.T, N = a.N, ld = a.ld;
     const int64_t nrb = (T + R - 1) / R;

@@ -3,7 +3,6 @@ partition rule, Eq. 5, neuron shards, the time-segment pipeline protocol (driven
 oracle as the per-segment compute) and the max-over-ranks timing reduction."""
 import math
 import os
-import socket
 
 import numpy as np
 import pytest
@@ -91,12 +90,12 @@ def test_pipeline_efficiency():
 
 # ----------------------------------------------------------------------------- multi-process
 
-def _free_port():
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    p = s.getsockname()[1]
-    s.close()
-    return p
+def _rendezvous_file():
+    import tempfile
+    fd, path = tempfile.mkstemp(prefix="snn_pg_")
+    os.close(fd)
+    os.remove(path)   # the FileStore creates it; a fresh name per test
+    return path
 
 
 def _oracle_fns(op):
@@ -115,8 +114,8 @@ def _oracle_fns(op):
 
 
 def _tsplit_worker(rank, world, port, T, N, n_chunks, out):
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # file-based rendezvous: no TCP port to race for between consecutive tests
+    dist.init_process_group("gloo", init_method=f"file://{port}", rank=rank, world_size=world)
     import oracle
     import snn_synth
     # v carries are exchanged as fp32 (the product's boundary payload); the
@@ -154,7 +153,7 @@ def test_time_split_over_gloo_matches_whole_axis(world, n_chunks):
     T, N = 23, 64
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = _free_port()
+    port = _rendezvous_file()
     procs = [ctx.Process(target=_tsplit_worker, args=(r, world, port, T, N, n_chunks, q))
              for r in range(world)]
     for p in procs:

@@ -2,7 +2,6 @@
 boundary V / dV through HostTransport (gloo); the result must be BITWISE equal to one
 whole-axis run (segmented execution carries exactly the register state)."""
 import os
-import socket
 
 import pytest
 import torch
@@ -15,17 +14,17 @@ if not torch.cuda.is_available():
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
 
-def _port():
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    p = s.getsockname()[1]
-    s.close()
-    return p
+def _rendezvous_file():
+    import tempfile
+    fd, path = tempfile.mkstemp(prefix="snn_pg_")
+    os.close(fd)
+    os.remove(path)   # the FileStore creates it; a fresh name per test
+    return path
 
 
 def _worker(rank, world, port, T, N, n_chunks, dtype, out):
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # file-based rendezvous: no TCP port to race for between consecutive tests
+    dist.init_process_group("gloo", init_method=f"file://{port}", rank=rank, world_size=world)
     torch.cuda.set_device(0)
     import paper_2408_00280_b200 as snn
     from paper_2408_00280_b200 import dist as D
@@ -57,7 +56,7 @@ def test_time_split_bitwise_equals_whole_axis(world, n_chunks, dtype):
     T, N = 70, 4096
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = _port()
+    port = _rendezvous_file()
     ps = [ctx.Process(target=_worker, args=(r, world, port, T, N, n_chunks, dtype, q)) for r in range(world)]
     for p in ps:
         p.start()
