@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--sweep", action="store_true",
                     help="cfg1: also time T in {8,32,128,512} (L2 flushed before every launch)")
     ap.add_argument("--chunks", type=int, default=32, help="cfg3 neuron chunks of the wavefront")
+    ap.add_argument("--serial", action="store_true",
+                    help="with --sweep: also time the paper's serial baselines (Fig. 3 / Fig. 5)")
     ap.add_argument("--save-mode", choices=["recompute", "h"], default="recompute")
     ap.add_argument("--spike-fmt", choices=["u8", "bits", "io"], default="u8")
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -278,6 +280,9 @@ def run_sweep(args, params, dev, stream):
         tb = [e[2].elapsed_time(e[3]) for e in evs]
         tf.sort(); tb.sort()
         mf, mb = tf[len(tf) // 2], tb[len(tb) // 2]
+        serial = None
+        if args.serial:
+            serial = time_serial_baselines(params, X, G, dev, flush)
         bf, bb = bytes_per_neuron_step(4, args.spike_fmt, args.save_mode, T)
         ns = N * T
         out.append({"T": T, "fwd_ms": round(mf, 4), "bwd_ms": round(mb, 4),
@@ -285,7 +290,55 @@ def run_sweep(args, params, dev, stream):
                     "fwd_GBps": round(bf * ns / (mf / 1e3) / 1e9, 1),
                     "bwd_GBps": round(bb * ns / (mb / 1e3) / 1e9, 1),
                     "fwdbwd_GBps": round((bf + bb) * ns / ((mf + mb) / 1e3) / 1e9, 1)})
+        if serial is not None:
+            out[-1]["serial"] = serial
+            out[-1]["speedup_vs_serial_cuda"] = round(serial["cuda_ms"] / (mf + mb), 2)
+            out[-1]["speedup_vs_serial_torch"] = round(serial["torch_ms"] / (mf + mb), 2)
         del X, G, f, gx, g
+    return out
+
+
+def time_serial_baselines(params, X, G, dev, flush, reps=5):
+    """The paper's self-built baselines of Fig. 5: "Serial (CUDA)" -- one
+    launch per time step through the C ABI (snn_lif_serial_*_step), state through HBM --
+    and "Serial (PyTorch)" -- the same per-step LIF written with eager torch ops.  Both run
+    fwd+bwd over the same inputs; median of `reps`, L2 flushed before each."""
+    import torch
+    from paper_2408_00280_b200.lif import lif_serial
+    T, N = X.shape
+    k = 1.0 - 1.0 / params.tau
+    vth, vr = params.v_th, params.v_reset
+
+    def torch_serial():
+        V = torch.full((N,), vr, device=dev)
+        Hs = []
+        for t in range(T):
+            H = k * V + X[t] + vr / params.tau
+            S = (H >= vth).to(X.dtype)
+            V = torch.where(S > 0, torch.full_like(H, vr), H)
+            Hs.append(H)
+        gV = torch.zeros(N, device=dev)
+        for t in range(T - 1, -1, -1):
+            H = Hs[t]
+            e = torch.exp(-params.alpha * (H - vth).abs())
+            d = params.alpha * e / (1 + e) ** 2
+            S = (H >= vth).to(H.dtype)
+            gH = G[t] * d + gV * ((1 - S) + (vr - H) * d)
+            gV = k * gH
+
+    out = {}
+    for name, fn in (("cuda_ms", lambda: lif_serial(X, G, params)), ("torch_ms", torch_serial)):
+        fn()
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize(dev)
+            ts.append(e0.elapsed_time(e1))
+        out[name] = round(sorted(ts)[reps // 2], 4)
     return out
 
 

@@ -157,6 +157,27 @@ snn_status snn_lif_backward(const snn_lif_params* params, const snn_lif_shape* s
                             const void* saved, const float* grad_v_final, void* grad_x,
                             float* grad_v_init, void* stream);
 
+/* ---- Baseline, not the method: the paper's "Serial (CUDA)" training of Fig. 3
+ * (Fig. 5 caption PAPER.md:419) -- ONE time step per call, the membrane
+ * state round-tripped through caller memory between steps, for the fused-vs-serial
+ * comparison (bench.py --serial).  Same per-step arithmetic as the fused kernels, so T
+ * chained calls are bitwise equal to one snn_lif_forward / snn_lif_backward (SAVE_H).
+ *   x_t        [N] io dtype   input currents of step t                       (read)
+ *   v          [N] fp32       in: V[t-1] (post-reset), out: V[t]              (read/write)
+ *   spikes_t   [N] uint8      S[t]                                             (write)
+ *   h_t        [N] fp32       H[t] (pre-reset; what the serial backward reads) (write)
+ * Backward step (call for t = T-1 .. 0):
+ *   grad_spikes_t [N] io dtype, h_t [N] fp32                                   (read)
+ *   grad_v     [N] fp32       in: dL/dV[t], out: dL/dV[t-1]                    (read/write)
+ *   grad_x_t   [N] io dtype   dL/dX[t]                                         (write)
+ * Contiguous [N] vectors; errors as for snn_lif_forward. */
+snn_status snn_lif_serial_forward_step(const snn_lif_params* params, int io_dtype, int64_t N,
+                                       const void* x_t, float* v, uint8_t* spikes_t, float* h_t,
+                                       void* stream);
+snn_status snn_lif_serial_backward_step(const snn_lif_params* params, int io_dtype, int64_t N,
+                                        const void* grad_spikes_t, const float* h_t, float* grad_v,
+                                        void* grad_x_t, void* stream);
+
 /* Status name, e.g. "SNN_ERR_INVALID_VALUE" (static storage). */
 const char* snn_status_string(snn_status status);
 

@@ -26,7 +26,8 @@ SNN_LIF_CKPT_INTERVAL = 16
 # Every symbol include/snn_lif.h declares (checked by tests/test_abi.py).
 EXPORTED_SYMBOLS = (
     "snn_lif_saved_bytes", "snn_lif_forward", "snn_lif_backward", "snn_status_string",
-    "snn_last_error_message", "snn_lif_abi_version",
+    "snn_last_error_message", "snn_lif_abi_version", "snn_lif_serial_forward_step",
+    "snn_lif_serial_backward_step",
 )
 
 
@@ -64,6 +65,11 @@ def _load() -> ctypes.CDLL:
     lib.snn_last_error_message.restype = ctypes.c_char_p
     lib.snn_lif_abi_version.argtypes = []
     lib.snn_lif_abi_version.restype = ctypes.c_int
+    i64 = ctypes.c_int64
+    lib.snn_lif_serial_forward_step.argtypes = [P, ctypes.c_int, i64, vp, vp, vp, vp, vp]
+    lib.snn_lif_serial_forward_step.restype = ctypes.c_int
+    lib.snn_lif_serial_backward_step.argtypes = [P, ctypes.c_int, i64, vp, vp, vp, vp, vp]
+    lib.snn_lif_serial_backward_step.restype = ctypes.c_int
     return lib
 
 
@@ -97,3 +103,14 @@ def snn_lif_backward(params, shape, grad_spikes, x, v_init, saved, grad_v_final,
                      grad_v_init, stream) -> None:
     check(lib.snn_lif_backward(ctypes.byref(params), ctypes.byref(shape), grad_spikes, x, v_init,
                                saved, grad_v_final, grad_x, grad_v_init, stream))
+
+
+def snn_lif_serial_forward_step(params, io_dtype, N, x_t, v, spikes_t, h_t, stream) -> None:
+    check(lib.snn_lif_serial_forward_step(ctypes.byref(params), io_dtype, N, x_t, v, spikes_t, h_t,
+                                          stream))
+
+
+def snn_lif_serial_backward_step(params, io_dtype, N, grad_spikes_t, h_t, grad_v, grad_x_t,
+                                 stream) -> None:
+    check(lib.snn_lif_serial_backward_step(ctypes.byref(params), io_dtype, N, grad_spikes_t, h_t,
+                                           grad_v, grad_x_t, stream))

@@ -79,6 +79,12 @@ snn_status launch_forward_tma_bf16(const snn_lif_shape* s, const snn::FwdArgs& a
 snn_status launch_backward_tma_f32(const snn_lif_shape* s, const snn::BwdArgs& a, int mode, cudaStream_t st);
 snn_status launch_backward_tma_bf16(const snn_lif_shape* s, const snn::BwdArgs& a, int mode, cudaStream_t st);
 int tma_vec_forward(int io_dtype);
+// Serial (one launch per time step) baseline of Fig. 3 -- comparison only (serial.cu).
+snn_status launch_serial_forward_step(int io_dtype, bool soft, const void* x_t, float* V, uint8_t* s_t,
+                                      float* h_t, int64_t N, const snn::LifConsts& c, cudaStream_t st);
+snn_status launch_serial_backward_step(int io_dtype, int mode, const void* gs_t, const float* h_t,
+                                       float* gV, void* gx_t, int64_t N, const snn::LifConsts& c,
+                                       cudaStream_t st);
 int tma_vec_backward(int io_dtype);
 
 }  // namespace snn_host

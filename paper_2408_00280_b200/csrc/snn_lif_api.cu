@@ -289,4 +289,36 @@ snn_status snn_lif_backward(const snn_lif_params* p, const snn_lif_shape* s,
     return launch_backward_generic(s, a, mode, fast, cs);
 }
 
+snn_status snn_lif_serial_forward_step(const snn_lif_params* p, int io_dtype, int64_t N,
+                                       const void* x_t, float* v, uint8_t* spikes_t, float* h_t,
+                                       void* stream) {
+    g_err[0] = 0;
+    snn_status st;
+    if ((st = check_params(p)) != SNN_OK) return st;
+    if (N < 1) return fail(SNN_ERR_INVALID_VALUE, "N=%lld must be >= 1", (long long)N);
+    if (io_dtype != SNN_F32 && io_dtype != SNN_BF16) return fail(SNN_ERR_INVALID_VALUE, "io_dtype %d", io_dtype);
+    if (!x_t || !v || !spikes_t || !h_t) return fail(SNN_ERR_NULL_POINTER, "a required pointer is NULL");
+    if (!aligned(x_t, io_size(io_dtype)) || !aligned(v, 4) || !aligned(h_t, 4))
+        return fail(SNN_ERR_MISALIGNED, "a pointer is not aligned to its element size");
+    return launch_serial_forward_step(io_dtype, p->reset_mode == SNN_RESET_SOFT, x_t, v, spikes_t, h_t, N,
+                                      make_consts(p), static_cast<cudaStream_t>(stream));
+}
+
+snn_status snn_lif_serial_backward_step(const snn_lif_params* p, int io_dtype, int64_t N,
+                                        const void* grad_spikes_t, const float* h_t, float* grad_v,
+                                        void* grad_x_t, void* stream) {
+    g_err[0] = 0;
+    snn_status st;
+    if ((st = check_params(p)) != SNN_OK) return st;
+    if (N < 1) return fail(SNN_ERR_INVALID_VALUE, "N=%lld must be >= 1", (long long)N);
+    if (io_dtype != SNN_F32 && io_dtype != SNN_BF16) return fail(SNN_ERR_INVALID_VALUE, "io_dtype %d", io_dtype);
+    if (!grad_spikes_t || !h_t || !grad_v || !grad_x_t)
+        return fail(SNN_ERR_NULL_POINTER, "a required pointer is NULL");
+    const size_t esz = io_size(io_dtype);
+    if (!aligned(grad_spikes_t, esz) || !aligned(grad_x_t, esz) || !aligned(h_t, 4) || !aligned(grad_v, 4))
+        return fail(SNN_ERR_MISALIGNED, "a pointer is not aligned to its element size");
+    return launch_serial_backward_step(io_dtype, mode_of(p), grad_spikes_t, h_t, grad_v, grad_x_t, N,
+                                       make_consts(p), static_cast<cudaStream_t>(stream));
+}
+
 }  // extern "C"

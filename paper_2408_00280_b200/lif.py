@@ -188,3 +188,28 @@ def unpack_bits(words: torch.Tensor, N: int) -> torch.Tensor:
     shifts = torch.arange(32, device=words.device, dtype=torch.int32)
     bits = (words.unsqueeze(-1) >> shifts) & 1
     return bits.reshape(T, W * 32)[:, :N].to(torch.uint8)
+
+
+# ----------------------------------------------------------------------------- baseline
+
+def lif_serial(x: torch.Tensor, grad_spikes: torch.Tensor, params: LIFParams = LIFParams(), *,
+               v_init: Optional[torch.Tensor] = None):
+    """The paper's "Serial (CUDA)" baseline (Fig. 3): T forward launches then T backward
+    launches, state through HBM between steps.  Comparison only; bitwise equal to the fused
+    path.  x, grad_spikes: contiguous CUDA [T, N].  Returns (spikes u8, H, v_final, grad_x,
+    grad_v_init)."""
+    T, N = x.shape
+    x = x.contiguous(); grad_spikes = grad_spikes.contiguous()
+    cp, io, st = params.to_c(), _DTYPES[x.dtype], _stream()
+    v = (v_init.clone() if v_init is not None else
+         torch.full((N,), float(params.v_reset), dtype=torch.float32, device=x.device))
+    S = torch.empty((T, N), dtype=torch.uint8, device=x.device)
+    H = torch.empty((T, N), dtype=torch.float32, device=x.device)
+    for t in range(T):
+        _lib.snn_lif_serial_forward_step(cp, io, N, _ptr(x[t]), _ptr(v), _ptr(S[t]), _ptr(H[t]), st)
+    gv = torch.zeros(N, dtype=torch.float32, device=x.device)
+    gX = torch.empty_like(x)
+    for t in range(T - 1, -1, -1):
+        _lib.snn_lif_serial_backward_step(cp, io, N, _ptr(grad_spikes[t]), _ptr(H[t]), _ptr(gv),
+                                          _ptr(gX[t]), st)
+    return S, H, v, gX, gv

@@ -241,3 +241,24 @@ def test_generic_and_tma_paths_agree_bitwise(monkeypatch, dtype, mode):
     monkeypatch.delenv("SNN_LIF_NO_TMA")
     rep, _ = run_gpu_and_oracle(p, T, N, dtype=dtype, with_v_init=True, with_grad_v_final=True)
     assert_ok(rep)
+
+
+# ------------------------------------------------------------------ serial baseline (f2)
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("mode", [0, 3, 6])
+def test_serial_baseline_equals_fused_bitwise(dtype, mode):
+    """the per-step serial engine (Fig. 3's "Serial (CUDA)") and the fused
+    kernels compose the same scalar steps, so every output is bitwise equal."""
+    p = LIFParams(tau=1.5, v_th=0.6, v_reset=-0.1, surrogate=("atan" if mode & 1 else "sigmoid"),
+                  reset=("soft" if mode & 2 else "hard"), detach_reset=bool(mode & 4))
+    T, N = 33, 5000
+    X = snn_synth.normal_tensor(51, T, N, dtype=dtype).cuda()
+    G = snn_synth.normal_tensor(52, T, N, dtype=dtype).cuda()
+    v0 = snn_synth.normal_tensor(53, 1, N)[0].cuda()
+    S, H, vf, gX, gvi = snn.lif.lif_serial(X, G, p, v_init=v0)
+    f, g, v = _run(p, X, G, "u8", "h", v0=v0)
+    torch.cuda.synchronize()
+    ldh = (N + 15) // 16 * 16
+    assert torch.equal(S, f.spikes) and torch.equal(H, f.saved.view(T, ldh)[:, :N])
+    assert torch.equal(vf, f.v_final) and torch.equal(gX, g) and torch.equal(gvi, v)
