@@ -3,6 +3,7 @@ boundary V / dV through HostTransport (gloo); the result must be BITWISE equal t
 whole-axis run (segmented execution carries exactly the register state)."""
 import os
 
+import numpy as np
 import pytest
 import torch
 import torch.distributed as dist
@@ -39,9 +40,11 @@ def _worker(rank, world, port, T, N, n_chunks, dtype, out):
     gxs, gvi = ts.backward(G, state, bwd_fn)
     torch.cuda.synchronize()
     objs = [None] * world
-    dist.all_gather_object(objs, (a, b, torch.cat(spikes, 1).cpu(), torch.cat(gxs, 1).cpu(),
-                                  None if v_final is None else v_final.cpu(),
-                                  None if gvi is None else gvi.cpu()))
+    # numpy (pickled by value): a torch CPU tensor put on an mp.Queue is shared through a
+    # file-descriptor socket that dies with this process, racing the parent's get().
+    np_ = lambda t: None if t is None else t.cpu().view(torch.int16 if t.dtype == torch.bfloat16 else t.dtype).numpy()
+    dist.all_gather_object(objs, (a, b, np_(torch.cat(spikes, 1)), np_(torch.cat(gxs, 1)),
+                                  np_(v_final), np_(gvi)))
     if rank == 0:
         out.put(objs)
     dist.barrier()
@@ -69,7 +72,8 @@ def test_time_split_bitwise_equals_whole_axis(world, n_chunks, dtype):
     f = snn.lif_forward(X, snn.LIFParams.paper())
     gx, gvi = snn.lif_backward(G, f)
     torch.cuda.synchronize()
-    assert torch.equal(torch.cat([o[2] for o in objs], 0), f.spikes.cpu())
-    assert torch.equal(torch.cat([o[3] for o in objs], 0), gx.cpu())
-    assert torch.equal(objs[-1][4], f.v_final.cpu())
-    assert torch.equal(objs[0][5], gvi.cpu())
+    as_np = lambda t: t.cpu().view(torch.int16 if t.dtype == torch.bfloat16 else t.dtype).numpy()
+    assert np.array_equal(np.concatenate([o[2] for o in objs], 0), as_np(f.spikes))
+    assert np.array_equal(np.concatenate([o[3] for o in objs], 0), as_np(gx))   # bitwise (int16 view for bf16)
+    assert np.array_equal(objs[-1][4], as_np(f.v_final))
+    assert np.array_equal(objs[0][5], as_np(gvi))
