@@ -262,3 +262,27 @@ def test_serial_baseline_equals_fused_bitwise(dtype, mode):
     ldh = (N + 15) // 16 * 16
     assert torch.equal(S, f.spikes) and torch.equal(H, f.saved.view(T, ldh)[:, :N])
     assert torch.equal(vf, f.v_final) and torch.equal(gX, g) and torch.equal(gvi, v)
+
+
+# ------------------------------------------------------------------ randomized (hypothesis)
+
+from hypothesis import given, settings, strategies as st, HealthCheck  # noqa: E402
+
+
+@settings(max_examples=40, deadline=None, suppress_health_check=list(HealthCheck))
+@given(T=st.integers(1, 70), N=st.integers(1, 3000), ld_pad=st.sampled_from([0, 0, 0, 1, 8]),
+       dtype=st.sampled_from([torch.float32, torch.bfloat16]), mode=st.integers(0, 7),
+       decay_input=st.booleans(), save_mode=st.sampled_from(["recompute", "h"]),
+       spike_fmt=st.sampled_from(["u8", "bits", "io"]), carries=st.booleans(),
+       v_reset=st.sampled_from([0.0, -0.2, 0.15]), x_mean=st.sampled_from([0.0, 0.5, 1.0]))
+def test_randomized_parity(T, N, ld_pad, dtype, mode, decay_input, save_mode, spike_fmt, carries,
+                           v_reset, x_mean):
+    """SURVEY 4 tier 2: random shapes (ragged N, odd ld), all flag combinations, both io
+    dtypes, all spike formats and save modes, with and without carries."""
+    p = LIFParams(tau=1.5, v_th=0.6, v_reset=v_reset, surrogate=("atan" if mode & 1 else "sigmoid"),
+                  reset=("soft" if mode & 2 else "hard"), detach_reset=bool(mode & 4),
+                  decay_input=decay_input, alpha=(2.0 if mode & 1 else 4.0))
+    rep, _ = run_gpu_and_oracle(p, T, N, dtype=dtype, spike_fmt=spike_fmt, save_mode=save_mode,
+                                x_mean=x_mean, with_v_init=carries, with_grad_v_final=carries,
+                                ld=N + ld_pad, seed_x=T * 7919 + N, seed_g=N * 31 + T)
+    assert_ok(rep)
