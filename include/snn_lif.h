@@ -157,6 +157,45 @@ snn_status snn_lif_backward(const snn_lif_params* params, const snn_lif_shape* s
                             const void* saved, const float* grad_v_final, void* grad_x,
                             float* grad_v_init, void* stream);
 
+/* ---- Time-segment split with the boundary handoff fused into the kernels (SURVEY 8(f)
+ * f1; rank d owns time steps [t_d, t_{d+1}) of every neuron, the boundary
+ * membrane state goes forward in time and dL/dV backward).  Per neuron tile the kernel
+ * waits for the previous rank's boundary state (ready flag, acquire at system scope),
+ * computes the tile over the whole local segment, stores its carry-out straight into the
+ * next rank's buffer through a peer-mapped pointer (CUDA IPC over NVLink) and releases
+ * that tile's flag -- no separate collective, wavefront lag = one tile.
+ * Flags are int32, one per SNN_LIF_HANDOFF_BLOCK neurons (snn_lif_handoff_blocks(N)
+ * words), zero-initialised by the caller before the first call; `epoch` starts at 1 and
+ * increases by one per call on every rank.  Credit-based flow control (ack flags) stops
+ * a fast rank from overwriting a buffer the receiver has not read yet.
+ * Forward: recv_* carry V (the previous segment's v_final), send_* the next segment's
+ *          v_init.  Backward: recv_* carry dL/dV from the LATER segment, send_* go to the
+ *          earlier one.  NULL recv_state = first segment (v_init / grad_v_final apply);
+ *          NULL send_state = last segment.
+ * Requires the TMA path (16-byte-aligned pointers, ld a multiple of 16 bytes, N a
+ * multiple of 8 for bf16 / 4 for fp32), else SNN_ERR_UNSUPPORTED. */
+#define SNN_LIF_HANDOFF_BLOCK 256
+
+typedef struct {
+    const float* recv_state;   /* [N] fp32, local: written by the sending rank            */
+    const int32_t* recv_ready; /* [blocks], local: sender sets = epoch when written       */
+    int32_t* recv_ack;         /* [blocks], peer: the sender's send_ack; we set = epoch    */
+    float* send_state;         /* [N] fp32, peer: the receiving rank's recv_state          */
+    int32_t* send_ready;       /* [blocks], peer: the receiving rank's recv_ready          */
+    const int32_t* send_ack;   /* [blocks], local: the receiver's acknowledgements         */
+    int32_t epoch;             /* >= 1, +1 per call                                        */
+} snn_lif_handoff;
+
+int64_t snn_lif_handoff_blocks(int64_t N);
+
+snn_status snn_lif_forward_handoff(const snn_lif_params* params, const snn_lif_shape* shape,
+                                   const void* x, const float* v_init, const snn_lif_handoff* handoff,
+                                   void* spikes, void* saved, float* v_final, void* stream);
+snn_status snn_lif_backward_handoff(const snn_lif_params* params, const snn_lif_shape* shape,
+                                    const void* grad_spikes, const void* x, const void* saved,
+                                    const float* grad_v_final, const snn_lif_handoff* handoff,
+                                    void* grad_x, float* grad_v_init, void* stream);
+
 /* ---- Baseline, not the method: the paper's "Serial (CUDA)" training of Fig. 3
  * (Fig. 5 caption PAPER.md:419) -- ONE time step per call, the membrane
  * state round-tripped through caller memory between steps, for the fused-vs-serial

@@ -27,8 +27,10 @@ SNN_LIF_CKPT_INTERVAL = 16
 EXPORTED_SYMBOLS = (
     "snn_lif_saved_bytes", "snn_lif_forward", "snn_lif_backward", "snn_status_string",
     "snn_last_error_message", "snn_lif_abi_version", "snn_lif_serial_forward_step",
-    "snn_lif_serial_backward_step",
+    "snn_lif_serial_backward_step", "snn_lif_handoff_blocks", "snn_lif_forward_handoff",
+    "snn_lif_backward_handoff",
 )
+SNN_LIF_HANDOFF_BLOCK = 256
 
 
 class snn_lif_params(ctypes.Structure):
@@ -42,6 +44,13 @@ class snn_lif_shape(ctypes.Structure):
     _fields_ = [("T", ctypes.c_int64), ("N", ctypes.c_int64), ("ld", ctypes.c_int64),
                 ("io_dtype", ctypes.c_int), ("spike_fmt", ctypes.c_int),
                 ("save_mode", ctypes.c_int)]
+
+
+class snn_lif_handoff(ctypes.Structure):
+    _fields_ = [("recv_state", ctypes.c_void_p), ("recv_ready", ctypes.c_void_p),
+                ("recv_ack", ctypes.c_void_p), ("send_state", ctypes.c_void_p),
+                ("send_ready", ctypes.c_void_p), ("send_ack", ctypes.c_void_p),
+                ("epoch", ctypes.c_int32)]
 
 
 def _load() -> ctypes.CDLL:
@@ -70,6 +79,13 @@ def _load() -> ctypes.CDLL:
     lib.snn_lif_serial_forward_step.restype = ctypes.c_int
     lib.snn_lif_serial_backward_step.argtypes = [P, ctypes.c_int, i64, vp, vp, vp, vp, vp]
     lib.snn_lif_serial_backward_step.restype = ctypes.c_int
+    Hp = ctypes.POINTER(snn_lif_handoff)
+    lib.snn_lif_handoff_blocks.argtypes = [i64]
+    lib.snn_lif_handoff_blocks.restype = i64
+    lib.snn_lif_forward_handoff.argtypes = [P, S, vp, fp, Hp, vp, vp, fp, vp]
+    lib.snn_lif_forward_handoff.restype = ctypes.c_int
+    lib.snn_lif_backward_handoff.argtypes = [P, S, vp, vp, vp, fp, Hp, vp, fp, vp]
+    lib.snn_lif_backward_handoff.restype = ctypes.c_int
     return lib
 
 
@@ -114,3 +130,15 @@ def snn_lif_serial_backward_step(params, io_dtype, N, grad_spikes_t, h_t, grad_v
                                  stream) -> None:
     check(lib.snn_lif_serial_backward_step(ctypes.byref(params), io_dtype, N, grad_spikes_t, h_t,
                                            grad_v, grad_x_t, stream))
+
+
+def snn_lif_forward_handoff(params, shape, x, v_init, handoff, spikes, saved, v_final, stream) -> None:
+    check(lib.snn_lif_forward_handoff(ctypes.byref(params), ctypes.byref(shape), x, v_init,
+                                      ctypes.byref(handoff), spikes, saved, v_final, stream))
+
+
+def snn_lif_backward_handoff(params, shape, grad_spikes, x, saved, grad_v_final, handoff, grad_x,
+                             grad_v_init, stream) -> None:
+    check(lib.snn_lif_backward_handoff(ctypes.byref(params), ctypes.byref(shape), grad_spikes, x,
+                                       saved, grad_v_final, ctypes.byref(handoff), grad_x,
+                                       grad_v_init, stream))

@@ -19,6 +19,19 @@ constexpr unsigned kFull = 0xffffffffu;
 enum { SPK_U8 = 0, SPK_BITS = 1, SPK_IO = 2 };
 enum { SAVE_H = 0, SAVE_RECOMPUTE = 1, SAVE_NONE = 2 };
 
+// Peer handoff of a segment boundary (time split; lif_handoff.cuh).
+// All pointers null = no handoff.  "peer" pointers are mapped addresses of the
+// neighbour rank's buffers (CUDA IPC over NVLink); flags are per kHandoffBlock neurons.
+struct Handoff {
+    const float* recv_state;  // [N] local: written by the previous sender
+    const int* recv_ready;    // [nblk] local: sender sets = epoch after writing recv_state
+    int* recv_ack;            // [nblk] peer (the sender's send_ack): we set = epoch once consumed
+    float* send_state;        // [N] peer: the next receiver's recv_state
+    int* send_ready;          // [nblk] peer: the next receiver's recv_ready
+    const int* send_ack;      // [nblk] local: the receiver acknowledges the previous epoch
+    int epoch;                // > 0, increases by one per call
+};
+
 struct FwdArgs {
     const void* x;        // [T, ld] IO
     const float* v_init;  // [N] or null
@@ -27,6 +40,7 @@ struct FwdArgs {
     float* v_final;       // [N] or null
     int64_t T, N, ld, ldh, nwords;
     LifConsts c;
+    Handoff h;            // boundary V from / to the neighbour time segment (TMA path only)
 };
 
 struct BwdArgs {
@@ -38,6 +52,7 @@ struct BwdArgs {
     float* grad_v_init;         // [N] or null
     int64_t T, N, ld, ldh;
     LifConsts c;
+    Handoff h;                  // boundary dL/dV from / to the neighbour segment (TMA path only)
 };
 
 // ------------------------------------------------------------------------------------

@@ -28,6 +28,7 @@
 #include <type_traits>
 
 #include "lif_async.cuh"
+#include "lif_handoff.cuh"
 #include "lif_kernels.cuh"
 
 namespace snn {
@@ -179,13 +180,14 @@ lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const FwdArgs a,
         const int nvalid = n0 < N ? VEC : 0;
         const bool tile_full = (int64_t)(tile + 1) * W <= N;   // uniform across the CTA
         float V[VEC];
-        if (a.v_init != nullptr && nvalid > 0) {
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) V[i] = c.v_reset;
+        if (a.h.recv_state != nullptr) {            // segment boundary from the previous rank
+            handoff_recv<VEC>(a.h, N, n0, nvalid > 0, V);
+        } else if (a.v_init != nullptr && nvalid > 0) {
             const Pack<float, VEC> v0 = ld_stream<float, VEC>(a.v_init + n0);
 #pragma unroll
             for (int i = 0; i < VEC; ++i) V[i] = v0.v[i];
-        } else {
-#pragma unroll
-            for (int i = 0; i < VEC; ++i) V[i] = c.v_reset;
         }
         unsigned char* spk_row = reinterpret_cast<unsigned char*>(a.spikes);
         float* h_row = a.saved + n0;   // SAVE_H: advanced one row per step
@@ -228,6 +230,8 @@ lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const FwdArgs a,
             __syncwarp();
             if (lane == 0) mbar_arrive(&bar->empty[s]);
         }
+        if (a.h.send_state != nullptr || a.h.recv_ack != nullptr)   // uniform across the CTA
+            handoff_send<VEC, NCONS>(a.h, tile, W, N, n0, nvalid > 0, V);
         if (a.v_final != nullptr && nvalid > 0) {
             Pack<float, VEC> vf;
 #pragma unroll
@@ -338,13 +342,14 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
         const bool valid = n0 < N;   // N % VEC == 0 on this path
         const bool tile_full = (int64_t)(tile + 1) * W <= N;   // uniform across the CTA
         float gV[VEC];
-        if (a.grad_v_final != nullptr && valid) {
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) gV[i] = 0.0f;
+        if (a.h.recv_state != nullptr) {            // dL/dV from the later segment's rank
+            handoff_recv<VEC>(a.h, N, n0, valid, gV);
+        } else if (a.grad_v_final != nullptr && valid) {
             const Pack<float, VEC> g0 = ld_stream<float, VEC>(a.grad_v_final + n0);
 #pragma unroll
             for (int i = 0; i < VEC; ++i) gV[i] = g0.v[i];
-        } else {
-#pragma unroll
-            for (int i = 0; i < VEC; ++i) gV[i] = 0.0f;
         }
         for (int64_t ch = nch - 1; ch >= 0; --ch, ++k) {
             if (ch < nch - 1) {
@@ -373,6 +378,8 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
             __syncwarp();
             if (lane == 0) mbar_arrive(&bar->empty[s]);
         }
+        if (a.h.send_state != nullptr || a.h.recv_ack != nullptr)   // uniform across the CTA
+            handoff_send<VEC, NCONS>(a.h, tile, W, N, n0, valid, gV);
         if (a.grad_v_init != nullptr && valid) {
             Pack<float, VEC> gi;
 #pragma unroll
@@ -447,13 +454,14 @@ lif_backward_saveh_tma_kernel(const __grid_constant__ CUtensorMap tmh,
         const bool valid = n0 < N;
         const bool tile_full = (int64_t)(tile + 1) * W <= N;   // uniform across the CTA
         float gV[VEC];
-        if (a.grad_v_final != nullptr && valid) {
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) gV[i] = 0.0f;
+        if (a.h.recv_state != nullptr) {            // dL/dV from the later segment's rank
+            handoff_recv<VEC>(a.h, N, n0, valid, gV);
+        } else if (a.grad_v_final != nullptr && valid) {
             const Pack<float, VEC> g0 = ld_stream<float, VEC>(a.grad_v_final + n0);
 #pragma unroll
             for (int i = 0; i < VEC; ++i) gV[i] = g0.v[i];
-        } else {
-#pragma unroll
-            for (int i = 0; i < VEC; ++i) gV[i] = 0.0f;
         }
         for (int64_t rb = nrb - 1; rb >= 0; --rb, ++k) {
             if (rb < nrb - 1) {
@@ -481,6 +489,8 @@ lif_backward_saveh_tma_kernel(const __grid_constant__ CUtensorMap tmh,
             __syncwarp();
             if (lane == 0) mbar_arrive(&bar->empty[s]);
         }
+        if (a.h.send_state != nullptr || a.h.recv_ack != nullptr)   // uniform across the CTA
+            handoff_send<VEC, NCONS>(a.h, tile, W, N, n0, valid, gV);
         if (a.grad_v_init != nullptr && valid) {
             Pack<float, VEC> gi;
 #pragma unroll

@@ -12,6 +12,7 @@
 #include <utility>
 
 #include "internal.h"
+#include "lif_handoff.cuh"
 
 namespace snn_host {
 
@@ -210,9 +211,32 @@ size_t snn_lif_saved_bytes(const snn_lif_params* p, const snn_lif_shape* s) {
     return (size_t)saved_rows(s) * (size_t)saved_ld(s) * sizeof(float);
 }
 
-snn_status snn_lif_forward(const snn_lif_params* p, const snn_lif_shape* s, const void* x,
-                           const float* v_init, void* spikes, void* saved, float* v_final,
-                           void* stream) {
+}  // extern "C"
+
+namespace {
+
+bool handoff_valid(const snn_lif_handoff* h) {
+    if (!h) return true;
+    if (h->epoch < 1) return false;
+    if (h->recv_state && !h->recv_ready) return false;
+    if (h->send_state && !h->send_ready) return false;
+    if (h->send_state && !h->send_ack) return false;
+    return true;
+}
+
+snn::Handoff to_dev(const snn_lif_handoff* h) {
+    snn::Handoff d = {};
+    if (h) {
+        d.recv_state = h->recv_state; d.recv_ready = h->recv_ready; d.recv_ack = h->recv_ack;
+        d.send_state = h->send_state; d.send_ready = h->send_ready; d.send_ack = h->send_ack;
+        d.epoch = h->epoch;
+    }
+    return d;
+}
+
+snn_status forward_impl(const snn_lif_params* p, const snn_lif_shape* s, const void* x,
+                        const float* v_init, const snn_lif_handoff* handoff, void* spikes, void* saved,
+                        float* v_final, void* stream) {
     g_err[0] = 0;
     snn_status st;
     if ((st = check_params(p)) != SNN_OK) return st;
@@ -235,10 +259,13 @@ snn_status snn_lif_forward(const snn_lif_params* p, const snn_lif_shape* s, cons
     a.c = make_consts(p);
     const bool soft = p->reset_mode == SNN_RESET_SOFT;
     cudaStream_t cs = static_cast<cudaStream_t>(stream);
+    if (!handoff_valid(handoff)) return fail(SNN_ERR_INVALID_VALUE, "handoff: epoch < 1 or missing flags");
+    a.h = to_dev(handoff);
 
     if (tma_ok(s, tma_vec_forward(s->io_dtype), {x, v_init, v_final, a.saved, spikes}))
         return s->io_dtype == SNN_BF16 ? launch_forward_tma_bf16(s, a, soft, cs)
                                        : launch_forward_tma_f32(s, a, soft, cs);
+    if (handoff) return fail(SNN_ERR_UNSUPPORTED, "the fused handoff needs the TMA path (aligned rows)");
     const int vec = s->io_dtype == SNN_BF16 ? 8 : 4;
     bool fast = (s->ld % vec) == 0 && aligned(x, 16) && (!v_init || aligned(v_init, 16)) &&
                 (!v_final || aligned(v_final, 16));
@@ -246,10 +273,10 @@ snn_status snn_lif_forward(const snn_lif_params* p, const snn_lif_shape* s, cons
     return launch_forward_generic(s, a, soft, fast, cs);
 }
 
-snn_status snn_lif_backward(const snn_lif_params* p, const snn_lif_shape* s,
-                            const void* grad_spikes, const void* x, const float* v_init,
-                            const void* saved, const float* grad_v_final, void* grad_x,
-                            float* grad_v_init, void* stream) {
+snn_status backward_impl(const snn_lif_params* p, const snn_lif_shape* s,
+                         const void* grad_spikes, const void* x, const void* saved,
+                         const float* grad_v_final, const snn_lif_handoff* handoff, void* grad_x,
+                         float* grad_v_init, void* stream) {
     g_err[0] = 0;
     snn_status st;
     if ((st = check_params(p)) != SNN_OK) return st;
@@ -266,8 +293,6 @@ snn_status snn_lif_backward(const snn_lif_params* p, const snn_lif_shape* s,
         !aligned(saved, 16) || (grad_v_final && !aligned(grad_v_final, 4)) ||
         (grad_v_init && !aligned(grad_v_init, 4)))
         return fail(SNN_ERR_MISALIGNED, "a pointer is not aligned to its element size (saved needs 16 B)");
-    (void)v_init;  // the RECOMPUTE checkpoints already hold V[-1]
-
     snn::BwdArgs a;
     a.gS = grad_spikes; a.x = x; a.saved = static_cast<const float*>(saved);
     a.grad_v_final = grad_v_final; a.gX = grad_x; a.grad_v_init = grad_v_init;
@@ -275,18 +300,58 @@ snn_status snn_lif_backward(const snn_lif_params* p, const snn_lif_shape* s,
     a.c = make_consts(p);
     const int mode = mode_of(p);
     cudaStream_t cs = static_cast<cudaStream_t>(stream);
+    if (!handoff_valid(handoff)) return fail(SNN_ERR_INVALID_VALUE, "handoff: epoch < 1 or missing flags");
+    a.h = to_dev(handoff);
 
     if (tma_ok(s, tma_vec_backward(s->io_dtype),
                {grad_spikes, grad_x, s->save_mode == SNN_SAVE_RECOMPUTE ? x : nullptr, saved,
                 grad_v_final, grad_v_init}))
         return s->io_dtype == SNN_BF16 ? launch_backward_tma_bf16(s, a, mode, cs)
                                        : launch_backward_tma_f32(s, a, mode, cs);
+    if (handoff) return fail(SNN_ERR_UNSUPPORTED, "the fused handoff needs the TMA path (aligned rows)");
     const int vec = s->io_dtype == SNN_BF16 ? 4 : 2;
     const bool fast = (s->ld % vec) == 0 && aligned(grad_spikes, 16) && aligned(grad_x, 16) &&
                       (!x || s->save_mode != SNN_SAVE_RECOMPUTE || aligned(x, 16)) &&
                       (!grad_v_final || aligned(grad_v_final, 16)) &&
                       (!grad_v_init || aligned(grad_v_init, 16));
     return launch_backward_generic(s, a, mode, fast, cs);
+}
+
+}  // namespace
+
+extern "C" {
+
+snn_status snn_lif_forward(const snn_lif_params* p, const snn_lif_shape* s, const void* x,
+                           const float* v_init, void* spikes, void* saved, float* v_final,
+                           void* stream) {
+    return forward_impl(p, s, x, v_init, nullptr, spikes, saved, v_final, stream);
+}
+
+snn_status snn_lif_backward(const snn_lif_params* p, const snn_lif_shape* s,
+                            const void* grad_spikes, const void* x, const float* v_init,
+                            const void* saved, const float* grad_v_final, void* grad_x,
+                            float* grad_v_init, void* stream) {
+    (void)v_init;  // the RECOMPUTE checkpoints already hold V[-1]
+    return backward_impl(p, s, grad_spikes, x, saved, grad_v_final, nullptr, grad_x, grad_v_init, stream);
+}
+
+int64_t snn_lif_handoff_blocks(int64_t N) {
+    return N < 1 ? 0 : (N + snn::kHandoffBlock - 1) / snn::kHandoffBlock;
+}
+
+snn_status snn_lif_forward_handoff(const snn_lif_params* p, const snn_lif_shape* s, const void* x,
+                                   const float* v_init, const snn_lif_handoff* h, void* spikes,
+                                   void* saved, float* v_final, void* stream) {
+    if (!h) return fail(SNN_ERR_NULL_POINTER, "handoff is NULL");
+    return forward_impl(p, s, x, v_init, h, spikes, saved, v_final, stream);
+}
+
+snn_status snn_lif_backward_handoff(const snn_lif_params* p, const snn_lif_shape* s,
+                                    const void* grad_spikes, const void* x, const void* saved,
+                                    const float* grad_v_final, const snn_lif_handoff* h, void* grad_x,
+                                    float* grad_v_init, void* stream) {
+    if (!h) return fail(SNN_ERR_NULL_POINTER, "handoff is NULL");
+    return backward_impl(p, s, grad_spikes, x, saved, grad_v_final, h, grad_x, grad_v_init, stream);
 }
 
 snn_status snn_lif_serial_forward_step(const snn_lif_params* p, int io_dtype, int64_t N,
