@@ -49,6 +49,12 @@ def parse():
     ap.add_argument("--sweep", action="store_true",
                     help="cfg1: also time T in {8,32,128,512} (L2 flushed before every launch)")
     ap.add_argument("--chunks", type=int, default=32, help="cfg3 neuron chunks of the wavefront")
+    ap.add_argument("--transport", choices=["handoff", "nccl"], default="handoff",
+                    help="cfg3 boundary exchange: fused in-kernel peer handoff (CUDA IPC over "
+                         "NVLink) or NCCL send/recv between per-chunk launches")
+    ap.add_argument("--debug-single-gpu", action="store_true",
+                    help="test harness only: every rank on cuda:0 with a gloo group (exercises "
+                         "the multi-rank code paths on a 1-GPU box; numbers are not bench values)")
     ap.add_argument("--serial", action="store_true",
                     help="with --sweep: also time the paper's serial baselines (Fig. 3 / Fig. 5)")
     ap.add_argument("--save-mode", choices=["recompute", "h"], default="recompute")
@@ -169,6 +175,24 @@ def workload_config(args, world, layers):
 
 
 # ----------------------------------------------------------------------------- helpers
+
+def init_group(args, local):
+    import torch
+    import torch.distributed as dist
+    if args.debug_single_gpu:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+
+def max_over_ranks(vals, dev, debug):
+    """MAX all-reduce of a few floats (NCCL on the GPU box; gloo/CPU in the debug harness)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(vals, dtype=torch.float64, device="cpu" if debug else dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(v) for v in t.tolist()]
+
 
 def measured_peak():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -359,9 +383,11 @@ def run_tsplit(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.debug_single_gpu:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        init_group(args, local)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
     params = snn.LIFParams.paper()
@@ -371,8 +397,26 @@ def run_tsplit(args):
     G = snn_synth.normal_tensor(4321, b - a, N, t_offset=a, device=dev)
     ts = D.TimeSplitLIF(rank, world, D.NcclTransport(), n_chunks=args.chunks if world > 1 else 1)
     fwd_fn, bwd_fn = D.lif_segment_fns(params, spike_fmt=args.spike_fmt, save_mode=args.save_mode)
+    use_handoff = world > 1 and args.transport == "handoff"
+    if use_handoff:
+        from paper_2408_00280_b200 import handoff as HO
+        ph = HO.PeerHandoff(N)
 
     def step():
+        if use_handoff:   # one fused launch per direction; boundary moves inside the kernels
+            f = HO.lif_forward_handoff(X, params, ph.forward_handoff(), spike_fmt=args.spike_fmt,
+                                       save_mode=args.save_mode, return_v_final=False)
+            if args.debug_single_gpu:
+                # k processes time-share ONE GPU here: a spinning receiver kernel may hold
+                # the GPU while its sender's context waits, so phases are separated (on a
+                # multi-GPU box every rank owns its GPU and the dependency graph is acyclic).
+                torch.cuda.synchronize(dev)
+                dist.barrier()
+            HO.lif_backward_handoff(G, f, ph.backward_handoff(), return_grad_v_init=False)
+            if args.debug_single_gpu:
+                torch.cuda.synchronize(dev)
+                dist.barrier()
+            return
         spikes, state, vf = ts.forward(X, fwd_fn)
         ts.backward(G, state, bwd_fn)
 
@@ -391,7 +435,7 @@ def run_tsplit(args):
     ms = e0.elapsed_time(e1)
     # T_c: one boundary hop of [N] fp32 (rank 0 -> 1), median of 20
     tc_ms = None
-    if world > 1:
+    if world > 1 and not args.debug_single_gpu:
         buf = torch.empty(N, dtype=torch.float32, device=dev)
         times = []
         for _ in range(23):
@@ -406,9 +450,7 @@ def run_tsplit(args):
             torch.cuda.synchronize(dev)
             times.append(c0.elapsed_time(c1))
         tc_ms = sorted(times[3:])[len(times[3:]) // 2]
-        tt = torch.tensor([ms, tc_ms if rank == 1 else 0.0], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms, tc_ms = float(tt[0].item()), float(tt[1].item())
+        ms, tc_ms = max_over_ranks([ms, tc_ms if rank == 1 else 0.0], dev, args.debug_single_gpu)
     value = N * T * args.steps / (ms / 1e3)
     if rank == 0:
         t_seg = ms / args.steps
@@ -416,15 +458,21 @@ def run_tsplit(args):
                 "warmup": max(3, args.warmup), "ms_per_step": t_seg, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": {"workload": f"BASELINE configs[3]: N=2^22, T={T}, time-segment split k={world}",
-                           "chunks": ts.n_chunks, "spike_fmt": args.spike_fmt, "save_mode": args.save_mode,
+                           "chunks": (None if use_handoff else ts.n_chunks), "spike_fmt": args.spike_fmt,
+                           "save_mode": args.save_mode,
                            "parallelism": f"time-split k={world}",
                            "l2": "no flush: per-rank inputs exceed the 126 MB L2"},
                 "tsplit": {"k": world, "T_c_ms": tc_ms,
-                           "pipeline_efficiency": D.pipeline_efficiency(ts.n_chunks, world),
+                           "transport": ("fused peer handoff (per-tile flags over NVLink)" if use_handoff
+                                         else f"NCCL send/recv, {ts.n_chunks} chunks"),
+                           "pipeline_efficiency": (1.0 if use_handoff else D.pipeline_efficiency(ts.n_chunks, world)),
                            "mu_model_eq5": (D.speedup_mu(world * t_seg, tc_ms, world) if tc_ms else 1.0),
                            "k_opt_eq5": (D.optimal_k(world * t_seg, tc_ms) if tc_ms else None)},
-                "gpu_launches": 2 * ts.n_chunks * args.steps, "clocks": clk.summary()}
+                "gpu_launches": (2 if use_handoff else 2 * ts.n_chunks) * args.steps,
+                "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
+    if use_handoff:
+        ph.close()
     if world > 1:
         dist.destroy_process_group()
 
@@ -473,9 +521,11 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.debug_single_gpu:
+        local = 0
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        init_group(args, local)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
     params = snn.LIFParams.paper()
@@ -546,9 +596,7 @@ def run_ours(args):
         dist.barrier()
     ms = t0.elapsed_time(t1)
     if world > 1:
-        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
+        ms = max_over_ranks([ms], dev, args.debug_single_gpu)[0]
     ns_rank = sum(b["T"] * b["N"] for b in bufs)
     total_ns = ns_rank * world * args.steps
     value = total_ns / (ms / 1e3)
@@ -620,9 +668,7 @@ def run_ours(args):
         torch.cuda.synchronize(dev)
         ems = a.elapsed_time(b_)
         if world > 1:
-            tt = torch.tensor([ems], device=dev, dtype=torch.float64)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            ems = float(tt.item())
+            ems = max_over_ranks([ems], dev, args.debug_single_gpu)[0]
         e2e = {"value": ns_rank * world * args.e2e_steps / (ems / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
                "ms_per_step": round(ems / args.e2e_steps, 3)}

@@ -1,0 +1,51 @@
+"""bench.py end to end on the GPU box: the default single-GPU line has every contract key,
+and the multi-rank code paths (neuron sharding, time split with the fused handoff) run
+under torchrun with every rank on cuda:0 (--debug-single-gpu: gloo group; numbers are not
+bench values)."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _run(args, nproc=1, port=29531):
+    if nproc == 1:
+        cmd = [sys.executable, "bench.py", *args]
+    else:
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+               "--master-addr", "127.0.0.1", f"--master-port={port}", "bench.py", *args]
+    out = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    return json.loads(lines[0])
+
+
+def test_default_line_contract_keys():
+    d = _run(["--steps", "5", "--warmup", "3", "--T", "64", "--cpu-seconds", "1", "--e2e-steps", "1"])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e",
+              "gpu_launches", "clocks"):
+        assert k in d, k
+    r = d["roofline"]
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s" and r["achieved"] > 0 and r["peak"] > 0
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] == 1
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["gpu_launches"] == 10
+
+
+@pytest.mark.parametrize("workload,extra", [("cfg1", ["--T", "32"]), ("cfg3", ["--T", "64"])])
+def test_multirank_paths_under_torchrun(workload, extra):
+    d = _run(["--gpus", "2", "--workload", workload, "--steps", "2", "--warmup", "3", "--no-e2e",
+              "--debug-single-gpu", *extra], nproc=2, port=29532 if workload == "cfg1" else 29533)
+    assert d["n_gpus"] == 2
+    assert d["scaling"] == ("weak" if workload == "cfg1" else "strong")

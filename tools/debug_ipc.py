@@ -13,15 +13,21 @@ def w(rank, world, path):
     from paper_2408_00280_b200 import handoff as HO, dist as D
     import snn_synth
     log("init")
-    N, T = 4096, 48
+    N, T = int(os.environ.get("DBG_N", 4096)), int(os.environ.get("DBG_T", 48))
     a, b = D.partition_time(T, world)[rank]
     X = snn_synth.normal_tensor(81, b - a, N, t_offset=a, device="cuda")
     ph = HO.PeerHandoff(N)
     log("peer ok", ph.f_send, ph.f_recv)
-    f = HO.lif_forward_handoff(X, snn.LIFParams.paper(), ph.forward_handoff())
-    log("launched fwd")
-    torch.cuda.synchronize()
-    log("fwd done", f.v_final[:4].tolist())
+    for it in range(int(os.environ.get("DBG_IT", 1))):
+        f = HO.lif_forward_handoff(X, snn.LIFParams.paper(), ph.forward_handoff())
+        log("launched fwd", it)
+        torch.cuda.synchronize()
+        log("fwd done", it, f.v_final[:2].tolist())
+        if os.environ.get("DBG_BWD"):
+            G = snn_synth.normal_tensor(82, b - a, N, t_offset=a, device="cuda")
+            gx, gvi = HO.lif_backward_handoff(G, f, ph.backward_handoff())
+            torch.cuda.synchronize()
+            log("bwd done", it, gvi[:2].tolist())
     ph.close()
     log("closed")
     dist.destroy_process_group()
