@@ -286,3 +286,40 @@ def test_randomized_parity(T, N, ld_pad, dtype, mode, decay_input, save_mode, sp
                                 x_mean=x_mean, with_v_init=carries, with_grad_v_final=carries,
                                 ld=N + ld_pad, seed_x=T * 7919 + N, seed_g=N * 31 + T)
     assert_ok(rep)
+
+
+# ------------------------------------------------------------------ other BASELINE configs, full size
+
+def _sampled_parity(p, T, N, dtype, cols=2048, seed_x=1234, seed_g=4321, spike_fmt="u8"):
+    X = snn_synth.normal_tensor(seed_x, T, N, device="cuda", dtype=dtype)
+    G = snn_synth.normal_tensor(seed_g, T, N, device="cuda", dtype=dtype)
+    fwd, gX, gvi = _run(p, X, G, spike_fmt=spike_fmt)
+    torch.cuda.synchronize()
+    del X, G
+    cols = np.sort(np.random.default_rng(T + N).choice(N, cols, replace=False))
+    ci = torch.as_tensor(cols, device="cuda")
+    Xh = snn_synth.normal_columns(seed_x, T, N, cols, dtype=dtype)
+    Gh = snn_synth.normal_columns(seed_g, T, N, cols, dtype=dtype)
+    ref = oracle_run(p, Xh, Gh)
+    S = fwd.spikes if spike_fmt != "bits" else snn.unpack_bits(fwd.spikes, N)
+    rep = compare(p, ref, ref["gX"], ref["gvi"], S[:, ci].cpu(), gX[:, ci].cpu(),
+                  vf_gpu=fwd.v_final[ci].cpu(), gvi_gpu=gvi[ci].cpu(), col_ids=cols,
+                  io_bf16=(dtype == torch.bfloat16))
+    assert_ok(rep)
+
+
+def test_cfg2_vgg_layer0_bf16_full_size_sampled():
+    """BASELINE configs[2]: the largest VGG-11 LIF layer, B=128 x 64x32x32 = 8,388,608
+    neurons, T=16, bf16 currents."""
+    _sampled_parity(PAPER, 16, 128 * 64 * 32 * 32, torch.bfloat16)
+
+
+def test_cfg3_long_horizon_full_size_sampled():
+    """BASELINE configs[3] at k=1: N=2^22, T=1024 (the whole axis on one GPU)."""
+    _sampled_parity(PAPER, 1024, 1 << 22, torch.float32, cols=1024)
+
+
+def test_cfg4_resnet_stem_full_size_sampled():
+    """BASELINE configs[4]: the Spiking-ResNet18 DVS stem LIF layer per rank, B=32 x
+    64x64x64 = 8,388,608 neurons, T=64, bit-packed spikes."""
+    _sampled_parity(PAPER, 64, 32 * 64 * 64 * 64, torch.float32, spike_fmt="bits")
