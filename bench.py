@@ -241,6 +241,7 @@ class OracleSample:
         self.op = oracle.OracleParams(tau=f32(1.25), v_th=f32(0.3), v_reset=0.0, alpha=4.0)
         self.desc = f"{name}: T={T}, {cols} of {N} neuron columns (stride-sampled)"
         self.ns = T * cols
+        self.idx, self.layer = idx, (name, T, N, dtype)
 
     def run(self, seconds):
         """Repeat fwd+bwd passes over the sample for ~`seconds`; returns neuron-steps/s."""
@@ -257,6 +258,21 @@ class OracleSample:
         v, t = self.run(seconds)
         return {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
                 "sample": f"{self.desc}, fwd+bwd, fp64 C oracle single-threaded, {t:.1f} s"}
+
+    def parity(self, spikes, grad_x, v_final=None):
+        """Compare the GPU outputs of the timed workload's first batch on the sampled columns
+        with the oracle (tests/parity.py protocol).  spikes / grad_x: [T, cols] host tensors."""
+        import torch
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        from parity import compare, oracle_run
+        from types import SimpleNamespace
+        p = SimpleNamespace(tau=1.25, v_th=0.3, v_reset=0.0, reset="hard", decay_input=False,
+                            detach_reset=False, surrogate="sigmoid", alpha=4.0)
+        ref = oracle_run(p, torch.from_numpy(self.X), torch.from_numpy(self.G))
+        rep = compare(p, ref, ref["gX"], ref["gvi"], spikes, grad_x, vf_gpu=v_final,
+                      io_bf16=(self.layer[3] == torch.bfloat16), col_ids=self.idx)
+        return {"pass": rep.ok, "cols": int(len(self.idx)), "tie_cols": rep.tie_cols,
+                "max_abs_err": rep.max_err, "failures": rep.failures[:3]}
 
 
 # ----------------------------------------------------------------------------- cfg1 sweep
@@ -634,6 +650,7 @@ def run_ours(args):
             "frac": round(achieved / peak, 4), "traffic": traffic,
             "kernel": f"lif_{'backward_recompute' if (dom == 'bwd' and args.save_mode == 'recompute') else ('backward_saveh' if dom == 'bwd' else 'forward')}_kernel",
             "peak_kind": peak_kind, "algorithmic_bytes_per_launch": dom_bytes / nlaunch,
+            "frac_of_nominal_8TBps": round(achieved / 8000.0, 4),
             "fwd_ms": round(fwd_ms, 4), "bwd_ms": round(bwd_ms, 4),
             "fwd_GBps": round(bpf / (fwd_ms / 1e3) / 1e9, 1),
             "bwd_GBps": round(bpb / (bwd_ms / 1e3) / 1e9, 1),
@@ -692,7 +709,16 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = OracleSample(layers).baseline(args.cpu_seconds)
+        smp = OracleSample(layers)
+        cpu = smp.baseline(args.cpu_seconds)
+        # parity of the timed path on the same sampled columns (batch 0 of the largest layer)
+        b = max(bufs, key=lambda q: q["T"] * q["N"])
+        f = snn.lif_forward(b["XX"][0], params, spike_fmt=args.spike_fmt, save_mode=args.save_mode)
+        gx, _ = snn.lif_backward(b["GG"][0], f, return_grad_v_init=False)
+        ci = torch.as_tensor(smp.idx, device=dev)
+        S = f.spikes if args.spike_fmt != "bits" else snn.unpack_bits(f.spikes, b["N"])
+        cpu["parity"] = smp.parity(S[:, ci].cpu(), gx[:, ci].cpu(), f.v_final[ci].cpu())
+        del f, gx
 
     if rank == 0:
         cfg = workload_config(args, world, layers)
