@@ -11,6 +11,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import importlib.util
+import sys
 
 from conftest import ROOT
 
@@ -186,3 +187,77 @@ def test_time_split_over_gloo_matches_whole_axis(world, n_chunks):
     assert sent[0] == n_eff and sent[-1] == n_eff
     assert sum(sent) == 2 * (world - 1) * n_eff
     assert objs[-1][5] is not None and objs[0][6] is not None
+
+
+# ----------------------------------------------------------------------------- f3 pipeline
+
+def _load_pipeline():
+    """pipeline.py imports `.dist`; provide it as a package-less module pair."""
+    import types
+    pkg = types.ModuleType("snn_pkg_cpu")
+    pkg.__path__ = []
+    sys.modules["snn_pkg_cpu"] = pkg
+    sys.modules["snn_pkg_cpu.dist"] = D
+    spec = importlib.util.spec_from_file_location("snn_pkg_cpu.pipeline",
+                                                  os.path.join(ROOT, "paper_2408_00280_b200", "pipeline.py"))
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules["snn_pkg_cpu.pipeline"] = mod
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def _build_model(P, rank, world, transport, op, seed=0):
+    torch.manual_seed(seed)
+    fwd_fn, bwd_fn = _oracle_fns(op)
+    lin1 = torch.nn.Linear(24, 40)
+    lin2 = torch.nn.Linear(40, 5)
+    return torch.nn.Sequential(P.TimeFolded(lin1),
+                               P.TimeSplitLIFLayer(rank, world, transport, fwd_fn, bwd_fn, n_chunks=3, align=4),
+                               P.TimeFolded(lin2))
+
+
+def _pipeline_worker(rank, world, path, T, out):
+    dist.init_process_group("gloo", init_method=f"file://{path}", rank=rank, world_size=world)
+    import oracle
+    import snn_synth
+    P = _load_pipeline()
+    op = oracle.OracleParams(tau=float(np.float32(1.25)), v_th=float(np.float32(0.3)), v_reset=0.0)
+    a, b = D.partition_time(T, world)[rank]
+    x = snn_synth.normal_tensor(91, b - a, 8 * 24, t_offset=a, n_global=8 * 24).reshape(b - a, 8, 24)
+    target = torch.arange(8) % 5
+    model = _build_model(P, rank, world, D.HostTransport(), op)
+    tr = P.TimeSplitTrainer(model, T)
+    loss = tr.step(x, torch.nn.functional.cross_entropy, target)
+    grads = [p.grad.detach().numpy().copy() for p in model.parameters()]
+    if rank == 0:
+        out.put((float(loss), grads))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_layer_pipelined_time_split_training_step_equals_whole_axis(world):
+    """SURVEY f3 / Fig. 1(b): Linear -> time-split LIF -> Linear, rate-coded cross-entropy.
+    k ranks each own a time segment of every layer; loss and (all-reduced) weight gradients
+    equal one whole-axis step (oracle as the LIF compute; gloo on CPU)."""
+    import oracle
+    import snn_synth
+    T = 13
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    path = _rendezvous_file()
+    procs = [ctx.Process(target=_pipeline_worker, args=(r, world, path, T, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    loss_k, grads_k = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    P = _load_pipeline()
+    op = oracle.OracleParams(tau=float(np.float32(1.25)), v_th=float(np.float32(0.3)), v_reset=0.0)
+    x = snn_synth.normal_tensor(91, T, 8 * 24).reshape(T, 8, 24)
+    model = _build_model(P, 0, 1, None, op)
+    loss_1 = P.TimeSplitTrainer(model, T).step(x, torch.nn.functional.cross_entropy, torch.arange(8) % 5)
+    assert loss_k == pytest.approx(float(loss_1), rel=1e-6)
+    for gk, p in zip(grads_k, model.parameters()):
+        np.testing.assert_allclose(gk, p.grad.numpy(), rtol=1e-5, atol=1e-6)

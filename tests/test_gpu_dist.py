@@ -77,3 +77,59 @@ def test_time_split_bitwise_equals_whole_axis(world, n_chunks, dtype):
     assert np.array_equal(np.concatenate([o[3] for o in objs], 0), as_np(gx))   # bitwise (int16 view for bf16)
     assert np.array_equal(objs[-1][4], as_np(f.v_final))
     assert np.array_equal(objs[0][5], as_np(gvi))
+
+
+def _pipe_worker(rank, world, path, T, out):
+    dist.init_process_group("gloo", init_method=f"file://{path}", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    import paper_2408_00280_b200 as snn
+    from paper_2408_00280_b200 import dist as D, pipeline as P
+    import snn_synth
+    torch.manual_seed(0)
+    fwd_fn, bwd_fn = D.lif_segment_fns(snn.LIFParams.paper(), spike_fmt="io")
+    model = torch.nn.Sequential(
+        P.TimeFolded(torch.nn.Conv2d(2, 16, 3, padding=1)),
+        P.TimeSplitLIFLayer(rank, world, D.HostTransport(), fwd_fn, bwd_fn, n_chunks=2),
+        P.TimeFolded(torch.nn.Flatten()), P.TimeFolded(torch.nn.Linear(16 * 16 * 16, 10))).cuda()
+    a, b = D.partition_time(T, world)[rank]
+    x = snn_synth.normal_tensor(93, b - a, 4 * 2 * 16 * 16, t_offset=a, device="cuda").reshape(b - a, 4, 2, 16, 16)
+    loss = P.TimeSplitTrainer(model, T).step(x, torch.nn.functional.cross_entropy,
+                                            torch.arange(4, device="cuda") % 10)
+    grads = [p.grad.detach().cpu().numpy() for p in model.parameters()]
+    if rank == 0:
+        out.put((float(loss), grads))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_conv_snn_time_split_training_step(world):
+    """SURVEY f3 / Fig. 1(b) with the CUDA kernels: Conv -> time-split LIF -> Linear,
+    k processes own time segments of every layer; loss and all-reduced weight gradients
+    match one whole-axis step (conv/linear run on different batch sizes, so tolerance)."""
+    import paper_2408_00280_b200 as snn
+    from paper_2408_00280_b200 import dist as D, pipeline as P
+    import snn_synth
+    T = 20
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    path = _rendezvous_file()
+    ps = [ctx.Process(target=_pipe_worker, args=(r, world, path, T, q)) for r in range(world)]
+    for pr in ps:
+        pr.start()
+    loss_k, grads_k = q.get(timeout=300)
+    for pr in ps:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    torch.manual_seed(0)
+    fwd_fn, bwd_fn = D.lif_segment_fns(snn.LIFParams.paper(), spike_fmt="io")
+    model = torch.nn.Sequential(
+        P.TimeFolded(torch.nn.Conv2d(2, 16, 3, padding=1)),
+        P.TimeSplitLIFLayer(0, 1, None, fwd_fn, bwd_fn, n_chunks=2),
+        P.TimeFolded(torch.nn.Flatten()), P.TimeFolded(torch.nn.Linear(16 * 16 * 16, 10))).cuda()
+    x = snn_synth.normal_tensor(93, T, 4 * 2 * 16 * 16, device="cuda").reshape(T, 4, 2, 16, 16)
+    loss_1 = P.TimeSplitTrainer(model, T).step(x, torch.nn.functional.cross_entropy,
+                                               torch.arange(4, device="cuda") % 10)
+    assert loss_k == pytest.approx(float(loss_1), rel=1e-5)
+    for gk, p in zip(grads_k, model.parameters()):
+        np.testing.assert_allclose(gk, p.grad.cpu().numpy(), rtol=2e-4, atol=2e-5)
