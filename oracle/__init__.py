@@ -18,4 +18,6 @@ from .oracle import (  # noqa: F401
     backward,
     surrogate,
     smooth_step,
+    affine_input,
+    affine_grads,
 )

@@ -196,3 +196,38 @@ void lif_oracle_backward(const lif_oracle_params* p, int64_t T, int64_t N,
     if (grad_v_init)
         for (int64_t n = 0; n < N; ++n) grad_v_init[n] = gV[n];
 }
+
+/*
+ * Per-channel affine prologue (a BatchNorm affine folded into the LIF
+ * input).  Plain definition: the layer's input current is
+ *     X'[t, n] = scale[c] * X[t, n] + shift[c],   c = (n / HW) % C,
+ * and, by the chain rule through that line,
+ *     dL/dX[t, n] = scale[c] * dL/dX'[t, n],
+ *     dL/dscale[c] = sum_{t, n: c(n) = c} dL/dX'[t, n] * X[t, n],
+ *     dL/dshift[c] = sum_{t, n: c(n) = c} dL/dX'[t, n].
+ * Pinned by finite differences of the smoothed model (tests/test_oracle_pins.py).
+ */
+void lif_oracle_affine_input(int64_t T, int64_t N, const double* x, const double* scale,
+                             const double* shift, int64_t C, int64_t HW, double* xout)
+{
+    for (int64_t t = 0; t < T; ++t)
+        for (int64_t n = 0; n < N; ++n) {
+            int64_t c = (n / HW) % C;
+            xout[t * N + n] = scale[c] * x[t * N + n] + shift[c];
+        }
+}
+
+void lif_oracle_affine_grads(int64_t T, int64_t N, const double* x, const double* gxp,
+                             const double* scale, int64_t C, int64_t HW,
+                             double* gx, double* gscale, double* gshift)
+{
+    for (int64_t c = 0; c < C; ++c) { gscale[c] = 0.0; gshift[c] = 0.0; }
+    for (int64_t t = 0; t < T; ++t)
+        for (int64_t n = 0; n < N; ++n) {
+            int64_t c = (n / HW) % C;
+            double g = gxp[t * N + n];
+            gx[t * N + n] = scale[c] * g;
+            gscale[c] += g * x[t * N + n];
+            gshift[c] += g;
+        }
+}

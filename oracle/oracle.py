@@ -86,6 +86,11 @@ def _load():
         lib.lif_oracle_backward.argtypes = [P, ctypes.c_int64, ctypes.c_int64, dp, dp, dp,
                                             dp, dp, dp, dp, dp]
         lib.lif_oracle_backward.restype = None
+        i64 = ctypes.c_int64
+        lib.lif_oracle_affine_input.argtypes = [i64, i64, dp, dp, dp, i64, i64, dp]
+        lib.lif_oracle_affine_input.restype = None
+        lib.lif_oracle_affine_grads.argtypes = [i64, i64, dp, dp, dp, i64, i64, dp, dp, dp]
+        lib.lif_oracle_affine_grads.restype = None
         _lib = lib
     return _lib
 
@@ -146,3 +151,22 @@ def backward(p: OracleParams, gS, H, grad_v_final=None, return_terms=False):
     if return_terms:
         return gX, gvi, {"delta": d, "dVdH": dv}
     return gX, gvi
+
+
+def affine_input(x, scale, shift, C, HW):
+    """X'[t, n] = scale[c] X[t, n] + shift[c], c = (n / HW) % C."""
+    x = _f64(x); scale = _f64(scale); shift = _f64(shift)
+    T, N = x.shape
+    out = np.empty((T, N))
+    _load().lif_oracle_affine_input(T, N, _dp(x), _dp(scale), _dp(shift), int(C), int(HW), _dp(out))
+    return out
+
+
+def affine_grads(x, gxp, scale, C, HW):
+    """(dL/dX, dL/dscale [C], dL/dshift [C]) from dL/dX' through the affine prologue."""
+    x = _f64(x); gxp = _f64(gxp); scale = _f64(scale)
+    T, N = x.shape
+    gx = np.empty((T, N)); gs = np.empty(int(C)); gb = np.empty(int(C))
+    _load().lif_oracle_affine_grads(T, N, _dp(x), _dp(gxp), _dp(scale), int(C), int(HW), _dp(gx),
+                                    _dp(gs), _dp(gb))
+    return gx, gs, gb

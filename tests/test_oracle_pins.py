@@ -392,3 +392,49 @@ def test_t1_n1_and_empty_carry_defaults():
     gX, gvi = backward(CFG0, np.ones((1, 1)), r["H"])
     assert gX[0, 0] == pytest.approx(0.5)   # s * delta(0) = 0.5 * 1
     assert gvi[0] == pytest.approx(0.5 * 1.0)
+
+
+# ----------------------------------------------------------------------------- affine prologue (f4)
+
+from oracle import affine_grads, affine_input  # noqa: E402
+
+
+def test_affine_identity_and_channel_map():
+    rng = np.random.default_rng(21)
+    T, B, C, HW = 3, 2, 3, 4
+    x = rng.normal(size=(T, B * C * HW))
+    np.testing.assert_array_equal(affine_input(x, np.ones(C), np.zeros(C), C, HW), x)
+    scale = np.array([2.0, -1.0, 0.5]); shift = np.array([0.25, 0.0, -1.0])
+    xp = affine_input(x, scale, shift, C, HW)
+    xr = x.reshape(T, B, C, HW)       # independent reshape-based definition of c(n)
+    np.testing.assert_allclose(xp, (xr * scale[None, None, :, None] + shift[None, None, :, None]).reshape(T, -1))
+
+
+@pytest.mark.parametrize("decay_input", [False, True])
+def test_affine_gradients_finite_differences(decay_input):
+    """Smoothed model: L(scale, shift, X) = sum W*S + w_v . V_final with the LIF input
+    X' = scale[c] X + shift[c]; oracle backward + affine_grads vs central differences."""
+    rng = np.random.default_rng(22)
+    T, B, C, HW = 5, 2, 2, 3
+    N = B * C * HW
+    p = OracleParams(tau=1.6, v_th=0.7, v_reset=0.1, decay_input=decay_input, alpha=2.5, smoothed=True)
+    X = rng.uniform(-0.5, 1.5, size=(T, N))
+    scale = np.array([1.3, 0.8]); shift = np.array([0.2, -0.1])
+    W = rng.normal(size=(T, N)); wv = rng.normal(size=N)
+
+    def loss(sc, sh, xx):
+        r = forward(p, affine_input(xx, sc, sh, C, HW))
+        return float((W * r["S"]).sum() + (wv * r["v_final"]).sum())
+
+    r = forward(p, affine_input(X, scale, shift, C, HW))
+    gxp, _ = backward(p, W, r["H"], grad_v_final=wv)
+    gx, gs, gb = affine_grads(X, gxp, scale, C, HW)
+    h = 1e-6
+    for c in range(C):
+        e = np.zeros(C); e[c] = h
+        assert gs[c] == pytest.approx((loss(scale + e, shift, X) - loss(scale - e, shift, X)) / (2 * h), rel=2e-6, abs=1e-8)
+        assert gb[c] == pytest.approx((loss(scale, shift + e, X) - loss(scale, shift - e, X)) / (2 * h), rel=2e-6, abs=1e-8)
+    for (t, n) in [(0, 0), (2, 5), (4, 11)]:
+        Xp = X.copy(); Xp[t, n] += h
+        Xm = X.copy(); Xm[t, n] -= h
+        assert gx[t, n] == pytest.approx((loss(scale, shift, Xp) - loss(scale, shift, Xm)) / (2 * h), rel=2e-6, abs=1e-8)
