@@ -196,6 +196,31 @@ snn_status snn_lif_backward_handoff(const snn_lif_params* params, const snn_lif_
                                     const float* grad_v_final, const snn_lif_handoff* handoff,
                                     void* grad_x, float* grad_v_init, void* stream);
 
+/* ---- Producer fusion: a per-channel affine prologue folded into the LIF
+ * input -- the layer's current is X' = scale[c] X + shift[c] with c = (n / HW) % C, e.g. the
+ * BatchNorm affine of a conv output [T, B, C, H, W] flattened to N = B C H W -- so the
+ * normalised tensor is never written to / re-read from HBM.  The backward returns
+ * dL/dX = scale[c] dL/dX' and the per-channel sums the BN backward needs,
+ * grad_scale[c] = sum_{t,n in c} dL/dX'[t,n] X[t,n] and grad_shift[c] = sum dL/dX'[t,n]
+ * (per-neuron partials in caller scratch, then a deterministic fixed-order reduction).
+ * Requirements: N % (C * HW) == 0; backward needs save_mode SAVE_RECOMPUTE. */
+typedef struct {
+    const float* scale;   /* [C] fp32 */
+    const float* shift;   /* [C] fp32 */
+    int64_t C;            /* channels (>= 1)                                          */
+    int64_t HW;           /* neurons per channel per sample (>= 1)                    */
+} snn_lif_affine;
+
+snn_status snn_lif_forward_affine(const snn_lif_params* params, const snn_lif_shape* shape,
+                                  const void* x, const float* v_init, const snn_lif_affine* affine,
+                                  void* spikes, void* saved, float* v_final, void* stream);
+/* part_a, part_b: [N] fp32 caller scratch; grad_scale, grad_shift: [C] fp32 outputs. */
+snn_status snn_lif_backward_affine(const snn_lif_params* params, const snn_lif_shape* shape,
+                                   const void* grad_spikes, const void* x, const void* saved,
+                                   const float* grad_v_final, const snn_lif_affine* affine,
+                                   void* grad_x, float* grad_v_init, float* part_a, float* part_b,
+                                   float* grad_scale, float* grad_shift, void* stream);
+
 /* ---- Baseline, not the method: the paper's "Serial (CUDA)" training of Fig. 3
  * (Fig. 5 caption PAPER.md:419) -- ONE time step per call, the membrane
  * state round-tripped through caller memory between steps, for the fused-vs-serial

@@ -7,7 +7,9 @@ library and raises if it is missing: there is no CPU fallback.
 """
 from . import _lib  # noqa: F401  (fails loudly when libsnn_lif.so is absent)
 from .lif import LIFForward, LIFParams, lif_backward, lif_forward, unpack_bits  # noqa: F401
-from .autograd import FusedLIF, LIFLayer  # noqa: F401
+from .autograd import AffineLIFLayer, FusedAffineLIF, FusedLIF, LIFLayer  # noqa: F401
+from .lif import AffineSpec, lif_backward_affine, lif_forward_affine  # noqa: F401
 
 __all__ = ["LIFParams", "LIFForward", "lif_forward", "lif_backward", "unpack_bits",
-           "FusedLIF", "LIFLayer"]
+           "FusedLIF", "LIFLayer", "FusedAffineLIF", "AffineLIFLayer", "AffineSpec",
+           "lif_forward_affine", "lif_backward_affine"]

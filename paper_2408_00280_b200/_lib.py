@@ -28,7 +28,7 @@ EXPORTED_SYMBOLS = (
     "snn_lif_saved_bytes", "snn_lif_forward", "snn_lif_backward", "snn_status_string",
     "snn_last_error_message", "snn_lif_abi_version", "snn_lif_serial_forward_step",
     "snn_lif_serial_backward_step", "snn_lif_handoff_blocks", "snn_lif_forward_handoff",
-    "snn_lif_backward_handoff",
+    "snn_lif_backward_handoff", "snn_lif_forward_affine", "snn_lif_backward_affine",
 )
 SNN_LIF_HANDOFF_BLOCK = 256
 
@@ -44,6 +44,11 @@ class snn_lif_shape(ctypes.Structure):
     _fields_ = [("T", ctypes.c_int64), ("N", ctypes.c_int64), ("ld", ctypes.c_int64),
                 ("io_dtype", ctypes.c_int), ("spike_fmt", ctypes.c_int),
                 ("save_mode", ctypes.c_int)]
+
+
+class snn_lif_affine(ctypes.Structure):
+    _fields_ = [("scale", ctypes.c_void_p), ("shift", ctypes.c_void_p), ("C", ctypes.c_int64),
+                ("HW", ctypes.c_int64)]
 
 
 class snn_lif_handoff(ctypes.Structure):
@@ -86,6 +91,11 @@ def _load() -> ctypes.CDLL:
     lib.snn_lif_forward_handoff.restype = ctypes.c_int
     lib.snn_lif_backward_handoff.argtypes = [P, S, vp, vp, vp, fp, Hp, vp, fp, vp]
     lib.snn_lif_backward_handoff.restype = ctypes.c_int
+    Ap = ctypes.POINTER(snn_lif_affine)
+    lib.snn_lif_forward_affine.argtypes = [P, S, vp, fp, Ap, vp, vp, fp, vp]
+    lib.snn_lif_forward_affine.restype = ctypes.c_int
+    lib.snn_lif_backward_affine.argtypes = [P, S, vp, vp, vp, fp, Ap, vp, fp, fp, fp, fp, fp, vp]
+    lib.snn_lif_backward_affine.restype = ctypes.c_int
     return lib
 
 
@@ -142,3 +152,15 @@ def snn_lif_backward_handoff(params, shape, grad_spikes, x, saved, grad_v_final,
     check(lib.snn_lif_backward_handoff(ctypes.byref(params), ctypes.byref(shape), grad_spikes, x,
                                        saved, grad_v_final, ctypes.byref(handoff), grad_x,
                                        grad_v_init, stream))
+
+
+def snn_lif_forward_affine(params, shape, x, v_init, affine, spikes, saved, v_final, stream) -> None:
+    check(lib.snn_lif_forward_affine(ctypes.byref(params), ctypes.byref(shape), x, v_init,
+                                     ctypes.byref(affine), spikes, saved, v_final, stream))
+
+
+def snn_lif_backward_affine(params, shape, grad_spikes, x, saved, grad_v_final, affine, grad_x,
+                            grad_v_init, part_a, part_b, grad_scale, grad_shift, stream) -> None:
+    check(lib.snn_lif_backward_affine(ctypes.byref(params), ctypes.byref(shape), grad_spikes, x, saved,
+                                      grad_v_final, ctypes.byref(affine), grad_x, grad_v_init, part_a,
+                                      part_b, grad_scale, grad_shift, stream))

@@ -12,7 +12,8 @@ from typing import Optional
 
 import torch
 
-from .lif import LIFParams, lif_backward, lif_forward
+from .lif import (AffineSpec, LIFParams, lif_backward, lif_backward_affine, lif_forward,
+                  lif_forward_affine)
 
 
 class FusedLIF(torch.autograd.Function):
@@ -54,3 +55,44 @@ class LIFLayer(torch.nn.Module):
 
     def extra_repr(self) -> str:
         return f"{self.params}, save_mode={self.save_mode!r}"
+
+
+class FusedAffineLIF(torch.autograd.Function):
+    """spikes = FusedAffineLIF.apply(x, scale, shift, params) for x [T, B, C, *spatial]:
+    the per-channel affine (e.g. BatchNorm's gamma/sigma, beta - mu gamma/sigma) is folded
+    into the LIF prologue, so the normalised tensor never touches HBM."""
+
+    @staticmethod
+    def forward(ctx, x, scale, shift, params: LIFParams):
+        T, B, C = x.shape[:3]
+        HW = x[0, 0, 0].numel()
+        x2 = x.reshape(T, -1)
+        x2 = x2 if x2.is_contiguous() else x2.contiguous()
+        fwd = lif_forward_affine(x2, params, AffineSpec(scale.contiguous(), shift.contiguous(), C, HW),
+                                 spike_fmt="io", return_v_final=False)
+        ctx.fwd = fwd
+        ctx.shape = x.shape
+        return fwd.spikes.reshape(x.shape)
+
+    @staticmethod
+    def backward(ctx, grad_spikes):
+        fwd = ctx.fwd
+        T = grad_spikes.shape[0]
+        gx, _, gsc, gsh = lif_backward_affine(grad_spikes.reshape(T, -1).to(fwd.x.dtype), fwd,
+                                              return_grad_v_init=False)
+        ctx.fwd = None
+        return gx.reshape(ctx.shape), gsc, gsh, None
+
+
+class AffineLIFLayer(torch.nn.Module):
+    """Per-channel affine (learnable scale / shift, init 1 / 0) fused with a LIF layer.
+    Input [T, B, C, *spatial] (time-major)."""
+
+    def __init__(self, channels: int, params: Optional[LIFParams] = None, **kw):
+        super().__init__()
+        self.params = params if params is not None else LIFParams(**kw)
+        self.scale = torch.nn.Parameter(torch.ones(channels))
+        self.shift = torch.nn.Parameter(torch.zeros(channels))
+
+    def forward(self, x):
+        return FusedAffineLIF.apply(x, self.scale, self.shift, self.params)

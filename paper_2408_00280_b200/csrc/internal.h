@@ -24,6 +24,7 @@ int num_sms();
 bool encode_2d(CUtensorMap* m, const void* base, size_t esz, int64_t inner, int64_t outer,
                int64_t ld, int box_inner, int box_outer);
 bool tma_available();
+const char* encode_detail();   // why the last encode_2d on this thread failed
 
 template <int V> using IC = std::integral_constant<int, V>;
 
@@ -79,6 +80,8 @@ snn_status launch_forward_tma_bf16(const snn_lif_shape* s, const snn::FwdArgs& a
 snn_status launch_backward_tma_f32(const snn_lif_shape* s, const snn::BwdArgs& a, int mode, cudaStream_t st);
 snn_status launch_backward_tma_bf16(const snn_lif_shape* s, const snn::BwdArgs& a, int mode, cudaStream_t st);
 int tma_vec_forward(int io_dtype);
+snn_status launch_affine_reduce(const float* part_a, const float* part_b, int64_t B, int64_t C,
+                                int64_t HW, float* grad_scale, float* grad_shift, cudaStream_t st);
 // Serial (one launch per time step) baseline of Fig. 3 -- comparison only (serial.cu).
 snn_status launch_serial_forward_step(int io_dtype, bool soft, const void* x_t, float* V, uint8_t* s_t,
                                       float* h_t, int64_t N, const snn::LifConsts& c, cudaStream_t st);

@@ -28,7 +28,7 @@ snn_status launch_forward_tma(const snn_lif_shape* s, const snn::FwdArgs& a, boo
     using Cfg = snn::FwdTma<IO, C::FV, C::FN, C::FR, C::FS>;
     CUtensorMap tmx;
     if (!encode_2d(&tmx, a.x, sizeof(IO), s->N, s->T, s->ld, Cfg::BW, C::FR))
-        return fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled failed for x");
+        return fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled failed for x%s", encode_detail());
     const int64_t ntiles = (s->N + Cfg::W - 1) / Cfg::W;
     auto go = [&](auto sfmt, auto save, auto sft) {
         auto k = snn::lif_forward_tma_kernel<IO, C::FV, decltype(sfmt)::value, decltype(save)::value,
@@ -56,15 +56,17 @@ snn_status launch_forward_tma(const snn_lif_shape* s, const snn::FwdArgs& a, boo
 template <typename IO, int MODE>
 snn_status launch_backward_tma_mode(const snn_lif_shape* s, const snn::BwdArgs& a, cudaStream_t st) {
     using C = TmaCfg<IO>;
+    if constexpr (MODE < 8) {   // SAVE_H has no affine-gradient variant (host rejects it)
     if (s->save_mode == SNN_SAVE_H) {
         using Cfg = snn::BwdHTma<IO, C::HV, C::HN, C::HR, C::HS>;
         CUtensorMap tmh, tmg;
         if (!encode_2d(&tmh, a.saved, 4, s->N, s->T, a.ldh, Cfg::BW, C::HR) ||
             !encode_2d(&tmg, a.gS, sizeof(IO), s->N, s->T, s->ld, Cfg::BW, C::HR))
-            return fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled failed (SAVE_H backward)");
+            return fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled failed (SAVE_H backward)%s", encode_detail());
         auto k = snn::lif_backward_saveh_tma_kernel<IO, C::HV, MODE, C::HN, C::HR, C::HS>;
         return launch_tiles(k, Cfg::THREADS, Cfg::SMEM, (s->N + Cfg::W - 1) / Cfg::W,
                             (s->T + C::HR - 1) / C::HR, st, "lif_backward_saveh_tma_kernel", tmh, tmg, a);
+    }
     }
     using Cfg = snn::BwdRecTma<IO, C::RV, C::RN, C::RS>;
     const int64_t nch = (s->T + snn::kCkpt - 1) / snn::kCkpt;
@@ -72,7 +74,7 @@ snn_status launch_backward_tma_mode(const snn_lif_shape* s, const snn::BwdArgs& 
     if (!encode_2d(&tmx, a.x, sizeof(IO), s->N, s->T, s->ld, Cfg::BW, snn::kCkpt) ||
         !encode_2d(&tmg, a.gS, sizeof(IO), s->N, s->T, s->ld, Cfg::BW, snn::kCkpt) ||
         !encode_2d(&tmck, a.saved, 4, s->N, nch, a.ldh, Cfg::BW, 1))
-        return fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled failed (RECOMPUTE backward)");
+        return fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled failed (RECOMPUTE backward)%s", encode_detail());
     auto k = snn::lif_backward_recompute_tma_kernel<IO, C::RV, MODE, C::RN, C::RS>;
     return launch_tiles(k, Cfg::THREADS, Cfg::SMEM, (s->N + Cfg::W - 1) / Cfg::W, nch, st,
                         "lif_backward_recompute_tma_kernel", tmx, tmg, tmck, a);
@@ -81,7 +83,7 @@ snn_status launch_backward_tma_mode(const snn_lif_shape* s, const snn::BwdArgs& 
 template <typename IO>
 snn_status launch_backward_tma(const snn_lif_shape* s, const snn::BwdArgs& a, int mode,
                                cudaStream_t st) {
-    switch (mode & 7) {
+    switch (mode & 15) {
         case 0: return launch_backward_tma_mode<IO, 0>(s, a, st);
         case 1: return launch_backward_tma_mode<IO, 1>(s, a, st);
         case 2: return launch_backward_tma_mode<IO, 2>(s, a, st);
@@ -89,7 +91,15 @@ snn_status launch_backward_tma(const snn_lif_shape* s, const snn::BwdArgs& a, in
         case 4: return launch_backward_tma_mode<IO, 4>(s, a, st);
         case 5: return launch_backward_tma_mode<IO, 5>(s, a, st);
         case 6: return launch_backward_tma_mode<IO, 6>(s, a, st);
-        default: return launch_backward_tma_mode<IO, 7>(s, a, st);
+        case 7: return launch_backward_tma_mode<IO, 7>(s, a, st);
+        case 8: return launch_backward_tma_mode<IO, 8>(s, a, st);
+        case 9: return launch_backward_tma_mode<IO, 9>(s, a, st);
+        case 10: return launch_backward_tma_mode<IO, 10>(s, a, st);
+        case 11: return launch_backward_tma_mode<IO, 11>(s, a, st);
+        case 12: return launch_backward_tma_mode<IO, 12>(s, a, st);
+        case 13: return launch_backward_tma_mode<IO, 13>(s, a, st);
+        case 14: return launch_backward_tma_mode<IO, 14>(s, a, st);
+        default: return launch_backward_tma_mode<IO, 15>(s, a, st);
     }
 }
 

@@ -38,6 +38,7 @@ struct Mode {
     static constexpr int SURR = MODE & 1;
     static constexpr bool SOFT = (MODE & 2) != 0;
     static constexpr bool DETACH = (MODE & 4) != 0;
+    static constexpr bool AFF = (MODE & 8) != 0;   // affine prologue gradients (RECOMPUTE only)
 };
 
 __device__ __forceinline__ float ex2_approx(float x) {  // MUFU.EX2, ftz

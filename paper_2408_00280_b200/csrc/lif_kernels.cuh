@@ -32,6 +32,41 @@ struct Handoff {
     int epoch;                // > 0, increases by one per call
 };
 
+// Per-channel affine prologue folded into the LIF input: the layer input
+// is X' = scale[c] X + shift[c] with c = (n / HW) % C (e.g. the BN affine of a conv
+// output [T, B, C, H, W] flattened to N = B C H W).  scale = null: identity (the plain path;
+// fma(1, X, 0) == X, so the arithmetic is unchanged).  Backward (RECOMPUTE only):
+// dL/dX = scale[c] dL/dX', and per-neuron partials part_a[n] = sum_t dL/dX'[t,n] X[t,n],
+// part_b[n] = sum_t dL/dX'[t,n], reduced per channel by affine_reduce_kernel.
+struct Affine {
+    const float* scale;   // [C] or null
+    const float* shift;   // [C]
+    int64_t C, HW;
+    float* part_a;        // [N] backward output (per-neuron sum over t) or null
+    float* part_b;        // [N]
+};
+
+template <int VEC>
+struct AffCoef {
+    float a[VEC], b[VEC];
+};
+
+template <int VEC>
+__device__ __forceinline__ AffCoef<VEC> load_affine(const Affine& af, int64_t n0, int nvalid) {
+    AffCoef<VEC> co;
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) {
+        co.a[i] = 1.0f;
+        co.b[i] = 0.0f;
+        if (af.scale != nullptr && i < nvalid) {
+            const int64_t ch = ((n0 + i) / af.HW) % af.C;
+            co.a[i] = __ldg(af.scale + ch);
+            co.b[i] = __ldg(af.shift + ch);
+        }
+    }
+    return co;
+}
+
 struct FwdArgs {
     const void* x;        // [T, ld] IO
     const float* v_init;  // [N] or null
@@ -41,6 +76,7 @@ struct FwdArgs {
     int64_t T, N, ld, ldh, nwords;
     LifConsts c;
     Handoff h;            // boundary V from / to the neighbour time segment (TMA path only)
+    Affine af;            // input prologue (identity when af.scale == null)
 };
 
 struct BwdArgs {
@@ -53,6 +89,7 @@ struct BwdArgs {
     int64_t T, N, ld, ldh;
     LifConsts c;
     Handoff h;                  // boundary dL/dV from / to the neighbour segment (TMA path only)
+    Affine af;                  // input prologue + its per-neuron gradient partials
 };
 
 // ------------------------------------------------------------------------------------
@@ -62,12 +99,15 @@ struct BwdArgs {
 // spike bits (bit i = neuron i of the group).
 template <bool SOFT, typename IO, int VEC>
 __device__ __forceinline__ unsigned fwd_compute(const LifConsts& c, float (&V)[VEC],
-                                                const Pack<IO, VEC>& xv, Pack<float, VEC>& hp) {
+                                                const Pack<IO, VEC>& xv, Pack<float, VEC>& hp,
+                                                const AffCoef<VEC>& co) {
     unsigned bits = 0;
     if constexpr (VEC % 2 == 0) {   // paired FFMA2 charge, same roundings as the scalar path
 #pragma unroll
         for (int i = 0; i < VEC; i += 2) {
-            const F2 H2 = lif_charge2(c, f2(V[i], V[i + 1]), f2(to_f32(xv.v[i]), to_f32(xv.v[i + 1])));
+            const F2 X2 = fma2(f2(co.a[i], co.a[i + 1]), f2(to_f32(xv.v[i]), to_f32(xv.v[i + 1])),
+                               f2(co.b[i], co.b[i + 1]));
+            const F2 H2 = lif_charge2(c, f2(V[i], V[i + 1]), X2);
             const float Ha = lo(H2), Hb = hi(H2);
             const bool Sa = lif_fire(c, Ha), Sb = lif_fire(c, Hb);
             V[i] = lif_reset<SOFT>(c, Ha, Sa);
@@ -79,7 +119,7 @@ __device__ __forceinline__ unsigned fwd_compute(const LifConsts& c, float (&V)[V
     } else {
 #pragma unroll
         for (int i = 0; i < VEC; ++i) {
-            const float H = lif_charge(c, V[i], to_f32(xv.v[i]));
+            const float H = lif_charge(c, V[i], __fmaf_rn(co.a[i], to_f32(xv.v[i]), co.b[i]));
             const bool S = lif_fire(c, H);
             V[i] = lif_reset<SOFT>(c, H, S);
             hp.v[i] = H;
@@ -92,11 +132,14 @@ __device__ __forceinline__ unsigned fwd_compute(const LifConsts& c, float (&V)[V
 // Re-run the charge / fire / reset (no outputs) -- the RECOMPUTE backward's forward pass.
 template <bool SOFT, typename IO, int VEC>
 __device__ __forceinline__ void fwd_recompute_step(const LifConsts& c, float (&V)[VEC],
-                                                   const Pack<IO, VEC>& xv, float (&h)[VEC]) {
+                                                   const Pack<IO, VEC>& xv, float (&h)[VEC],
+                                                   const AffCoef<VEC>& co) {
     if constexpr (VEC % 2 == 0) {
 #pragma unroll
         for (int i = 0; i < VEC; i += 2) {
-            const F2 H2 = lif_charge2(c, f2(V[i], V[i + 1]), f2(to_f32(xv.v[i]), to_f32(xv.v[i + 1])));
+            const F2 X2 = fma2(f2(co.a[i], co.a[i + 1]), f2(to_f32(xv.v[i]), to_f32(xv.v[i + 1])),
+                               f2(co.b[i], co.b[i + 1]));
+            const F2 H2 = lif_charge2(c, f2(V[i], V[i + 1]), X2);
             h[i] = lo(H2);
             h[i + 1] = hi(H2);
             V[i] = lif_reset<SOFT>(c, h[i], lif_fire(c, h[i]));
@@ -105,7 +148,7 @@ __device__ __forceinline__ void fwd_recompute_step(const LifConsts& c, float (&V
     } else {
 #pragma unroll
         for (int i = 0; i < VEC; ++i) {
-            h[i] = lif_charge(c, V[i], to_f32(xv.v[i]));
+            h[i] = lif_charge(c, V[i], __fmaf_rn(co.a[i], to_f32(xv.v[i]), co.b[i]));
             V[i] = lif_reset<SOFT>(c, h[i], lif_fire(c, h[i]));
         }
     }
@@ -168,9 +211,14 @@ __device__ __forceinline__ int64_t spike_row_bytes(const FwdArgs& a) {
 
 // One reverse step of Eq. 3 for this thread's VEC neurons: returns gX[t] (io dtype) and
 // carries gV <- k gH.
-template <typename IO, int VEC, int MODE>
+// AFF = with the affine prologue: gX = scale (s gH) and the per-neuron partials
+// pa += (s gH) X_raw, pb += (s gH) accumulate over the time walk (xr = raw X of this row).
+template <typename IO, int VEC, int MODE, bool AFF = false>
 __device__ __forceinline__ Pack<IO, VEC> bwd_step(const LifConsts& c, float (&gV)[VEC],
-                                                  const float (&h)[VEC], const Pack<IO, VEC>& gs) {
+                                                  const float (&h)[VEC], const Pack<IO, VEC>& gs,
+                                                  const AffCoef<VEC>* co = nullptr,
+                                                  const Pack<IO, VEC>* xr = nullptr,
+                                                  float* pa = nullptr, float* pb = nullptr) {
     Pack<IO, VEC> out;
     if constexpr (VEC % 2 == 0) {   // paired FFMA2/FMUL2/FADD2, same roundings as scalar
 #pragma unroll
@@ -178,7 +226,15 @@ __device__ __forceinline__ Pack<IO, VEC> bwd_step(const LifConsts& c, float (&gV
             const F2 gH = lif_grad_step2<MODE>(c, f2(h[i], h[i + 1]),
                                                f2(to_f32(gs.v[i]), to_f32(gs.v[i + 1])),
                                                f2(gV[i], gV[i + 1]));
-            const F2 gx = mul2(f2(c.s), gH);
+            F2 gx = mul2(f2(c.s), gH);
+            if constexpr (AFF) {
+                const F2 x2 = f2(to_f32(xr->v[i]), to_f32(xr->v[i + 1]));
+                const F2 pa2 = fma2(gx, x2, f2(pa[i], pa[i + 1]));
+                const F2 pb2 = add2(gx, f2(pb[i], pb[i + 1]));
+                pa[i] = lo(pa2); pa[i + 1] = hi(pa2);
+                pb[i] = lo(pb2); pb[i + 1] = hi(pb2);
+                gx = mul2(f2(co->a[i], co->a[i + 1]), gx);
+            }
             const F2 gv = mul2(f2(c.k), gH);
             out.v[i] = from_f32<IO>(lo(gx));
             out.v[i + 1] = from_f32<IO>(hi(gx));
@@ -189,7 +245,13 @@ __device__ __forceinline__ Pack<IO, VEC> bwd_step(const LifConsts& c, float (&gV
 #pragma unroll
         for (int i = 0; i < VEC; ++i) {
             const float gH = lif_grad_step<MODE>(c, h[i], to_f32(gs.v[i]), gV[i]);
-            out.v[i] = from_f32<IO>(__fmul_rn(c.s, gH));
+            float gx = __fmul_rn(c.s, gH);
+            if constexpr (AFF) {
+                pa[i] = __fmaf_rn(gx, to_f32(xr->v[i]), pa[i]);
+                pb[i] = __fadd_rn(gx, pb[i]);
+                gx = __fmul_rn(co->a[i], gx);
+            }
+            out.v[i] = from_f32<IO>(gx);
             gV[i] = __fmul_rn(c.k, gH);
         }
     }
@@ -219,6 +281,7 @@ lif_forward_kernel(const FwdArgs a) {
 #pragma unroll
         for (int i = 0; i < VEC; ++i) V[i] = c.v_reset;
     }
+    const AffCoef<VEC> co = load_affine<VEC>(a.af, n0, nvalid);
 
     Pack<IO, VEC> buf[PF];
 #pragma unroll
@@ -243,7 +306,7 @@ lif_forward_kernel(const FwdArgs a) {
                     }
                 }
                 Pack<float, VEC> hp;
-                const unsigned bits = fwd_compute<SOFT>(c, V, xv, hp);
+                const unsigned bits = fwd_compute<SOFT>(c, V, xv, hp, co);
                 if constexpr (SAVE == SAVE_H) {
                     if (nvalid > 0) st_group<float, VEC>(a.saved + t * a.ldh + n0, hp, nvalid);
                 }
@@ -348,6 +411,11 @@ lif_backward_recompute_kernel(const BwdArgs a) {
         for (int i = 0; i < VEC; ++i) gV[i] = 0.0f;
     }
 
+    constexpr bool AFF = Mode<MODE>::AFF;
+    const AffCoef<VEC> co = load_affine<VEC>(a.af, n0, nvalid);
+    float pa[VEC], pb[VEC];
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) pa[i] = pb[i] = 0.0f;
     const int64_t nchunks = (T + kCkpt - 1) / kCkpt;
     for (int64_t ch = nchunks - 1; ch >= 0; --ch) {
         const int64_t t0 = ch * kCkpt;
@@ -368,14 +436,22 @@ lif_backward_recompute_kernel(const BwdArgs a) {
         for (int i = 0; i < VEC; ++i) V[i] = v0.v[i];
 #pragma unroll
         for (int j = 0; j < kCkpt; ++j) {
-            if (j < len) fwd_recompute_step<Mode<MODE>::SOFT>(c, V, xb[j], h[j]);
+            if (j < len) fwd_recompute_step<Mode<MODE>::SOFT>(c, V, xb[j], h[j], co);
         }
 #pragma unroll
         for (int j = kCkpt - 1; j >= 0; --j) {
             if (j < len)
-                st_group<IO, VEC>(gx + (t0 + j) * ld, bwd_step<IO, VEC, MODE>(c, gV, h[j], gb[j]),
+                st_group<IO, VEC>(gx + (t0 + j) * ld,
+                                  bwd_step<IO, VEC, MODE, AFF>(c, gV, h[j], gb[j], &co, &xb[j], pa, pb),
                                   nvalid);
         }
+    }
+    if constexpr (AFF) {
+        Pack<float, VEC> qa, qb;
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) { qa.v[i] = pa[i]; qb.v[i] = pb[i]; }
+        st_group<float, VEC>(a.af.part_a + n0, qa, nvalid);
+        st_group<float, VEC>(a.af.part_b + n0, qb, nvalid);
     }
     if (a.grad_v_init != nullptr) {
         Pack<float, VEC> gi;

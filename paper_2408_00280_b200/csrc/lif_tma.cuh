@@ -189,6 +189,7 @@ lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const FwdArgs a,
 #pragma unroll
             for (int i = 0; i < VEC; ++i) V[i] = v0.v[i];
         }
+        const AffCoef<VEC> co = load_affine<VEC>(a.af, n0, nvalid);
         unsigned char* spk_row = reinterpret_cast<unsigned char*>(a.spikes);
         float* h_row = a.saved + n0;   // SAVE_H: advanced one row per step
         for (int64_t rb = 0; rb < nrb; ++rb, ++k) {
@@ -216,7 +217,7 @@ lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const FwdArgs a,
                         }
                     }
                     Pack<float, VEC> hp;
-                    const unsigned bits = fwd_compute<SOFT>(c, V, xv, hp);
+                    const unsigned bits = fwd_compute<SOFT>(c, V, xv, hp, co);
                     if constexpr (SAVE == SAVE_H) {
                         if (nv > 0) st_stream<float, VEC>(h_row, hp);
                         h_row += a.ldh;
@@ -265,12 +266,19 @@ struct BwdRecTma {
 template <typename IO, int VEC, int MODE, int BW, int ROWS_MAX>
 __device__ __forceinline__ void bwd_chunk(const LifConsts& c, float (&gV)[VEC],
                                           const float (&h)[ROWS_MAX][VEC], const IO* gsm,
-                                          IO* gxp, int64_t ld, int rows, bool valid) {
+                                          IO* gxp, int64_t ld, int rows, bool valid,
+                                          const AffCoef<VEC>& co, const IO* xs, float* pa, float* pb) {
 #pragma unroll
     for (int j = ROWS_MAX - 1; j >= 0; --j) {
         if (j < rows) {
             const Pack<IO, VEC> gv = *reinterpret_cast<const Pack<IO, VEC>*>(gsm + j * BW);
-            const Pack<IO, VEC> out = bwd_step<IO, VEC, MODE>(c, gV, h[j], gv);
+            Pack<IO, VEC> out;
+            if constexpr (Mode<MODE>::AFF) {
+                const Pack<IO, VEC> xr = *reinterpret_cast<const Pack<IO, VEC>*>(xs + j * BW);
+                out = bwd_step<IO, VEC, MODE, true>(c, gV, h[j], gv, &co, &xr, pa, pb);
+            } else {
+                out = bwd_step<IO, VEC, MODE>(c, gV, h[j], gv);
+            }
             if (valid) st_stream<IO, VEC>(gxp, out);
             gxp -= ld;
         }
@@ -279,12 +287,13 @@ __device__ __forceinline__ void bwd_chunk(const LifConsts& c, float (&gV)[VEC],
 
 template <typename IO, int VEC, int MODE, int BW>
 __device__ __forceinline__ void recompute_chunk(const LifConsts& c, float (&V)[VEC],
-                                                float (&h)[kCkpt][VEC], const IO* xs, int rows) {
+                                                float (&h)[kCkpt][VEC], const IO* xs, int rows,
+                                                const AffCoef<VEC>& co) {
 #pragma unroll
     for (int j = 0; j < kCkpt; ++j) {
         if (j < rows) {
             const Pack<IO, VEC> xv = *reinterpret_cast<const Pack<IO, VEC>*>(xs + j * BW);
-            fwd_recompute_step<Mode<MODE>::SOFT>(c, V, xv, h[j]);
+            fwd_recompute_step<Mode<MODE>::SOFT>(c, V, xv, h[j], co);
         }
     }
 }
@@ -341,6 +350,10 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
         const int64_t n0 = (int64_t)tile * W + nt;
         const bool valid = n0 < N;   // N % VEC == 0 on this path
         const bool tile_full = (int64_t)(tile + 1) * W <= N;   // uniform across the CTA
+        const AffCoef<VEC> co = load_affine<VEC>(a.af, n0, valid ? VEC : 0);
+        float pa[VEC], pb[VEC];
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) pa[i] = pb[i] = 0.0f;
         float gV[VEC];
 #pragma unroll
         for (int i = 0; i < VEC; ++i) gV[i] = 0.0f;
@@ -369,17 +382,26 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
             float h[kCkpt][VEC];
             IO* gxp = gx + (t0 + rows - 1) * ld + n0;
             if (rows == kCkpt && tile_full) {   // full chunk of a full tile: guard-free code
-                recompute_chunk<IO, VEC, MODE, BW>(c, V, h, xs, kCkpt);
-                bwd_chunk<IO, VEC, MODE, BW, kCkpt>(c, gV, h, gsm, gxp, ld, kCkpt, true);
+                recompute_chunk<IO, VEC, MODE, BW>(c, V, h, xs, kCkpt, co);
+                bwd_chunk<IO, VEC, MODE, BW, kCkpt>(c, gV, h, gsm, gxp, ld, kCkpt, true, co, xs, pa, pb);
             } else {
-                recompute_chunk<IO, VEC, MODE, BW>(c, V, h, xs, rows);
-                bwd_chunk<IO, VEC, MODE, BW, kCkpt>(c, gV, h, gsm, gxp, ld, rows, valid);
+                recompute_chunk<IO, VEC, MODE, BW>(c, V, h, xs, rows, co);
+                bwd_chunk<IO, VEC, MODE, BW, kCkpt>(c, gV, h, gsm, gxp, ld, rows, valid, co, xs, pa, pb);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&bar->empty[s]);
         }
         if (a.h.send_state != nullptr || a.h.recv_ack != nullptr)   // uniform across the CTA
             handoff_send<VEC, NCONS>(a.h, tile, W, N, n0, valid, gV);
+        if constexpr (Mode<MODE>::AFF) {
+            if (valid) {
+                Pack<float, VEC> qa, qb;
+#pragma unroll
+                for (int i = 0; i < VEC; ++i) { qa.v[i] = pa[i]; qb.v[i] = pb[i]; }
+                st_stream<float, VEC>(a.af.part_a + n0, qa);
+                st_stream<float, VEC>(a.af.part_b + n0, qb);
+            }
+        }
         if (a.grad_v_init != nullptr && valid) {
             Pack<float, VEC> gi;
 #pragma unroll

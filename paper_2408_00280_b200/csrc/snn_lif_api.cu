@@ -18,6 +18,7 @@ namespace snn_host {
 
 namespace {
 thread_local char g_err[512] = "";
+thread_local char g_enc[256] = "";
 }
 
 snn_status fail(snn_status st, const char* fmt, ...) {
@@ -74,10 +75,26 @@ bool encode_2d(CUtensorMap* m, const void* base, size_t esz, int64_t inner, int6
     const cuuint64_t strides[1] = {(cuuint64_t)(ld * (int64_t)esz)};
     const cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
     const cuuint32_t estr[2] = {1, 1};
-    return fn(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    auto encode = [&] {
+        return fn(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    };
+    CUresult r = encode();
+    if (r == CUDA_ERROR_INVALID_CONTEXT) {
+        // A thread whose first CUDA call is this driver entry point (e.g. torch's autograd
+        // worker) has no current context yet: let the runtime bind the device's primary one.
+        cudaFree(nullptr);
+        r = encode();
+    }
+    if (r != CUDA_SUCCESS)
+        snprintf(g_enc, sizeof(g_enc), " [CUresult %d: base %p map %p dims %lld x %lld ld %lld box %d x %d]",
+                 (int)r, base, (void*)m, (long long)inner, (long long)outer, (long long)ld, box_inner,
+                 box_outer);
+    return r == CUDA_SUCCESS;
 }
+
+const char* encode_detail() { return g_enc; }
 
 int cached_occupancy(const void* k, int threads, int smem, int (*prep)(const void*, int, int)) {
     static std::mutex mu;
@@ -234,9 +251,22 @@ snn::Handoff to_dev(const snn_lif_handoff* h) {
     return d;
 }
 
+bool affine_valid(const snn_lif_affine* af, const snn_lif_shape* s) {
+    if (!af) return true;
+    if (!af->scale || !af->shift || af->C < 1 || af->HW < 1) return false;
+    if (af->C > INT64_MAX / af->HW || s->N % (af->C * af->HW) != 0) return false;
+    return true;
+}
+
+snn::Affine to_dev(const snn_lif_affine* af) {
+    snn::Affine d = {};
+    if (af) { d.scale = af->scale; d.shift = af->shift; d.C = af->C; d.HW = af->HW; }
+    return d;
+}
+
 snn_status forward_impl(const snn_lif_params* p, const snn_lif_shape* s, const void* x,
                         const float* v_init, const snn_lif_handoff* handoff, void* spikes, void* saved,
-                        float* v_final, void* stream) {
+                        float* v_final, void* stream, const snn_lif_affine* affine = nullptr) {
     g_err[0] = 0;
     snn_status st;
     if ((st = check_params(p)) != SNN_OK) return st;
@@ -251,7 +281,7 @@ snn_status forward_impl(const snn_lif_params* p, const snn_lif_shape* s, const v
         (v_final && !aligned(v_final, 4)) || (saved && s->save_mode != SNN_SAVE_NONE && !aligned(saved, 16)))
         return fail(SNN_ERR_MISALIGNED, "a pointer is not aligned to its element size (saved needs 16 B)");
 
-    snn::FwdArgs a;
+    snn::FwdArgs a{};
     a.x = x; a.v_init = v_init; a.spikes = spikes;
     a.saved = s->save_mode == SNN_SAVE_NONE ? nullptr : static_cast<float*>(saved);
     a.v_final = v_final;
@@ -260,7 +290,10 @@ snn_status forward_impl(const snn_lif_params* p, const snn_lif_shape* s, const v
     const bool soft = p->reset_mode == SNN_RESET_SOFT;
     cudaStream_t cs = static_cast<cudaStream_t>(stream);
     if (!handoff_valid(handoff)) return fail(SNN_ERR_INVALID_VALUE, "handoff: epoch < 1 or missing flags");
+    if (!affine_valid(affine, s))
+        return fail(SNN_ERR_INVALID_VALUE, "affine: need scale/shift, C >= 1, HW >= 1, N %% (C*HW) == 0");
     a.h = to_dev(handoff);
+    a.af = to_dev(affine);
 
     if (tma_ok(s, tma_vec_forward(s->io_dtype), {x, v_init, v_final, a.saved, spikes}))
         return s->io_dtype == SNN_BF16 ? launch_forward_tma_bf16(s, a, soft, cs)
@@ -276,7 +309,8 @@ snn_status forward_impl(const snn_lif_params* p, const snn_lif_shape* s, const v
 snn_status backward_impl(const snn_lif_params* p, const snn_lif_shape* s,
                          const void* grad_spikes, const void* x, const void* saved,
                          const float* grad_v_final, const snn_lif_handoff* handoff, void* grad_x,
-                         float* grad_v_init, void* stream) {
+                         float* grad_v_init, void* stream, const snn_lif_affine* affine = nullptr,
+                         float* part_a = nullptr, float* part_b = nullptr) {
     g_err[0] = 0;
     snn_status st;
     if ((st = check_params(p)) != SNN_OK) return st;
@@ -293,15 +327,28 @@ snn_status backward_impl(const snn_lif_params* p, const snn_lif_shape* s,
         !aligned(saved, 16) || (grad_v_final && !aligned(grad_v_final, 4)) ||
         (grad_v_init && !aligned(grad_v_init, 4)))
         return fail(SNN_ERR_MISALIGNED, "a pointer is not aligned to its element size (saved needs 16 B)");
-    snn::BwdArgs a;
+    snn::BwdArgs a{};
     a.gS = grad_spikes; a.x = x; a.saved = static_cast<const float*>(saved);
     a.grad_v_final = grad_v_final; a.gX = grad_x; a.grad_v_init = grad_v_init;
     a.T = s->T; a.N = s->N; a.ld = s->ld; a.ldh = saved_ld(s);
     a.c = make_consts(p);
-    const int mode = mode_of(p);
+    int mode = mode_of(p);
     cudaStream_t cs = static_cast<cudaStream_t>(stream);
     if (!handoff_valid(handoff)) return fail(SNN_ERR_INVALID_VALUE, "handoff: epoch < 1 or missing flags");
     a.h = to_dev(handoff);
+    if (affine) {
+        if (!affine_valid(affine, s))
+            return fail(SNN_ERR_INVALID_VALUE, "affine: need scale/shift, C >= 1, HW >= 1, N %% (C*HW) == 0");
+        if (s->save_mode != SNN_SAVE_RECOMPUTE)
+            return fail(SNN_ERR_UNSUPPORTED, "affine backward needs save_mode SAVE_RECOMPUTE");
+        if (!part_a || !part_b) return fail(SNN_ERR_NULL_POINTER, "affine backward needs part_a / part_b");
+        if (!aligned(part_a, 16) || !aligned(part_b, 16))
+            return fail(SNN_ERR_MISALIGNED, "part_a / part_b must be 16-byte aligned");
+        a.af = to_dev(affine);
+        a.af.part_a = part_a;
+        a.af.part_b = part_b;
+        mode |= 8;
+    }
 
     if (tma_ok(s, tma_vec_backward(s->io_dtype),
                {grad_spikes, grad_x, s->save_mode == SNN_SAVE_RECOMPUTE ? x : nullptr, saved,
@@ -333,6 +380,27 @@ snn_status snn_lif_backward(const snn_lif_params* p, const snn_lif_shape* s,
                             float* grad_v_init, void* stream) {
     (void)v_init;  // the RECOMPUTE checkpoints already hold V[-1]
     return backward_impl(p, s, grad_spikes, x, saved, grad_v_final, nullptr, grad_x, grad_v_init, stream);
+}
+
+snn_status snn_lif_forward_affine(const snn_lif_params* p, const snn_lif_shape* s, const void* x,
+                                  const float* v_init, const snn_lif_affine* af, void* spikes,
+                                  void* saved, float* v_final, void* stream) {
+    if (!af) return fail(SNN_ERR_NULL_POINTER, "affine is NULL");
+    return forward_impl(p, s, x, v_init, nullptr, spikes, saved, v_final, stream, af);
+}
+
+snn_status snn_lif_backward_affine(const snn_lif_params* p, const snn_lif_shape* s,
+                                   const void* grad_spikes, const void* x, const void* saved,
+                                   const float* grad_v_final, const snn_lif_affine* af, void* grad_x,
+                                   float* grad_v_init, float* part_a, float* part_b,
+                                   float* grad_scale, float* grad_shift, void* stream) {
+    if (!af) return fail(SNN_ERR_NULL_POINTER, "affine is NULL");
+    if (!grad_scale || !grad_shift) return fail(SNN_ERR_NULL_POINTER, "grad_scale / grad_shift is NULL");
+    snn_status st = backward_impl(p, s, grad_spikes, x, saved, grad_v_final, nullptr, grad_x, grad_v_init,
+                                  stream, af, part_a, part_b);
+    if (st != SNN_OK) return st;
+    return launch_affine_reduce(part_a, part_b, s->N / (af->C * af->HW), af->C, af->HW, grad_scale,
+                                grad_shift, static_cast<cudaStream_t>(stream));
 }
 
 int64_t snn_lif_handoff_blocks(int64_t N) {

@@ -213,3 +213,69 @@ def lif_serial(x: torch.Tensor, grad_spikes: torch.Tensor, params: LIFParams = L
         _lib.snn_lif_serial_backward_step(cp, io, N, _ptr(grad_spikes[t]), _ptr(H[t]), _ptr(gv),
                                           _ptr(gX[t]), st)
     return S, H, v, gX, gv
+
+
+
+# ----------------------------------------------------------------------------- f4: affine prologue
+
+@dataclass
+class AffineSpec:
+    """Per-channel affine folded into the LIF input: X' = scale[c] X + shift[c],
+    c = (n / HW) % C (include/snn_lif.h snn_lif_affine)."""
+    scale: torch.Tensor   # [C] fp32 CUDA
+    shift: torch.Tensor   # [C] fp32 CUDA
+    C: int
+    HW: int
+
+    def to_c(self) -> _lib.snn_lif_affine:
+        for name, t in (("scale", self.scale), ("shift", self.shift)):
+            if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous() and t.numel() == self.C):
+                raise ValueError(f"affine {name} must be a contiguous fp32 CUDA tensor of C={self.C}")
+        return _lib.snn_lif_affine(self.scale.data_ptr(), self.shift.data_ptr(), self.C, self.HW)
+
+
+def lif_forward_affine(x: torch.Tensor, params: LIFParams, affine: AffineSpec, *,
+                       v_init: Optional[torch.Tensor] = None, spike_fmt: str = "u8",
+                       return_v_final: bool = True) -> LIFForward:
+    """Forward with the affine prologue fused in (RECOMPUTE save mode: the backward re-reads x)."""
+    _check_2d("x", x)
+    T, N = x.shape
+    shape = make_shape(x, spike_fmt, "recompute")
+    cp = params.to_c()
+    v_init = _vec("v_init", v_init, N, x.device)
+    spikes = alloc_spikes(x, spike_fmt)
+    if spike_fmt != "bits" and shape.ld != N:
+        spikes = torch.empty((T, shape.ld), dtype=spikes.dtype, device=x.device)[:, :N]
+    saved = torch.empty(_lib.snn_lif_saved_bytes(cp, shape) // 4, dtype=torch.float32, device=x.device)
+    v_final = torch.empty(N, dtype=torch.float32, device=x.device) if return_v_final else None
+    ca = affine.to_c()
+    _lib.snn_lif_forward_affine(cp, shape, _ptr(x), _ptr(v_init), ca, _ptr(spikes), _ptr(saved),
+                                _ptr(v_final), _stream())
+    f = LIFForward(spikes, saved, v_final, x, v_init, params, shape)
+    f.affine = affine
+    return f
+
+
+def lif_backward_affine(grad_spikes: torch.Tensor, fwd: LIFForward, *,
+                        grad_v_final: Optional[torch.Tensor] = None, return_grad_v_init: bool = True):
+    """Returns (grad_x [T, N] w.r.t. the raw input, grad_v_init, grad_scale [C], grad_shift [C])."""
+    x = fwd.x
+    T, N = x.shape
+    if grad_spikes.dim() == 2 and grad_spikes.size(1) > 1 and grad_spikes.stride(1) != 1:
+        grad_spikes = grad_spikes.contiguous()
+    _check_2d("grad_spikes", grad_spikes)
+    ld = fwd.shape.ld
+    if T > 1 and grad_spikes.stride(0) != ld:
+        grad_spikes = grad_spikes.contiguous() if ld == N else _restride(grad_spikes, ld)
+    af = fwd.affine
+    grad_x = torch.empty((T, ld), dtype=x.dtype, device=x.device)[:, :N]
+    gvi = torch.empty(N, dtype=torch.float32, device=x.device) if return_grad_v_init else None
+    npad = (N + 3) // 4 * 4                      # each partial row 16-byte aligned
+    part = torch.empty((2, npad), dtype=torch.float32, device=x.device)
+    gsc = torch.empty(af.C, dtype=torch.float32, device=x.device)
+    gsh = torch.empty(af.C, dtype=torch.float32, device=x.device)
+    _lib.snn_lif_backward_affine(fwd.params.to_c(), fwd.shape, _ptr(grad_spikes), _ptr(x), _ptr(fwd.saved),
+                                 _ptr(_vec("grad_v_final", grad_v_final, N, x.device)), af.to_c(),
+                                 _ptr(grad_x), _ptr(gvi), _ptr(part[0]), _ptr(part[1]), _ptr(gsc),
+                                 _ptr(gsh), _stream())
+    return grad_x, gvi, gsc, gsh

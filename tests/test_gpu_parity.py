@@ -323,3 +323,123 @@ def test_cfg4_resnet_stem_full_size_sampled():
     """BASELINE configs[4]: the Spiking-ResNet18 DVS stem LIF layer per rank, B=32 x
     64x64x64 = 8,388,608 neurons, T=64, bit-packed spikes."""
     _sampled_parity(PAPER, 64, 32 * 64 * 64 * 64, torch.float32, spike_fmt="bits")
+
+
+# ------------------------------------------------------------------ f4: affine prologue
+
+def _affine_case(p, T, B, C, HW, dtype, seed):
+    N = B * C * HW
+    X = snn_synth.normal_tensor(seed, T, N, dtype=dtype)
+    G = snn_synth.normal_tensor(seed + 1, T, N, dtype=dtype)
+    sc = snn_synth.normal_tensor(seed + 2, 1, C, mean=1.0, std=0.3)[0]
+    sh = snn_synth.normal_tensor(seed + 3, 1, C, std=0.3)[0]
+    return X, G, sc, sh
+
+
+@pytest.mark.parametrize("T,B,C,HW,dtype", [(16, 4, 8, 64, torch.float32), (23, 2, 3, 50, torch.float32),
+                                            (16, 8, 16, 16, torch.bfloat16), (5, 3, 7, 1, torch.float32)])
+def test_affine_prologue_parity(T, B, C, HW, dtype):
+    p = PAPER
+    X, G, sc, sh = _affine_case(p, T, B, C, HW, dtype, 101 + T)
+    N = B * C * HW
+    af = snn.AffineSpec(sc.cuda(), sh.cuda(), C, HW)
+    f = snn.lif_forward_affine(X.cuda(), p, af)
+    gx, gvi, gsc, gsh = snn.lif_backward_affine(G.cuda(), f)
+    torch.cuda.synchronize()
+    Xp = oracle.affine_input(X.double().numpy(), sc.double().numpy(), sh.double().numpy(), C, HW)
+    ref = oracle_run(p, Xp, G)
+    rgx, rgs, rgb = oracle.affine_grads(X.double().numpy(), ref["gX"], sc.double().numpy(), C, HW)
+    # dL/dX = scale * dL/dX': scale the oracle's per-element bound with |scale[c]|
+    cidx = (np.arange(N) // HW) % C
+    ref_scaled = dict(ref)
+    ref_scaled["gX_bound"] = ref["gX_bound"] * np.abs(sc.double().numpy())[cidx][None, :]
+    ref_scaled["gX_sens"] = ref["gX_sens"] * np.abs(sc.double().numpy())[cidx][None, :]
+    rep = compare(p, ref_scaled, rgx, ref["gvi"], f.spikes.cpu(), gx.cpu(), vf_gpu=f.v_final.cpu(),
+                  gvi_gpu=gvi.cpu(), io_bf16=(dtype == torch.bfloat16))
+    assert_ok(rep)
+    assert rep.tie_cols == 0
+    # per-channel sums: bound = rtol * sum of |terms| (+ conditioning w.r.t. H)
+    Xd = X.double().numpy()
+    bnd = ref["gX_bound"] + 4 * ref["gX_sens"]
+    tol_s = np.zeros(C); tol_b = np.zeros(C)
+    np.add.at(tol_s, cidx, (bnd * np.abs(Xd)).sum(0)); np.add.at(tol_b, cidx, bnd.sum(0))
+    rtol = 1e-2 if dtype == torch.bfloat16 else 1e-5
+    assert np.all(np.abs(gsc.cpu().numpy() - rgs) <= rtol * tol_s + 1e-30)
+    assert np.all(np.abs(gsh.cpu().numpy() - rgb) <= rtol * tol_b + 1e-30)
+
+
+def test_affine_identity_equals_plain_path_bitwise_and_deterministic(monkeypatch):
+    T, B, C, HW = 33, 4, 6, 100
+    N = B * C * HW
+    X = snn_synth.normal_tensor(111, T, N).cuda()
+    G = snn_synth.normal_tensor(112, T, N).cuda()
+    af = snn.AffineSpec(torch.ones(C, device="cuda"), torch.zeros(C, device="cuda"), C, HW)
+    f0 = snn.lif_forward(X, PAPER)
+    g0, v0 = snn.lif_backward(G, f0)
+    f1 = snn.lif_forward_affine(X, PAPER, af)
+    g1, v1, s1, b1 = snn.lif_backward_affine(G, f1)
+    torch.cuda.synchronize()
+    assert torch.equal(f0.spikes, f1.spikes) and torch.equal(f0.v_final, f1.v_final)
+    assert torch.equal(g0, g1) and torch.equal(v0, v1)
+    # deterministic across runs and across the TMA / generic kernel paths
+    sc = torch.linspace(0.5, 1.5, C, device="cuda"); sh = torch.linspace(-0.2, 0.2, C, device="cuda")
+    af2 = snn.AffineSpec(sc, sh, C, HW)
+    outs = []
+    for no_tma in ("0", "0", "1"):
+        monkeypatch.setenv("SNN_LIF_NO_TMA", no_tma)
+        f = snn.lif_forward_affine(X, PAPER, af2)
+        outs.append((f.spikes.clone(),) + tuple(t.clone() for t in snn.lif_backward_affine(G, f)))
+        torch.cuda.synchronize()
+    for o in outs[1:]:
+        for a_, b_ in zip(outs[0], o):
+            assert torch.equal(a_, b_)
+
+
+def test_affine_lif_layer_matches_unfused_autograd():
+    """AffineLIFLayer (fused) vs torch affine followed by LIFLayer: same spikes and close
+    gradients (the unfused path rounds the affine separately)."""
+    torch.manual_seed(0)
+    T, B, C, H, W = 12, 4, 8, 6, 6
+    layer = snn.AffineLIFLayer(C, PAPER).cuda()
+    with torch.no_grad():
+        layer.scale.copy_(torch.rand(C) + 0.5)
+        layer.shift.copy_(torch.randn(C) * 0.2)
+    x = torch.randn(T, B, C, H, W, device="cuda", requires_grad=True)
+    y = layer(x)
+    gy = torch.randn_like(y)
+    y.backward(gy)
+    ref_layer = snn.LIFLayer(PAPER)
+    x2 = x.detach().clone().requires_grad_(True)
+    sc = layer.scale.detach().clone().requires_grad_(True)
+    sh = layer.shift.detach().clone().requires_grad_(True)
+    y2 = ref_layer(x2 * sc.view(1, 1, C, 1, 1) + sh.view(1, 1, C, 1, 1))
+    y2.backward(gy)
+    assert (y != y2).float().mean().item() < 1e-3      # rare threshold ties may differ
+    torch.testing.assert_close(layer.scale.grad, sc.grad, rtol=1e-3, atol=1e-3)
+    torch.testing.assert_close(layer.shift.grad, sh.grad, rtol=1e-3, atol=1e-3)
+
+
+@pytest.mark.gpu
+def test_fresh_host_thread_without_current_context():
+    """The first CUDA call of a fresh host thread (torch's autograd worker is one) may be our
+    tensor-map encode, before any runtime call made a context current: it must still work."""
+    import threading
+    x = snn_synth.normal_tensor(31, 16, 4096).cuda()
+    gs = snn_synth.normal_tensor(32, 16, 4096).cuda()
+    fwd0 = snn.lif_forward(x, PAPER, save_mode="recompute")
+    gx0, _ = snn.lif_backward(gs, fwd0)
+    out, err = {}, []
+
+    def run():
+        try:
+            f = snn.lif_forward(x, PAPER, save_mode="recompute")
+            out["gx"], _ = snn.lif_backward(gs, f)
+            torch.cuda.synchronize()
+        except Exception as e:   # noqa: BLE001 -- surfaced below
+            err.append(e)
+
+    th = threading.Thread(target=run)
+    th.start()
+    th.join()
+    assert not err, err
+    assert torch.equal(out["gx"], gx0)
