@@ -57,6 +57,9 @@ def parse():
                          "the multi-rank code paths on a 1-GPU box; numbers are not bench values)")
     ap.add_argument("--serial", action="store_true",
                     help="with --sweep: also time the paper's serial baselines (Fig. 3 / Fig. 5)")
+    ap.add_argument("--affine", action="store_true",
+                    help="also time the fused per-channel affine prologue (SURVEY 8(f) f4) against "
+                         "an unfused torch affine + plain LIF on a [T=64, B=16, C=64, 32x32] layer")
     ap.add_argument("--save-mode", choices=["recompute", "h"], default="recompute")
     ap.add_argument("--spike-fmt", choices=["u8", "bits", "io"], default="u8")
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -337,6 +340,67 @@ def run_sweep(args, params, dev, stream):
             out[-1]["speedup_vs_serial_torch"] = round(serial["torch_ms"] / (mf + mb), 2)
         del X, G, f, gx, g
     return out
+
+
+def run_affine(args, params, dev):
+    """one BN-style layer, fwd+bwd, fused (X' = scale[c] X + shift[c] inside
+    the LIF kernels, dscale/dshift from per-neuron partials) vs unfused (torch elementwise
+    affine, plain fused LIF, torch grad_x = scale * dL/dX' and the two channel reductions).
+    Median of 20 graph-launched steps each; inputs exceed L2 (2 x 256 MiB per batch)."""
+    import torch
+    import paper_2408_00280_b200 as snn
+    import snn_synth
+    T, B, C, HW = 64, 16, 64, 1024
+    N = B * C * HW
+    X = snn_synth.normal_tensor(1234, T, N, device=dev)
+    G = snn_synth.normal_tensor(4321, T, N, device=dev)
+    scale = (torch.rand(C, device=dev, generator=torch.Generator(dev).manual_seed(5)) + 0.5)
+    shift = torch.randn(C, device=dev, generator=torch.Generator(dev).manual_seed(6)) * 0.2
+    spec = snn.AffineSpec(scale, shift, C, HW)
+    sc5, sh5 = scale.view(1, 1, C, 1), shift.view(1, 1, C, 1)
+
+    def fused():
+        f = snn.lif_forward_affine(X, params, spec, spike_fmt=args.spike_fmt, return_v_final=False)
+        snn.lif_backward_affine(G, f, return_grad_v_init=False)
+
+    def unfused():
+        xa = (X.view(T, B, C, HW) * sc5 + sh5).view(T, N)
+        f = snn.lif_forward(xa, params, spike_fmt=args.spike_fmt, save_mode="recompute",
+                            return_v_final=False)
+        gxa, _ = snn.lif_backward(G, f, return_grad_v_init=False)
+        g4 = gxa.view(T, B, C, HW)
+        _ = g4 * sc5
+        _ = (g4 * X.view(T, B, C, HW)).sum(dim=(0, 1, 3))
+        _ = g4.sum(dim=(0, 1, 3))
+
+    def plain():       # the LIF layer alone: the floor the fused prologue should sit on
+        f = snn.lif_forward(X, params, spike_fmt=args.spike_fmt, save_mode="recompute",
+                            return_v_final=False)
+        snn.lif_backward(G, f, return_grad_v_init=False)
+
+    res = {"shape": {"T": T, "B": B, "C": C, "HW": HW}}
+    for name, fn in (("fused", fused), ("unfused", unfused), ("plain_lif", plain)):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize(dev)
+        evs = []
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(20):
+                e = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(2)]
+                e[0].record()
+                fn()
+                e[1].record()
+                evs.append(e)
+        g.replay()
+        torch.cuda.synchronize(dev)
+        ts = sorted(e[0].elapsed_time(e[1]) for e in evs)
+        res[name + "_ms"] = round(ts[len(ts) // 2], 4)
+        del g
+    res["speedup_fused_vs_unfused"] = round(res["unfused_ms"] / res["fused_ms"], 3)
+    res["fused_overhead_vs_plain_lif"] = round(res["fused_ms"] / res["plain_lif_ms"] - 1, 4)
+    res["neuron_steps_per_s_fused"] = N * T / (res["fused_ms"] / 1e3)
+    return res
 
 
 def time_serial_baselines(params, X, G, dev, flush, reps=5):
@@ -706,6 +770,7 @@ def run_ours(args):
     sweep = None
     if args.sweep and args.workload == "cfg1" and rank == 0:
         sweep = run_sweep(args, params, dev, stream)
+    affine = run_affine(args, params, dev) if args.affine and rank == 0 else None
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -730,6 +795,8 @@ def run_ours(args):
                 "gpu_launches": 2 * nlaunch * args.steps, "clocks": clk.summary()}
         if sweep is not None:
             line["sweep"] = sweep
+        if affine is not None:
+            line["affine"] = affine
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

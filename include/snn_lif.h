@@ -214,7 +214,8 @@ typedef struct {
 snn_status snn_lif_forward_affine(const snn_lif_params* params, const snn_lif_shape* shape,
                                   const void* x, const float* v_init, const snn_lif_affine* affine,
                                   void* spikes, void* saved, float* v_final, void* stream);
-/* part_a, part_b: [N] fp32 caller scratch; grad_scale, grad_shift: [C] fp32 outputs. */
+/* part_a, part_b: [N] fp32 caller scratch (16-B aligned; contents undefined on return);
+ * grad_scale, grad_shift: [C] fp32 outputs, bitwise deterministic run to run. */
 snn_status snn_lif_backward_affine(const snn_lif_params* params, const snn_lif_shape* shape,
                                    const void* grad_spikes, const void* x, const void* saved,
                                    const float* grad_v_final, const snn_lif_affine* affine,

@@ -2,37 +2,80 @@
 // own 8 bytes of io per row (2 fp32 / 4 bf16 neurons): the RECOMPUTE walk keeps
 // 2 x kCkpt rows of x and gS in registers, so a narrow group keeps occupancy up.
 #include "internal.h"
+#include "lif_async.cuh"
 
 namespace snn {
 // ------------------------------------------------------------------------------------
 // Affine prologue gradients: grad_scale[c] = sum_{b, hw} part_a[(b C + c) HW + hw], same for
-// shift.  One CTA per channel, fixed per-thread strides and a fixed tree: deterministic.
+// shift.  Two passes with a fixed partition and fixed summation orders, so the result is
+// deterministic (bitwise run to run):
+//   1. grid (S, C): CTA (j, c) sums piece j = flat indices [j L, min((j+1) L, B HW)) of channel
+//      c's B x HW elements (per-thread strided sums, then a fixed shuffle/smem tree) and
+//      writes its partial over the piece's first element (the CTA owns that piece; scratch);
+//   2. warp c adds its S piece partials: lane l sums pieces l, l+32, ... in order, then a
+//      fixed xor-shuffle tree.
+// Both run under programmatic dependent launch (they wait for the backward in pdl_wait()).
+__device__ __forceinline__ int64_t piece_first(int64_t j, int64_t L, int64_t C, int64_t HW, int64_t c) {
+    const int64_t i = j * L;
+    return ((i / HW) * C + c) * HW + i % HW;
+}
+
 __global__ void __launch_bounds__(256)
-affine_reduce_kernel(const float* __restrict__ part_a, const float* __restrict__ part_b, int64_t B,
-                     int64_t C, int64_t HW, float* __restrict__ grad_scale, float* __restrict__ grad_shift) {
-    __shared__ float sa[256], sb[256];
-    const int64_t ch = blockIdx.x;
+affine_partial_kernel(float* __restrict__ part_a, float* __restrict__ part_b, int64_t B, int64_t C,
+                      int64_t HW, int64_t L) {
+    pdl_wait();
+    pdl_trigger();
+    const int64_t c = blockIdx.y, j = blockIdx.x;
+    const int64_t i0 = j * L, i1 = min(i0 + L, B * HW);
     float acc_a = 0.0f, acc_b = 0.0f;
-    const int64_t per = B * HW;
-    for (int64_t i = threadIdx.x; i < per; i += blockDim.x) {
-        const int64_t b = i / HW, hw = i % HW;
-        const int64_t n = (b * C + ch) * HW + hw;
-        acc_a = __fadd_rn(acc_a, part_a[n]);
-        acc_b = __fadd_rn(acc_b, part_b[n]);
-    }
-    sa[threadIdx.x] = acc_a;
-    sb[threadIdx.x] = acc_b;
-    __syncthreads();
-    for (int w = 128; w > 0; w >>= 1) {
-        if ((int)threadIdx.x < w) {
-            sa[threadIdx.x] = __fadd_rn(sa[threadIdx.x], sa[threadIdx.x + w]);
-            sb[threadIdx.x] = __fadd_rn(sb[threadIdx.x], sb[threadIdx.x + w]);
+    for (int64_t b = i0 / HW; b * HW < i1; ++b) {       // rows of this piece, each contiguous
+        const int64_t lo = max(i0, b * HW) - b * HW, hi = min(i1, (b + 1) * HW) - b * HW;
+        const int64_t base = (b * C + c) * HW;
+        for (int64_t hw = lo + threadIdx.x; hw < hi; hw += blockDim.x) {
+            acc_a = __fadd_rn(acc_a, part_a[base + hw]);
+            acc_b = __fadd_rn(acc_b, part_b[base + hw]);
         }
-        __syncthreads();
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        acc_a = __fadd_rn(acc_a, __shfl_xor_sync(0xffffffffu, acc_a, o));
+        acc_b = __fadd_rn(acc_b, __shfl_xor_sync(0xffffffffu, acc_b, o));
+    }
+    __shared__ float sa[8], sb[8];
+    const int warp = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) { sa[warp] = acc_a; sb[warp] = acc_b; }
+    __syncthreads();                                     // every read of the piece is done
     if (threadIdx.x == 0) {
-        grad_scale[ch] = sa[0];
-        grad_shift[ch] = sb[0];
+        float ta = sa[0], tb = sb[0];
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) { ta = __fadd_rn(ta, sa[w]); tb = __fadd_rn(tb, sb[w]); }
+        const int64_t n = piece_first(j, L, C, HW, c);
+        part_a[n] = ta;
+        part_b[n] = tb;
+    }
+}
+
+__global__ void __launch_bounds__(256)
+affine_finish_kernel(const float* __restrict__ part_a, const float* __restrict__ part_b, int64_t C,
+                     int64_t HW, int64_t L, int64_t S, float* __restrict__ grad_scale,
+                     float* __restrict__ grad_shift) {
+    pdl_wait();
+    const int64_t c = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (c >= C) return;                                   // whole warps exit together
+    float ta = 0.0f, tb = 0.0f;
+    for (int64_t j = lane; j < S; j += 32) {
+        const int64_t n = piece_first(j, L, C, HW, c);
+        ta = __fadd_rn(ta, part_a[n]);
+        tb = __fadd_rn(tb, part_b[n]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        ta = __fadd_rn(ta, __shfl_xor_sync(0xffffffffu, ta, o));
+        tb = __fadd_rn(tb, __shfl_xor_sync(0xffffffffu, tb, o));
+    }
+    if (lane == 0) {
+        grad_scale[c] = ta;
+        grad_shift[c] = tb;
     }
 }
 
@@ -87,10 +130,20 @@ snn_status launch_backward_generic(const snn_lif_shape* s, const snn::BwdArgs& a
     return vec ? go<float, 2>(s, a, mode, st) : go<float, 1>(s, a, mode, st);
 }
 
-snn_status launch_affine_reduce(const float* part_a, const float* part_b, int64_t B, int64_t C,
-                                int64_t HW, float* grad_scale, float* grad_shift, cudaStream_t st) {
-    snn::affine_reduce_kernel<<<(unsigned)C, 256, 0, st>>>(part_a, part_b, B, C, HW, grad_scale, grad_shift);
-    return launch_status("affine_reduce_kernel");
+snn_status launch_affine_reduce(float* part_a, float* part_b, int64_t B, int64_t C, int64_t HW,
+                                float* grad_scale, float* grad_shift, cudaStream_t st) {
+    // pieces of >= 2048 elements, about 4 CTAs per SM over all channels
+    const int64_t M = B * HW;
+    int64_t S = std::max<int64_t>(1, std::min<int64_t>((M + 2047) / 2048, (4 * num_sms() + C - 1) / C));
+    const int64_t L = (M + S - 1) / S;
+    S = (M + L - 1) / L;                                 // every piece non-empty
+    if (C > 65535) return fail(SNN_ERR_INVALID_VALUE, "affine: C > 65535 channels");
+    snn_status r = launch_pdl(snn::affine_partial_kernel, dim3((unsigned)S, (unsigned)C), dim3(256), st,
+                              "affine_partial_kernel", part_a, part_b, B, C, HW, L);
+    if (r != SNN_OK) return r;
+    return launch_pdl(snn::affine_finish_kernel, dim3((unsigned)((C + 7) / 8)), dim3(256), st,
+                      "affine_finish_kernel", (const float*)part_a, (const float*)part_b, C, HW, L, S,
+                      grad_scale, grad_shift);
 }
 
 }  // namespace snn_host

@@ -12,9 +12,13 @@ template <typename IO, int VEC>
 snn_status go(const snn_lif_shape* s, const snn::FwdArgs& a, bool soft, cudaStream_t st) {
     const int64_t groups = (s->N + VEC - 1) / VEC;
     const dim3 grid((unsigned)((groups + snn::kBlock - 1) / snn::kBlock));
-    auto launch = [&](auto sfmt, auto save, auto sft) {
+    auto go_aff = [&](auto sfmt, auto save, auto sft, auto aff) {
         snn::lif_forward_kernel<IO, VEC, decltype(sfmt)::value, decltype(save)::value,
-                                (bool)decltype(sft)::value, kFwdPF><<<grid, snn::kBlock, 0, st>>>(a);
+                                (bool)decltype(sft)::value, (bool)decltype(aff)::value, kFwdPF>
+            <<<grid, snn::kBlock, 0, st>>>(a);
+    };
+    auto launch = [&](auto sfmt, auto save, auto sft) {
+        if (a.af.scale != nullptr) go_aff(sfmt, save, sft, IC<1>{}); else go_aff(sfmt, save, sft, IC<0>{});
     };
     auto by_soft = [&](auto sfmt, auto save) {
         if (soft) launch(sfmt, save, IC<1>{}); else launch(sfmt, save, IC<0>{});

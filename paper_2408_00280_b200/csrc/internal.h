@@ -68,6 +68,25 @@ snn_status launch_tiles(Kernel k, int threads, int smem, int64_t ntiles, int64_t
     return launch_status(what);
 }
 
+// Plain launch with programmatic dependent launch allowed: the kernel must call pdl_wait()
+// before touching global memory.
+template <typename Kernel, typename... Args>
+snn_status launch_pdl(Kernel k, dim3 grid, dim3 block, cudaStream_t st, const char* what,
+                      const Args&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, k, args...);
+    if (e != cudaSuccess) return fail(SNN_ERR_CUDA, "%s launch failed: %s", what, cudaGetErrorString(e));
+    return launch_status(what);
+}
+
 // ---- launchers (one translation unit each, compiled in parallel) -------------------
 // Generic path: any alignment; `vec` selects the 128-bit vector variant.
 snn_status launch_forward_generic(const snn_lif_shape* s, const snn::FwdArgs& a, bool soft, bool vec,
@@ -80,7 +99,8 @@ snn_status launch_forward_tma_bf16(const snn_lif_shape* s, const snn::FwdArgs& a
 snn_status launch_backward_tma_f32(const snn_lif_shape* s, const snn::BwdArgs& a, int mode, cudaStream_t st);
 snn_status launch_backward_tma_bf16(const snn_lif_shape* s, const snn::BwdArgs& a, int mode, cudaStream_t st);
 int tma_vec_forward(int io_dtype);
-snn_status launch_affine_reduce(const float* part_a, const float* part_b, int64_t B, int64_t C,
+// part_a / part_b are scratch: the reduction overwrites some of their entries.
+snn_status launch_affine_reduce(float* part_a, float* part_b, int64_t B, int64_t C,
                                 int64_t HW, float* grad_scale, float* grad_shift, cudaStream_t st);
 // Serial (one launch per time step) baseline of Fig. 3 -- comparison only (serial.cu).
 snn_status launch_serial_forward_step(int io_dtype, bool soft, const void* x_t, float* V, uint8_t* s_t,

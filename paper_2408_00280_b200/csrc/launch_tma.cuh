@@ -30,14 +30,18 @@ snn_status launch_forward_tma(const snn_lif_shape* s, const snn::FwdArgs& a, boo
     if (!encode_2d(&tmx, a.x, sizeof(IO), s->N, s->T, s->ld, Cfg::BW, C::FR))
         return fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled failed for x%s", encode_detail());
     const int64_t ntiles = (s->N + Cfg::W - 1) / Cfg::W;
-    auto go = [&](auto sfmt, auto save, auto sft) {
+    auto go = [&](auto sfmt, auto save, auto sft, auto aff) {
         auto k = snn::lif_forward_tma_kernel<IO, C::FV, decltype(sfmt)::value, decltype(save)::value,
-                                             (bool)decltype(sft)::value, C::FN, C::FR, C::FS>;
+                                             (bool)decltype(sft)::value, (bool)decltype(aff)::value,
+                                             C::FN, C::FR, C::FS>;
         return launch_tiles(k, Cfg::THREADS, Cfg::SMEM, ntiles, (s->T + C::FR - 1) / C::FR, st,
                             "lif_forward_tma_kernel", tmx, a);
     };
+    auto by_aff = [&](auto sfmt, auto save, auto sft) {
+        return a.af.scale != nullptr ? go(sfmt, save, sft, IC<1>{}) : go(sfmt, save, sft, IC<0>{});
+    };
     auto by_soft = [&](auto sfmt, auto save) {
-        return soft ? go(sfmt, save, IC<1>{}) : go(sfmt, save, IC<0>{});
+        return soft ? by_aff(sfmt, save, IC<1>{}) : by_aff(sfmt, save, IC<0>{});
     };
     auto by_save = [&](auto sfmt) {
         switch (s->save_mode) {

@@ -123,18 +123,11 @@ __device__ __forceinline__ F2 f2(float a, float b) {
     return r;
 }
 __device__ __forceinline__ F2 f2(float a) { return f2(a, a); }
-__device__ __forceinline__ float lo(F2 a) {
-    float x, y;
+__device__ __forceinline__ void split(F2 a, float& x, float& y) {
     asm("mov.b64 {%0, %1}, %2;" : "=f"(x), "=f"(y) : "l"(a.v));
-    (void)y;
-    return x;
 }
-__device__ __forceinline__ float hi(F2 a) {
-    float x, y;
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(x), "=f"(y) : "l"(a.v));
-    (void)x;
-    return y;
-}
+__device__ __forceinline__ float lo(F2 a) { float x, y; split(a, x, y); return x; }
+__device__ __forceinline__ float hi(F2 a) { float x, y; split(a, x, y); return y; }
 __device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) {
     F2 r;
     asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(a.v), "l"(b.v), "l"(c.v));

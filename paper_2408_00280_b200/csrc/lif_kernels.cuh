@@ -51,14 +51,15 @@ struct AffCoef {
     float a[VEC], b[VEC];
 };
 
-template <int VEC>
+// AFF = false: the prologue is compiled out (the coefficients are never read).
+template <int VEC, bool AFF>
 __device__ __forceinline__ AffCoef<VEC> load_affine(const Affine& af, int64_t n0, int nvalid) {
     AffCoef<VEC> co;
 #pragma unroll
     for (int i = 0; i < VEC; ++i) {
         co.a[i] = 1.0f;
         co.b[i] = 0.0f;
-        if (af.scale != nullptr && i < nvalid) {
+        if (AFF && i < nvalid) {
             const int64_t ch = ((n0 + i) / af.HW) % af.C;
             co.a[i] = __ldg(af.scale + ch);
             co.b[i] = __ldg(af.shift + ch);
@@ -97,7 +98,20 @@ struct BwdArgs {
 
 // Eq. 1-2 + reset for this thread's VEC neurons: updates V, returns H in `hp` and the
 // spike bits (bit i = neuron i of the group).
-template <bool SOFT, typename IO, int VEC>
+// AFF: the input is X' = fma(a, X, b); otherwise X itself.
+template <bool AFF, typename IO, int VEC>
+__device__ __forceinline__ F2 input2(const AffCoef<VEC>& co, const Pack<IO, VEC>& xv, int i) {
+    const F2 X2 = f2(to_f32(xv.v[i]), to_f32(xv.v[i + 1]));
+    if constexpr (AFF) return fma2(f2(co.a[i], co.a[i + 1]), X2, f2(co.b[i], co.b[i + 1]));
+    return X2;
+}
+template <bool AFF, typename IO, int VEC>
+__device__ __forceinline__ float input1(const AffCoef<VEC>& co, const Pack<IO, VEC>& xv, int i) {
+    if constexpr (AFF) return input1<AFF>(co, xv, i);
+    return to_f32(xv.v[i]);
+}
+
+template <bool SOFT, bool AFF, typename IO, int VEC>
 __device__ __forceinline__ unsigned fwd_compute(const LifConsts& c, float (&V)[VEC],
                                                 const Pack<IO, VEC>& xv, Pack<float, VEC>& hp,
                                                 const AffCoef<VEC>& co) {
@@ -105,8 +119,7 @@ __device__ __forceinline__ unsigned fwd_compute(const LifConsts& c, float (&V)[V
     if constexpr (VEC % 2 == 0) {   // paired FFMA2 charge, same roundings as the scalar path
 #pragma unroll
         for (int i = 0; i < VEC; i += 2) {
-            const F2 X2 = fma2(f2(co.a[i], co.a[i + 1]), f2(to_f32(xv.v[i]), to_f32(xv.v[i + 1])),
-                               f2(co.b[i], co.b[i + 1]));
+            const F2 X2 = input2<AFF>(co, xv, i);
             const F2 H2 = lif_charge2(c, f2(V[i], V[i + 1]), X2);
             const float Ha = lo(H2), Hb = hi(H2);
             const bool Sa = lif_fire(c, Ha), Sb = lif_fire(c, Hb);
@@ -119,7 +132,7 @@ __device__ __forceinline__ unsigned fwd_compute(const LifConsts& c, float (&V)[V
     } else {
 #pragma unroll
         for (int i = 0; i < VEC; ++i) {
-            const float H = lif_charge(c, V[i], __fmaf_rn(co.a[i], to_f32(xv.v[i]), co.b[i]));
+            const float H = lif_charge(c, V[i], input1<AFF>(co, xv, i));
             const bool S = lif_fire(c, H);
             V[i] = lif_reset<SOFT>(c, H, S);
             hp.v[i] = H;
@@ -130,15 +143,14 @@ __device__ __forceinline__ unsigned fwd_compute(const LifConsts& c, float (&V)[V
 }
 
 // Re-run the charge / fire / reset (no outputs) -- the RECOMPUTE backward's forward pass.
-template <bool SOFT, typename IO, int VEC>
+template <bool SOFT, bool AFF, typename IO, int VEC>
 __device__ __forceinline__ void fwd_recompute_step(const LifConsts& c, float (&V)[VEC],
                                                    const Pack<IO, VEC>& xv, float (&h)[VEC],
                                                    const AffCoef<VEC>& co) {
     if constexpr (VEC % 2 == 0) {
 #pragma unroll
         for (int i = 0; i < VEC; i += 2) {
-            const F2 X2 = fma2(f2(co.a[i], co.a[i + 1]), f2(to_f32(xv.v[i]), to_f32(xv.v[i + 1])),
-                               f2(co.b[i], co.b[i + 1]));
+            const F2 X2 = input2<AFF>(co, xv, i);
             const F2 H2 = lif_charge2(c, f2(V[i], V[i + 1]), X2);
             h[i] = lo(H2);
             h[i + 1] = hi(H2);
@@ -148,7 +160,7 @@ __device__ __forceinline__ void fwd_recompute_step(const LifConsts& c, float (&V
     } else {
 #pragma unroll
         for (int i = 0; i < VEC; ++i) {
-            h[i] = lif_charge(c, V[i], __fmaf_rn(co.a[i], to_f32(xv.v[i]), co.b[i]));
+            h[i] = lif_charge(c, V[i], input1<AFF>(co, xv, i));
             V[i] = lif_reset<SOFT>(c, h[i], lif_fire(c, h[i]));
         }
     }
@@ -260,7 +272,7 @@ __device__ __forceinline__ Pack<IO, VEC> bwd_step(const LifConsts& c, float (&gV
 
 // ------------------------------------------------------------------------------------
 // Generic forward: PF-deep register prefetch ring along T.
-template <typename IO, int VEC, int SFMT, int SAVE, bool SOFT, int PF>
+template <typename IO, int VEC, int SFMT, int SAVE, bool SOFT, bool AFF, int PF>
 __global__ void __launch_bounds__(kBlock)
 lif_forward_kernel(const FwdArgs a) {
     const int64_t g = (int64_t)blockIdx.x * kBlock + threadIdx.x;
@@ -281,7 +293,7 @@ lif_forward_kernel(const FwdArgs a) {
 #pragma unroll
         for (int i = 0; i < VEC; ++i) V[i] = c.v_reset;
     }
-    const AffCoef<VEC> co = load_affine<VEC>(a.af, n0, nvalid);
+    const AffCoef<VEC> co = load_affine<VEC, AFF>(a.af, n0, nvalid);
 
     Pack<IO, VEC> buf[PF];
 #pragma unroll
@@ -306,7 +318,7 @@ lif_forward_kernel(const FwdArgs a) {
                     }
                 }
                 Pack<float, VEC> hp;
-                const unsigned bits = fwd_compute<SOFT>(c, V, xv, hp, co);
+                const unsigned bits = fwd_compute<SOFT, AFF>(c, V, xv, hp, co);
                 if constexpr (SAVE == SAVE_H) {
                     if (nvalid > 0) st_group<float, VEC>(a.saved + t * a.ldh + n0, hp, nvalid);
                 }
@@ -412,7 +424,7 @@ lif_backward_recompute_kernel(const BwdArgs a) {
     }
 
     constexpr bool AFF = Mode<MODE>::AFF;
-    const AffCoef<VEC> co = load_affine<VEC>(a.af, n0, nvalid);
+    const AffCoef<VEC> co = load_affine<VEC, AFF>(a.af, n0, nvalid);
     float pa[VEC], pb[VEC];
 #pragma unroll
     for (int i = 0; i < VEC; ++i) pa[i] = pb[i] = 0.0f;
@@ -436,7 +448,7 @@ lif_backward_recompute_kernel(const BwdArgs a) {
         for (int i = 0; i < VEC; ++i) V[i] = v0.v[i];
 #pragma unroll
         for (int j = 0; j < kCkpt; ++j) {
-            if (j < len) fwd_recompute_step<Mode<MODE>::SOFT>(c, V, xb[j], h[j], co);
+            if (j < len) fwd_recompute_step<Mode<MODE>::SOFT, AFF>(c, V, xb[j], h[j], co);
         }
 #pragma unroll
         for (int j = kCkpt - 1; j >= 0; --j) {

@@ -136,7 +136,7 @@ struct FwdTma {
     static_assert(W % BW == 0 && BW % VEC == 0, "tile geometry");
 };
 
-template <typename IO, int VEC, int SFMT, int SAVE, bool SOFT, int NCONS, int R, int S>
+template <typename IO, int VEC, int SFMT, int SAVE, bool SOFT, bool AFF, int NCONS, int R, int S>
 __global__ void __launch_bounds__(NCONS + 32)
 lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const FwdArgs a, const int clc_depth) {
     using Cfg = FwdTma<IO, VEC, NCONS, R, S>;
@@ -189,7 +189,7 @@ lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const FwdArgs a,
 #pragma unroll
             for (int i = 0; i < VEC; ++i) V[i] = v0.v[i];
         }
-        const AffCoef<VEC> co = load_affine<VEC>(a.af, n0, nvalid);
+        const AffCoef<VEC> co = load_affine<VEC, AFF>(a.af, n0, nvalid);
         unsigned char* spk_row = reinterpret_cast<unsigned char*>(a.spikes);
         float* h_row = a.saved + n0;   // SAVE_H: advanced one row per step
         for (int64_t rb = 0; rb < nrb; ++rb, ++k) {
@@ -217,7 +217,7 @@ lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const FwdArgs a,
                         }
                     }
                     Pack<float, VEC> hp;
-                    const unsigned bits = fwd_compute<SOFT>(c, V, xv, hp, co);
+                    const unsigned bits = fwd_compute<SOFT, AFF>(c, V, xv, hp, co);
                     if constexpr (SAVE == SAVE_H) {
                         if (nv > 0) st_stream<float, VEC>(h_row, hp);
                         h_row += a.ldh;
@@ -293,7 +293,7 @@ __device__ __forceinline__ void recompute_chunk(const LifConsts& c, float (&V)[V
     for (int j = 0; j < kCkpt; ++j) {
         if (j < rows) {
             const Pack<IO, VEC> xv = *reinterpret_cast<const Pack<IO, VEC>*>(xs + j * BW);
-            fwd_recompute_step<Mode<MODE>::SOFT>(c, V, xv, h[j], co);
+            fwd_recompute_step<Mode<MODE>::SOFT, Mode<MODE>::AFF>(c, V, xv, h[j], co);
         }
     }
 }
@@ -350,7 +350,7 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
         const int64_t n0 = (int64_t)tile * W + nt;
         const bool valid = n0 < N;   // N % VEC == 0 on this path
         const bool tile_full = (int64_t)(tile + 1) * W <= N;   // uniform across the CTA
-        const AffCoef<VEC> co = load_affine<VEC>(a.af, n0, valid ? VEC : 0);
+        const AffCoef<VEC> co = load_affine<VEC, Mode<MODE>::AFF>(a.af, n0, valid ? VEC : 0);
         float pa[VEC], pb[VEC];
 #pragma unroll
         for (int i = 0; i < VEC; ++i) pa[i] = pb[i] = 0.0f;

@@ -149,6 +149,9 @@ class PeerHandoff:
                        if r + 1 < w else None)
         self.f_epoch = 0
         self.b_epoch = 0
+        # cudaMemset is asynchronous: without this a peer could publish its first flag into
+        # a buffer whose zeroing is still queued here, and the zeroing would then erase it.
+        _check(cudart().cudaDeviceSynchronize(), "cudaDeviceSynchronize")
         dist.barrier(group=group)   # every buffer zeroed and mapped before anyone sends
 
     def forward_handoff(self):
