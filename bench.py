@@ -67,6 +67,8 @@ def parse():
     ap.add_argument("--no-graph", action="store_true",
                     help="launch the timed steps eagerly instead of as one captured CUDA graph")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cpu-all-cores", action="store_true",
+                    help="skip the all-cores (one oracle process per core) CPU figure")
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
                     help="target CPU time of the oracle baseline sample")
     a = ap.parse_args()
@@ -225,6 +227,30 @@ def cpu_cores():
         return os.cpu_count()
 
 
+def _oracle_worker(job):
+    """One process of OracleSample.baseline_all_cores (top level: spawn-picklable)."""
+    T, N, cols, dt, seconds = job
+    import numpy as np
+    import torch
+    import oracle
+    import snn_synth
+    torch.set_num_threads(1)
+    dtype = torch.bfloat16 if dt == "bf16" else torch.float32
+    idx = np.asarray(cols)
+    X = snn_synth.normal_columns(1234, T, N, idx, dtype=dtype).double().numpy()
+    G = snn_synth.normal_columns(4321, T, N, idx, dtype=dtype).double().numpy()
+    f32 = lambda v: float(np.float32(v))
+    op = oracle.OracleParams(tau=f32(1.25), v_th=f32(0.3), v_reset=0.0, alpha=4.0)
+    total_t, total_ns = 0.0, 0
+    while total_t < seconds or total_ns == 0:
+        t0 = time.perf_counter()
+        ref = oracle.forward(op, X)
+        oracle.backward(op, G, ref["H"])
+        total_t += time.perf_counter() - t0
+        total_ns += T * len(idx)
+    return total_ns, total_t
+
+
 class OracleSample:
     """The fp64 C oracle (as it stands, 1 thread) on a bounded column sample of the
     workload's largest layer: `cols` stride-sampled neuron columns over all T steps,
@@ -261,6 +287,24 @@ class OracleSample:
         v, t = self.run(seconds)
         return {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
                 "sample": f"{self.desc}, fwd+bwd, fp64 C oracle single-threaded, {t:.1f} s"}
+
+    def baseline_all_cores(self, seconds, procs=None):
+        """The same oracle, unchanged, in one process per host core, each on its own share
+        of the sampled columns (neurons are independent), run concurrently for
+        ~`seconds`: the aggregate rate is the sum of the per-process rates."""
+        import multiprocessing as mp
+        procs = procs or cpu_cores()
+        name, T, N, dtype = self.layer
+        shares = [self.idx[i::procs] for i in range(procs)]
+        shares = [sh for sh in shares if len(sh)]
+        jobs = [(T, N, sh.tolist(), "bf16" if str(dtype).endswith("bfloat16") else "f32", seconds)
+                for sh in shares]
+        with mp.get_context("spawn").Pool(len(jobs)) as pool:
+            res = pool.map(_oracle_worker, jobs)
+        rate = sum(ns / t for ns, t in res)
+        return {"value": rate, "unit": UNIT, "cores": len(jobs), "kind": "oracle",
+                "sample": f"{self.desc}, fwd+bwd, fp64 C oracle, {len(jobs)} concurrent single-threaded "
+                          f"processes on disjoint column shares, ~{seconds:.0f} s each"}
 
     def parity(self, spikes, grad_x, v_final=None):
         """Compare the GPU outputs of the timed workload's first batch on the sampled columns
@@ -776,6 +820,8 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         smp = OracleSample(layers)
         cpu = smp.baseline(args.cpu_seconds)
+        if cpu_cores() > 1 and not args.no_cpu_all_cores:
+            cpu["all_cores"] = smp.baseline_all_cores(max(2.0, args.cpu_seconds / 2))
         # parity of the timed path on the same sampled columns (batch 0 of the largest layer)
         b = max(bufs, key=lambda q: q["T"] * q["N"])
         f = snn.lif_forward(b["XX"][0], params, spike_fmt=args.spike_fmt, save_mode=args.save_mode)
