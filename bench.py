@@ -784,15 +784,17 @@ def run_ours(args):
         h2d = sum(h["X"].numel() * h["X"].element_size() + h["G"].numel() * h["G"].element_size() for h in hb)
         d2h = sum(h["S"].numel() * h["S"].element_size() + h["gX"].numel() * h["gX"].element_size() for h in hb)
 
+        # the public host-buffer call (snn_lif_fwd_bwd_host): neuron chunks stream through
+        # device staging slots with copy-in, the fused kernels and copy-out overlapped
+        for h in hb:
+            h["ws"] = snn.host_workspace(h["X"].shape[0], h["X"].shape[1], params, h["X"].dtype,
+                                         spike_fmt=args.spike_fmt, save_mode=args.save_mode, device=dev)
+
         def e2e_step():
             for h in hb:
-                x = h["X"].to(dev, non_blocking=True)
-                g = h["G"].to(dev, non_blocking=True)
-                f = snn.lif_forward(x, params, spike_fmt=args.spike_fmt, save_mode=args.save_mode,
-                                    return_v_final=False)
-                gx, _ = snn.lif_backward(g, f, return_grad_v_init=False)
-                h["S"].copy_(f.spikes, non_blocking=True)
-                h["gX"].copy_(gx, non_blocking=True)
+                snn.lif_fwd_bwd_host(h["X"], h["G"], params, spike_fmt=args.spike_fmt,
+                                     save_mode=args.save_mode, spikes=h["S"], grad_x=h["gX"],
+                                     workspace=h["ws"])
 
         e2e_step(); torch.cuda.synchronize(dev)
         if world > 1:

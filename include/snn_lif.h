@@ -21,9 +21,11 @@
  *  (column range) of a wider tensor.  [N] vectors are dense fp32.
  *
  *  Ownership.  Every data pointer is a DEVICE pointer owned by the caller (PyTorch
- *  allocates).  The library never allocates, frees or synchronises; every call only
+ *  allocates).  The device calls never allocate, free or synchronise; every call only
  *  enqueues kernels on `stream` (a cudaStream_t passed as void*; NULL = legacy default
- *  stream) and returns.  Outputs are valid once that stream's work completes.
+ *  stream) and returns.  Outputs are valid once that stream's work completes.  The one
+ *  exception is the host-buffer runtime call snn_lif_fwd_bwd_host (host pointers, its own
+ *  copy streams, blocking), documented where it is declared.
  *
  *  Errors.  Arguments are validated synchronously, before anything is enqueued; a
  *  non-OK status means nothing was launched.  A launch failure is reported as
@@ -242,6 +244,31 @@ snn_status snn_lif_serial_forward_step(const snn_lif_params* params, int io_dtyp
 snn_status snn_lif_serial_backward_step(const snn_lif_params* params, int io_dtype, int64_t N,
                                         const void* grad_spikes_t, const float* h_t, float* grad_v,
                                         void* grad_x_t, void* stream);
+
+/* ---- Host-buffer training step (runtime, not a kernel): one layer's forward + backward
+ * over HOST buffers, as a user without the tensors on the device calls it (bench.py's e2e).
+ * The neuron axis is cut into chunks of `chunk_neurons` columns (neurons are independent,
+ * PAPER.md:191-193); each chunk goes host -> device (x, grad_spikes), through
+ * snn_lif_forward + snn_lif_backward, and device -> host (spikes, grad_x), with up to
+ * `nslots` chunks in flight on three streams (copy-in, the caller's `stream` for the
+ * kernels, copy-out), so both PCIe directions and the kernels overlap.
+ *   x_host, grad_spikes_host  [T, ld] io dtype      host memory (pinned for full speed)  (read)
+ *   spikes_host               per spike_fmt, row stride ld (u8/io) or ceil(N/32) words (write)
+ *   grad_x_host               [T, ld] io dtype                                        (write)
+ *   workspace                 device memory of snn_lif_host_workspace_bytes() bytes,
+ *                             256-B aligned, caller-owned (the staging slots)
+ * Carries: V[-1] = v_reset and dL/dV[T-1] = 0 (use the device calls for carries).
+ * chunk_neurons <= 0 picks ~32 MiB of x per chunk; it is rounded up to a multiple of 512.
+ * nslots in [2, 8] (<= 0: 3).  save_mode must be SAVE_H or SAVE_RECOMPUTE (saved state stays
+ * in the slot).  The call BLOCKS until every output is in host memory; the copy streams and
+ * events it needs are created and destroyed inside the call.  Errors: as snn_lif_forward,
+ * plus SNN_ERR_INVALID_VALUE for a too-small workspace. */
+size_t snn_lif_host_workspace_bytes(const snn_lif_params* params, const snn_lif_shape* shape,
+                                    int64_t chunk_neurons, int nslots);
+snn_status snn_lif_fwd_bwd_host(const snn_lif_params* params, const snn_lif_shape* shape,
+                                const void* x_host, const void* grad_spikes_host, void* spikes_host,
+                                void* grad_x_host, int64_t chunk_neurons, int nslots,
+                                void* workspace, size_t workspace_bytes, void* stream);
 
 /* Status name, e.g. "SNN_ERR_INVALID_VALUE" (static storage). */
 const char* snn_status_string(snn_status status);

@@ -29,6 +29,7 @@ EXPORTED_SYMBOLS = (
     "snn_last_error_message", "snn_lif_abi_version", "snn_lif_serial_forward_step",
     "snn_lif_serial_backward_step", "snn_lif_handoff_blocks", "snn_lif_forward_handoff",
     "snn_lif_backward_handoff", "snn_lif_forward_affine", "snn_lif_backward_affine",
+    "snn_lif_host_workspace_bytes", "snn_lif_fwd_bwd_host",
 )
 SNN_LIF_HANDOFF_BLOCK = 256
 
@@ -96,6 +97,11 @@ def _load() -> ctypes.CDLL:
     lib.snn_lif_forward_affine.restype = ctypes.c_int
     lib.snn_lif_backward_affine.argtypes = [P, S, vp, vp, vp, fp, Ap, vp, fp, fp, fp, fp, fp, vp]
     lib.snn_lif_backward_affine.restype = ctypes.c_int
+    lib.snn_lif_host_workspace_bytes.argtypes = [P, S, ctypes.c_int64, ctypes.c_int]
+    lib.snn_lif_host_workspace_bytes.restype = ctypes.c_size_t
+    lib.snn_lif_fwd_bwd_host.argtypes = [P, S, vp, vp, vp, vp, ctypes.c_int64, ctypes.c_int, vp,
+                                         ctypes.c_size_t, vp]
+    lib.snn_lif_fwd_bwd_host.restype = ctypes.c_int
     return lib
 
 
@@ -164,3 +170,15 @@ def snn_lif_backward_affine(params, shape, grad_spikes, x, saved, grad_v_final, 
     check(lib.snn_lif_backward_affine(ctypes.byref(params), ctypes.byref(shape), grad_spikes, x, saved,
                                       grad_v_final, ctypes.byref(affine), grad_x, grad_v_init, part_a,
                                       part_b, grad_scale, grad_shift, stream))
+
+
+def snn_lif_host_workspace_bytes(params, shape, chunk_neurons, nslots) -> int:
+    return int(lib.snn_lif_host_workspace_bytes(ctypes.byref(params), ctypes.byref(shape),
+                                                chunk_neurons, nslots))
+
+
+def snn_lif_fwd_bwd_host(params, shape, x_host, grad_spikes_host, spikes_host, grad_x_host,
+                         chunk_neurons, nslots, workspace, workspace_bytes, stream) -> None:
+    check(lib.snn_lif_fwd_bwd_host(ctypes.byref(params), ctypes.byref(shape), x_host, grad_spikes_host,
+                                   spikes_host, grad_x_host, chunk_neurons, nslots, workspace,
+                                   workspace_bytes, stream))

@@ -279,3 +279,52 @@ def lif_backward_affine(grad_spikes: torch.Tensor, fwd: LIFForward, *,
                                  _ptr(grad_x), _ptr(gvi), _ptr(part[0]), _ptr(part[1]), _ptr(gsc),
                                  _ptr(gsh), _stream())
     return grad_x, gvi, gsc, gsh
+
+
+def host_workspace(T: int, N: int, params: LIFParams, dtype=torch.float32, *, spike_fmt: str = "u8",
+                   save_mode: str = "recompute", chunk_neurons: int = 0, nslots: int = 3,
+                   device=None) -> torch.Tensor:
+    """Device staging memory for lif_fwd_bwd_host (allocate once, reuse across calls)."""
+    shape = _lib.snn_lif_shape(T, N, N, _DTYPES[dtype], _SPIKE_FMTS[spike_fmt], _SAVE_MODES[save_mode])
+    nbytes = _lib.snn_lif_host_workspace_bytes(params.to_c(), shape, chunk_neurons, nslots)
+    if nbytes == 0:
+        raise ValueError("invalid shape / chunk_neurons / nslots for the host-buffer path")
+    return torch.empty(nbytes, dtype=torch.uint8, device=device or torch.device("cuda"))
+
+
+def lif_fwd_bwd_host(x: torch.Tensor, grad_spikes: torch.Tensor, params: LIFParams = LIFParams(), *,
+                     spike_fmt: str = "u8", save_mode: str = "recompute",
+                     spikes: Optional[torch.Tensor] = None, grad_x: Optional[torch.Tensor] = None,
+                     chunk_neurons: int = 0, nslots: int = 3,
+                     workspace: Optional[torch.Tensor] = None):
+    """One layer's forward + backward on HOST tensors (pin them for full PCIe speed):
+    x, grad_spikes [T, N] fp32/bf16 CPU -> (spikes, grad_x) CPU.  Streams neuron chunks
+    through the device with copy-in, the fused kernels and copy-out overlapped
+    (snn_lif_fwd_bwd_host); blocks until the outputs are in host memory."""
+    for name, t in (("x", x), ("grad_spikes", grad_spikes)):
+        if t.is_cuda or t.dim() != 2 or (t.size(1) > 1 and t.stride(1) != 1):
+            raise ValueError(f"{name} must be a [T, N] host tensor with unit column stride")
+    if grad_spikes.shape != x.shape or grad_spikes.dtype != x.dtype or grad_spikes.stride() != x.stride():
+        raise ValueError("grad_spikes must match x in shape, dtype and strides")
+    T, N = x.shape
+    shape = make_shape(x, spike_fmt, save_mode)
+    if spikes is None:
+        pin = x.is_pinned()
+        if spike_fmt == "u8":
+            spikes = torch.empty((T, shape.ld), dtype=torch.uint8, pin_memory=pin)[:, :N]
+        elif spike_fmt == "bits":
+            spikes = torch.empty((T, (N + 31) // 32), dtype=torch.int32, pin_memory=pin)
+        else:
+            spikes = torch.empty((T, shape.ld), dtype=x.dtype, pin_memory=pin)[:, :N]
+    if grad_x is None:
+        grad_x = torch.empty((T, shape.ld), dtype=x.dtype, pin_memory=x.is_pinned())[:, :N]
+    if grad_x.stride() != x.stride() or grad_x.dtype != x.dtype:
+        raise ValueError("grad_x must match x in dtype and strides")
+    cp = params.to_c()
+    need = _lib.snn_lif_host_workspace_bytes(cp, shape, chunk_neurons, nslots)
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(need, dtype=torch.uint8, device="cuda")
+    _lib.snn_lif_fwd_bwd_host(cp, shape, x.data_ptr(), grad_spikes.data_ptr(), spikes.data_ptr(),
+                              grad_x.data_ptr(), chunk_neurons, nslots, workspace.data_ptr(),
+                              workspace.numel(), _stream())
+    return spikes, grad_x
