@@ -107,7 +107,7 @@ __device__ __forceinline__ F2 input2(const AffCoef<VEC>& co, const Pack<IO, VEC>
 }
 template <bool AFF, typename IO, int VEC>
 __device__ __forceinline__ float input1(const AffCoef<VEC>& co, const Pack<IO, VEC>& xv, int i) {
-    if constexpr (AFF) return input1<AFF>(co, xv, i);
+    if constexpr (AFF) return __fmaf_rn(co.a[i], to_f32(xv.v[i]), co.b[i]);
     return to_f32(xv.v[i]);
 }
 
