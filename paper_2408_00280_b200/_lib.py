@@ -9,7 +9,9 @@ import ctypes
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libsnn_lif.so")
+# SNN_LIF_LIBRARY: load another build of the same library (A/B timing of kernel changes,
+# tools/kbench.py); it is still this package's CUDA library, never a fallback.
+LIB_PATH = os.environ.get("SNN_LIF_LIBRARY") or os.path.join(_PKG, "libsnn_lif.so")
 
 # enums (include/snn_lif.h)
 SNN_OK = 0

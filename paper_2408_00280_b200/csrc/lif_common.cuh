@@ -8,6 +8,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace snn {
 
 // ------------------------------------------------------------------------------------
@@ -200,6 +202,30 @@ template <typename T> __device__ __forceinline__ T from_f32(float v);
 template <> __device__ __forceinline__ float from_f32<float>(float v) { return v; }
 template <> __device__ __forceinline__ __nv_bfloat16 from_f32<__nv_bfloat16>(float v) {
     return __float2bfloat16_rn(v);
+}
+
+// Step a row pointer by `ldb` bytes (a 64-bit IADD3 + IADD3.X pair; the kernels walk
+// their output rows this way instead of scaling an element index every row).
+template <typename T>
+__device__ __forceinline__ T* step_bytes(T* p, int64_t ldb) {
+    return reinterpret_cast<T*>(reinterpret_cast<char*>(p) + ldb);
+}
+
+// Elements i, i+1 (i even) of a pack widened to fp32 as one pair.  bf16 -> fp32 is exact
+// (the bf16 bits are the high half of the fp32 word), so for a bf16x2 word w the pair is
+// (w << 16, w & 0xffff0000): two integer ops, where the generic per-element conversion costs
+// the compiler a PRMT and two shifts.
+template <typename T, int VEC>
+__device__ __forceinline__ F2 load2(const Pack<T, VEC>& p, int i) {
+    if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+        const uint32_t w = *reinterpret_cast<const uint32_t*>(&p.v[i]);
+        F2 r;
+        asm("{\n\t.reg .b32 lo, hi;\n\tshl.b32 lo, %1, 16;\n\tand.b32 hi, %1, 0xffff0000;\n\t"
+            "mov.b64 %0, {lo, hi};\n\t}" : "=l"(r.v) : "r"(w));
+        return r;
+    } else {
+        return f2(to_f32(p.v[i]), to_f32(p.v[i + 1]));
+    }
 }
 
 // Streaming loads: read once, never re-read by this kernel -> evict-first in L2 (.cs).

@@ -101,7 +101,7 @@ struct BwdArgs {
 // AFF: the input is X' = fma(a, X, b); otherwise X itself.
 template <bool AFF, typename IO, int VEC>
 __device__ __forceinline__ F2 input2(const AffCoef<VEC>& co, const Pack<IO, VEC>& xv, int i) {
-    const F2 X2 = f2(to_f32(xv.v[i]), to_f32(xv.v[i + 1]));
+    const F2 X2 = load2(xv, i);
     if constexpr (AFF) return fma2(f2(co.a[i], co.a[i + 1]), X2, f2(co.b[i], co.b[i + 1]));
     return X2;
 }
@@ -236,11 +236,11 @@ __device__ __forceinline__ Pack<IO, VEC> bwd_step(const LifConsts& c, float (&gV
 #pragma unroll
         for (int i = 0; i < VEC; i += 2) {
             const F2 gH = lif_grad_step2<MODE>(c, f2(h[i], h[i + 1]),
-                                               f2(to_f32(gs.v[i]), to_f32(gs.v[i + 1])),
+                                               load2(gs, i),
                                                f2(gV[i], gV[i + 1]));
             F2 gx = mul2(f2(c.s), gH);
             if constexpr (AFF) {
-                const F2 x2 = f2(to_f32(xr->v[i]), to_f32(xr->v[i + 1]));
+                const F2 x2 = load2(*xr, i);
                 const F2 pa2 = fma2(gx, x2, f2(pa[i], pa[i + 1]));
                 const F2 pb2 = add2(gx, f2(pb[i], pb[i + 1]));
                 pa[i] = lo(pa2); pa[i + 1] = hi(pa2);

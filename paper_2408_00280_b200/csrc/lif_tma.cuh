@@ -262,11 +262,11 @@ struct BwdRecTma {
 };
 
 // Reverse walk over rows [0, rows) of one chunk.  h = recomputed H; gsm = gS rows in smem;
-// gxp = gX row of the chunk's LAST row, walked backwards by ld.
+// gxp = gX at the chunk's LAST row, walked backwards by ldb bytes.
 template <typename IO, int VEC, int MODE, int BW, int ROWS_MAX>
 __device__ __forceinline__ void bwd_chunk(const LifConsts& c, float (&gV)[VEC],
                                           const float (&h)[ROWS_MAX][VEC], const IO* gsm,
-                                          IO* gxp, int64_t ld, int rows, bool valid,
+                                          IO* gxp, int64_t ldb, int rows, bool valid,
                                           const AffCoef<VEC>& co, const IO* xs, float* pa, float* pb) {
 #pragma unroll
     for (int j = ROWS_MAX - 1; j >= 0; --j) {
@@ -280,7 +280,7 @@ __device__ __forceinline__ void bwd_chunk(const LifConsts& c, float (&gV)[VEC],
                 out = bwd_step<IO, VEC, MODE>(c, gV, h[j], gv);
             }
             if (valid) st_stream<IO, VEC>(gxp, out);
-            gxp -= ld;
+            gxp = step_bytes(gxp, -ldb);
         }
     }
 }
@@ -341,6 +341,7 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
     const int roff = box_off<VEC, BW, kCkpt>(nt, 0);
     const int ckoff = box_off<VEC, BW, 1>(nt, 0);
     IO* gx = reinterpret_cast<IO*>(a.gX);
+    const int64_t ldb = ld * (int64_t)sizeof(IO);
     uint32_t k = 0;
     while (true) {
         int s = k % S;
@@ -383,10 +384,10 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
             IO* gxp = gx + (t0 + rows - 1) * ld + n0;
             if (rows == kCkpt && tile_full) {   // full chunk of a full tile: guard-free code
                 recompute_chunk<IO, VEC, MODE, BW>(c, V, h, xs, kCkpt, co);
-                bwd_chunk<IO, VEC, MODE, BW, kCkpt>(c, gV, h, gsm, gxp, ld, kCkpt, true, co, xs, pa, pb);
+                bwd_chunk<IO, VEC, MODE, BW, kCkpt>(c, gV, h, gsm, gxp, ldb, kCkpt, true, co, xs, pa, pb);
             } else {
                 recompute_chunk<IO, VEC, MODE, BW>(c, V, h, xs, rows, co);
-                bwd_chunk<IO, VEC, MODE, BW, kCkpt>(c, gV, h, gsm, gxp, ld, rows, valid, co, xs, pa, pb);
+                bwd_chunk<IO, VEC, MODE, BW, kCkpt>(c, gV, h, gsm, gxp, ldb, rows, valid, co, xs, pa, pb);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&bar->empty[s]);
@@ -466,6 +467,7 @@ lif_backward_saveh_tma_kernel(const __grid_constant__ CUtensorMap tmh,
     const int nt = ct * VEC;
     const int roff = box_off<VEC, BW, R>(nt, 0);
     IO* gx = reinterpret_cast<IO*>(a.gX);
+    const int64_t ldb = ld * (int64_t)sizeof(IO);
     uint32_t k = 0;
     while (true) {
         int s = k % S;
@@ -503,7 +505,7 @@ lif_backward_saveh_tma_kernel(const __grid_constant__ CUtensorMap tmh,
                         const Pack<IO, VEC> gv = *reinterpret_cast<const Pack<IO, VEC>*>(gsm + r * BW);
                         const Pack<IO, VEC> out = bwd_step<IO, VEC, MODE>(c, gV, hv.v, gv);
                         if (decltype(full)::value || valid) st_stream<IO, VEC>(gxp, out);
-                        gxp -= ld;
+                        gxp = step_bytes(gxp, -ldb);
                     }
                 }
             };

@@ -1,0 +1,77 @@
+"""Per-kernel timing of the fused LIF forward / backward on a list of shapes (tuning aid, not
+the bench contract): CUDA events around each launch on the launch stream, two input batches
+alternated so consecutive launches do not hit each other's data in L2, algorithmic bytes
+per DESIGN.md section 6.
+
+    python tools/kbench.py [--reps 20] [--cases cfg1,cfg2,t16]
+"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import paper_2408_00280_b200 as snn  # noqa: E402
+import snn_synth  # noqa: E402
+
+CASES = {
+    "cfg1": [("f32", 512, 1 << 20)],
+    "sweep": [("f32", 8, 1 << 20), ("f32", 32, 1 << 20), ("f32", 128, 1 << 20)],
+    "cfg2": [("bf16", 16, 128 * 64 * 32 * 32), ("bf16", 16, 128 * 128 * 16 * 16),
+             ("bf16", 16, 128 * 256 * 8 * 8), ("bf16", 16, 128 * 512 * 4 * 4),
+             ("bf16", 16, 128 * 512 * 2 * 2)],
+    "t16": [("f32", 16, 1 << 23)],
+    "bf512": [("bf16", 512, 1 << 20)],
+}
+
+
+def alg_bytes(dt, T, N, save_mode="recompute"):
+    e = 4 if dt == "f32" else 2
+    ck = 4.0 / 16
+    return (e + 1 + ck) * T * N, (3 * e + ck) * T * N
+
+
+def time_case(dt, T, N, reps):
+    dtype = torch.float32 if dt == "f32" else torch.bfloat16
+    p = snn.LIFParams.paper()
+    xs = [snn_synth.normal_tensor(1234 + i, T, N, device="cuda", dtype=dtype) for i in range(2)]
+    gs = [snn_synth.normal_tensor(4321 + i, T, N, device="cuda", dtype=dtype) for i in range(2)]
+    st = torch.cuda.current_stream()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(reps)]
+    for i in range(3):
+        f = snn.lif_forward(xs[i % 2], p, return_v_final=False)
+        snn.lif_backward(gs[i % 2], f, return_grad_v_init=False)
+    torch.cuda.synchronize()
+    torch.cuda._sleep(int(3e6 + 2.5e5 * reps))   # keep the GPU busy while the host enqueues
+    for i in range(reps):
+        e = ev[i]
+        e[0].record(st)
+        f = snn.lif_forward(xs[i % 2], p, return_v_final=False)
+        e[1].record(st)
+        e[2].record(st)
+        snn.lif_backward(gs[i % 2], f, return_grad_v_init=False)
+        e[3].record(st)
+    torch.cuda.synchronize()
+    tf = sorted(e[0].elapsed_time(e[1]) for e in ev)[reps // 2]
+    tb = sorted(e[2].elapsed_time(e[3]) for e in ev)[reps // 2]
+    bf, bb = alg_bytes(dt, T, N)
+    print(f"{dt:5s} T={T:4d} N={N:9d}  fwd {tf * 1e3:8.1f} us {bf / tf / 1e6:7.0f} GB/s   "
+          f"bwd {tb * 1e3:8.1f} us {bb / tb / 1e6:7.0f} GB/s", flush=True)
+    return tf, tb
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--cases", default="cfg1,cfg2,t16")
+    a = ap.parse_args()
+    torch.cuda.set_device(0)
+    for c in a.cases.split(","):
+        for dt, T, N in CASES[c]:
+            time_case(dt, T, N, a.reps)
+
+
+if __name__ == "__main__":
+    main()
