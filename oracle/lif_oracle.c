@@ -231,3 +231,25 @@ void lif_oracle_affine_grads(int64_t T, int64_t N, const double* x, const double
             gshift[c] += g;
         }
 }
+
+/*
+ * Residual add in the prologue ("fold the preceding BN affine / residual
+ * add into the LIF prologue"; the spiking-ResNet block feeds its LIF neuron with
+ * BN(conv(.)) + shortcut).  Plain definition: the layer's input current is
+ *     X'[t, n] = scale[c] * X[t, n] + shift[c] + R[t, n],   c = (n / HW) % C,
+ * with R the shortcut tensor, and by the chain rule
+ *     dL/dR[t, n] = dL/dX'[t, n]
+ * while dL/dX, dL/dscale and dL/dshift are lif_oracle_affine_grads' (R does not enter them).
+ * Pinned by finite differences of the smoothed model with respect to R
+ * (tests/test_oracle_pins.py).
+ */
+void lif_oracle_affine_residual_input(int64_t T, int64_t N, const double* x, const double* scale,
+                                      const double* shift, const double* r, int64_t C, int64_t HW,
+                                      double* xout)
+{
+    for (int64_t t = 0; t < T; ++t)
+        for (int64_t n = 0; n < N; ++n) {
+            int64_t c = (n / HW) % C;
+            xout[t * N + n] = scale[c] * x[t * N + n] + shift[c] + r[t * N + n];
+        }
+}

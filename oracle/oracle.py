@@ -89,6 +89,8 @@ def _load():
         i64 = ctypes.c_int64
         lib.lif_oracle_affine_input.argtypes = [i64, i64, dp, dp, dp, i64, i64, dp]
         lib.lif_oracle_affine_input.restype = None
+        lib.lif_oracle_affine_residual_input.argtypes = [i64, i64, dp, dp, dp, dp, i64, i64, dp]
+        lib.lif_oracle_affine_residual_input.restype = None
         lib.lif_oracle_affine_grads.argtypes = [i64, i64, dp, dp, dp, i64, i64, dp, dp, dp]
         lib.lif_oracle_affine_grads.restype = None
         _lib = lib
@@ -153,12 +155,19 @@ def backward(p: OracleParams, gS, H, grad_v_final=None, return_terms=False):
     return gX, gvi
 
 
-def affine_input(x, scale, shift, C, HW):
-    """X'[t, n] = scale[c] X[t, n] + shift[c], c = (n / HW) % C."""
+def affine_input(x, scale, shift, C, HW, residual=None):
+    """X'[t, n] = scale[c] X[t, n] + shift[c] (+ R[t, n]), c = (n / HW) % C.
+    The gradient of the residual R is dL/dX' itself (lif_oracle_affine_residual_input)."""
     x = _f64(x); scale = _f64(scale); shift = _f64(shift)
     T, N = x.shape
     out = np.empty((T, N))
-    _load().lif_oracle_affine_input(T, N, _dp(x), _dp(scale), _dp(shift), int(C), int(HW), _dp(out))
+    if residual is None:
+        _load().lif_oracle_affine_input(T, N, _dp(x), _dp(scale), _dp(shift), int(C), int(HW), _dp(out))
+    else:
+        r = _f64(residual)
+        assert r.shape == x.shape
+        _load().lif_oracle_affine_residual_input(T, N, _dp(x), _dp(scale), _dp(shift), _dp(r), int(C),
+                                                 int(HW), _dp(out))
     return out
 
 

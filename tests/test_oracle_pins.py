@@ -438,3 +438,52 @@ def test_affine_gradients_finite_differences(decay_input):
         Xp = X.copy(); Xp[t, n] += h
         Xm = X.copy(); Xm[t, n] -= h
         assert gx[t, n] == pytest.approx((loss(scale, shift, Xp) - loss(scale, shift, Xm)) / (2 * h), rel=2e-6, abs=1e-8)
+
+
+def test_affine_residual_input_definition():
+    """X' = scale[c] X + shift[c] + R: reduces to the plain affine at R = 0, to R itself at
+    scale = 0, shift = 0, and equals an independent reshape-based evaluation."""
+    rng = np.random.default_rng(23)
+    T, B, C, HW = 3, 2, 3, 4
+    x = rng.normal(size=(T, B * C * HW))
+    R = rng.normal(size=x.shape)
+    scale = np.array([2.0, -1.0, 0.5]); shift = np.array([0.25, 0.0, -1.0])
+    np.testing.assert_array_equal(affine_input(x, scale, shift, C, HW, residual=np.zeros_like(x)),
+                                  affine_input(x, scale, shift, C, HW))
+    np.testing.assert_array_equal(affine_input(x, np.zeros(C), np.zeros(C), C, HW, residual=R), R)
+    xr = x.reshape(T, B, C, HW)
+    ref = (xr * scale[None, None, :, None] + shift[None, None, :, None]).reshape(T, -1) + R
+    np.testing.assert_allclose(affine_input(x, scale, shift, C, HW, residual=R), ref, rtol=0, atol=1e-15)
+
+
+@pytest.mark.parametrize("soft", [False, True])
+def test_affine_residual_gradient_finite_differences(soft):
+    """dL/dR = dL/dX' (the oracle backward's gX at the input X' = scale X + shift + R), and the
+    affine gradients are unchanged by R: central differences of the smoothed model in R,
+    scale and X."""
+    rng = np.random.default_rng(24)
+    T, B, C, HW = 4, 2, 2, 3
+    N = B * C * HW
+    p = OracleParams(tau=1.4, v_th=0.6, v_reset=0.0, soft_reset=soft, alpha=3.0, smoothed=True)
+    X = rng.uniform(-0.5, 1.0, size=(T, N))
+    R = rng.uniform(-0.5, 0.8, size=(T, N))
+    scale = np.array([1.1, 0.7]); shift = np.array([0.1, -0.2])
+    W = rng.normal(size=(T, N)); wv = rng.normal(size=N)
+
+    def loss(sc, xx, rr):
+        r = forward(p, affine_input(xx, sc, shift, C, HW, residual=rr))
+        return float((W * r["S"]).sum() + (wv * r["v_final"]).sum())
+
+    r = forward(p, affine_input(X, scale, shift, C, HW, residual=R))
+    gxp, _ = backward(p, W, r["H"], grad_v_final=wv)
+    gx, gs, _ = affine_grads(X, gxp, scale, C, HW)
+    h = 1e-6
+    for (t, n) in [(0, 0), (1, 7), (3, 11)]:
+        Rp = R.copy(); Rp[t, n] += h
+        Rm = R.copy(); Rm[t, n] -= h
+        assert gxp[t, n] == pytest.approx((loss(scale, X, Rp) - loss(scale, X, Rm)) / (2 * h), rel=2e-6, abs=1e-8)
+        Xp = X.copy(); Xp[t, n] += h
+        Xm = X.copy(); Xm[t, n] -= h
+        assert gx[t, n] == pytest.approx((loss(scale, Xp, R) - loss(scale, Xm, R)) / (2 * h), rel=2e-6, abs=1e-8)
+    e = np.array([h, 0.0])
+    assert gs[0] == pytest.approx((loss(scale + e, X, R) - loss(scale - e, X, R)) / (2 * h), rel=2e-6, abs=1e-8)
