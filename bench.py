@@ -422,8 +422,27 @@ def run_affine(args, params, dev):
                             return_v_final=False)
         snn.lif_backward(G, f, return_grad_v_init=False)
 
+    # + residual shortcut R (the spiking-ResNet block input BN(conv) + R)
+    Rr = snn_synth.normal_tensor(999, T, N, device=dev, std=0.5)
+
+    def fused_res():
+        f = snn.lif_forward_affine(X, params, spec, spike_fmt=args.spike_fmt, return_v_final=False,
+                                   residual=Rr)
+        snn.lif_backward_affine(G, f, return_grad_v_init=False)
+
+    def unfused_res():   # dL/dR is dL/dX' itself (autograd hands the same tensor to both branches)
+        xa = (X.view(T, B, C, HW) * sc5 + sh5).view(T, N) + Rr
+        f = snn.lif_forward(xa, params, spike_fmt=args.spike_fmt, save_mode="recompute",
+                            return_v_final=False)
+        gxa, _ = snn.lif_backward(G, f, return_grad_v_init=False)
+        g4 = gxa.view(T, B, C, HW)
+        _ = g4 * sc5
+        _ = (g4 * X.view(T, B, C, HW)).sum(dim=(0, 1, 3))
+        _ = g4.sum(dim=(0, 1, 3))
+
     res = {"shape": {"T": T, "B": B, "C": C, "HW": HW}}
-    for name, fn in (("fused", fused), ("unfused", unfused), ("plain_lif", plain)):
+    for name, fn in (("fused", fused), ("unfused", unfused), ("plain_lif", plain),
+                     ("fused_residual", fused_res), ("unfused_residual", unfused_res)):
         for _ in range(3):
             fn()
         torch.cuda.synchronize(dev)
@@ -442,6 +461,7 @@ def run_affine(args, params, dev):
         res[name + "_ms"] = round(ts[len(ts) // 2], 4)
         del g
     res["speedup_fused_vs_unfused"] = round(res["unfused_ms"] / res["fused_ms"], 3)
+    res["speedup_fused_vs_unfused_residual"] = round(res["unfused_residual_ms"] / res["fused_residual_ms"], 3)
     res["fused_overhead_vs_plain_lif"] = round(res["fused_ms"] / res["plain_lif_ms"] - 1, 4)
     res["neuron_steps_per_s_fused"] = N * T / (res["fused_ms"] / 1e3)
     return res

@@ -55,7 +55,7 @@
 extern "C" {
 #endif
 
-#define SNN_LIF_ABI_VERSION 1
+#define SNN_LIF_ABI_VERSION 2
 
 typedef enum {
     SNN_OK = 0,
@@ -198,19 +198,29 @@ snn_status snn_lif_backward_handoff(const snn_lif_params* params, const snn_lif_
                                     const float* grad_v_final, const snn_lif_handoff* handoff,
                                     void* grad_x, float* grad_v_init, void* stream);
 
-/* ---- Producer fusion: a per-channel affine prologue folded into the LIF
- * input -- the layer's current is X' = scale[c] X + shift[c] with c = (n / HW) % C, e.g. the
- * BatchNorm affine of a conv output [T, B, C, H, W] flattened to N = B C H W -- so the
- * normalised tensor is never written to / re-read from HBM.  The backward returns
- * dL/dX = scale[c] dL/dX' and the per-channel sums the BN backward needs,
- * grad_scale[c] = sum_{t,n in c} dL/dX'[t,n] X[t,n] and grad_shift[c] = sum dL/dX'[t,n]
- * (per-neuron partials in caller scratch, then a deterministic fixed-order reduction).
- * Requirements: N % (C * HW) == 0; backward needs save_mode SAVE_RECOMPUTE. */
+/* ---- Producer fusion ("fold the preceding BN affine / residual add into
+ * the LIF prologue"): a per-channel affine prologue folded into the LIF input -- the
+ * layer's current is X' = scale[c] X + shift[c] (+ R) with c = (n / HW) % C, e.g. the
+ * BatchNorm affine of a conv output [T, B, C, H, W] flattened to N = B C H W, plus
+ * optionally a residual shortcut R (the spiking-ResNet block's LIF input BN(conv) + R) --
+ * so neither the normalised tensor nor the sum is ever written to / re-read from HBM.
+ * The backward returns dL/dX = scale[c] dL/dX', dL/dR = dL/dX' (when R is given) and the
+ * per-channel sums the BN backward needs, grad_scale[c] = sum_{t,n in c} dL/dX'[t,n] X[t,n]
+ * and grad_shift[c] = sum dL/dX'[t,n] (per-neuron partials in caller scratch, then a
+ * deterministic fixed-order reduction).
+ * Requirements: N % (C * HW) == 0; backward needs save_mode SAVE_RECOMPUTE.  With a
+ * residual: forward save_mode SAVE_RECOMPUTE or SAVE_NONE, and the TMA path (16-byte-aligned
+ * pointers, ld a multiple of 16 bytes, N a multiple of 8 for bf16 / 4 for fp32; the
+ * backward: N a multiple of 2), else SNN_ERR_UNSUPPORTED.  The backward must get the same
+ * residual the forward got (the RECOMPUTE backward re-derives X'). */
 typedef struct {
     const float* scale;   /* [C] fp32 */
     const float* shift;   /* [C] fp32 */
     int64_t C;            /* channels (>= 1)                                          */
     int64_t HW;           /* neurons per channel per sample (>= 1)                    */
+    const void* residual; /* [T, ld] io dtype shortcut R added to the input, or NULL  (read) */
+    void* grad_residual;  /* backward only: [T, ld] io dtype dL/dR, required iff residual;
+                             ignored by the forward                                  (write) */
 } snn_lif_affine;
 
 snn_status snn_lif_forward_affine(const snn_lif_params* params, const snn_lif_shape* shape,

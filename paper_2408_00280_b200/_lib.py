@@ -51,7 +51,10 @@ class snn_lif_shape(ctypes.Structure):
 
 class snn_lif_affine(ctypes.Structure):
     _fields_ = [("scale", ctypes.c_void_p), ("shift", ctypes.c_void_p), ("C", ctypes.c_int64),
-                ("HW", ctypes.c_int64)]
+                ("HW", ctypes.c_int64), ("residual", ctypes.c_void_p), ("grad_residual", ctypes.c_void_p)]
+
+
+ABI_VERSION = 2   # include/snn_lif.h SNN_LIF_ABI_VERSION these structs mirror
 
 
 class snn_lif_handoff(ctypes.Structure):
@@ -82,6 +85,9 @@ def _load() -> ctypes.CDLL:
     lib.snn_last_error_message.restype = ctypes.c_char_p
     lib.snn_lif_abi_version.argtypes = []
     lib.snn_lif_abi_version.restype = ctypes.c_int
+    if lib.snn_lif_abi_version() != ABI_VERSION:
+        raise ImportError(f"{LIB_PATH} has ABI version {lib.snn_lif_abi_version()}, the binding "
+                          f"expects {ABI_VERSION}: rebuild the library")
     i64 = ctypes.c_int64
     lib.snn_lif_serial_forward_step.argtypes = [P, ctypes.c_int, i64, vp, vp, vp, vp, vp]
     lib.snn_lif_serial_forward_step.restype = ctypes.c_int

@@ -58,30 +58,39 @@ class LIFLayer(torch.nn.Module):
 
 
 class FusedAffineLIF(torch.autograd.Function):
-    """spikes = FusedAffineLIF.apply(x, scale, shift, params) for x [T, B, C, *spatial]:
-    the per-channel affine (e.g. BatchNorm's gamma/sigma, beta - mu gamma/sigma) is folded
-    into the LIF prologue, so the normalised tensor never touches HBM."""
+    """spikes = FusedAffineLIF.apply(x, scale, shift, params[, residual]) for x [T, B, C, *spatial]:
+    the per-channel affine (e.g. BatchNorm's gamma/sigma, beta - mu gamma/sigma) and, when
+    given, the residual shortcut (same shape as x) are folded into the LIF prologue
+    (SURVEY 8(f) f4), so neither the normalised tensor nor the sum touches HBM."""
 
     @staticmethod
-    def forward(ctx, x, scale, shift, params: LIFParams):
+    def forward(ctx, x, scale, shift, params: LIFParams, residual=None):
         T, B, C = x.shape[:3]
         HW = x[0, 0, 0].numel()
         x2 = x.reshape(T, -1)
         x2 = x2 if x2.is_contiguous() else x2.contiguous()
+        r2 = None
+        if residual is not None:   # the spiking-ResNet shortcut added to the LIF input
+            r2 = residual.reshape(T, -1).to(x.dtype)
+            r2 = r2 if r2.is_contiguous() else r2.contiguous()
         fwd = lif_forward_affine(x2, params, AffineSpec(scale.contiguous(), shift.contiguous(), C, HW),
-                                 spike_fmt="io", return_v_final=False)
+                                 spike_fmt="io", return_v_final=False, residual=r2)
         ctx.fwd = fwd
         ctx.shape = x.shape
+        ctx.res_shape = None if residual is None else (residual.shape, residual.dtype)
         return fwd.spikes.reshape(x.shape)
 
     @staticmethod
     def backward(ctx, grad_spikes):
         fwd = ctx.fwd
         T = grad_spikes.shape[0]
-        gx, _, gsc, gsh = lif_backward_affine(grad_spikes.reshape(T, -1).to(fwd.x.dtype), fwd,
-                                              return_grad_v_init=False)
+        out = lif_backward_affine(grad_spikes.reshape(T, -1).to(fwd.x.dtype), fwd, return_grad_v_init=False)
         ctx.fwd = None
-        return gx.reshape(ctx.shape), gsc, gsh, None
+        gres = None
+        if ctx.res_shape is not None:
+            shape, dtype = ctx.res_shape
+            gres = out[4].reshape(shape).to(dtype)
+        return out[0].reshape(ctx.shape), out[2], out[3], None, gres
 
 
 class AffineLIFLayer(torch.nn.Module):
@@ -94,5 +103,6 @@ class AffineLIFLayer(torch.nn.Module):
         self.scale = torch.nn.Parameter(torch.ones(channels))
         self.shift = torch.nn.Parameter(torch.zeros(channels))
 
-    def forward(self, x):
-        return FusedAffineLIF.apply(x, self.scale, self.shift, self.params)
+    def forward(self, x, residual=None):
+        """spikes = LIF(scale[c] x + shift[c] (+ residual)); residual has x's shape."""
+        return FusedAffineLIF.apply(x, self.scale, self.shift, self.params, residual)

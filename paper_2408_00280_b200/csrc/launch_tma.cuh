@@ -13,11 +13,13 @@ template <typename IO> struct TmaCfg;
 template <> struct TmaCfg<float> {
     static constexpr int FV = 4, FN = 128, FR = 8, FS = 6;   // forward: 16 KB stages, 2 CTAs/SM
     static constexpr int RV = 2, RN = 256, RS = 3;           // backward RECOMPUTE: 66 KB chunks, FFMA2 pairs
+    static constexpr int RS_RES = 2;                         // + residual rows: 99 KB chunks
     static constexpr int HV = 2, HN = 256, HR = 8, HS = 6;   // backward SAVE_H: 32 KB stages
 };
 template <> struct TmaCfg<__nv_bfloat16> {
     static constexpr int FV = 8, FN = 128, FR = 8, FS = 6;
     static constexpr int RV = 2, RN = 256, RS = 3;           // 34 KB chunks, 2 CTAs/SM
+    static constexpr int RS_RES = 2;                         // + residual rows: 51 KB chunks
     static constexpr int HV = 2, HN = 512, HR = 8, HS = 4;
 };
 
@@ -26,19 +28,32 @@ snn_status launch_forward_tma(const snn_lif_shape* s, const snn::FwdArgs& a, boo
                               cudaStream_t st) {
     using C = TmaCfg<IO>;
     using Cfg = snn::FwdTma<IO, C::FV, C::FN, C::FR, C::FS>;
-    CUtensorMap tmx;
+    CUtensorMap tmx, tmr;
     if (!encode_2d(&tmx, a.x, sizeof(IO), s->N, s->T, s->ld, Cfg::BW, C::FR))
         return fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled failed for x%s", encode_detail());
+    tmr = tmx;
+    if (a.af.residual != nullptr &&
+        !encode_2d(&tmr, a.af.residual, sizeof(IO), s->N, s->T, s->ld, Cfg::BW, C::FR))
+        return fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled failed for the residual%s", encode_detail());
     const int64_t ntiles = (s->N + Cfg::W - 1) / Cfg::W;
-    auto go = [&](auto sfmt, auto save, auto sft, auto aff) {
+    // pro: 0 plain, 1 affine, 2 affine + residual (the residual stage is twice as large, so
+    // half the ring depth keeps two CTAs per SM).
+    auto go = [&](auto sfmt, auto save, auto sft, auto pro) {
+        constexpr int P = decltype(pro)::value;
+        constexpr int NS = P == 2 ? C::FS / 2 : C::FS;
+        using K = snn::FwdTma<IO, C::FV, C::FN, C::FR, NS, P == 2 ? 2 : 1>;
         auto k = snn::lif_forward_tma_kernel<IO, C::FV, decltype(sfmt)::value, decltype(save)::value,
-                                             (bool)decltype(sft)::value, (bool)decltype(aff)::value,
-                                             C::FN, C::FR, C::FS>;
-        return launch_tiles(k, Cfg::THREADS, Cfg::SMEM, ntiles, (s->T + C::FR - 1) / C::FR, st,
-                            "lif_forward_tma_kernel", tmx, a);
+                                             (bool)decltype(sft)::value, P >= 1, P == 2,
+                                             C::FN, C::FR, NS>;
+        return launch_tiles(k, K::THREADS, K::SMEM, ntiles, (s->T + C::FR - 1) / C::FR, st,
+                            "lif_forward_tma_kernel", tmx, tmr, a);
     };
     auto by_aff = [&](auto sfmt, auto save, auto sft) {
-        return a.af.scale != nullptr ? go(sfmt, save, sft, IC<1>{}) : go(sfmt, save, sft, IC<0>{});
+        if (a.af.scale == nullptr) return go(sfmt, save, sft, IC<0>{});
+        if (a.af.residual == nullptr) return go(sfmt, save, sft, IC<1>{});
+        if constexpr (decltype(save)::value == snn::SAVE_H)   // host rejects SAVE_H + residual
+            return fail(SNN_ERR_UNSUPPORTED, "the residual prologue needs SAVE_RECOMPUTE or SAVE_NONE");
+        else return go(sfmt, save, sft, IC<2>{});
     };
     auto by_soft = [&](auto sfmt, auto save) {
         return soft ? by_aff(sfmt, save, IC<1>{}) : by_aff(sfmt, save, IC<0>{});
@@ -72,22 +87,27 @@ snn_status launch_backward_tma_mode(const snn_lif_shape* s, const snn::BwdArgs& 
                             (s->T + C::HR - 1) / C::HR, st, "lif_backward_saveh_tma_kernel", tmh, tmg, a);
     }
     }
-    using Cfg = snn::BwdRecTma<IO, C::RV, C::RN, C::RS>;
+    constexpr bool RES = snn::Mode<MODE>::RES;
+    constexpr int NS = RES ? C::RS_RES : C::RS;
+    using Cfg = snn::BwdRecTma<IO, C::RV, C::RN, NS, RES>;
     const int64_t nch = (s->T + snn::kCkpt - 1) / snn::kCkpt;
-    CUtensorMap tmx, tmg, tmck;
+    CUtensorMap tmx, tmg, tmck, tmr;
     if (!encode_2d(&tmx, a.x, sizeof(IO), s->N, s->T, s->ld, Cfg::BW, snn::kCkpt) ||
         !encode_2d(&tmg, a.gS, sizeof(IO), s->N, s->T, s->ld, Cfg::BW, snn::kCkpt) ||
         !encode_2d(&tmck, a.saved, 4, s->N, nch, a.ldh, Cfg::BW, 1))
         return fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled failed (RECOMPUTE backward)%s", encode_detail());
-    auto k = snn::lif_backward_recompute_tma_kernel<IO, C::RV, MODE, C::RN, C::RS>;
+    tmr = tmx;
+    if (RES && !encode_2d(&tmr, a.af.residual, sizeof(IO), s->N, s->T, s->ld, Cfg::BW, snn::kCkpt))
+        return fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled failed for the residual%s", encode_detail());
+    auto k = snn::lif_backward_recompute_tma_kernel<IO, C::RV, MODE, C::RN, NS>;
     return launch_tiles(k, Cfg::THREADS, Cfg::SMEM, (s->N + Cfg::W - 1) / Cfg::W, nch, st,
-                        "lif_backward_recompute_tma_kernel", tmx, tmg, tmck, a);
+                        "lif_backward_recompute_tma_kernel", tmx, tmg, tmck, tmr, a);
 }
 
 template <typename IO>
 snn_status launch_backward_tma(const snn_lif_shape* s, const snn::BwdArgs& a, int mode,
                                cudaStream_t st) {
-    switch (mode & 15) {
+    switch (mode & 31) {
         case 0: return launch_backward_tma_mode<IO, 0>(s, a, st);
         case 1: return launch_backward_tma_mode<IO, 1>(s, a, st);
         case 2: return launch_backward_tma_mode<IO, 2>(s, a, st);
@@ -103,7 +123,16 @@ snn_status launch_backward_tma(const snn_lif_shape* s, const snn::BwdArgs& a, in
         case 12: return launch_backward_tma_mode<IO, 12>(s, a, st);
         case 13: return launch_backward_tma_mode<IO, 13>(s, a, st);
         case 14: return launch_backward_tma_mode<IO, 14>(s, a, st);
-        default: return launch_backward_tma_mode<IO, 15>(s, a, st);
+        case 15: return launch_backward_tma_mode<IO, 15>(s, a, st);
+        case 24: return launch_backward_tma_mode<IO, 24>(s, a, st);
+        case 25: return launch_backward_tma_mode<IO, 25>(s, a, st);
+        case 26: return launch_backward_tma_mode<IO, 26>(s, a, st);
+        case 27: return launch_backward_tma_mode<IO, 27>(s, a, st);
+        case 28: return launch_backward_tma_mode<IO, 28>(s, a, st);
+        case 29: return launch_backward_tma_mode<IO, 29>(s, a, st);
+        case 30: return launch_backward_tma_mode<IO, 30>(s, a, st);
+        case 31: return launch_backward_tma_mode<IO, 31>(s, a, st);
+        default: return fail(SNN_ERR_UNSUPPORTED, "backward variant %d (residual without affine)", mode);
     }
 }
 

@@ -34,13 +34,14 @@ __device__ __forceinline__ void pin(LifConsts& c) {
 }
 
 // Compile-time variant of the backward: bit 0 surrogate (0 sigmoid, 1 arctan), bit 1 soft
-// reset, bit 2 detach_reset.  Branch-free inner loops.
+// reset, bit 2 detach_reset, bit 3 affine prologue, bit 4 residual prologue.  Branch-free inner loops.
 template <int MODE>
 struct Mode {
     static constexpr int SURR = MODE & 1;
     static constexpr bool SOFT = (MODE & 2) != 0;
     static constexpr bool DETACH = (MODE & 4) != 0;
     static constexpr bool AFF = (MODE & 8) != 0;   // affine prologue gradients (RECOMPUTE only)
+    static constexpr bool RES = (MODE & 16) != 0;  // + residual add (implies AFF; TMA path only)
 };
 
 __device__ __forceinline__ float ex2_approx(float x) {  // MUFU.EX2, ftz

@@ -44,6 +44,8 @@ struct Affine {
     int64_t C, HW;
     float* part_a;        // [N] backward output (per-neuron sum over t) or null
     float* part_b;        // [N]
+    const void* residual; // [T, ld] IO shortcut R added to the input (X' = a X + b + R) or null
+    void* grad_residual;  // [T, ld] IO backward output dL/dR = dL/dX' (iff residual)
 };
 
 template <int VEC>
@@ -99,27 +101,34 @@ struct BwdArgs {
 // Eq. 1-2 + reset for this thread's VEC neurons: updates V, returns H in `hp` and the
 // spike bits (bit i = neuron i of the group).
 // AFF: the input is X' = fma(a, X, b); otherwise X itself.
-template <bool AFF, typename IO, int VEC>
-__device__ __forceinline__ F2 input2(const AffCoef<VEC>& co, const Pack<IO, VEC>& xv, int i) {
-    const F2 X2 = load2(xv, i);
-    if constexpr (AFF) return fma2(f2(co.a[i], co.a[i + 1]), X2, f2(co.b[i], co.b[i + 1]));
+// RES (with AFF): X' = fma(a, X, b) + R, R the residual shortcut row (rv).
+template <bool AFF, bool RES = false, typename IO, int VEC>
+__device__ __forceinline__ F2 input2(const AffCoef<VEC>& co, const Pack<IO, VEC>& xv, int i,
+                                     const Pack<IO, VEC>* rv = nullptr) {
+    F2 X2 = load2(xv, i);
+    if constexpr (AFF) X2 = fma2(f2(co.a[i], co.a[i + 1]), X2, f2(co.b[i], co.b[i + 1]));
+    if constexpr (RES) X2 = add2(X2, load2(*rv, i));
     return X2;
 }
-template <bool AFF, typename IO, int VEC>
-__device__ __forceinline__ float input1(const AffCoef<VEC>& co, const Pack<IO, VEC>& xv, int i) {
-    if constexpr (AFF) return __fmaf_rn(co.a[i], to_f32(xv.v[i]), co.b[i]);
-    return to_f32(xv.v[i]);
+template <bool AFF, bool RES = false, typename IO, int VEC>
+__device__ __forceinline__ float input1(const AffCoef<VEC>& co, const Pack<IO, VEC>& xv, int i,
+                                        const Pack<IO, VEC>* rv = nullptr) {
+    float X = to_f32(xv.v[i]);
+    if constexpr (AFF) X = __fmaf_rn(co.a[i], X, co.b[i]);
+    if constexpr (RES) X = __fadd_rn(X, to_f32(rv->v[i]));
+    return X;
 }
 
-template <bool SOFT, bool AFF, typename IO, int VEC>
+template <bool SOFT, bool AFF, bool RES = false, typename IO, int VEC>
 __device__ __forceinline__ unsigned fwd_compute(const LifConsts& c, float (&V)[VEC],
                                                 const Pack<IO, VEC>& xv, Pack<float, VEC>& hp,
-                                                const AffCoef<VEC>& co) {
+                                                const AffCoef<VEC>& co,
+                                                const Pack<IO, VEC>* rv = nullptr) {
     unsigned bits = 0;
     if constexpr (VEC % 2 == 0) {   // paired FFMA2 charge, same roundings as the scalar path
 #pragma unroll
         for (int i = 0; i < VEC; i += 2) {
-            const F2 X2 = input2<AFF>(co, xv, i);
+            const F2 X2 = input2<AFF, RES>(co, xv, i, rv);
             const F2 H2 = lif_charge2(c, f2(V[i], V[i + 1]), X2);
             const float Ha = lo(H2), Hb = hi(H2);
             const bool Sa = lif_fire(c, Ha), Sb = lif_fire(c, Hb);
@@ -132,7 +141,7 @@ __device__ __forceinline__ unsigned fwd_compute(const LifConsts& c, float (&V)[V
     } else {
 #pragma unroll
         for (int i = 0; i < VEC; ++i) {
-            const float H = lif_charge(c, V[i], input1<AFF>(co, xv, i));
+            const float H = lif_charge(c, V[i], input1<AFF, RES>(co, xv, i, rv));
             const bool S = lif_fire(c, H);
             V[i] = lif_reset<SOFT>(c, H, S);
             hp.v[i] = H;
@@ -143,14 +152,15 @@ __device__ __forceinline__ unsigned fwd_compute(const LifConsts& c, float (&V)[V
 }
 
 // Re-run the charge / fire / reset (no outputs) -- the RECOMPUTE backward's forward pass.
-template <bool SOFT, bool AFF, typename IO, int VEC>
+template <bool SOFT, bool AFF, bool RES = false, typename IO, int VEC>
 __device__ __forceinline__ void fwd_recompute_step(const LifConsts& c, float (&V)[VEC],
                                                    const Pack<IO, VEC>& xv, float (&h)[VEC],
-                                                   const AffCoef<VEC>& co) {
+                                                   const AffCoef<VEC>& co,
+                                                   const Pack<IO, VEC>* rv = nullptr) {
     if constexpr (VEC % 2 == 0) {
 #pragma unroll
         for (int i = 0; i < VEC; i += 2) {
-            const F2 X2 = input2<AFF>(co, xv, i);
+            const F2 X2 = input2<AFF, RES>(co, xv, i, rv);
             const F2 H2 = lif_charge2(c, f2(V[i], V[i + 1]), X2);
             h[i] = lo(H2);
             h[i + 1] = hi(H2);
@@ -160,7 +170,7 @@ __device__ __forceinline__ void fwd_recompute_step(const LifConsts& c, float (&V
     } else {
 #pragma unroll
         for (int i = 0; i < VEC; ++i) {
-            h[i] = lif_charge(c, V[i], input1<AFF>(co, xv, i));
+            h[i] = lif_charge(c, V[i], input1<AFF, RES>(co, xv, i, rv));
             V[i] = lif_reset<SOFT>(c, h[i], lif_fire(c, h[i]));
         }
     }
@@ -225,12 +235,15 @@ __device__ __forceinline__ int64_t spike_row_bytes(const FwdArgs& a) {
 // carries gV <- k gH.
 // AFF = with the affine prologue: gX = scale (s gH) and the per-neuron partials
 // pa += (s gH) X_raw, pb += (s gH) accumulate over the time walk (xr = raw X of this row).
+// RES (with AFF): also returns dL/dR = dL/dX' = s gH in *outr.
 template <typename IO, int VEC, int MODE, bool AFF = false>
 __device__ __forceinline__ Pack<IO, VEC> bwd_step(const LifConsts& c, float (&gV)[VEC],
                                                   const float (&h)[VEC], const Pack<IO, VEC>& gs,
                                                   const AffCoef<VEC>* co = nullptr,
                                                   const Pack<IO, VEC>* xr = nullptr,
-                                                  float* pa = nullptr, float* pb = nullptr) {
+                                                  float* pa = nullptr, float* pb = nullptr,
+                                                  Pack<IO, VEC>* outr = nullptr) {
+    constexpr bool RES = AFF && Mode<MODE>::RES;
     Pack<IO, VEC> out;
     if constexpr (VEC % 2 == 0) {   // paired FFMA2/FMUL2/FADD2, same roundings as scalar
 #pragma unroll
@@ -245,6 +258,10 @@ __device__ __forceinline__ Pack<IO, VEC> bwd_step(const LifConsts& c, float (&gV
                 const F2 pb2 = add2(gx, f2(pb[i], pb[i + 1]));
                 pa[i] = lo(pa2); pa[i + 1] = hi(pa2);
                 pb[i] = lo(pb2); pb[i + 1] = hi(pb2);
+                if constexpr (RES) {
+                    outr->v[i] = from_f32<IO>(lo(gx));
+                    outr->v[i + 1] = from_f32<IO>(hi(gx));
+                }
                 gx = mul2(f2(co->a[i], co->a[i + 1]), gx);
             }
             const F2 gv = mul2(f2(c.k), gH);
@@ -261,6 +278,7 @@ __device__ __forceinline__ Pack<IO, VEC> bwd_step(const LifConsts& c, float (&gV
             if constexpr (AFF) {
                 pa[i] = __fmaf_rn(gx, to_f32(xr->v[i]), pa[i]);
                 pb[i] = __fadd_rn(gx, pb[i]);
+                if constexpr (RES) outr->v[i] = from_f32<IO>(gx);
                 gx = __fmul_rn(co->a[i], gx);
             }
             out.v[i] = from_f32<IO>(gx);

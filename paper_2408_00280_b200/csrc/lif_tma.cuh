@@ -124,22 +124,26 @@ __device__ __forceinline__ int box_off(int nt, int r) {
 // ------------------------------------------------------------------------------------
 // Forward.  Stage = R time rows of a W-neuron tile.  Warp 0 lane 0 = producer;
 // warps 1..NCONS/32 = consumers, each lane owning VEC neurons.
-template <typename IO, int VEC, int NCONS, int R, int S>
+// NIN = 2: the stage also holds the residual rows R at R_OFF.
+template <typename IO, int VEC, int NCONS, int R, int S, int NIN = 1>
 struct FwdTma {
     static constexpr int W = NCONS * VEC;
     static constexpr int BW = W < 256 ? W : 256;
     static constexpr int NB = W / BW;
     static constexpr int BOX_BYTES = BW * R * (int)sizeof(IO);
-    static constexpr int STAGE_BYTES = NB * BOX_BYTES;
+    static constexpr int R_OFF = NB * BOX_BYTES;
+    static constexpr int STAGE_BYTES = NIN * NB * BOX_BYTES;
     static constexpr int SMEM = S * STAGE_BYTES + (int)sizeof(Barriers<S>) + kAlignSlack;
     static constexpr int THREADS = NCONS + 32;
     static_assert(W % BW == 0 && BW % VEC == 0, "tile geometry");
 };
 
-template <typename IO, int VEC, int SFMT, int SAVE, bool SOFT, bool AFF, int NCONS, int R, int S>
+template <typename IO, int VEC, int SFMT, int SAVE, bool SOFT, bool AFF, bool RES, int NCONS, int R, int S>
 __global__ void __launch_bounds__(NCONS + 32)
-lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const FwdArgs a, const int clc_depth) {
-    using Cfg = FwdTma<IO, VEC, NCONS, R, S>;
+lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmr,
+                       const FwdArgs a, const int clc_depth) {
+    static_assert(!RES || AFF, "the residual prologue rides on the affine one");
+    using Cfg = FwdTma<IO, VEC, NCONS, R, S, RES ? 2 : 1>;
     constexpr int W = Cfg::W, BW = Cfg::BW, NB = Cfg::NB;
     unsigned char* smem = smem_base();
     auto* bar = reinterpret_cast<Barriers<S>*>(smem + S * Cfg::STAGE_BYTES);
@@ -153,11 +157,16 @@ lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const FwdArgs a,
     if (warp == 0) {  // ---------------- producer
         if (lane == 0) {
             tma_prefetch_desc(&tmx);
+            if constexpr (RES) tma_prefetch_desc(&tmr);
             const uint64_t pol = policy_evict_first();
             produce<S, Cfg::STAGE_BYTES>(smem, bar, nrb, clc_depth, [&](unsigned char* stg, int tile, int64_t rb, uint64_t* fb) {
 #pragma unroll
-                for (int b = 0; b < NB; ++b)
+                for (int b = 0; b < NB; ++b) {
                     tma_load_2d(stg + b * Cfg::BOX_BYTES, &tmx, tile * W + b * BW, (int)(rb * R), fb, pol);
+                    if constexpr (RES)
+                        tma_load_2d(stg + Cfg::R_OFF + b * Cfg::BOX_BYTES, &tmr, tile * W + b * BW,
+                                    (int)(rb * R), fb, pol);
+                }
             });
         }
         return;
@@ -206,6 +215,10 @@ lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const FwdArgs a,
             for (int r = 0; r < R; ++r) {
                 if (F || r < rows) {
                     const Pack<IO, VEC> xv = *reinterpret_cast<const Pack<IO, VEC>*>(xs + r * BW);
+                    Pack<IO, VEC> rv;
+                    if constexpr (RES)
+                        rv = *reinterpret_cast<const Pack<IO, VEC>*>(
+                            reinterpret_cast<const IO*>(smem + s * Cfg::STAGE_BYTES + Cfg::R_OFF) + xoff + r * BW);
                     if constexpr (SAVE == SAVE_RECOMPUTE) {
                         // checkpoint the V entering step t when t % kCkpt == 0
                         const int64_t t = rb * R + r;
@@ -217,7 +230,7 @@ lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const FwdArgs a,
                         }
                     }
                     Pack<float, VEC> hp;
-                    const unsigned bits = fwd_compute<SOFT, AFF>(c, V, xv, hp, co);
+                    const unsigned bits = fwd_compute<SOFT, AFF, RES>(c, V, xv, hp, co, &rv);
                     if constexpr (SAVE == SAVE_H) {
                         if (nv > 0) st_stream<float, VEC>(h_row, hp);
                         h_row += a.ldh;
@@ -245,17 +258,20 @@ lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const FwdArgs a,
 // ------------------------------------------------------------------------------------
 // Backward, RECOMPUTE.  Stage = one kCkpt-step chunk of the tile: x rows, gS rows and the
 // chunk's entry-V checkpoint row.  Chunks of a tile are streamed last-first.
-template <typename IO, int VEC, int NCONS, int S>
+// RES: the stage also holds the chunk's residual rows at R_OFF.
+template <typename IO, int VEC, int NCONS, int S, bool RES = false>
 struct BwdRecTma {
     static constexpr int W = NCONS * VEC;
     static constexpr int BW = W < 256 ? W : 256;
     static constexpr int NB = W / BW;
     static constexpr int BOX_BYTES = BW * kCkpt * (int)sizeof(IO);
     static constexpr int CK_BOX_BYTES = BW * 4;
+    static constexpr int NIN = RES ? 3 : 2;
     static constexpr int X_OFF = 0;
     static constexpr int G_OFF = NB * BOX_BYTES;
-    static constexpr int CK_OFF = 2 * NB * BOX_BYTES;
-    static constexpr int STAGE_BYTES = 2 * NB * BOX_BYTES + NB * CK_BOX_BYTES;
+    static constexpr int R_OFF = 2 * NB * BOX_BYTES;
+    static constexpr int CK_OFF = NIN * NB * BOX_BYTES;
+    static constexpr int STAGE_BYTES = NIN * NB * BOX_BYTES + NB * CK_BOX_BYTES;
     static constexpr int SMEM = S * STAGE_BYTES + (int)sizeof(Barriers<S>) + kAlignSlack;
     static constexpr int THREADS = NCONS + 32;
     static_assert(W % BW == 0 && BW % VEC == 0 && STAGE_BYTES % 128 == 0, "tile geometry");
@@ -263,24 +279,30 @@ struct BwdRecTma {
 
 // Reverse walk over rows [0, rows) of one chunk.  h = recomputed H; gsm = gS rows in smem;
 // gxp = gX at the chunk's LAST row, walked backwards by ldb bytes.
+// RES: grp = dL/dR at the chunk's last row, walked like gxp.
 template <typename IO, int VEC, int MODE, int BW, int ROWS_MAX>
 __device__ __forceinline__ void bwd_chunk(const LifConsts& c, float (&gV)[VEC],
                                           const float (&h)[ROWS_MAX][VEC], const IO* gsm,
                                           IO* gxp, int64_t ldb, int rows, bool valid,
-                                          const AffCoef<VEC>& co, const IO* xs, float* pa, float* pb) {
+                                          const AffCoef<VEC>& co, const IO* xs, float* pa, float* pb,
+                                          IO* grp = nullptr) {
 #pragma unroll
     for (int j = ROWS_MAX - 1; j >= 0; --j) {
         if (j < rows) {
             const Pack<IO, VEC> gv = *reinterpret_cast<const Pack<IO, VEC>*>(gsm + j * BW);
-            Pack<IO, VEC> out;
+            Pack<IO, VEC> out, outr;
             if constexpr (Mode<MODE>::AFF) {
                 const Pack<IO, VEC> xr = *reinterpret_cast<const Pack<IO, VEC>*>(xs + j * BW);
-                out = bwd_step<IO, VEC, MODE, true>(c, gV, h[j], gv, &co, &xr, pa, pb);
+                out = bwd_step<IO, VEC, MODE, true>(c, gV, h[j], gv, &co, &xr, pa, pb, &outr);
             } else {
                 out = bwd_step<IO, VEC, MODE>(c, gV, h[j], gv);
             }
             if (valid) st_stream<IO, VEC>(gxp, out);
             gxp = step_bytes(gxp, -ldb);
+            if constexpr (Mode<MODE>::RES) {
+                if (valid) st_stream<IO, VEC>(grp, outr);
+                grp = step_bytes(grp, -ldb);
+            }
         }
     }
 }
@@ -288,12 +310,14 @@ __device__ __forceinline__ void bwd_chunk(const LifConsts& c, float (&gV)[VEC],
 template <typename IO, int VEC, int MODE, int BW>
 __device__ __forceinline__ void recompute_chunk(const LifConsts& c, float (&V)[VEC],
                                                 float (&h)[kCkpt][VEC], const IO* xs, int rows,
-                                                const AffCoef<VEC>& co) {
+                                                const AffCoef<VEC>& co, const IO* rs = nullptr) {
 #pragma unroll
     for (int j = 0; j < kCkpt; ++j) {
         if (j < rows) {
             const Pack<IO, VEC> xv = *reinterpret_cast<const Pack<IO, VEC>*>(xs + j * BW);
-            fwd_recompute_step<Mode<MODE>::SOFT, Mode<MODE>::AFF>(c, V, xv, h[j], co);
+            Pack<IO, VEC> rv;
+            if constexpr (Mode<MODE>::RES) rv = *reinterpret_cast<const Pack<IO, VEC>*>(rs + j * BW);
+            fwd_recompute_step<Mode<MODE>::SOFT, Mode<MODE>::AFF, Mode<MODE>::RES>(c, V, xv, h[j], co, &rv);
         }
     }
 }
@@ -302,9 +326,12 @@ template <typename IO, int VEC, int MODE, int NCONS, int S>
 __global__ void __launch_bounds__(NCONS + 32)
 lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
                                   const __grid_constant__ CUtensorMap tmg,
-                                  const __grid_constant__ CUtensorMap tmck, const BwdArgs a,
+                                  const __grid_constant__ CUtensorMap tmck,
+                                  const __grid_constant__ CUtensorMap tmr, const BwdArgs a,
                                   const int clc_depth) {
-    using Cfg = BwdRecTma<IO, VEC, NCONS, S>;
+    constexpr bool RES = Mode<MODE>::RES;
+    static_assert(!RES || Mode<MODE>::AFF, "the residual prologue rides on the affine one");
+    using Cfg = BwdRecTma<IO, VEC, NCONS, S, RES>;
     constexpr int W = Cfg::W, BW = Cfg::BW, NB = Cfg::NB;
     unsigned char* smem = smem_base();
     auto* bar = reinterpret_cast<Barriers<S>*>(smem + S * Cfg::STAGE_BYTES);
@@ -318,6 +345,7 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
     if (warp == 0) {  // ---------------- producer: chunks of a tile, last first
         if (lane == 0) {
             tma_prefetch_desc(&tmx); tma_prefetch_desc(&tmg); tma_prefetch_desc(&tmck);
+            if constexpr (RES) tma_prefetch_desc(&tmr);
             const uint64_t pol = policy_evict_first();
             produce<S, Cfg::STAGE_BYTES>(smem, bar, nch, clc_depth, [&](unsigned char* stg, int tile, int64_t j, uint64_t* fb) {
                 const int ch = (int)(nch - 1 - j);
@@ -327,6 +355,8 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
                     tma_load_2d(stg + Cfg::CK_OFF + b * Cfg::CK_BOX_BYTES, &tmck, c0, ch, fb, pol);
                     tma_load_2d(stg + Cfg::X_OFF + b * Cfg::BOX_BYTES, &tmx, c0, ch * kCkpt, fb, pol);
                     tma_load_2d(stg + Cfg::G_OFF + b * Cfg::BOX_BYTES, &tmg, c0, ch * kCkpt, fb, pol);
+                    if constexpr (RES)
+                        tma_load_2d(stg + Cfg::R_OFF + b * Cfg::BOX_BYTES, &tmr, c0, ch * kCkpt, fb, pol);
                 }
             });
         }
@@ -382,12 +412,18 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
             for (int i = 0; i < VEC; ++i) V[i] = v0.v[i];
             float h[kCkpt][VEC];
             IO* gxp = gx + (t0 + rows - 1) * ld + n0;
+            const IO* rs = nullptr;
+            IO* grp = nullptr;
+            if constexpr (RES) {
+                rs = reinterpret_cast<const IO*>(stg + Cfg::R_OFF) + roff;
+                grp = reinterpret_cast<IO*>(a.af.grad_residual) + (t0 + rows - 1) * ld + n0;
+            }
             if (rows == kCkpt && tile_full) {   // full chunk of a full tile: guard-free code
-                recompute_chunk<IO, VEC, MODE, BW>(c, V, h, xs, kCkpt, co);
-                bwd_chunk<IO, VEC, MODE, BW, kCkpt>(c, gV, h, gsm, gxp, ldb, kCkpt, true, co, xs, pa, pb);
+                recompute_chunk<IO, VEC, MODE, BW>(c, V, h, xs, kCkpt, co, rs);
+                bwd_chunk<IO, VEC, MODE, BW, kCkpt>(c, gV, h, gsm, gxp, ldb, kCkpt, true, co, xs, pa, pb, grp);
             } else {
-                recompute_chunk<IO, VEC, MODE, BW>(c, V, h, xs, rows, co);
-                bwd_chunk<IO, VEC, MODE, BW, kCkpt>(c, gV, h, gsm, gxp, ldb, rows, valid, co, xs, pa, pb);
+                recompute_chunk<IO, VEC, MODE, BW>(c, V, h, xs, rows, co, rs);
+                bwd_chunk<IO, VEC, MODE, BW, kCkpt>(c, gV, h, gsm, gxp, ldb, rows, valid, co, xs, pa, pb, grp);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&bar->empty[s]);

@@ -260,7 +260,10 @@ bool affine_valid(const snn_lif_affine* af, const snn_lif_shape* s) {
 
 snn::Affine to_dev(const snn_lif_affine* af) {
     snn::Affine d = {};
-    if (af) { d.scale = af->scale; d.shift = af->shift; d.C = af->C; d.HW = af->HW; }
+    if (af) {
+        d.scale = af->scale; d.shift = af->shift; d.C = af->C; d.HW = af->HW;
+        d.residual = af->residual; d.grad_residual = af->grad_residual;
+    }
     return d;
 }
 
@@ -294,10 +297,19 @@ snn_status forward_impl(const snn_lif_params* p, const snn_lif_shape* s, const v
         return fail(SNN_ERR_INVALID_VALUE, "affine: need scale/shift, C >= 1, HW >= 1, N %% (C*HW) == 0");
     a.h = to_dev(handoff);
     a.af = to_dev(affine);
+    const void* res = affine ? affine->residual : nullptr;
+    if (res) {
+        if (!aligned(res, esz)) return fail(SNN_ERR_MISALIGNED, "residual is not aligned to its element size");
+        if (s->save_mode == SNN_SAVE_H)
+            return fail(SNN_ERR_UNSUPPORTED, "the residual prologue needs save_mode SAVE_RECOMPUTE or SAVE_NONE");
+    }
 
-    if (tma_ok(s, tma_vec_forward(s->io_dtype), {x, v_init, v_final, a.saved, spikes}))
+    if (tma_ok(s, tma_vec_forward(s->io_dtype), {x, v_init, v_final, a.saved, spikes, res}))
         return s->io_dtype == SNN_BF16 ? launch_forward_tma_bf16(s, a, soft, cs)
                                        : launch_forward_tma_f32(s, a, soft, cs);
+    if (res)
+        return fail(SNN_ERR_UNSUPPORTED, "the residual prologue needs the TMA path (16-B aligned rows, "
+                                         "N a multiple of %d)", tma_vec_forward(s->io_dtype));
     if (handoff) return fail(SNN_ERR_UNSUPPORTED, "the fused handoff needs the TMA path (aligned rows)");
     const int vec = s->io_dtype == SNN_BF16 ? 8 : 4;
     bool fast = (s->ld % vec) == 0 && aligned(x, 16) && (!v_init || aligned(v_init, 16)) &&
@@ -348,13 +360,25 @@ snn_status backward_impl(const snn_lif_params* p, const snn_lif_shape* s,
         a.af.part_a = part_a;
         a.af.part_b = part_b;
         mode |= 8;
+        if ((affine->residual == nullptr) != (affine->grad_residual == nullptr))
+            return fail(SNN_ERR_NULL_POINTER, "residual and grad_residual go together");
+        if (affine->residual) {
+            if (!aligned(affine->residual, esz) || !aligned(affine->grad_residual, esz))
+                return fail(SNN_ERR_MISALIGNED, "residual / grad_residual not aligned to their element size");
+            mode |= 16;
+        }
     }
+    const void* res = (mode & 16) ? affine->residual : nullptr;
+    void* gres = (mode & 16) ? affine->grad_residual : nullptr;
 
     if (tma_ok(s, tma_vec_backward(s->io_dtype),
                {grad_spikes, grad_x, s->save_mode == SNN_SAVE_RECOMPUTE ? x : nullptr, saved,
-                grad_v_final, grad_v_init}))
+                grad_v_final, grad_v_init, res, gres}))
         return s->io_dtype == SNN_BF16 ? launch_backward_tma_bf16(s, a, mode, cs)
                                        : launch_backward_tma_f32(s, a, mode, cs);
+    if (res)
+        return fail(SNN_ERR_UNSUPPORTED, "the residual prologue needs the TMA path (16-B aligned rows, "
+                                         "N a multiple of %d)", tma_vec_backward(s->io_dtype));
     if (handoff) return fail(SNN_ERR_UNSUPPORTED, "the fused handoff needs the TMA path (aligned rows)");
     const int vec = s->io_dtype == SNN_BF16 ? 4 : 2;
     const bool fast = (s->ld % vec) == 0 && aligned(grad_spikes, 16) && aligned(grad_x, 16) &&

@@ -227,20 +227,38 @@ class AffineSpec:
     C: int
     HW: int
 
-    def to_c(self) -> _lib.snn_lif_affine:
+    def to_c(self, residual: Optional[torch.Tensor] = None,
+             grad_residual: Optional[torch.Tensor] = None) -> _lib.snn_lif_affine:
         for name, t in (("scale", self.scale), ("shift", self.shift)):
             if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous() and t.numel() == self.C):
                 raise ValueError(f"affine {name} must be a contiguous fp32 CUDA tensor of C={self.C}")
-        return _lib.snn_lif_affine(self.scale.data_ptr(), self.shift.data_ptr(), self.C, self.HW)
+        return _lib.snn_lif_affine(self.scale.data_ptr(), self.shift.data_ptr(), self.C, self.HW,
+                                   _ptr(residual), _ptr(grad_residual))
+
+
+def _like_x(name: str, t: torch.Tensor, x: torch.Tensor, ld: int) -> torch.Tensor:
+    """A [T, N] operand laid out like x (same dtype, device, row stride ld)."""
+    if t.shape != x.shape or t.dtype != x.dtype or t.device != x.device:
+        raise ValueError(f"{name} must match x: {tuple(x.shape)} {x.dtype} on {x.device}")
+    if t.dim() == 2 and t.size(1) > 1 and t.stride(1) != 1:
+        t = t.contiguous()
+    if t.shape[0] > 1 and t.stride(0) != ld:
+        t = t.contiguous() if ld == t.shape[1] else _restride(t, ld)
+    return t
 
 
 def lif_forward_affine(x: torch.Tensor, params: LIFParams, affine: AffineSpec, *,
                        v_init: Optional[torch.Tensor] = None, spike_fmt: str = "u8",
-                       return_v_final: bool = True) -> LIFForward:
-    """Forward with the affine prologue fused in (RECOMPUTE save mode: the backward re-reads x)."""
+                       return_v_final: bool = True,
+                       residual: Optional[torch.Tensor] = None) -> LIFForward:
+    """Forward with the affine prologue fused in (RECOMPUTE save mode: the backward re-reads x).
+    ``residual`` [T, N] (x's dtype): the LIF input becomes scale[c] x + shift[c] + residual
+    (the spiking-ResNet shortcut); the backward then also returns dL/dresidual."""
     _check_2d("x", x)
     T, N = x.shape
     shape = make_shape(x, spike_fmt, "recompute")
+    if residual is not None:
+        residual = _like_x("residual", residual, x, shape.ld)
     cp = params.to_c()
     v_init = _vec("v_init", v_init, N, x.device)
     spikes = alloc_spikes(x, spike_fmt)
@@ -248,17 +266,19 @@ def lif_forward_affine(x: torch.Tensor, params: LIFParams, affine: AffineSpec, *
         spikes = torch.empty((T, shape.ld), dtype=spikes.dtype, device=x.device)[:, :N]
     saved = torch.empty(_lib.snn_lif_saved_bytes(cp, shape) // 4, dtype=torch.float32, device=x.device)
     v_final = torch.empty(N, dtype=torch.float32, device=x.device) if return_v_final else None
-    ca = affine.to_c()
+    ca = affine.to_c(residual)
     _lib.snn_lif_forward_affine(cp, shape, _ptr(x), _ptr(v_init), ca, _ptr(spikes), _ptr(saved),
                                 _ptr(v_final), _stream())
     f = LIFForward(spikes, saved, v_final, x, v_init, params, shape)
     f.affine = affine
+    f.residual = residual
     return f
 
 
 def lif_backward_affine(grad_spikes: torch.Tensor, fwd: LIFForward, *,
                         grad_v_final: Optional[torch.Tensor] = None, return_grad_v_init: bool = True):
-    """Returns (grad_x [T, N] w.r.t. the raw input, grad_v_init, grad_scale [C], grad_shift [C])."""
+    """Returns (grad_x [T, N] w.r.t. the raw input, grad_v_init, grad_scale [C], grad_shift [C]),
+    plus grad_residual [T, N] as a fifth element when the forward had a residual."""
     x = fwd.x
     T, N = x.shape
     if grad_spikes.dim() == 2 and grad_spikes.size(1) > 1 and grad_spikes.stride(1) != 1:
@@ -274,10 +294,14 @@ def lif_backward_affine(grad_spikes: torch.Tensor, fwd: LIFForward, *,
     part = torch.empty((2, npad), dtype=torch.float32, device=x.device)
     gsc = torch.empty(af.C, dtype=torch.float32, device=x.device)
     gsh = torch.empty(af.C, dtype=torch.float32, device=x.device)
+    res = getattr(fwd, "residual", None)
+    grad_res = None if res is None else torch.empty((T, ld), dtype=x.dtype, device=x.device)[:, :N]
     _lib.snn_lif_backward_affine(fwd.params.to_c(), fwd.shape, _ptr(grad_spikes), _ptr(x), _ptr(fwd.saved),
-                                 _ptr(_vec("grad_v_final", grad_v_final, N, x.device)), af.to_c(),
-                                 _ptr(grad_x), _ptr(gvi), _ptr(part[0]), _ptr(part[1]), _ptr(gsc),
-                                 _ptr(gsh), _stream())
+                                 _ptr(_vec("grad_v_final", grad_v_final, N, x.device)),
+                                 af.to_c(res, grad_res), _ptr(grad_x), _ptr(gvi), _ptr(part[0]),
+                                 _ptr(part[1]), _ptr(gsc), _ptr(gsh), _stream())
+    if res is not None:
+        return grad_x, gvi, gsc, gsh, grad_res
     return grad_x, gvi, gsc, gsh
 
 

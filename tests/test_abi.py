@@ -35,7 +35,7 @@ def test_every_declared_symbol_is_exported(lib):
 
 
 def test_abi_version_and_status_strings(lib):
-    assert lib.lib.snn_lif_abi_version() == 1
+    assert lib.lib.snn_lif_abi_version() == lib.ABI_VERSION == 2
     assert lib.lib.snn_status_string(0) == b"SNN_OK"
     assert lib.lib.snn_status_string(3) == b"SNN_ERR_MISALIGNED"
 

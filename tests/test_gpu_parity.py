@@ -443,3 +443,104 @@ def test_fresh_host_thread_without_current_context():
     th.join()
     assert not err, err
     assert torch.equal(out["gx"], gx0)
+
+
+# ------------------------------------------------------------------ residual prologue (f4)
+
+@pytest.mark.parametrize("T,B,C,HW,dtype", [(16, 4, 8, 64, torch.float32), (23, 2, 4, 50, torch.float32),
+                                            (16, 8, 16, 16, torch.bfloat16), (33, 2, 3, 40, torch.bfloat16)])
+def test_affine_residual_prologue_parity(T, B, C, HW, dtype):
+    """X' = scale[c] X + shift[c] + R fused into the LIF kernels vs the oracle: spikes, V_final,
+    dL/dX = scale dL/dX', dL/dR = dL/dX', grad_v_init, grad_scale / grad_shift."""
+    p = PAPER
+    X, G, sc, sh = _affine_case(p, T, B, C, HW, dtype, 201 + T)
+    N = B * C * HW
+    R = snn_synth.normal_tensor(301 + T, T, N, std=0.5, dtype=dtype)
+    af = snn.AffineSpec(sc.cuda(), sh.cuda(), C, HW)
+    f = snn.lif_forward_affine(X.cuda(), p, af, residual=R.cuda())
+    gx, gvi, gsc, gsh, gres = snn.lif_backward_affine(G.cuda(), f)
+    torch.cuda.synchronize()
+    Xp = oracle.affine_input(X.double().numpy(), sc.double().numpy(), sh.double().numpy(), C, HW,
+                             residual=R.double().numpy())
+    ref = oracle_run(p, Xp, G)
+    rgx, rgs, rgb = oracle.affine_grads(X.double().numpy(), ref["gX"], sc.double().numpy(), C, HW)
+    bf = dtype == torch.bfloat16
+    # dL/dR = dL/dX': the plain comparator on the oracle's own gX
+    rep_r = compare(p, ref, ref["gX"], ref["gvi"], f.spikes.cpu(), gres.cpu(), vf_gpu=f.v_final.cpu(),
+                    gvi_gpu=gvi.cpu(), io_bf16=bf)
+    assert_ok(rep_r)
+    assert rep_r.tie_cols == 0
+    cidx = (np.arange(N) // HW) % C
+    ref_scaled = dict(ref)
+    ref_scaled["gX_bound"] = ref["gX_bound"] * np.abs(sc.double().numpy())[cidx][None, :]
+    ref_scaled["gX_sens"] = ref["gX_sens"] * np.abs(sc.double().numpy())[cidx][None, :]
+    rep = compare(p, ref_scaled, rgx, ref["gvi"], f.spikes.cpu(), gx.cpu(), io_bf16=bf)
+    assert_ok(rep)
+    Xd = X.double().numpy()
+    bnd = ref["gX_bound"] + 4 * ref["gX_sens"]
+    tol_s = np.zeros(C); tol_b = np.zeros(C)
+    np.add.at(tol_s, cidx, (bnd * np.abs(Xd)).sum(0)); np.add.at(tol_b, cidx, bnd.sum(0))
+    rtol = 1e-2 if bf else 1e-5
+    assert np.all(np.abs(gsc.cpu().numpy() - rgs) <= rtol * tol_s + 1e-30)
+    assert np.all(np.abs(gsh.cpu().numpy() - rgb) <= rtol * tol_b + 1e-30)
+
+
+def test_affine_residual_zero_equals_affine_path_bitwise():
+    """R = 0 changes nothing: X' + 0 is X' exactly, so spikes, V_final and every gradient
+    equal the affine-only kernels' bit for bit, and dL/dR is dL/dX' = dL/dX / scale (scale 1)."""
+    T, B, C, HW = 37, 2, 4, 64
+    N = B * C * HW
+    X = snn_synth.normal_tensor(121, T, N).cuda()
+    G = snn_synth.normal_tensor(122, T, N).cuda()
+    sc = torch.linspace(0.5, 1.5, C, device="cuda"); sh = torch.linspace(-0.2, 0.2, C, device="cuda")
+    af = snn.AffineSpec(sc, sh, C, HW)
+    f0 = snn.lif_forward_affine(X, PAPER, af)
+    g0 = snn.lif_backward_affine(G, f0)
+    f1 = snn.lif_forward_affine(X, PAPER, af, residual=torch.zeros_like(X))
+    g1 = snn.lif_backward_affine(G, f1)
+    torch.cuda.synchronize()
+    assert torch.equal(f0.spikes, f1.spikes) and torch.equal(f0.v_final, f1.v_final)
+    for a_, b_ in zip(g0, g1[:4]):
+        assert torch.equal(a_, b_)
+    ones = snn.AffineSpec(torch.ones(C, device="cuda"), sh, C, HW)
+    f2 = snn.lif_forward_affine(X, PAPER, ones, residual=torch.zeros_like(X))
+    g2 = snn.lif_backward_affine(G, f2)
+    torch.cuda.synchronize()
+    assert torch.equal(g2[0], g2[4])    # scale 1: dL/dX == dL/dR
+
+
+def test_affine_residual_needs_tma_path():
+    """The residual prologue runs only on the TMA path: a ragged N reports SNN_ERR_UNSUPPORTED
+    (no silent fallback)."""
+    T, C, HW = 8, 3, 7            # N = 21: not a multiple of the lane group
+    X = torch.randn(T, C * HW, device="cuda")
+    af = snn.AffineSpec(torch.ones(C, device="cuda"), torch.zeros(C, device="cuda"), C, HW)
+    with pytest.raises(RuntimeError, match="UNSUPPORTED"):
+        snn.lif_forward_affine(X, PAPER, af, residual=torch.zeros_like(X))
+
+
+def test_affine_lif_layer_residual_matches_unfused_autograd():
+    """AffineLIFLayer(x, residual) vs torch (affine + residual) followed by LIFLayer: same
+    spikes, close gradients for x, residual, scale, shift."""
+    torch.manual_seed(1)
+    T, B, C, H, W = 12, 4, 8, 6, 6
+    layer = snn.AffineLIFLayer(C, PAPER).cuda()
+    with torch.no_grad():
+        layer.scale.copy_(torch.rand(C) + 0.5)
+        layer.shift.copy_(torch.randn(C) * 0.2)
+    x = torch.randn(T, B, C, H, W, device="cuda", requires_grad=True)
+    r = (0.5 * torch.randn(T, B, C, H, W, device="cuda")).requires_grad_(True)
+    y = layer(x, r)
+    gy = torch.randn_like(y)
+    y.backward(gy)
+    x2 = x.detach().clone().requires_grad_(True)
+    r2 = r.detach().clone().requires_grad_(True)
+    sc = layer.scale.detach().clone().requires_grad_(True)
+    sh = layer.shift.detach().clone().requires_grad_(True)
+    y2 = snn.LIFLayer(PAPER)(x2 * sc.view(1, 1, C, 1, 1) + sh.view(1, 1, C, 1, 1) + r2)
+    y2.backward(gy)
+    assert (y != y2).float().mean().item() < 1e-3
+    torch.testing.assert_close(r.grad, r2.grad, rtol=1e-3, atol=1e-3)
+    torch.testing.assert_close(x.grad, x2.grad, rtol=1e-3, atol=1e-3)
+    torch.testing.assert_close(layer.scale.grad, sc.grad, rtol=1e-3, atol=1e-3)
+    torch.testing.assert_close(layer.shift.grad, sh.grad, rtol=1e-3, atol=1e-3)

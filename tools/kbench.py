@@ -24,7 +24,24 @@ CASES = {
              ("bf16", 16, 128 * 512 * 2 * 2)],
     "t16": [("f32", 16, 1 << 23)],
     "bf512": [("bf16", 512, 1 << 20)],
+    "small": [("bf16", 16, 1 << 14), ("bf16", 16, 1 << 16), ("bf16", 16, 1 << 18), ("bf16", 1, 1 << 14),
+              ("f32", 16, 1 << 18), ("f32", 1, 1 << 14)],
 }
+
+
+def time_null(reps):
+    """Event-to-event time of a trivial kernel under the same queueing (the floor)."""
+    b = torch.zeros(1, device="cuda")
+    st = torch.cuda.current_stream()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    torch.cuda._sleep(int(2e6))
+    for e0, e1 in ev:
+        e0.record(st)
+        b.add_(1.0)
+        e1.record(st)
+    torch.cuda.synchronize()
+    t = sorted(e0.elapsed_time(e1) for e0, e1 in ev)[reps // 2]
+    print(f"null kernel (torch add_ on 1 element): {t * 1e3:.1f} us", flush=True)
 
 
 def alg_bytes(dt, T, N, save_mode="recompute"):
@@ -68,6 +85,7 @@ def main():
     ap.add_argument("--cases", default="cfg1,cfg2,t16")
     a = ap.parse_args()
     torch.cuda.set_device(0)
+    time_null(a.reps)
     for c in a.cases.split(","):
         for dt, T, N in CASES[c]:
             time_case(dt, T, N, a.reps)
