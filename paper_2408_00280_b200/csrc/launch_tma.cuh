@@ -18,7 +18,7 @@ template <> struct TmaCfg<float> {
 };
 template <> struct TmaCfg<__nv_bfloat16> {
     static constexpr int FV = 8, FN = 128, FR = 8, FS = 6;
-    static constexpr int RV = 2, RN = 256, RS = 3;           // 34 KB chunks, 2 CTAs/SM
+    static constexpr int RV = 2, RN = 256, RS = 3;           // 34 KB chunks, 2 CTAs/SM (VEC 4 x 128 lanes measured 6% slower at T=16)
     static constexpr int RS_RES = 2;                         // + residual rows: 51 KB chunks
     static constexpr int HV = 2, HN = 512, HR = 8, HS = 4;
 };
