@@ -776,7 +776,7 @@ def run_ours(args):
     traffic = ncu_traffic(key)
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": traffic,
-            "kernel": f"lif_{'backward_recompute' if (dom == 'bwd' and args.save_mode == 'recompute') else ('backward_saveh' if dom == 'bwd' else 'forward')}_kernel",
+            "kernel": f"lif_{'backward_recompute' if (dom == 'bwd' and args.save_mode == 'recompute') else ('backward_saveh' if dom == 'bwd' else 'forward')}_tma_kernel",
             "peak_kind": peak_kind, "algorithmic_bytes_per_launch": dom_bytes / nlaunch,
             "frac_of_nominal_8TBps": round(achieved / 8000.0, 4),
             "fwd_ms": round(fwd_ms, 4), "bwd_ms": round(bwd_ms, 4),

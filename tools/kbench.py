@@ -24,6 +24,8 @@ CASES = {
              ("bf16", 16, 128 * 512 * 2 * 2)],
     "t16": [("f32", 16, 1 << 23)],
     "bf512": [("bf16", 512, 1 << 20)],
+    "short": [("f32", 8, 1 << 20), ("f32", 16, 1 << 20), ("f32", 16, 1 << 23), ("bf16", 16, 1 << 23),
+              ("bf16", 16, 1 << 21), ("f32", 64, 1 << 22)],
     "small": [("bf16", 16, 1 << 14), ("bf16", 16, 1 << 16), ("bf16", 16, 1 << 18), ("bf16", 1, 1 << 14),
               ("f32", 16, 1 << 18), ("f32", 1, 1 << 14)],
 }

@@ -89,7 +89,9 @@ def full(args):
 
 
 def launches(args):
-    rows = [r for r in csv.reader(open(args.report)) if len(r) > 10]
+    rows = list(csv.reader(open(args.report)))
+    start = next(i for i, r in enumerate(rows) if r and r[0] == "ID")   # skip program stdout
+    rows = [r for r in rows[start:] if len(r) > 10]
     h = rows[0]
     ix = {k: i for i, k in enumerate(h)}
     agg = defaultdict(lambda: defaultdict(list))
