@@ -544,3 +544,28 @@ def test_affine_lif_layer_residual_matches_unfused_autograd():
     torch.testing.assert_close(x.grad, x2.grad, rtol=1e-3, atol=1e-3)
     torch.testing.assert_close(layer.scale.grad, sc.grad, rtol=1e-3, atol=1e-3)
     torch.testing.assert_close(layer.shift.grad, sh.grad, rtol=1e-3, atol=1e-3)
+
+
+@pytest.mark.parametrize("spike_fmt", ["u8", "bits", "io"])
+def test_affine_residual_carries_and_formats(spike_fmt):
+    """Residual prologue with carries in and out (v_init, grad_v_final) and every spike format:
+    parity vs the oracle run from the same carries; the three formats agree bitwise."""
+    T, B, C, HW = 21, 2, 4, 32
+    N = B * C * HW
+    X, G, sc, sh = _affine_case(PAPER, T, B, C, HW, torch.float32, 401)
+    R = snn_synth.normal_tensor(402, T, N, std=0.5)
+    v0 = snn_synth.normal_tensor(403, 1, N, std=0.2)[0]
+    gvf = snn_synth.normal_tensor(404, 1, N)[0]
+    af = snn.AffineSpec(sc.cuda(), sh.cuda(), C, HW)
+    f = snn.lif_forward_affine(X.cuda(), PAPER, af, residual=R.cuda(), v_init=v0.cuda(), spike_fmt=spike_fmt)
+    gx, gvi, gsc, gsh, gres = snn.lif_backward_affine(G.cuda(), f, grad_v_final=gvf.cuda())
+    torch.cuda.synchronize()
+    Xp = oracle.affine_input(X.double().numpy(), sc.double().numpy(), sh.double().numpy(), C, HW,
+                             residual=R.double().numpy())
+    ref = oracle_run(PAPER, Xp, G, v0=v0, gvf=gvf)
+    spikes = f.spikes.cpu()
+    if spike_fmt == "bits":
+        spikes = snn.unpack_bits(f.spikes, N).cpu()
+    rep = compare(PAPER, ref, ref["gX"], ref["gvi"], spikes.to(torch.uint8), gres.cpu(),
+                  vf_gpu=f.v_final.cpu(), gvi_gpu=gvi.cpu())
+    assert_ok(rep)
