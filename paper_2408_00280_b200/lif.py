@@ -48,6 +48,14 @@ class LIFParams:
         return replace(LIFParams(tau=2.0, v_th=1.0, v_reset=0.0, decay_input=True), **kw)
 
     def to_c(self) -> _lib.snn_lif_params:
+        """The C struct, built once per (frozen) parameter set and reused by every call."""
+        c = self.__dict__.get("_c_struct")
+        if c is None:
+            c = self._build_c()
+            object.__setattr__(self, "_c_struct", c)
+        return c
+
+    def _build_c(self) -> _lib.snn_lif_params:
         return _lib.snn_lif_params(
             float(self.tau), float(self.v_th), float(self.v_reset),
             {"hard": _lib.SNN_RESET_HARD, "soft": _lib.SNN_RESET_SOFT}[self.reset],
@@ -72,8 +80,10 @@ def _ptr(t: Optional[torch.Tensor]):
     return None if t is None else t.data_ptr()
 
 
-def _stream() -> int:
-    return torch.cuda.current_stream().cuda_stream
+def _stream(device: Optional[torch.device] = None) -> int:
+    """cudaStream_t of torch's current stream on `device` (default: the current device)."""
+    idx = torch.cuda.current_device() if device is None or device.index is None else device.index
+    return torch._C._cuda_getCurrentRawStream(idx)
 
 
 def _check_2d(name: str, t: torch.Tensor) -> None:
@@ -92,11 +102,28 @@ def _vec(name, t, N, device):
     return t
 
 
-def make_shape(x: torch.Tensor, spike_fmt: str, save_mode: str) -> _lib.snn_lif_shape:
+_SHAPES: dict = {}      # (T, N, ld, dtype, spike_fmt, save_mode) -> (snn_lif_shape, saved bytes)
+
+
+def _shape_entry(x: torch.Tensor, spike_fmt: str, save_mode: str):
+    """The C shape struct and its saved-buffer size, built once per distinct layout (host
+    overhead of an eager call; the structs are only read by the library)."""
     T, N = x.shape
-    ld = x.stride(0) if T > 1 else N
-    return _lib.snn_lif_shape(T, N, max(ld, N), _DTYPES[x.dtype], _SPIKE_FMTS[spike_fmt],
-                              _SAVE_MODES[save_mode])
+    ld = max(x.stride(0) if T > 1 else N, N)
+    key = (T, N, ld, x.dtype, spike_fmt, save_mode)
+    e = _SHAPES.get(key)
+    if e is None:
+        shape = _lib.snn_lif_shape(T, N, ld, _DTYPES[x.dtype], _SPIKE_FMTS[spike_fmt], _SAVE_MODES[save_mode])
+        # the saved size depends on the shape only (any valid params give the same answer)
+        e = (shape, _lib.snn_lif_saved_bytes(LIFParams().to_c(), shape))
+        if len(_SHAPES) > 4096:
+            _SHAPES.clear()
+        _SHAPES[key] = e
+    return e
+
+
+def make_shape(x: torch.Tensor, spike_fmt: str, save_mode: str) -> _lib.snn_lif_shape:
+    return _shape_entry(x, spike_fmt, save_mode)[0]
 
 
 def saved_bytes(params: LIFParams, shape: _lib.snn_lif_shape) -> int:
@@ -127,21 +154,22 @@ def lif_forward(x: torch.Tensor, params: LIFParams = LIFParams(), *,
     if x.dtype not in _DTYPES:
         raise ValueError(f"x dtype {x.dtype} unsupported (fp32 / bf16)")
     T, N = x.shape
-    shape = make_shape(x, spike_fmt, save_mode)
+    shape, nbytes = _shape_entry(x, spike_fmt, save_mode)
     cp = params.to_c()
     v_init = _vec("v_init", v_init, N, x.device)
     if spikes is None:
-        spikes = alloc_spikes(x, spike_fmt)
         if spike_fmt != "bits" and shape.ld != N:
             # keep the caller's ld for views: allocate [T, ld] and view its first N columns
-            spikes = torch.empty((T, shape.ld), dtype=spikes.dtype, device=x.device)[:, :N]
-    nbytes = _lib.snn_lif_saved_bytes(cp, shape)
+            spikes = torch.empty((T, shape.ld), dtype=torch.uint8 if spike_fmt == "u8" else x.dtype,
+                                 device=x.device)[:, :N]
+        else:
+            spikes = alloc_spikes(x, spike_fmt)
     if save_mode != "none" and saved is None:
         saved = torch.empty(nbytes // 4, dtype=torch.float32, device=x.device)
     if return_v_final and v_final is None:
         v_final = torch.empty(N, dtype=torch.float32, device=x.device)
     _lib.snn_lif_forward(cp, shape, _ptr(x), _ptr(v_init), _ptr(spikes),
-                         _ptr(saved) if save_mode != "none" else None, _ptr(v_final), _stream())
+                         _ptr(saved) if save_mode != "none" else None, _ptr(v_final), _stream(x.device))
     return LIFForward(spikes, saved if save_mode != "none" else None, v_final, x, v_init,
                       params, shape)
 
@@ -171,7 +199,7 @@ def lif_backward(grad_spikes: torch.Tensor, fwd: LIFForward, *,
     grad_v_init = torch.empty(N, dtype=torch.float32, device=x.device) if return_grad_v_init else None
     _lib.snn_lif_backward(fwd.params.to_c(), fwd.shape, _ptr(grad_spikes), _ptr(x),
                           _ptr(fwd.v_init), _ptr(fwd.saved), _ptr(grad_v_final), _ptr(grad_x),
-                          _ptr(grad_v_init), _stream())
+                          _ptr(grad_v_init), _stream(x.device))
     return grad_x, grad_v_init
 
 
