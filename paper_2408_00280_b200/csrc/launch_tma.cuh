@@ -11,13 +11,17 @@ namespace snn_host {
 // consumer threads = W-neuron tile; R rows per stage; S stages in the smem ring.
 template <typename IO> struct TmaCfg;
 template <> struct TmaCfg<float> {
-    static constexpr int FV = 4, FN = 128, FR = 8, FS = 6;   // forward: 16 KB stages, 2 CTAs/SM
+    // forward: 1024-neuron tiles, 8 consumer warps, 32 KB stages x 3, 2 CTAs/SM (measured 5%
+    // faster at T=512 than 512-neuron tiles with 4 warps and 16 KB x 6 stages)
+    static constexpr int FV = 4, FN = 256, FR = 8, FS = 3;
+    static constexpr int FN_RES = 128, FS_RES = 3;           // + residual rows: 32 KB stages
     static constexpr int RV = 2, RN = 256, RS = 3;           // backward RECOMPUTE: 66 KB chunks, FFMA2 pairs
     static constexpr int RS_RES = 2;                         // + residual rows: 99 KB chunks
     static constexpr int HV = 2, HN = 256, HR = 8, HS = 6;   // backward SAVE_H: 32 KB stages
 };
 template <> struct TmaCfg<__nv_bfloat16> {
-    static constexpr int FV = 8, FN = 128, FR = 8, FS = 6;
+    static constexpr int FV = 8, FN = 128, FR = 8, FS = 6;   // (8 warps x 2048-neuron tiles: slower on mid layers)
+    static constexpr int FN_RES = 128, FS_RES = 3;
     static constexpr int RV = 2, RN = 256, RS = 3;           // 34 KB chunks, 2 CTAs/SM (VEC 4 x 128 lanes measured 6% slower at T=16)
     static constexpr int RS_RES = 2;                         // + residual rows: 51 KB chunks
     static constexpr int HV = 2, HN = 512, HR = 8, HS = 4;
@@ -27,26 +31,26 @@ template <typename IO>
 snn_status launch_forward_tma(const snn_lif_shape* s, const snn::FwdArgs& a, bool soft,
                               cudaStream_t st) {
     using C = TmaCfg<IO>;
-    using Cfg = snn::FwdTma<IO, C::FV, C::FN, C::FR, C::FS>;
     CUtensorMap tmx, tmr;
-    if (!encode_2d(&tmx, a.x, sizeof(IO), s->N, s->T, s->ld, Cfg::BW, C::FR))
+    // pro: 0 plain, 1 affine, 2 affine + residual (the residual doubles the stage, so that
+    // variant has its own, shallower tile configuration).
+    const bool res = a.af.residual != nullptr;
+    const int bw = res ? snn::FwdTma<IO, C::FV, C::FN_RES, C::FR, C::FS_RES, 2>::BW
+                       : snn::FwdTma<IO, C::FV, C::FN, C::FR, C::FS>::BW;
+    if (!encode_2d(&tmx, a.x, sizeof(IO), s->N, s->T, s->ld, bw, C::FR))
         return fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled failed for x%s", encode_detail());
     tmr = tmx;
-    if (a.af.residual != nullptr &&
-        !encode_2d(&tmr, a.af.residual, sizeof(IO), s->N, s->T, s->ld, Cfg::BW, C::FR))
+    if (res && !encode_2d(&tmr, a.af.residual, sizeof(IO), s->N, s->T, s->ld, bw, C::FR))
         return fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled failed for the residual%s", encode_detail());
-    const int64_t ntiles = (s->N + Cfg::W - 1) / Cfg::W;
-    // pro: 0 plain, 1 affine, 2 affine + residual (the residual stage is twice as large, so
-    // half the ring depth keeps two CTAs per SM).
     auto go = [&](auto sfmt, auto save, auto sft, auto pro) {
         constexpr int P = decltype(pro)::value;
-        constexpr int NS = P == 2 ? C::FS / 2 : C::FS;
-        using K = snn::FwdTma<IO, C::FV, C::FN, C::FR, NS, P == 2 ? 2 : 1>;
+        constexpr int NS = P == 2 ? C::FS_RES : C::FS;
+        constexpr int NC = P == 2 ? C::FN_RES : C::FN;
+        using K = snn::FwdTma<IO, C::FV, NC, C::FR, NS, P == 2 ? 2 : 1>;
         auto k = snn::lif_forward_tma_kernel<IO, C::FV, decltype(sfmt)::value, decltype(save)::value,
-                                             (bool)decltype(sft)::value, P >= 1, P == 2,
-                                             C::FN, C::FR, NS>;
-        return launch_tiles(k, K::THREADS, K::SMEM, ntiles, (s->T + C::FR - 1) / C::FR, st,
-                            "lif_forward_tma_kernel", tmx, tmr, a);
+                                             (bool)decltype(sft)::value, P >= 1, P == 2, NC, C::FR, NS>;
+        return launch_tiles(k, K::THREADS, K::SMEM, (s->N + K::W - 1) / K::W, (s->T + C::FR - 1) / C::FR,
+                            st, "lif_forward_tma_kernel", tmx, tmr, a);
     };
     auto by_aff = [&](auto sfmt, auto save, auto sft) {
         if (a.af.scale == nullptr) return go(sfmt, save, sft, IC<0>{});
