@@ -569,3 +569,41 @@ def test_affine_residual_carries_and_formats(spike_fmt):
     rep = compare(PAPER, ref, ref["gX"], ref["gvi"], spikes.to(torch.uint8), gres.cpu(),
                   vf_gpu=f.v_final.cpu(), gvi_gpu=gvi.cpu())
     assert_ok(rep)
+
+
+@settings(max_examples=30, deadline=None, suppress_health_check=list(HealthCheck))
+@given(T=st.integers(1, 50), B=st.integers(1, 3), C=st.integers(1, 5), HW=st.sampled_from([8, 16, 24, 40]),
+       dtype=st.sampled_from([torch.float32, torch.bfloat16]), mode=st.integers(0, 7),
+       decay_input=st.booleans(), residual=st.booleans(), spike_fmt=st.sampled_from(["u8", "bits", "io"]))
+def test_randomized_affine_residual_parity(T, B, C, HW, dtype, mode, decay_input, residual, spike_fmt):
+    """Randomized f4 prologue: every reset/surrogate/detach mode, both io dtypes, ragged T,
+    with and without the residual shortcut (N a multiple of 8: the TMA path)."""
+    p = LIFParams(tau=1.5, v_th=0.6, v_reset=0.0, surrogate=("atan" if mode & 1 else "sigmoid"),
+                  reset=("soft" if mode & 2 else "hard"), detach_reset=bool(mode & 4),
+                  decay_input=decay_input, alpha=(2.0 if mode & 1 else 4.0))
+    N = B * C * HW
+    seed = T * 7919 + N * 13 + C
+    X, G, sc, sh = _affine_case(p, T, B, C, HW, dtype, seed)
+    R = snn_synth.normal_tensor(seed + 5, T, N, std=0.5, dtype=dtype) if residual else None
+    af = snn.AffineSpec(sc.cuda(), sh.cuda(), C, HW)
+    f = snn.lif_forward_affine(X.cuda(), p, af, spike_fmt=spike_fmt,
+                               residual=None if R is None else R.cuda())
+    out = snn.lif_backward_affine(G.cuda(), f)
+    torch.cuda.synchronize()
+    Xp = oracle.affine_input(X.double().numpy(), sc.double().numpy(), sh.double().numpy(), C, HW,
+                             residual=None if R is None else R.double().numpy())
+    ref = oracle_run(p, Xp, G)
+    S = f.spikes if spike_fmt != "bits" else snn.unpack_bits(f.spikes, N)
+    bf = dtype == torch.bfloat16
+    if residual:    # dL/dR = dL/dX' checks the whole backward recursion unscaled
+        rep = compare(p, ref, ref["gX"], ref["gvi"], S.cpu().to(torch.uint8), out[4].cpu(),
+                      vf_gpu=f.v_final.cpu(), gvi_gpu=out[1].cpu(), io_bf16=bf)
+        assert_ok(rep)
+    rgx, _, _ = oracle.affine_grads(X.double().numpy(), ref["gX"], sc.double().numpy(), C, HW)
+    cidx = (np.arange(N) // HW) % C
+    ref_scaled = dict(ref)
+    ref_scaled["gX_bound"] = ref["gX_bound"] * np.abs(sc.double().numpy())[cidx][None, :]
+    ref_scaled["gX_sens"] = ref["gX_sens"] * np.abs(sc.double().numpy())[cidx][None, :]
+    rep = compare(p, ref_scaled, rgx, ref["gvi"], S.cpu().to(torch.uint8), out[0].cpu(),
+                  vf_gpu=f.v_final.cpu(), gvi_gpu=out[1].cpu(), io_bf16=bf)
+    assert_ok(rep)
