@@ -280,6 +280,32 @@ snn_status snn_lif_fwd_bwd_host(const snn_lif_params* params, const snn_lif_shap
                                 void* grad_x_host, int64_t chunk_neurons, int nslots,
                                 void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- Plans (runtime, not new arithmetic): validate a layer's call once -- parameters,
+ * shape, buffers, kernel variant, TMA tensor maps, launch geometry -- and replay it with
+ * nothing but the launches.  For fixed-shape loops (serving, a training step whose
+ * activations live in the same buffers every iteration) the per-call host work drops to
+ * the launch itself.  Same kernels, same results, bit for bit, as snn_lif_forward /
+ * snn_lif_backward with the same arguments.
+ *   snn_lif_plan_create  binds the forward's buffers (as snn_lif_forward) and, when
+ *                        grad_spikes / grad_x are non-NULL, the backward's (as
+ *                        snn_lif_backward; both NULL = forward-only plan).  Errors as those
+ *                        calls (nothing is launched); *plan = NULL on failure.
+ *   snn_lif_plan_forward / _backward  enqueue the recorded launches on `stream`; the
+ *                        buffers' CONTENTS may change between replays, their addresses
+ *                        may not.  Must run with the device current at creation
+ *                        (SNN_ERR_INVALID_VALUE otherwise).  _backward on a forward-only
+ *                        plan: SNN_ERR_INVALID_VALUE.
+ *   snn_lif_plan_destroy frees the host-side plan (no device memory is owned). */
+typedef struct snn_lif_plan snn_lif_plan;
+
+snn_status snn_lif_plan_create(snn_lif_plan** plan, const snn_lif_params* params,
+                               const snn_lif_shape* shape, const void* x, const float* v_init,
+                               void* spikes, void* saved, float* v_final, const void* grad_spikes,
+                               const float* grad_v_final, void* grad_x, float* grad_v_init);
+snn_status snn_lif_plan_forward(const snn_lif_plan* plan, void* stream);
+snn_status snn_lif_plan_backward(const snn_lif_plan* plan, void* stream);
+void snn_lif_plan_destroy(snn_lif_plan* plan);
+
 /* Status name, e.g. "SNN_ERR_INVALID_VALUE" (static storage). */
 const char* snn_status_string(snn_status status);
 

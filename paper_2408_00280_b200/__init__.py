@@ -10,7 +10,8 @@ from .lif import LIFForward, LIFParams, lif_backward, lif_forward, unpack_bits  
 from .autograd import AffineLIFLayer, FusedAffineLIF, FusedLIF, LIFLayer  # noqa: F401
 from .lif import AffineSpec, lif_backward_affine, lif_forward_affine  # noqa: F401
 from .lif import host_workspace, lif_fwd_bwd_host  # noqa: F401
+from .lif import LIFPlan  # noqa: F401
 
-__all__ = ["LIFParams", "LIFForward", "lif_forward", "lif_backward", "unpack_bits",
+__all__ = ["LIFPlan", "LIFParams", "LIFForward", "lif_forward", "lif_backward", "unpack_bits",
            "FusedLIF", "LIFLayer", "FusedAffineLIF", "AffineLIFLayer", "AffineSpec",
            "lif_forward_affine", "lif_backward_affine", "host_workspace", "lif_fwd_bwd_host"]

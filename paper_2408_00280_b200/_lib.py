@@ -31,7 +31,8 @@ EXPORTED_SYMBOLS = (
     "snn_last_error_message", "snn_lif_abi_version", "snn_lif_serial_forward_step",
     "snn_lif_serial_backward_step", "snn_lif_handoff_blocks", "snn_lif_forward_handoff",
     "snn_lif_backward_handoff", "snn_lif_forward_affine", "snn_lif_backward_affine",
-    "snn_lif_host_workspace_bytes", "snn_lif_fwd_bwd_host",
+    "snn_lif_host_workspace_bytes", "snn_lif_fwd_bwd_host", "snn_lif_plan_create",
+    "snn_lif_plan_forward", "snn_lif_plan_backward", "snn_lif_plan_destroy",
 )
 SNN_LIF_HANDOFF_BLOCK = 256
 
@@ -110,6 +111,14 @@ def _load() -> ctypes.CDLL:
     lib.snn_lif_fwd_bwd_host.argtypes = [P, S, vp, vp, vp, vp, ctypes.c_int64, ctypes.c_int, vp,
                                          ctypes.c_size_t, vp]
     lib.snn_lif_fwd_bwd_host.restype = ctypes.c_int
+    lib.snn_lif_plan_create.argtypes = [ctypes.POINTER(ctypes.c_void_p), P, S, vp, fp, vp, vp, fp, vp, fp, vp, fp]
+    lib.snn_lif_plan_create.restype = ctypes.c_int
+    lib.snn_lif_plan_forward.argtypes = [vp, vp]
+    lib.snn_lif_plan_forward.restype = ctypes.c_int
+    lib.snn_lif_plan_backward.argtypes = [vp, vp]
+    lib.snn_lif_plan_backward.restype = ctypes.c_int
+    lib.snn_lif_plan_destroy.argtypes = [vp]
+    lib.snn_lif_plan_destroy.restype = None
     return lib
 
 
@@ -190,3 +199,24 @@ def snn_lif_fwd_bwd_host(params, shape, x_host, grad_spikes_host, spikes_host, g
     check(lib.snn_lif_fwd_bwd_host(ctypes.byref(params), ctypes.byref(shape), x_host, grad_spikes_host,
                                    spikes_host, grad_x_host, chunk_neurons, nslots, workspace,
                                    workspace_bytes, stream))
+
+
+def snn_lif_plan_create(params, shape, x, v_init, spikes, saved, v_final, grad_spikes, grad_v_final,
+                        grad_x, grad_v_init) -> int:
+    """Returns the opaque plan handle (an int)."""
+    h = ctypes.c_void_p()
+    check(lib.snn_lif_plan_create(ctypes.byref(h), ctypes.byref(params), ctypes.byref(shape), x, v_init,
+                                  spikes, saved, v_final, grad_spikes, grad_v_final, grad_x, grad_v_init))
+    return h.value
+
+
+def snn_lif_plan_forward(plan, stream) -> None:
+    check(lib.snn_lif_plan_forward(plan, stream))
+
+
+def snn_lif_plan_backward(plan, stream) -> None:
+    check(lib.snn_lif_plan_backward(plan, stream))
+
+
+def snn_lif_plan_destroy(plan) -> None:
+    lib.snn_lif_plan_destroy(plan)

@@ -92,12 +92,12 @@ snn_status go_mode(const snn_lif_shape* s, const snn::BwdArgs& a, cudaStream_t s
     const dim3 grid((unsigned)((groups + snn::kBlock - 1) / snn::kBlock));
     if constexpr (MODE < 8) {   // SAVE_H has no affine-gradient variant (host rejects it)
         if (s->save_mode == SNN_SAVE_H) {
-            snn::lif_backward_saveh_kernel<IO, VEC, MODE, kBwdPF><<<grid, snn::kBlock, 0, st>>>(a);
-            return launch_status("lif_backward_kernel");
+            return launch_kernel(snn::lif_backward_saveh_kernel<IO, VEC, MODE, kBwdPF>, grid, dim3(snn::kBlock),
+                                 0, st, false, "lif_backward_saveh_kernel", a);
         }
     }
-    snn::lif_backward_recompute_kernel<IO, VEC, MODE><<<grid, snn::kBlock, 0, st>>>(a);
-    return launch_status("lif_backward_kernel");
+    return launch_kernel(snn::lif_backward_recompute_kernel<IO, VEC, MODE>, grid, dim3(snn::kBlock), 0, st,
+                         false, "lif_backward_recompute_kernel", a);
 }
 
 template <typename IO, int VEC>

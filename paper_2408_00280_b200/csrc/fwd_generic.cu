@@ -13,29 +13,28 @@ snn_status go(const snn_lif_shape* s, const snn::FwdArgs& a, bool soft, cudaStre
     const int64_t groups = (s->N + VEC - 1) / VEC;
     const dim3 grid((unsigned)((groups + snn::kBlock - 1) / snn::kBlock));
     auto go_aff = [&](auto sfmt, auto save, auto sft, auto aff) {
-        snn::lif_forward_kernel<IO, VEC, decltype(sfmt)::value, decltype(save)::value,
-                                (bool)decltype(sft)::value, (bool)decltype(aff)::value, kFwdPF>
-            <<<grid, snn::kBlock, 0, st>>>(a);
+        return launch_kernel(snn::lif_forward_kernel<IO, VEC, decltype(sfmt)::value, decltype(save)::value,
+                                                     (bool)decltype(sft)::value, (bool)decltype(aff)::value, kFwdPF>,
+                             grid, dim3(snn::kBlock), 0, st, false, "lif_forward_kernel", a);
     };
     auto launch = [&](auto sfmt, auto save, auto sft) {
-        if (a.af.scale != nullptr) go_aff(sfmt, save, sft, IC<1>{}); else go_aff(sfmt, save, sft, IC<0>{});
+        return a.af.scale != nullptr ? go_aff(sfmt, save, sft, IC<1>{}) : go_aff(sfmt, save, sft, IC<0>{});
     };
     auto by_soft = [&](auto sfmt, auto save) {
-        if (soft) launch(sfmt, save, IC<1>{}); else launch(sfmt, save, IC<0>{});
+        return soft ? launch(sfmt, save, IC<1>{}) : launch(sfmt, save, IC<0>{});
     };
     auto by_save = [&](auto sfmt) {
         switch (s->save_mode) {
-            case SNN_SAVE_H: by_soft(sfmt, IC<snn::SAVE_H>{}); break;
-            case SNN_SAVE_RECOMPUTE: by_soft(sfmt, IC<snn::SAVE_RECOMPUTE>{}); break;
-            default: by_soft(sfmt, IC<snn::SAVE_NONE>{}); break;
+            case SNN_SAVE_H: return by_soft(sfmt, IC<snn::SAVE_H>{});
+            case SNN_SAVE_RECOMPUTE: return by_soft(sfmt, IC<snn::SAVE_RECOMPUTE>{});
+            default: return by_soft(sfmt, IC<snn::SAVE_NONE>{});
         }
     };
     switch (s->spike_fmt) {
-        case SNN_SPK_U8: by_save(IC<snn::SPK_U8>{}); break;
-        case SNN_SPK_BITS: by_save(IC<snn::SPK_BITS>{}); break;
-        default: by_save(IC<snn::SPK_IO>{}); break;
+        case SNN_SPK_U8: return by_save(IC<snn::SPK_U8>{});
+        case SNN_SPK_BITS: return by_save(IC<snn::SPK_BITS>{});
+        default: return by_save(IC<snn::SPK_IO>{});
     }
-    return launch_status("lif_forward_kernel");
 }
 }  // namespace
 

@@ -6,7 +6,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <memory>
 #include <type_traits>
+#include <vector>
 
 #include "../../include/snn_lif.h"
 #include "lif_kernels.cuh"
@@ -27,6 +29,60 @@ bool tma_available();
 const char* encode_detail();   // why the last encode_2d on this thread failed
 
 template <int V> using IC = std::integral_constant<int, V>;
+
+// ---- launch recording (snn_lif_plan_*): with a Recorder installed on the calling thread,
+// the launch helpers below store each launch -- kernel, geometry and a copy of every
+// argument -- instead of enqueuing it; a plan replays them later with cudaLaunchKernelExC.
+struct RecordedLaunch {
+    const void* func = nullptr;
+    dim3 grid, block;
+    size_t smem = 0;
+    bool pdl = false;
+    std::vector<std::shared_ptr<void>> arg_store;   // one heap copy per parameter (alignment kept)
+    std::vector<void*> args;                        // pointers into arg_store, in order
+};
+struct Recorder {
+    std::vector<RecordedLaunch> launches;
+};
+Recorder*& current_recorder();   // thread-local; nullptr = launch immediately
+
+template <typename P>
+void record_arg(RecordedLaunch& r, const P& v) {
+    std::shared_ptr<void> p(new P(v), [](void* q) { delete static_cast<P*>(q); });
+    r.args.push_back(p.get());
+    r.arg_store.push_back(std::move(p));
+}
+
+// Launch kernel `k` (PDL attribute when `pdl`), or record it when a Recorder is installed.
+template <typename... Params, typename... Args>
+snn_status launch_kernel(void (*k)(Params...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                         bool pdl, const char* what, const Args&... args) {
+    static_assert(sizeof...(Params) == sizeof...(Args), "kernel arity");
+    if (Recorder* rec = current_recorder()) {
+        RecordedLaunch r;
+        r.func = reinterpret_cast<const void*>(k);
+        r.grid = grid; r.block = block; r.smem = smem; r.pdl = pdl;
+        (record_arg<std::remove_cv_t<std::remove_reference_t<Params>>>(r, args), ...);
+        rec->launches.push_back(std::move(r));
+        return SNN_OK;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL (lif_async.cuh)
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, k, static_cast<Params>(args)...);
+    if (e != cudaSuccess) return fail(SNN_ERR_CUDA, "%s launch failed: %s", what, cudaGetErrorString(e));
+    return launch_status(what);
+}
+
+// Replay one recorded launch on `st`.
+snn_status replay(const RecordedLaunch& r, cudaStream_t st);
 
 // Opt the kernel into its dynamic shared memory and return resident CTAs per SM.
 template <typename Kernel>
@@ -53,19 +109,7 @@ snn_status launch_tiles(Kernel k, int threads, int smem, int64_t ntiles, int64_t
     });
     if (ntiles > INT32_MAX) return fail(SNN_ERR_INVALID_VALUE, "too many tiles");
     const int depth = (int)std::max<int64_t>(1, std::min<int64_t>(4, (8 + stages_per_tile - 1) / stages_per_tile));
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)ntiles);
-    cfg.blockDim = dim3(threads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL (lif_async.cuh)
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, k, args..., depth);
-    if (e != cudaSuccess) return fail(SNN_ERR_CUDA, "%s launch failed: %s", what, cudaGetErrorString(e));
-    return launch_status(what);
+    return launch_kernel(k, dim3((unsigned)ntiles), dim3(threads), (size_t)smem, st, true, what, args..., depth);
 }
 
 // Plain launch with programmatic dependent launch allowed: the kernel must call pdl_wait()
@@ -73,18 +117,7 @@ snn_status launch_tiles(Kernel k, int threads, int smem, int64_t ntiles, int64_t
 template <typename Kernel, typename... Args>
 snn_status launch_pdl(Kernel k, dim3 grid, dim3 block, cudaStream_t st, const char* what,
                       const Args&... args) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = grid;
-    cfg.blockDim = block;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, k, args...);
-    if (e != cudaSuccess) return fail(SNN_ERR_CUDA, "%s launch failed: %s", what, cudaGetErrorString(e));
-    return launch_status(what);
+    return launch_kernel(k, grid, block, 0, st, true, what, args...);
 }
 
 // ---- launchers (one translation unit each, compiled in parallel) -------------------

@@ -29,6 +29,27 @@ snn_status fail(snn_status st, const char* fmt, ...) {
     return st;
 }
 
+Recorder*& current_recorder() {
+    static thread_local Recorder* rec = nullptr;
+    return rec;
+}
+
+snn_status replay(const RecordedLaunch& r, cudaStream_t st) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = r.grid;
+    cfg.blockDim = r.block;
+    cfg.dynamicSmemBytes = r.smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = r.pdl ? 1 : 0;
+    const cudaError_t e = cudaLaunchKernelExC(&cfg, r.func, const_cast<void**>(r.args.data()));
+    if (e != cudaSuccess) return fail(SNN_ERR_CUDA, "plan replay launch failed: %s", cudaGetErrorString(e));
+    return launch_status("plan replay");
+}
+
 snn_status launch_status(const char* what) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(SNN_ERR_CUDA, "%s launch failed: %s", what, cudaGetErrorString(e));
@@ -477,5 +498,86 @@ snn_status snn_lif_serial_backward_step(const snn_lif_params* p, int io_dtype, i
     return launch_serial_backward_step(io_dtype, mode_of(p), grad_spikes_t, h_t, grad_v, grad_x_t, N,
                                        make_consts(p), static_cast<cudaStream_t>(stream));
 }
+
+}  // extern "C"
+
+// ---- plans: record once, replay many times (include/snn_lif.h snn_lif_plan_*) -----------
+
+struct snn_lif_plan {
+    int device = -1;
+    bool has_backward = false;
+    std::vector<snn_host::RecordedLaunch> fwd, bwd;
+};
+
+namespace {
+
+// Run `body` with a Recorder installed on this thread; its launches land in `out`.
+template <typename F>
+snn_status record_into(std::vector<snn_host::RecordedLaunch>& out, F body) {
+    snn_host::Recorder rec;
+    snn_host::Recorder*& slot = snn_host::current_recorder();
+    snn_host::Recorder* prev = slot;
+    slot = &rec;
+    const snn_status st = body();
+    slot = prev;
+    if (st == SNN_OK) out = std::move(rec.launches);
+    return st;
+}
+
+snn_status replay_all(const snn_lif_plan* plan, const std::vector<snn_host::RecordedLaunch>& v, void* stream) {
+    int dev = -1;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev != plan->device)
+        return fail(SNN_ERR_INVALID_VALUE, "plan was created on device %d, current device is %d", plan->device, dev);
+    for (const auto& r : v) {
+        const snn_status st = snn_host::replay(r, static_cast<cudaStream_t>(stream));
+        if (st != SNN_OK) return st;
+    }
+    return SNN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+snn_status snn_lif_plan_create(snn_lif_plan** out, const snn_lif_params* p, const snn_lif_shape* s,
+                               const void* x, const float* v_init, void* spikes, void* saved,
+                               float* v_final, const void* grad_spikes, const float* grad_v_final,
+                               void* grad_x, float* grad_v_init) {
+    g_err[0] = 0;
+    if (!out) return fail(SNN_ERR_NULL_POINTER, "plan output pointer is NULL");
+    *out = nullptr;
+    if ((grad_spikes == nullptr) != (grad_x == nullptr))
+        return fail(SNN_ERR_NULL_POINTER, "grad_spikes and grad_x go together (both NULL: forward-only plan)");
+    auto plan = std::make_unique<snn_lif_plan>();
+    snn_status st = record_into(plan->fwd, [&] {   // validation first: nothing touches the device on error
+        return forward_impl(p, s, x, v_init, nullptr, spikes, saved, v_final, nullptr);
+    });
+    if (st != SNN_OK) return st;
+    if (grad_spikes) {
+        st = record_into(plan->bwd, [&] {
+            return backward_impl(p, s, grad_spikes, x, saved, grad_v_final, nullptr, grad_x, grad_v_init, nullptr);
+        });
+        if (st != SNN_OK) return st;
+        plan->has_backward = true;
+    }
+    if (cudaGetDevice(&plan->device) != cudaSuccess) return fail(SNN_ERR_CUDA, "cudaGetDevice failed");
+    *out = plan.release();
+    return SNN_OK;
+}
+
+snn_status snn_lif_plan_forward(const snn_lif_plan* plan, void* stream) {
+    g_err[0] = 0;
+    if (!plan) return fail(SNN_ERR_NULL_POINTER, "plan is NULL");
+    return replay_all(plan, plan->fwd, stream);
+}
+
+snn_status snn_lif_plan_backward(const snn_lif_plan* plan, void* stream) {
+    g_err[0] = 0;
+    if (!plan) return fail(SNN_ERR_NULL_POINTER, "plan is NULL");
+    if (!plan->has_backward) return fail(SNN_ERR_INVALID_VALUE, "forward-only plan (created without grad buffers)");
+    return replay_all(plan, plan->bwd, stream);
+}
+
+void snn_lif_plan_destroy(snn_lif_plan* plan) { delete plan; }
 
 }  // extern "C"

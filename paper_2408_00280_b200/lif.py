@@ -380,3 +380,59 @@ def lif_fwd_bwd_host(x: torch.Tensor, grad_spikes: torch.Tensor, params: LIFPara
                               grad_x.data_ptr(), chunk_neurons, nslots, workspace.data_ptr(),
                               workspace.numel(), _stream())
     return spikes, grad_x
+
+
+# ----------------------------------------------------------------------------- plans
+
+class LIFPlan:
+    """A fused LIF layer bound to fixed buffers: the C ABI validates the call once
+    (snn_lif_plan_create: parameters, layout, kernel variant, TMA tensor maps) and every
+    ``forward()`` / ``backward()`` replays only the kernel launches on torch's current
+    stream -- for serving loops or training steps that reuse their activation buffers.
+    Write new inputs into ``x`` / ``grad_spikes`` in place between calls; results land in
+    ``spikes`` / ``grad_x`` (bitwise what lif_forward / lif_backward return)."""
+
+    def __init__(self, x: torch.Tensor, params: LIFParams = LIFParams(), *, spike_fmt: str = "u8",
+                 save_mode: str = "recompute", v_init: Optional[torch.Tensor] = None,
+                 grad_spikes: Optional[torch.Tensor] = None, grad_v_final: Optional[torch.Tensor] = None,
+                 with_v_final: bool = False, with_grad_v_init: bool = False):
+        _check_2d("x", x)
+        T, N = x.shape
+        self.x, self.params, self.device = x, params, x.device
+        self.shape, nbytes = _shape_entry(x, spike_fmt, save_mode)
+        self.v_init = _vec("v_init", v_init, N, x.device)
+        if spike_fmt != "bits" and self.shape.ld != N:
+            self.spikes = torch.empty((T, self.shape.ld), dtype=torch.uint8 if spike_fmt == "u8" else x.dtype,
+                                      device=x.device)[:, :N]
+        else:
+            self.spikes = alloc_spikes(x, spike_fmt)
+        self.saved = torch.empty(nbytes // 4, dtype=torch.float32, device=x.device) if save_mode != "none" else None
+        self.v_final = torch.empty(N, dtype=torch.float32, device=x.device) if with_v_final else None
+        self.grad_spikes = grad_spikes
+        self.grad_x = self.grad_v_init = None
+        if grad_spikes is not None:
+            _check_2d("grad_spikes", grad_spikes)
+            if tuple(grad_spikes.shape) != (T, N) or grad_spikes.dtype != x.dtype or \
+                    (T > 1 and grad_spikes.stride(0) != self.shape.ld):
+                raise ValueError("grad_spikes must match x in shape, dtype and row stride")
+            self.grad_x = torch.empty((T, self.shape.ld), dtype=x.dtype, device=x.device)[:, :N]
+            self.grad_v_init = torch.empty(N, dtype=torch.float32, device=x.device) if with_grad_v_init else None
+        self.grad_v_final = _vec("grad_v_final", grad_v_final, N, x.device)
+        self._plan = _lib.snn_lif_plan_create(
+            params.to_c(), self.shape, _ptr(x), _ptr(self.v_init), _ptr(self.spikes), _ptr(self.saved),
+            _ptr(self.v_final), _ptr(grad_spikes), _ptr(self.grad_v_final), _ptr(self.grad_x),
+            _ptr(self.grad_v_init))
+
+    def forward(self) -> torch.Tensor:
+        _lib.snn_lif_plan_forward(self._plan, _stream(self.device))
+        return self.spikes
+
+    def backward(self) -> torch.Tensor:
+        _lib.snn_lif_plan_backward(self._plan, _stream(self.device))
+        return self.grad_x
+
+    def __del__(self):
+        plan = getattr(self, "_plan", None)
+        if plan:
+            _lib.snn_lif_plan_destroy(plan)
+            self._plan = None

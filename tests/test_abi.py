@@ -93,3 +93,21 @@ def test_null_and_misaligned_pointers(lib):
 def test_python_errors_are_loud(lib):
     err = lib.SNNError(1)
     assert "SNN_ERR_INVALID_VALUE" in str(err)
+
+
+def test_plan_validation_before_any_device_work(lib):
+    """snn_lif_plan_create validates like snn_lif_forward / _backward and returns before any
+    launch; replaying a NULL plan is an error, not a crash."""
+    P, S = ctypes.byref(_p(lib)), ctypes.byref(_s(lib))
+    h = ctypes.c_void_p()
+    assert lib.lib.snn_lif_plan_create(None, P, S, 16, None, 16, 16, None, None, None, None, None) == 2
+    assert lib.lib.snn_lif_plan_create(ctypes.byref(h), ctypes.byref(_p(lib, tau=0.5)), S, 16, None, 16, 16,
+                                       None, None, None, None, None) == 1
+    assert h.value is None
+    # grad_spikes without grad_x (and vice versa)
+    assert lib.lib.snn_lif_plan_create(ctypes.byref(h), P, S, 16, None, 16, 16, None, 16, None, None, None) == 2
+    assert lib.lib.snn_lif_plan_create(ctypes.byref(h), P, S, 16, None, 16, 16, None, None, None, 16, None) == 2
+    assert lib.lib.snn_lif_plan_create(ctypes.byref(h), P, S, None, None, 16, 16, None, None, None, None, None) == 2
+    assert lib.lib.snn_lif_plan_forward(None, None) == 2
+    assert lib.lib.snn_lif_plan_backward(None, None) == 2
+    lib.lib.snn_lif_plan_destroy(None)

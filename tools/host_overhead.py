@@ -53,6 +53,13 @@ def main():
     out["snn_lif_backward (C ABI only)"] = per_call(
         lambda: _lib.snn_lif_backward(cp, shape, g.data_ptr(), x.data_ptr(), None, f.saved.data_ptr(),
                                       None, gx.data_ptr(), None, st), a.calls)
+    xb, gb = x.clone(), g.clone()
+    plan = snn.LIFPlan(xb, p, grad_spikes=gb)
+    out["LIFPlan.forward (recorded launch)"] = per_call(plan.forward, a.calls)
+    out["LIFPlan.backward (recorded launch)"] = per_call(plan.backward, a.calls)
+    h = plan._plan
+    st2 = torch.cuda.current_stream().cuda_stream
+    out["snn_lif_plan_forward (C ABI only)"] = per_call(lambda: _lib.lib.snn_lif_plan_forward(h, st2), a.calls)
     layer = snn.LIFLayer(p)
     xr = torch.randn(T, N, device="cuda", requires_grad=True)
 
