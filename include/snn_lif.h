@@ -302,6 +302,15 @@ snn_status snn_lif_plan_create(snn_lif_plan** plan, const snn_lif_params* params
                                const snn_lif_shape* shape, const void* x, const float* v_init,
                                void* spikes, void* saved, float* v_final, const void* grad_spikes,
                                const float* grad_v_final, void* grad_x, float* grad_v_init);
+/* The same for the affine / residual prologue calls (snn_lif_forward_affine /
+ * snn_lif_backward_affine's arguments; the backward's scratch and per-channel outputs are
+ * bound too).  A forward-only affine plan is BN-folded inference. */
+snn_status snn_lif_plan_create_affine(snn_lif_plan** plan, const snn_lif_params* params,
+                                      const snn_lif_shape* shape, const void* x, const float* v_init,
+                                      const snn_lif_affine* affine, void* spikes, void* saved,
+                                      float* v_final, const void* grad_spikes, const float* grad_v_final,
+                                      void* grad_x, float* grad_v_init, float* part_a, float* part_b,
+                                      float* grad_scale, float* grad_shift);
 snn_status snn_lif_plan_forward(const snn_lif_plan* plan, void* stream);
 snn_status snn_lif_plan_backward(const snn_lif_plan* plan, void* stream);
 void snn_lif_plan_destroy(snn_lif_plan* plan);

@@ -31,7 +31,7 @@ EXPORTED_SYMBOLS = (
     "snn_last_error_message", "snn_lif_abi_version", "snn_lif_serial_forward_step",
     "snn_lif_serial_backward_step", "snn_lif_handoff_blocks", "snn_lif_forward_handoff",
     "snn_lif_backward_handoff", "snn_lif_forward_affine", "snn_lif_backward_affine",
-    "snn_lif_host_workspace_bytes", "snn_lif_fwd_bwd_host", "snn_lif_plan_create",
+    "snn_lif_host_workspace_bytes", "snn_lif_fwd_bwd_host", "snn_lif_plan_create", "snn_lif_plan_create_affine",
     "snn_lif_plan_forward", "snn_lif_plan_backward", "snn_lif_plan_destroy",
 )
 SNN_LIF_HANDOFF_BLOCK = 256
@@ -113,6 +113,9 @@ def _load() -> ctypes.CDLL:
     lib.snn_lif_fwd_bwd_host.restype = ctypes.c_int
     lib.snn_lif_plan_create.argtypes = [ctypes.POINTER(ctypes.c_void_p), P, S, vp, fp, vp, vp, fp, vp, fp, vp, fp]
     lib.snn_lif_plan_create.restype = ctypes.c_int
+    lib.snn_lif_plan_create_affine.argtypes = [ctypes.POINTER(ctypes.c_void_p), P, S, vp, fp, Ap, vp, vp, fp,
+                                               vp, fp, vp, fp, fp, fp, fp, fp]
+    lib.snn_lif_plan_create_affine.restype = ctypes.c_int
     lib.snn_lif_plan_forward.argtypes = [vp, vp]
     lib.snn_lif_plan_forward.restype = ctypes.c_int
     lib.snn_lif_plan_backward.argtypes = [vp, vp]
@@ -220,3 +223,13 @@ def snn_lif_plan_backward(plan, stream) -> None:
 
 def snn_lif_plan_destroy(plan) -> None:
     lib.snn_lif_plan_destroy(plan)
+
+
+def snn_lif_plan_create_affine(params, shape, x, v_init, affine, spikes, saved, v_final, grad_spikes,
+                               grad_v_final, grad_x, grad_v_init, part_a, part_b, grad_scale,
+                               grad_shift) -> int:
+    h = ctypes.c_void_p()
+    check(lib.snn_lif_plan_create_affine(ctypes.byref(h), ctypes.byref(params), ctypes.byref(shape), x, v_init,
+                                         ctypes.byref(affine), spikes, saved, v_final, grad_spikes, grad_v_final,
+                                         grad_x, grad_v_init, part_a, part_b, grad_scale, grad_shift))
+    return h.value

@@ -565,6 +565,35 @@ snn_status snn_lif_plan_create(snn_lif_plan** out, const snn_lif_params* p, cons
     return SNN_OK;
 }
 
+snn_status snn_lif_plan_create_affine(snn_lif_plan** out, const snn_lif_params* p, const snn_lif_shape* s,
+                                      const void* x, const float* v_init, const snn_lif_affine* af,
+                                      void* spikes, void* saved, float* v_final, const void* grad_spikes,
+                                      const float* grad_v_final, void* grad_x, float* grad_v_init,
+                                      float* part_a, float* part_b, float* grad_scale, float* grad_shift) {
+    g_err[0] = 0;
+    if (!out) return fail(SNN_ERR_NULL_POINTER, "plan output pointer is NULL");
+    *out = nullptr;
+    if (!af) return fail(SNN_ERR_NULL_POINTER, "affine is NULL");
+    if ((grad_spikes == nullptr) != (grad_x == nullptr))
+        return fail(SNN_ERR_NULL_POINTER, "grad_spikes and grad_x go together (both NULL: forward-only plan)");
+    auto plan = std::make_unique<snn_lif_plan>();
+    snn_status st = record_into(plan->fwd, [&] {
+        return snn_lif_forward_affine(p, s, x, v_init, af, spikes, saved, v_final, nullptr);
+    });
+    if (st != SNN_OK) return st;
+    if (grad_spikes) {
+        st = record_into(plan->bwd, [&] {
+            return snn_lif_backward_affine(p, s, grad_spikes, x, saved, grad_v_final, af, grad_x, grad_v_init,
+                                           part_a, part_b, grad_scale, grad_shift, nullptr);
+        });
+        if (st != SNN_OK) return st;
+        plan->has_backward = true;
+    }
+    if (cudaGetDevice(&plan->device) != cudaSuccess) return fail(SNN_ERR_CUDA, "cudaGetDevice failed");
+    *out = plan.release();
+    return SNN_OK;
+}
+
 snn_status snn_lif_plan_forward(const snn_lif_plan* plan, void* stream) {
     g_err[0] = 0;
     if (!plan) return fail(SNN_ERR_NULL_POINTER, "plan is NULL");

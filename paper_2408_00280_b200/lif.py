@@ -395,7 +395,11 @@ class LIFPlan:
     def __init__(self, x: torch.Tensor, params: LIFParams = LIFParams(), *, spike_fmt: str = "u8",
                  save_mode: str = "recompute", v_init: Optional[torch.Tensor] = None,
                  grad_spikes: Optional[torch.Tensor] = None, grad_v_final: Optional[torch.Tensor] = None,
-                 with_v_final: bool = False, with_grad_v_init: bool = False):
+                 with_v_final: bool = False, with_grad_v_init: bool = False,
+                 affine: Optional["AffineSpec"] = None, residual: Optional[torch.Tensor] = None):
+        """affine / residual: the f4 prologue (lif_forward_affine); the backward then also fills
+        ``grad_scale`` / ``grad_shift`` (and ``grad_residual``).  save_mode must be "recompute"
+        (or "none" for a forward-only, BN-folded inference plan)."""
         _check_2d("x", x)
         T, N = x.shape
         self.x, self.params, self.device = x, params, x.device
@@ -418,10 +422,30 @@ class LIFPlan:
             self.grad_x = torch.empty((T, self.shape.ld), dtype=x.dtype, device=x.device)[:, :N]
             self.grad_v_init = torch.empty(N, dtype=torch.float32, device=x.device) if with_grad_v_init else None
         self.grad_v_final = _vec("grad_v_final", grad_v_final, N, x.device)
-        self._plan = _lib.snn_lif_plan_create(
-            params.to_c(), self.shape, _ptr(x), _ptr(self.v_init), _ptr(self.spikes), _ptr(self.saved),
-            _ptr(self.v_final), _ptr(grad_spikes), _ptr(self.grad_v_final), _ptr(self.grad_x),
-            _ptr(self.grad_v_init))
+        if affine is None:
+            if residual is not None:
+                raise ValueError("residual needs an affine (use scale 1, shift 0 for a plain shortcut)")
+            self._plan = _lib.snn_lif_plan_create(
+                params.to_c(), self.shape, _ptr(x), _ptr(self.v_init), _ptr(self.spikes), _ptr(self.saved),
+                _ptr(self.v_final), _ptr(grad_spikes), _ptr(self.grad_v_final), _ptr(self.grad_x),
+                _ptr(self.grad_v_init))
+            return
+        self.affine, self.residual = affine, residual
+        if residual is not None:
+            residual = self.residual = _like_x("residual", residual, x, self.shape.ld)
+        self.grad_residual = self.grad_scale = self.grad_shift = self._part = None
+        if grad_spikes is not None:
+            if residual is not None:
+                self.grad_residual = torch.empty((T, self.shape.ld), dtype=x.dtype, device=x.device)[:, :N]
+            self._part = torch.empty((2, (N + 3) // 4 * 4), dtype=torch.float32, device=x.device)
+            self.grad_scale = torch.empty(affine.C, dtype=torch.float32, device=x.device)
+            self.grad_shift = torch.empty(affine.C, dtype=torch.float32, device=x.device)
+        self._c_affine = affine.to_c(residual, self.grad_residual)   # kept alive with the plan
+        self._plan = _lib.snn_lif_plan_create_affine(
+            params.to_c(), self.shape, _ptr(x), _ptr(self.v_init), self._c_affine, _ptr(self.spikes),
+            _ptr(self.saved), _ptr(self.v_final), _ptr(grad_spikes), _ptr(self.grad_v_final), _ptr(self.grad_x),
+            _ptr(self.grad_v_init), None if self._part is None else _ptr(self._part[0]),
+            None if self._part is None else _ptr(self._part[1]), _ptr(self.grad_scale), _ptr(self.grad_shift))
 
     def forward(self) -> torch.Tensor:
         _lib.snn_lif_plan_forward(self._plan, _stream(self.device))

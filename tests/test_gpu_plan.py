@@ -65,3 +65,29 @@ def test_plan_inside_cuda_graph():
     f = snn.lif_forward(X, P); gx, _ = snn.lif_backward(G, f)
     torch.cuda.synchronize()
     assert torch.equal(plan.spikes, f.spikes) and torch.equal(plan.grad_x, gx)
+
+
+@pytest.mark.parametrize("residual", [False, True])
+def test_affine_plan_equals_direct_calls_bitwise(residual):
+    T, B, C, HW = 24, 4, 8, 64
+    N = B * C * HW
+    X = snn_synth.normal_tensor(71, T, N, device="cuda")
+    G = snn_synth.normal_tensor(72, T, N, device="cuda")
+    R = snn_synth.normal_tensor(73, T, N, std=0.5, device="cuda") if residual else None
+    af = snn.AffineSpec(torch.linspace(0.5, 1.5, C, device="cuda"), torch.linspace(-0.2, 0.2, C, device="cuda"),
+                        C, HW)
+    x_buf, g_buf = X.clone(), G.clone()
+    r_buf = None if R is None else R.clone()
+    plan = snn.LIFPlan(x_buf, P, grad_spikes=g_buf, affine=af, residual=r_buf, with_v_final=True)
+    s = plan.forward().clone(); gx = plan.backward().clone()
+    f = snn.lif_forward_affine(X, P, af, residual=R)
+    out = snn.lif_backward_affine(G, f)
+    torch.cuda.synchronize()
+    assert torch.equal(s, f.spikes) and torch.equal(plan.v_final, f.v_final)
+    assert torch.equal(gx, out[0]) and torch.equal(plan.grad_scale, out[2]) and torch.equal(plan.grad_shift, out[3])
+    if residual:
+        assert torch.equal(plan.grad_residual, out[4])
+    inf = snn.LIFPlan(x_buf, P, save_mode="none", affine=af, residual=r_buf)   # BN-folded inference
+    s2 = inf.forward()
+    torch.cuda.synchronize()
+    assert torch.equal(s2, f.spikes)
