@@ -307,12 +307,12 @@ __device__ __forceinline__ void bwd_chunk(const LifConsts& c, float (&gV)[VEC],
     }
 }
 
-template <typename IO, int VEC, int MODE, int BW>
+template <typename IO, int VEC, int MODE, int BW, int ROWS_MAX = kCkpt>
 __device__ __forceinline__ void recompute_chunk(const LifConsts& c, float (&V)[VEC],
                                                 float (&h)[kCkpt][VEC], const IO* xs, int rows,
                                                 const AffCoef<VEC>& co, const IO* rs = nullptr) {
 #pragma unroll
-    for (int j = 0; j < kCkpt; ++j) {
+    for (int j = 0; j < ROWS_MAX; ++j) {
         if (j < rows) {
             const Pack<IO, VEC> xv = *reinterpret_cast<const Pack<IO, VEC>*>(xs + j * BW);
             Pack<IO, VEC> rv;
@@ -421,6 +421,11 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
             if (rows == kCkpt && tile_full) {   // full chunk of a full tile: guard-free code
                 recompute_chunk<IO, VEC, MODE, BW>(c, V, h, xs, kCkpt, co, rs);
                 bwd_chunk<IO, VEC, MODE, BW, kCkpt>(c, gV, h, gsm, gxp, ldb, kCkpt, true, co, xs, pa, pb, grp);
+            } else if (rows == kCkpt / 2 && tile_full) {   // half chunk (T % 16 == 8, e.g. T = 8): guard-free too
+                constexpr int HR = kCkpt / 2;
+                recompute_chunk<IO, VEC, MODE, BW, HR>(c, V, h, xs, HR, co, rs);
+                bwd_chunk<IO, VEC, MODE, BW, HR>(c, gV, reinterpret_cast<const float(&)[HR][VEC]>(h), gsm, gxp, ldb,
+                                                 HR, true, co, xs, pa, pb, grp);
             } else {
                 recompute_chunk<IO, VEC, MODE, BW>(c, V, h, xs, rows, co, rs);
                 bwd_chunk<IO, VEC, MODE, BW, kCkpt>(c, gV, h, gsm, gxp, ldb, rows, valid, co, xs, pa, pb, grp);
