@@ -208,36 +208,44 @@ lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_con
             }
             const int rows = (int)min((int64_t)R, T - rb * R);
             const IO* xs = reinterpret_cast<const IO*>(smem + s * Cfg::STAGE_BYTES) + xoff;
+            // F: a full stage of a full tile.  Otherwise (the last stage when T % R != 0, or a
+            // ragged tile) every row is still computed -- rows past T were zero-filled by the
+            // TMA -- and only the V update (a select on the uniform `act`) and the stores are
+            // conditional, so the rows stay one basic block (cf. bwd_chunk_masked).
             auto rowloop = [&](auto full) {
             constexpr bool F = decltype(full)::value;
             const int nv = F ? VEC : nvalid;
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-                if (F || r < rows) {
-                    const Pack<IO, VEC> xv = *reinterpret_cast<const Pack<IO, VEC>*>(xs + r * BW);
-                    Pack<IO, VEC> rv;
-                    if constexpr (RES)
-                        rv = *reinterpret_cast<const Pack<IO, VEC>*>(
-                            reinterpret_cast<const IO*>(smem + s * Cfg::STAGE_BYTES + Cfg::R_OFF) + xoff + r * BW);
-                    if constexpr (SAVE == SAVE_RECOMPUTE) {
-                        // checkpoint the V entering step t when t % kCkpt == 0
-                        const int64_t t = rb * R + r;
-                        if ((t % kCkpt) == 0 && nv > 0) {
-                            Pack<float, VEC> ck;
+                const bool act = F || r < rows;
+                const Pack<IO, VEC> xv = *reinterpret_cast<const Pack<IO, VEC>*>(xs + r * BW);
+                Pack<IO, VEC> rv;
+                if constexpr (RES)
+                    rv = *reinterpret_cast<const Pack<IO, VEC>*>(
+                        reinterpret_cast<const IO*>(smem + s * Cfg::STAGE_BYTES + Cfg::R_OFF) + xoff + r * BW);
+                if constexpr (SAVE == SAVE_RECOMPUTE) {
+                    // checkpoint the V entering step t when t % kCkpt == 0
+                    const int64_t t = rb * R + r;
+                    if (act && (t % kCkpt) == 0 && nv > 0) {
+                        Pack<float, VEC> ck;
 #pragma unroll
-                            for (int i = 0; i < VEC; ++i) ck.v[i] = V[i];
-                            st_stream<float, VEC>(h_row + (t / kCkpt) * a.ldh, ck);
-                        }
+                        for (int i = 0; i < VEC; ++i) ck.v[i] = V[i];
+                        st_stream<float, VEC>(h_row + (t / kCkpt) * a.ldh, ck);
                     }
-                    Pack<float, VEC> hp;
-                    const unsigned bits = fwd_compute<SOFT, AFF, RES>(c, V, xv, hp, co, &rv);
-                    if constexpr (SAVE == SAVE_H) {
-                        if (nv > 0) st_stream<float, VEC>(h_row, hp);
-                        h_row += a.ldh;
-                    }
-                    store_spikes<IO, VEC, SFMT>(spk_row, g, n0, bits, nv, a.nwords);
-                    spk_row += spk_step;
                 }
+                Pack<float, VEC> hp;
+                float Vn[VEC];
+#pragma unroll
+                for (int i = 0; i < VEC; ++i) Vn[i] = V[i];
+                const unsigned bits = fwd_compute<SOFT, AFF, RES>(c, Vn, xv, hp, co, &rv);
+#pragma unroll
+                for (int i = 0; i < VEC; ++i) V[i] = act ? Vn[i] : V[i];
+                if constexpr (SAVE == SAVE_H) {
+                    if (act && nv > 0) st_stream<float, VEC>(h_row, hp);
+                    h_row += a.ldh;
+                }
+                if (act) store_spikes<IO, VEC, SFMT>(spk_row, g, n0, bits, nv, a.nwords);
+                spk_row += spk_step;
             }
             };
             if (rows == R && tile_full) rowloop(std::true_type{}); else rowloop(std::false_type{});
@@ -303,6 +311,44 @@ __device__ __forceinline__ void bwd_chunk(const LifConsts& c, float (&gV)[VEC],
                 if (valid) st_stream<IO, VEC>(grp, outr);
                 grp = step_bytes(grp, -ldb);
             }
+        }
+    }
+}
+
+// Partial chunk (rows < ROWS_MAX, or a ragged last tile): every row of the ROWS_MAX block is
+// computed unconditionally -- rows past T were zero-filled by the TMA, so their arithmetic
+// is finite and independent of the carried gV until the select -- and only the carry update
+// (a select on the uniform `act`) and the stores are conditional.  One basic block per chunk
+// lets the compiler interleave the rows' independent surrogate math, which a per-row branch
+// (the old guarded loop) serialised: T=10 cost as much as T=16.  gx0 / gr0 = row 0 of the chunk.
+template <typename IO, int VEC, int MODE, int BW, int ROWS_MAX>
+__device__ __forceinline__ void bwd_chunk_masked(const LifConsts& c, float (&gV)[VEC],
+                                                 const float (&h)[kCkpt][VEC], const IO* gsm,
+                                                 IO* gx0, int64_t ldb, int rows, bool valid,
+                                                 const AffCoef<VEC>& co, const IO* xs, float* pa, float* pb,
+                                                 IO* gr0 = nullptr) {
+#pragma unroll
+    for (int j = ROWS_MAX - 1; j >= 0; --j) {
+        const bool act = j < rows;   // uniform across the CTA
+        const Pack<IO, VEC> gv = *reinterpret_cast<const Pack<IO, VEC>*>(gsm + j * BW);
+        Pack<IO, VEC> out, outr;
+        float g2[VEC], pa2[VEC], pb2[VEC];
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) { g2[i] = gV[i]; pa2[i] = pa[i]; pb2[i] = pb[i]; }
+        if constexpr (Mode<MODE>::AFF) {
+            const Pack<IO, VEC> xr = *reinterpret_cast<const Pack<IO, VEC>*>(xs + j * BW);
+            out = bwd_step<IO, VEC, MODE, true>(c, g2, h[j], gv, &co, &xr, pa2, pb2, &outr);
+        } else {
+            out = bwd_step<IO, VEC, MODE>(c, g2, h[j], gv);
+        }
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) {
+            gV[i] = act ? g2[i] : gV[i];
+            if constexpr (Mode<MODE>::AFF) { pa[i] = act ? pa2[i] : pa[i]; pb[i] = act ? pb2[i] : pb[i]; }
+        }
+        if (act && valid) {
+            st_stream<IO, VEC>(step_bytes(gx0, j * ldb), out);
+            if constexpr (Mode<MODE>::RES) st_stream<IO, VEC>(step_bytes(gr0, j * ldb), outr);
         }
     }
 }
@@ -426,9 +472,22 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
                 recompute_chunk<IO, VEC, MODE, BW, HR>(c, V, h, xs, HR, co, rs);
                 bwd_chunk<IO, VEC, MODE, BW, HR>(c, gV, reinterpret_cast<const float(&)[HR][VEC]>(h), gsm, gxp, ldb,
                                                  HR, true, co, xs, pa, pb, grp);
-            } else {
-                recompute_chunk<IO, VEC, MODE, BW>(c, V, h, xs, rows, co, rs);
-                bwd_chunk<IO, VEC, MODE, BW, kCkpt>(c, gV, h, gsm, gxp, ldb, rows, valid, co, xs, pa, pb, grp);
+            } else {                            // partial chunk or ragged tile: masked rows
+                IO* gx0 = gx + t0 * ld + n0;
+                IO* gr0 = RES ? reinterpret_cast<IO*>(a.af.grad_residual) + t0 * ld + n0 : nullptr;
+                if (rows <= kCkpt / 4) {
+                    recompute_chunk<IO, VEC, MODE, BW, kCkpt / 4>(c, V, h, xs, kCkpt / 4, co, rs);
+                    bwd_chunk_masked<IO, VEC, MODE, BW, kCkpt / 4>(c, gV, h, gsm, gx0, ldb, rows, valid, co, xs,
+                                                                   pa, pb, gr0);
+                } else if (rows <= kCkpt / 2) {
+                    recompute_chunk<IO, VEC, MODE, BW, kCkpt / 2>(c, V, h, xs, kCkpt / 2, co, rs);
+                    bwd_chunk_masked<IO, VEC, MODE, BW, kCkpt / 2>(c, gV, h, gsm, gx0, ldb, rows, valid, co, xs,
+                                                                   pa, pb, gr0);
+                } else {
+                    recompute_chunk<IO, VEC, MODE, BW>(c, V, h, xs, kCkpt, co, rs);
+                    bwd_chunk_masked<IO, VEC, MODE, BW, kCkpt>(c, gV, h, gsm, gx0, ldb, rows, valid, co, xs,
+                                                               pa, pb, gr0);
+                }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&bar->empty[s]);

@@ -26,6 +26,8 @@ CASES = {
     "bf512": [("bf16", 512, 1 << 20)],
     "short": [("f32", 8, 1 << 20), ("f32", 16, 1 << 20), ("f32", 16, 1 << 23), ("bf16", 16, 1 << 23),
               ("bf16", 16, 1 << 21), ("f32", 64, 1 << 22)],
+    "ragged": [("f32", 4, 1 << 21), ("f32", 10, 1 << 21), ("f32", 16, 1 << 21), ("f32", 20, 1 << 21),
+               ("f32", 32, 1 << 21), ("bf16", 10, 1 << 22), ("bf16", 16, 1 << 22)],
     "small": [("bf16", 16, 1 << 14), ("bf16", 16, 1 << 16), ("bf16", 16, 1 << 18), ("bf16", 1, 1 << 14),
               ("f32", 16, 1 << 18), ("f32", 1, 1 << 14)],
 }
