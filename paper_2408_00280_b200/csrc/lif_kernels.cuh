@@ -447,18 +447,21 @@ lif_backward_recompute_kernel(const BwdArgs a) {
 #pragma unroll
     for (int i = 0; i < VEC; ++i) pa[i] = pb[i] = 0.0f;
     const int64_t nchunks = (T + kCkpt - 1) / kCkpt;
-    for (int64_t ch = nchunks - 1; ch >= 0; --ch) {
+    // One chunk; FULL (16 rows) is branch-free so the rows' independent math interleaves,
+    // a partial chunk (only the last one, when T % 16 != 0) keeps the per-row guards.
+    auto chunk = [&](int64_t ch, auto full) {
+        constexpr bool FULL = decltype(full)::value;
         const int64_t t0 = ch * kCkpt;
-        const int len = (int)min((int64_t)kCkpt, T - t0);
+        const int len = FULL ? kCkpt : (int)min((int64_t)kCkpt, T - t0);
         const Pack<float, VEC> v0 = ld_group<float, VEC>(ck + ch * ldh, nvalid);
         Pack<IO, VEC> xb[kCkpt];
         Pack<IO, VEC> gb[kCkpt];
 #pragma unroll
         for (int j = 0; j < kCkpt; ++j)
-            if (j < len) xb[j] = ld_group<IO, VEC>(xs + (t0 + j) * ld, nvalid);
+            if (FULL || j < len) xb[j] = ld_group<IO, VEC>(xs + (t0 + j) * ld, nvalid);
 #pragma unroll
         for (int j = 0; j < kCkpt; ++j)
-            if (j < len) gb[j] = ld_group<IO, VEC>(gs + (t0 + j) * ld, nvalid);
+            if (FULL || j < len) gb[j] = ld_group<IO, VEC>(gs + (t0 + j) * ld, nvalid);
 
         float h[kCkpt][VEC];
         float V[VEC];
@@ -466,15 +469,19 @@ lif_backward_recompute_kernel(const BwdArgs a) {
         for (int i = 0; i < VEC; ++i) V[i] = v0.v[i];
 #pragma unroll
         for (int j = 0; j < kCkpt; ++j) {
-            if (j < len) fwd_recompute_step<Mode<MODE>::SOFT, AFF>(c, V, xb[j], h[j], co);
+            if (FULL || j < len) fwd_recompute_step<Mode<MODE>::SOFT, AFF>(c, V, xb[j], h[j], co);
         }
 #pragma unroll
         for (int j = kCkpt - 1; j >= 0; --j) {
-            if (j < len)
+            if (FULL || j < len)
                 st_group<IO, VEC>(gx + (t0 + j) * ld,
                                   bwd_step<IO, VEC, MODE, AFF>(c, gV, h[j], gb[j], &co, &xb[j], pa, pb),
                                   nvalid);
         }
+    };
+    for (int64_t ch = nchunks - 1; ch >= 0; --ch) {
+        if ((ch + 1) * kCkpt <= T) chunk(ch, std::true_type{});
+        else chunk(ch, std::false_type{});
     }
     if constexpr (AFF) {
         Pack<float, VEC> qa, qb;
