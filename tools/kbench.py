@@ -54,6 +54,9 @@ def alg_bytes(dt, T, N, save_mode="recompute"):
     return (e + 1 + ck) * T * N, (3 * e + ck) * T * N
 
 
+SAVE_MODE = "recompute"
+
+
 def time_case(dt, T, N, reps):
     dtype = torch.float32 if dt == "f32" else torch.bfloat16
     p = snn.LIFParams.paper()
@@ -62,14 +65,14 @@ def time_case(dt, T, N, reps):
     st = torch.cuda.current_stream()
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(reps)]
     for i in range(3):
-        f = snn.lif_forward(xs[i % 2], p, return_v_final=False)
+        f = snn.lif_forward(xs[i % 2], p, return_v_final=False, save_mode=SAVE_MODE)
         snn.lif_backward(gs[i % 2], f, return_grad_v_init=False)
     torch.cuda.synchronize()
     torch.cuda._sleep(int(3e6 + 2.5e5 * reps))   # keep the GPU busy while the host enqueues
     for i in range(reps):
         e = ev[i]
         e[0].record(st)
-        f = snn.lif_forward(xs[i % 2], p, return_v_final=False)
+        f = snn.lif_forward(xs[i % 2], p, return_v_final=False, save_mode=SAVE_MODE)
         e[1].record(st)
         e[2].record(st)
         snn.lif_backward(gs[i % 2], f, return_grad_v_init=False)
@@ -87,7 +90,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--cases", default="cfg1,cfg2,t16")
+    ap.add_argument("--save-mode", default="recompute")
     a = ap.parse_args()
+    global SAVE_MODE
+    SAVE_MODE = a.save_mode
     torch.cuda.set_device(0)
     time_null(a.reps)
     for c in a.cases.split(","):
