@@ -604,25 +604,8 @@ lif_backward_saveh_tma_kernel(const __grid_constant__ CUtensorMap tmh,
                     }
                 }
             };
-            // partial row block / ragged tile: every row computed on the zero-filled stage,
-            // carry by select, stores predicated (cf. bwd_chunk_masked)
-            auto walk_masked = [&]() {
-                IO* g0 = gx + rb * R * ld + n0;
-#pragma unroll
-                for (int r = R - 1; r >= 0; --r) {
-                    const bool act = r < rows;
-                    const Pack<float, VEC> hv = *reinterpret_cast<const Pack<float, VEC>*>(hs + r * BW);
-                    const Pack<IO, VEC> gv = *reinterpret_cast<const Pack<IO, VEC>*>(gsm + r * BW);
-                    float g2[VEC];
-#pragma unroll
-                    for (int i = 0; i < VEC; ++i) g2[i] = gV[i];
-                    const Pack<IO, VEC> out = bwd_step<IO, VEC, MODE>(c, g2, hv.v, gv);
-#pragma unroll
-                    for (int i = 0; i < VEC; ++i) gV[i] = act ? g2[i] : gV[i];
-                    if (act && valid) st_stream<IO, VEC>(step_bytes(g0, r * ldb), out);
-                }
-            };
-            if (rows == R && tile_full) walk(std::true_type{}); else walk_masked();
+            // (a masked walk, as the RECOMPUTE backward's partial chunks use, measured slower here)
+            if (rows == R && tile_full) walk(std::true_type{}); else walk(std::false_type{});
             __syncwarp();
             if (lane == 0) mbar_arrive(&bar->empty[s]);
         }
