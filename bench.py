@@ -57,6 +57,9 @@ def parse():
                          "the multi-rank code paths on a 1-GPU box; numbers are not bench values)")
     ap.add_argument("--serial", action="store_true",
                     help="with --sweep: also time the paper's serial baselines (Fig. 3 / Fig. 5)")
+    ap.add_argument("--inference", action="store_true",
+                    help="also time the forward alone with save_mode none (serving) and a BN-folded "
+                         "inference LIFPlan on the default shape")
     ap.add_argument("--affine", action="store_true",
                     help="also time the fused per-channel affine prologue (SURVEY 8(f) f4) against "
                          "an unfused torch affine + plain LIF on a [T=64, B=16, C=64, 32x32] layer")
@@ -384,6 +387,46 @@ def run_sweep(args, params, dev, stream):
             out[-1]["speedup_vs_serial_torch"] = round(serial["torch_ms"] / (mf + mb), 2)
         del X, G, f, gx, g
     return out
+
+
+def run_inference(args, params, dev):
+    """Serving-shaped leg: the forward alone with save_mode "none" (no state kept for a
+    backward), on the default workload's shape (N = 2^20, T = 512, fp32) and on BN-folded
+    inference through a LIFPlan (affine prologue, 64 channels).  Two input batches alternate;
+    20 graph-launched forwards each, median of the per-launch CUDA-event times."""
+    import torch
+    import paper_2408_00280_b200 as snn
+    import snn_synth
+    T, N = 512, 1 << 20
+    X = [snn_synth.normal_tensor(1234 + i, T, N, device=dev) for i in range(2)]
+    spikes = torch.empty(T, N, dtype=torch.uint8, device=dev)
+    C = 64
+    spec = snn.AffineSpec(torch.linspace(0.5, 1.5, C, device=dev), torch.linspace(-0.2, 0.2, C, device=dev),
+                          C, N // (16 * C))
+    plans = [snn.LIFPlan(X[i], params, save_mode="none", affine=spec) for i in range(2)]
+    res = {"shape": {"T": T, "N": N}, "save_mode": "none", "spike_fmt": "u8"}
+    for name, fn in (("forward_only", lambda i: snn.lif_forward(X[i], params, save_mode="none", spikes=spikes,
+                                                                 return_v_final=False)),
+                     ("bn_folded_plan", lambda i: plans[i].forward())):
+        for i in range(3):
+            fn(i % 2)
+        torch.cuda.synchronize(dev)
+        evs = []
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for i in range(20):
+                e = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(2)]
+                e[0].record(); fn(i % 2); e[1].record()
+                evs.append(e)
+        g.replay()
+        torch.cuda.synchronize(dev)
+        ts = sorted(a.elapsed_time(b) for a, b in evs)
+        ms = ts[len(ts) // 2]
+        res[name + "_ms"] = round(ms, 4)
+        res[name + "_neuron_steps_per_s"] = T * N / (ms / 1e3)
+        res[name + "_GBps"] = round(5.0 * T * N / (ms / 1e3) / 1e9, 1)   # 4 B x + 1 B spike
+        del g
+    return res
 
 
 def run_affine(args, params, dev):
@@ -837,6 +880,7 @@ def run_ours(args):
     if args.sweep and args.workload == "cfg1" and rank == 0:
         sweep = run_sweep(args, params, dev, stream)
     affine = run_affine(args, params, dev) if args.affine and rank == 0 else None
+    inference = run_inference(args, params, dev) if args.inference and rank == 0 else None
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -865,6 +909,8 @@ def run_ours(args):
             line["sweep"] = sweep
         if affine is not None:
             line["affine"] = affine
+        if inference is not None:
+            line["inference"] = inference
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
