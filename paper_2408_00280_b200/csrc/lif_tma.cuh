@@ -79,7 +79,7 @@ template <int S, int STAGE_BYTES, typename Issue>
 __device__ __forceinline__ void produce(unsigned char* smem, Barriers<S>* bar, int64_t nstages,
                                         int depth, Issue issue) {
     uint32_t k = 0;
-    uint32_t phase[kMaxClc] = {0, 0, 0, 0};
+    uint32_t phases = 0;   // bit i = parity of CLC slot i (a bit set, not an array: no local memory)
     int issued = 0, consumed = 0;
     bool stop = false;
     for (int i = 0; i < depth; ++i, ++issued) clc_request(&bar->clc[i]);
@@ -95,7 +95,9 @@ __device__ __forceinline__ void produce(unsigned char* smem, Barriers<S>* bar, i
         tile = -1;
         while (consumed < issued) {
             const int i = consumed % depth;
-            const int r = clc_next_tile(&bar->clc[i], phase[i]);
+            uint32_t ph = (phases >> i) & 1u;
+            const int r = clc_next_tile(&bar->clc[i], ph);
+            phases ^= 1u << i;
             ++consumed;
             if (r >= 0) {
                 tile = r;
