@@ -49,3 +49,11 @@ def test_multirank_paths_under_torchrun(workload, extra):
               "--debug-single-gpu", *extra], nproc=2, port=29532 if workload == "cfg1" else 29533)
     assert d["n_gpus"] == 2
     assert d["scaling"] == ("weak" if workload == "cfg1" else "strong")
+
+
+def test_affine_and_inference_legs():
+    d = _run(["--steps", "3", "--warmup", "3", "--T", "32", "--no-e2e", "--no-cpu-baseline", "--affine",
+              "--inference"])
+    a, inf = d["affine"], d["inference"]
+    assert a["fused_ms"] > 0 and a["fused_residual_ms"] > 0 and a["speedup_fused_vs_unfused"] > 1
+    assert inf["forward_only_ms"] > 0 and inf["bn_folded_plan_neuron_steps_per_s"] > 0
