@@ -57,6 +57,9 @@ def parse():
                          "the multi-rank code paths on a 1-GPU box; numbers are not bench values)")
     ap.add_argument("--serial", action="store_true",
                     help="with --sweep: also time the paper's serial baselines (Fig. 3 / Fig. 5)")
+    ap.add_argument("--prologue", action="store_true",
+                    help="also time configs[4]'s ResNet LIF layers with their BN affine and residual "
+                         "shortcut fused in (LIFPlans, fwd+bwd), against the same layers without")
     ap.add_argument("--inference", action="store_true",
                     help="also time the forward alone with save_mode none (serving) and a BN-folded "
                          "inference LIFPlan on the default shape")
@@ -427,6 +430,63 @@ def run_inference(args, params, dev):
         res[name + "_GBps"] = round(5.0 * T * N / (ms / 1e3) / 1e9, 1)   # 4 B x + 1 B spike
         del g
     return res
+
+
+def run_resnet_prologue(args, params, dev):
+    """BASELINE configs[4]'s 17 Spiking-ResNet18 DVS LIF layers (B=32 per rank, T=64, fp32)
+    as a training step actually feeds them: every LIF takes its BatchNorm affine, and the
+    second LIF of each basic block also the residual shortcut (BN(conv) + identity), fused
+    into the kernels' prologue.  One step = all forwards in layer order,
+    then all backwards in reverse, through LIFPlans (bound buffers), K steps graph-launched;
+    compared with the same layers and plans without the prologue."""
+    import torch
+    import paper_2408_00280_b200 as snn
+    import snn_synth
+    B, T = 32, 64
+    plans_p, plans_0, nbytes_p, nbytes_0, ns = [], [], 0.0, 0.0, 0
+    for i, (c, h, w) in enumerate(RESNET18_DVS_LAYERS):
+        N, HW = B * c * h * w, h * w
+        X = snn_synth.normal_tensor(1234 + i, T, N, device=dev)
+        G = snn_synth.normal_tensor(4321 + i, T, N, device=dev)
+        res = i > 0 and i % 2 == 0            # block-second LIF: BN(conv2) + shortcut
+        R = snn_synth.normal_tensor(999 + i, T, N, device=dev, std=0.5) if res else None
+        gen = torch.Generator(dev).manual_seed(i)
+        spec = snn.AffineSpec(torch.rand(c, device=dev, generator=gen) + 0.5,
+                              0.2 * torch.randn(c, device=dev, generator=gen), c, HW)
+        plans_p.append(snn.LIFPlan(X, params, grad_spikes=G, affine=spec, residual=R))
+        plans_0.append(snn.LIFPlan(X, params, grad_spikes=G))
+        ck = 4.0 * math.ceil(T / 16) / T
+        base = (4 + 1 + ck) + (12 + ck)
+        nbytes_0 += base * T * N
+        nbytes_p += (base + 8.0 / T + (12.0 if res else 0.0)) * T * N   # partials; R in x2, dL/dR out
+        ns += T * N
+    out = {"layers": len(plans_p), "B": B, "T": T, "neurons": ns // T,
+           "residual_layers": sum(1 for p_ in plans_p if getattr(p_, "residual", None) is not None)}
+    for name, plans, nbytes in (("prologue", plans_p, nbytes_p), ("plain", plans_0, nbytes_0)):
+        def step():
+            for p_ in plans:
+                p_.forward()
+            for p_ in reversed(plans):
+                p_.backward()
+        for _ in range(3):
+            step()
+        torch.cuda.synchronize(dev)
+        g = torch.cuda.CUDAGraph()
+        K = max(3, min(args.steps, 20))
+        with torch.cuda.graph(g):
+            for _ in range(K):
+                step()
+        g.replay()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(); g.replay(); e1.record()
+        torch.cuda.synchronize(dev)
+        ms = e0.elapsed_time(e1) / K
+        out[name] = {"ms_per_step": round(ms, 4), "neuron_steps_per_s": ns / (ms / 1e3),
+                     "algorithmic_GBps": round(nbytes / (ms / 1e3) / 1e9, 1)}
+        del g
+    out["prologue_overhead"] = round(out["prologue"]["ms_per_step"] / out["plain"]["ms_per_step"] - 1, 4)
+    return out
 
 
 def run_affine(args, params, dev):
@@ -881,6 +941,7 @@ def run_ours(args):
         sweep = run_sweep(args, params, dev, stream)
     affine = run_affine(args, params, dev) if args.affine and rank == 0 else None
     inference = run_inference(args, params, dev) if args.inference and rank == 0 else None
+    prologue = run_resnet_prologue(args, params, dev) if args.prologue and rank == 0 else None
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -911,6 +972,8 @@ def run_ours(args):
             line["affine"] = affine
         if inference is not None:
             line["inference"] = inference
+        if prologue is not None:
+            line["resnet_prologue"] = prologue
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
