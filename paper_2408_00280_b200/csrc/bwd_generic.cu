@@ -126,7 +126,7 @@ snn_status go(const snn_lif_shape* s, const snn::BwdArgs& a, int mode, cudaStrea
 snn_status launch_backward_generic(const snn_lif_shape* s, const snn::BwdArgs& a, int mode, bool vec,
                                    cudaStream_t st) {
     if (s->io_dtype == SNN_BF16)
-        return vec ? go<__nv_bfloat16, 4>(s, a, mode, st) : go<__nv_bfloat16, 1>(s, a, mode, st);
+        return vec ? go<__nv_bfloat16, 2>(s, a, mode, st) : go<__nv_bfloat16, 1>(s, a, mode, st);
     return vec ? go<float, 2>(s, a, mode, st) : go<float, 1>(s, a, mode, st);
 }
 

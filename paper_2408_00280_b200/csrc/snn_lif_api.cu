@@ -401,7 +401,7 @@ snn_status backward_impl(const snn_lif_params* p, const snn_lif_shape* s,
         return fail(SNN_ERR_UNSUPPORTED, "the residual prologue needs the TMA path (16-B aligned rows, "
                                          "N a multiple of %d)", tma_vec_backward(s->io_dtype));
     if (handoff) return fail(SNN_ERR_UNSUPPORTED, "the fused handoff needs the TMA path (aligned rows)");
-    const int vec = s->io_dtype == SNN_BF16 ? 4 : 2;
+    const int vec = 2;   // bf16 and fp32: 2 neurons per thread (bf16 x 4 held too many registers)
     const bool fast = (s->ld % vec) == 0 && aligned(grad_spikes, 16) && aligned(grad_x, 16) &&
                       (!x || s->save_mode != SNN_SAVE_RECOMPUTE || aligned(x, 16)) &&
                       (!grad_v_final || aligned(grad_v_final, 16)) &&
