@@ -41,7 +41,7 @@ snn_status go(const snn_lif_shape* s, const snn::FwdArgs& a, bool soft, cudaStre
 snn_status launch_forward_generic(const snn_lif_shape* s, const snn::FwdArgs& a, bool soft, bool vec,
                                   cudaStream_t st) {
     if (s->io_dtype == SNN_BF16)
-        return vec ? go<__nv_bfloat16, 8>(s, a, soft, st) : go<__nv_bfloat16, 1>(s, a, soft, st);
+        return vec ? go<__nv_bfloat16, 4>(s, a, soft, st) : go<__nv_bfloat16, 1>(s, a, soft, st);
     return vec ? go<float, 4>(s, a, soft, st) : go<float, 1>(s, a, soft, st);
 }
 
