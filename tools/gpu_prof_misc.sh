@@ -1,3 +1,4 @@
+# Sweep bench line + bf16 T=512 backward and cfg1 T=8 ncu captures, for profiles/ (1x B200).
 O=gpurun_out/prof; mkdir -p $O
 NCU=/usr/local/cuda/bin/ncu
 timeout 300 python bench.py --sweep --serial --no-cpu-baseline --no-e2e > $O/bench_sweep.json 2> $O/bench_sweep.err
