@@ -79,7 +79,8 @@ snn_status launch_forward_tma(const snn_lif_shape* s, const snn::FwdArgs& a, boo
 template <typename IO, int MODE>
 snn_status launch_backward_tma_mode(const snn_lif_shape* s, const snn::BwdArgs& a, cudaStream_t st) {
     using C = TmaCfg<IO>;
-    if constexpr (MODE < 8) {   // SAVE_H has no affine-gradient variant (host rejects it)
+    static_assert(MODE < 32 || (MODE & 24) == 0, "P0 variants are plain-path only");
+    if constexpr (MODE < 8) {   // SAVE_H has no affine-gradient or P0 variant (host never asks)
     if (s->save_mode == SNN_SAVE_H) {
         using Cfg = snn::BwdHTma<IO, C::HV, C::HN, C::HR, C::HS>;
         CUtensorMap tmh, tmg;
@@ -111,7 +112,7 @@ snn_status launch_backward_tma_mode(const snn_lif_shape* s, const snn::BwdArgs& 
 template <typename IO>
 snn_status launch_backward_tma(const snn_lif_shape* s, const snn::BwdArgs& a, int mode,
                                cudaStream_t st) {
-    switch (mode & 31) {
+    switch (mode & 63) {
         case 0: return launch_backward_tma_mode<IO, 0>(s, a, st);
         case 1: return launch_backward_tma_mode<IO, 1>(s, a, st);
         case 2: return launch_backward_tma_mode<IO, 2>(s, a, st);
@@ -136,6 +137,14 @@ snn_status launch_backward_tma(const snn_lif_shape* s, const snn::BwdArgs& a, in
         case 29: return launch_backward_tma_mode<IO, 29>(s, a, st);
         case 30: return launch_backward_tma_mode<IO, 30>(s, a, st);
         case 31: return launch_backward_tma_mode<IO, 31>(s, a, st);
+        case 32: return launch_backward_tma_mode<IO, 32>(s, a, st);
+        case 33: return launch_backward_tma_mode<IO, 33>(s, a, st);
+        case 34: return launch_backward_tma_mode<IO, 34>(s, a, st);
+        case 35: return launch_backward_tma_mode<IO, 35>(s, a, st);
+        case 36: return launch_backward_tma_mode<IO, 36>(s, a, st);
+        case 37: return launch_backward_tma_mode<IO, 37>(s, a, st);
+        case 38: return launch_backward_tma_mode<IO, 38>(s, a, st);
+        case 39: return launch_backward_tma_mode<IO, 39>(s, a, st);
         default: return fail(SNN_ERR_UNSUPPORTED, "backward variant %d (residual without affine)", mode);
     }
 }

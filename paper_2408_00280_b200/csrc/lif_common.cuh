@@ -42,6 +42,10 @@ struct Mode {
     static constexpr bool DETACH = (MODE & 4) != 0;
     static constexpr bool AFF = (MODE & 8) != 0;   // affine prologue gradients (RECOMPUTE only)
     static constexpr bool RES = (MODE & 16) != 0;  // + residual add (implies AFF; TMA path only)
+    // Paper-mode constants (decay_input = 0, V_reset = 0: s = 1, c0 = 0): the charge is
+    // fma(k, V, X) and gX = gH -- the same values up to the sign of a zero (fma(1, -0, +0) is
+    // +0), two fewer paired ops per backward step.  Plain TMA path only.
+    static constexpr bool P0 = (MODE & 32) != 0;
 };
 
 __device__ __forceinline__ float ex2_approx(float x) {  // MUFU.EX2, ftz
@@ -152,8 +156,10 @@ __device__ __forceinline__ F2 sub2(F2 a, F2 b) {
     return r;
 }
 
-// Charge for two neurons: H = k V + (s X + c0)   (same roundings as lif_charge).
+// Charge for two neurons: H = k V + (s X + c0)   (same roundings as lif_charge); P0: s = 1, c0 = 0.
+template <bool P0 = false>
 __device__ __forceinline__ F2 lif_charge2(const LifConsts& c, F2 V, F2 X) {
+    if constexpr (P0) return fma2(f2(c.k), V, X);
     return fma2(f2(c.k), V, fma2(f2(c.s), X, f2(c.c0)));
 }
 

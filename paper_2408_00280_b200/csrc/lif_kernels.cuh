@@ -152,7 +152,7 @@ __device__ __forceinline__ unsigned fwd_compute(const LifConsts& c, float (&V)[V
 }
 
 // Re-run the charge / fire / reset (no outputs) -- the RECOMPUTE backward's forward pass.
-template <bool SOFT, bool AFF, bool RES = false, typename IO, int VEC>
+template <bool SOFT, bool AFF, bool RES = false, bool P0 = false, typename IO, int VEC>
 __device__ __forceinline__ void fwd_recompute_step(const LifConsts& c, float (&V)[VEC],
                                                    const Pack<IO, VEC>& xv, float (&h)[VEC],
                                                    const AffCoef<VEC>& co,
@@ -161,7 +161,7 @@ __device__ __forceinline__ void fwd_recompute_step(const LifConsts& c, float (&V
 #pragma unroll
         for (int i = 0; i < VEC; i += 2) {
             const F2 X2 = input2<AFF, RES>(co, xv, i, rv);
-            const F2 H2 = lif_charge2(c, f2(V[i], V[i + 1]), X2);
+            const F2 H2 = lif_charge2<P0>(c, f2(V[i], V[i + 1]), X2);
             h[i] = lo(H2);
             h[i + 1] = hi(H2);
             V[i] = lif_reset<SOFT>(c, h[i], lif_fire(c, h[i]));
@@ -251,7 +251,7 @@ __device__ __forceinline__ Pack<IO, VEC> bwd_step(const LifConsts& c, float (&gV
             const F2 gH = lif_grad_step2<MODE>(c, f2(h[i], h[i + 1]),
                                                load2(gs, i),
                                                f2(gV[i], gV[i + 1]));
-            F2 gx = mul2(f2(c.s), gH);
+            F2 gx = Mode<MODE>::P0 ? gH : mul2(f2(c.s), gH);
             if constexpr (AFF) {
                 const F2 x2 = load2(*xr, i);
                 const F2 pa2 = fma2(gx, x2, f2(pa[i], pa[i + 1]));

@@ -360,7 +360,8 @@ __device__ __forceinline__ void recompute_chunk(const LifConsts& c, float (&V)[V
             const Pack<IO, VEC> xv = *reinterpret_cast<const Pack<IO, VEC>*>(xs + j * BW);
             Pack<IO, VEC> rv;
             if constexpr (Mode<MODE>::RES) rv = *reinterpret_cast<const Pack<IO, VEC>*>(rs + j * BW);
-            fwd_recompute_step<Mode<MODE>::SOFT, Mode<MODE>::AFF, Mode<MODE>::RES>(c, V, xv, h[j], co, &rv);
+            fwd_recompute_step<Mode<MODE>::SOFT, Mode<MODE>::AFF, Mode<MODE>::RES, Mode<MODE>::P0>(c, V, xv, h[j],
+                                                                                               co, &rv);
         }
     }
 }

@@ -394,9 +394,14 @@ snn_status backward_impl(const snn_lif_params* p, const snn_lif_shape* s,
 
     if (tma_ok(s, tma_vec_backward(s->io_dtype),
                {grad_spikes, grad_x, s->save_mode == SNN_SAVE_RECOMPUTE ? x : nullptr, saved,
-                grad_v_final, grad_v_init, res, gres}))
-        return s->io_dtype == SNN_BF16 ? launch_backward_tma_bf16(s, a, mode, cs)
-                                       : launch_backward_tma_f32(s, a, mode, cs);
+                grad_v_final, grad_v_init, res, gres})) {
+        // paper-mode constants on the plain RECOMPUTE path: the P0 variants (lif_common.cuh
+        // Mode::P0; the SAVE_H kernel has no P0 instantiation)
+        const int tmode = (mode < 8 && s->save_mode == SNN_SAVE_RECOMPUTE && !p->decay_input &&
+                           p->v_reset == 0.0f) ? (mode | 32) : mode;
+        return s->io_dtype == SNN_BF16 ? launch_backward_tma_bf16(s, a, tmode, cs)
+                                       : launch_backward_tma_f32(s, a, tmode, cs);
+    }
     if (res)
         return fail(SNN_ERR_UNSUPPORTED, "the residual prologue needs the TMA path (16-B aligned rows, "
                                          "N a multiple of %d)", tma_vec_backward(s->io_dtype));
