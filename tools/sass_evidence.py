@@ -17,9 +17,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OBJ = os.path.join(ROOT, "paper_2408_00280_b200", "build")
 KERNELS = [
     ("fwd_tma_f32.o", r"lif_forward_tma_kernelIfLi4ELi0ELi1ELb0ELb0ELb0ELi256ELi8ELi3E", "forward fp32 (default bench kernel)"),
-    ("bwd_tma_f32.o", r"lif_backward_recompute_tma_kernelIfLi2ELi0ELi256ELi3E", "backward RECOMPUTE fp32 (dominant kernel)"),
+    ("bwd_tma_f32.o", r"lif_backward_recompute_tma_kernelIfLi2ELi32ELi256ELi3E", "backward RECOMPUTE fp32, paper-mode variant (dominant kernel)"),
     ("fwd_tma_bf16.o", r"lif_forward_tma_kernelI13__nv_bfloat16Li8ELi0ELi1ELb0ELb0ELb0ELi128ELi8ELi6E", "forward bf16 (cfg2)"),
-    ("bwd_tma_bf16.o", r"lif_backward_recompute_tma_kernelI13__nv_bfloat16Li2ELi0ELi256ELi3E", "backward RECOMPUTE bf16 (cfg2)"),
+    ("bwd_tma_bf16.o", r"lif_backward_recompute_tma_kernelI13__nv_bfloat16Li2ELi32ELi256ELi3E", "backward RECOMPUTE bf16, paper-mode variant (cfg2)"),
 ]
 WATCH = ["UTMALDG", "UTMACCTL", "SYNCS", "UGETNEXTWORKID", "PREEXIT", "ACQBULK", "ELECT", "FFMA2", "FMUL2", "FADD2", "FFMA", "FMUL", "FADD",
          "MUFU", "LDS", "STG", "LDG", "LDL", "STL", "NANOSLEEP", "UTMASTG", "HMMA", "UTCHMMA"]
