@@ -104,11 +104,15 @@ int cached_occupancy(const void* k, int threads, int smem, int (*prep)(const voi
 template <typename Kernel, typename... Args>
 snn_status launch_tiles(Kernel k, int threads, int smem, int64_t ntiles, int64_t stages_per_tile,
                         cudaStream_t st, const char* what, const Args&... args) {
-    cached_occupancy(reinterpret_cast<const void*>(k), threads, smem, [](const void* kk, int t, int sm) {
+    const int occ = cached_occupancy(reinterpret_cast<const void*>(k), threads, smem, [](const void* kk, int t, int sm) {
         return prepare(reinterpret_cast<Kernel>(const_cast<void*>(kk)), t, sm);
     });
     if (ntiles > INT32_MAX) return fail(SNN_ERR_INVALID_VALUE, "too many tiles");
-    const int depth = (int)std::max<int64_t>(1, std::min<int64_t>(4, (8 + stages_per_tile - 1) / stages_per_tile));
+    // Steal requests in flight: none when every CTA is resident from the start (nothing can
+    // ever be pending, and a CTA would only wait for the failed responses before exiting).
+    const int depth = ntiles <= (int64_t)occ * num_sms()
+                          ? 0
+                          : (int)std::max<int64_t>(1, std::min<int64_t>(4, (8 + stages_per_tile - 1) / stages_per_tile));
     return launch_kernel(k, dim3((unsigned)ntiles), dim3(threads), (size_t)smem, st, true, what, args..., depth);
 }
 
