@@ -607,3 +607,39 @@ def test_randomized_affine_residual_parity(T, B, C, HW, dtype, mode, decay_input
     rep = compare(p, ref_scaled, rgx, ref["gvi"], S.cpu().to(torch.uint8), out[0].cpu(),
                   vf_gpu=f.v_final.cpu(), gvi_gpu=out[1].cpu(), io_bf16=bf)
     assert_ok(rep)
+
+
+def test_cfg4_stem_with_bn_and_residual_full_size_sampled():
+    """BASELINE configs[4]'s stem-sized layer (B=32, C=64, 64x64, T=64: 8.4 M neurons, fp32) with
+    the BN affine and a residual shortcut fused in, at full size in the bench's launch
+    configuration; 1024 sampled columns checked against the oracle (spikes, V_final, dL/dX,
+    dL/dR, grad_v_init)."""
+    T, B, C, H, W = 64, 32, 64, 64, 64
+    HW, N = H * W, B * C * H * W
+    X = snn_synth.normal_tensor(1234, T, N, device="cuda")
+    G = snn_synth.normal_tensor(4321, T, N, device="cuda")
+    R = snn_synth.normal_tensor(999, T, N, std=0.5, device="cuda")
+    sc = torch.linspace(0.5, 1.5, C); sh = torch.linspace(-0.2, 0.2, C)
+    af = snn.AffineSpec(sc.cuda(), sh.cuda(), C, HW)
+    f = snn.lif_forward_affine(X, PAPER, af, residual=R)
+    gx, gvi, _, _, gres = snn.lif_backward_affine(G, f)
+    torch.cuda.synchronize()
+    del X, G, R
+    cols = np.sort(np.random.default_rng(7).choice(N, 1024, replace=False))
+    ci = torch.as_tensor(cols, device="cuda")
+    Xh = snn_synth.normal_columns(1234, T, N, cols).double().numpy()
+    Gh = snn_synth.normal_columns(4321, T, N, cols)
+    Rh = snn_synth.normal_columns(999, T, N, cols, std=0.5).double().numpy()
+    cidx = (cols // HW) % C
+    a, b = sc.double().numpy()[cidx], sh.double().numpy()[cidx]
+    Xp = a[None, :] * Xh + b[None, :] + Rh          # the definition, per sampled column
+    ref = oracle_run(PAPER, Xp, Gh)
+    rep = compare(PAPER, ref, ref["gX"], ref["gvi"], f.spikes[:, ci].cpu(), gres[:, ci].cpu(),
+                  vf_gpu=f.v_final[ci].cpu(), gvi_gpu=gvi[ci].cpu(), col_ids=cols)
+    assert_ok(rep)
+    ref_scaled = dict(ref)
+    ref_scaled["gX_bound"] = ref["gX_bound"] * np.abs(a)[None, :]
+    ref_scaled["gX_sens"] = ref["gX_sens"] * np.abs(a)[None, :]
+    rep = compare(PAPER, ref_scaled, ref["gX"] * a[None, :], ref["gvi"], f.spikes[:, ci].cpu(),
+                  gx[:, ci].cpu(), col_ids=cols)
+    assert_ok(rep)
