@@ -91,3 +91,28 @@ def test_affine_plan_equals_direct_calls_bitwise(residual):
     s2 = inf.forward()
     torch.cuda.synchronize()
     assert torch.equal(s2, f.spikes)
+
+
+from hypothesis import HealthCheck, given, settings, strategies as st  # noqa: E402
+
+
+@settings(max_examples=25, deadline=None, suppress_health_check=list(HealthCheck))
+@given(T=st.integers(1, 40), N=st.integers(1, 3000), dtype=st.sampled_from([torch.float32, torch.bfloat16]),
+       mode=st.integers(0, 7), decay_input=st.booleans(), v_reset=st.sampled_from([0.0, 0.1]),
+       save_mode=st.sampled_from(["recompute", "h"]), spike_fmt=st.sampled_from(["u8", "bits", "io"]))
+def test_randomized_plan_equals_direct(T, N, dtype, mode, decay_input, v_reset, save_mode, spike_fmt):
+    """Random shapes (TMA and generic paths), every reset/surrogate/detach mode, paper-mode and
+    general constants: a plan's replay is bitwise the direct calls."""
+    p = snn.LIFParams(tau=1.5, v_th=0.6, v_reset=v_reset, surrogate=("atan" if mode & 1 else "sigmoid"),
+                      reset=("soft" if mode & 2 else "hard"), detach_reset=bool(mode & 4),
+                      decay_input=decay_input, alpha=(2.0 if mode & 1 else 4.0))
+    X = snn_synth.normal_tensor(T * 31 + N, T, N, mean=0.5, dtype=dtype, device="cuda")
+    G = snn_synth.normal_tensor(T * 37 + N, T, N, dtype=dtype, device="cuda")
+    plan = snn.LIFPlan(X, p, spike_fmt=spike_fmt, save_mode=save_mode, grad_spikes=G, with_v_final=True,
+                       with_grad_v_init=True)
+    s = plan.forward().clone(); gx = plan.backward().clone()
+    f = snn.lif_forward(X, p, spike_fmt=spike_fmt, save_mode=save_mode)
+    gx_ref, gvi_ref = snn.lif_backward(G, f)
+    torch.cuda.synchronize()
+    assert torch.equal(s, f.spikes) and torch.equal(plan.v_final, f.v_final)
+    assert torch.equal(gx, gx_ref) and torch.equal(plan.grad_v_init, gvi_ref)
