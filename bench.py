@@ -974,6 +974,10 @@ def run_ours(args):
                 "gpu_launches": 2 * nlaunch * args.steps, "clocks": clk.summary()}
         if sweep is not None:
             line["sweep"] = sweep
+            # context only: the paper's A100 claim for the same comparison
+            line["paper_context"] = ("fused monolayer LIF up to 40x over traditional implementations, 5-40x over "
+                                     "SNN libraries, on an A100 (PAPER.md:30, :454-459, Fig. 5); the sweep's "
+                                     "speedup_vs_serial_* are this B200's figures for that comparison")
         if affine is not None:
             line["affine"] = affine
         if inference is not None:
