@@ -110,6 +110,7 @@ void lif_oracle_forward(const lif_oracle_params* p, int64_t T, int64_t N,
                         double* V_work /* [N] scratch owned by the caller */)
 {
     double* V = V_work;
+    const double k = 1.0 - 1.0 / p->tau;   /* k_tau = 1 - 1/tau */
     for (int64_t n = 0; n < N; ++n) V[n] = v_init ? v_init[n] : p->v_reset;
 
     for (int64_t t = 0; t < T; ++t) {
@@ -120,8 +121,9 @@ void lif_oracle_forward(const lif_oracle_params* p, int64_t T, int64_t N,
             /* charge (Eq. 1 / BJ.north_star; SURVEY 0.1 shows they are one family) */
             if (p->decay_input)
                 H = Vp + (X - (Vp - p->v_reset)) / p->tau;   /* BJ.north_star, verbatim */
-            else
-                H = Vp - (Vp - p->v_reset) / p->tau + X;     /* = k V + X at V_reset = 0: Eq. 1 */
+            else   /* Eq. 1 as printed, k_tau v^(t-1) + x^(t), plus the
+                      V_reset/tau offset of the family (0 at the paper's V_rest = 0) */
+                H = k * Vp + p->v_reset / p->tau + X;
             /* fire (Eq. 2) */
             double S = fire(p, H);
             /* reset: hard = V_rest*y + (1-y)*(...) of Eq. 1; soft = BJ.north_star */

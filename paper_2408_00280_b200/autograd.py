@@ -12,7 +12,7 @@ from typing import Optional
 
 import torch
 
-from .lif import (AffineSpec, LIFParams, lif_backward, lif_backward_affine, lif_forward,
+from .lif import (AffineSpec, LIFForward, LIFParams, lif_backward, lif_backward_affine, lif_forward,
                   lif_forward_affine)
 
 
@@ -26,16 +26,20 @@ class FusedLIF(torch.autograd.Function):
         x = x if x.stride(-1) == 1 else x.contiguous()
         fwd = lif_forward(x, params, v_init=v_init, spike_fmt="io", save_mode=save_mode,
                           return_v_final=False)
-        ctx.fwd = fwd
+        # through save_for_backward (not as attributes of ctx): autograd's version check
+        # then catches an in-place edit of x before the RECOMPUTE backward re-reads it, a
+        # retained graph can run backward twice, and the output is not kept alive by ctx.
+        ctx.save_for_backward(x, fwd.saved, v_init)
+        ctx.params, ctx.shape = params, fwd.shape
         ctx.has_v_init = v_init is not None
         return fwd.spikes
 
     @staticmethod
     def backward(ctx, grad_spikes: torch.Tensor):
-        fwd = ctx.fwd
-        gx, gvi = lif_backward(grad_spikes.to(fwd.x.dtype), fwd,
+        x, saved, v_init = ctx.saved_tensors
+        fwd = LIFForward(None, saved, None, x, v_init, ctx.params, ctx.shape)
+        gx, gvi = lif_backward(grad_spikes.to(x.dtype), fwd,
                                return_grad_v_init=ctx.has_v_init and ctx.needs_input_grad[2])
-        ctx.fwd = None
         return gx, None, gvi, None
 
 
@@ -73,19 +77,22 @@ class FusedAffineLIF(torch.autograd.Function):
         if residual is not None:   # the spiking-ResNet shortcut added to the LIF input
             r2 = residual.reshape(T, -1).to(x.dtype)
             r2 = r2 if r2.is_contiguous() else r2.contiguous()
-        fwd = lif_forward_affine(x2, params, AffineSpec(scale.contiguous(), shift.contiguous(), C, HW),
-                                 spike_fmt="io", return_v_final=False, residual=r2)
-        ctx.fwd = fwd
+        spec = AffineSpec(scale.contiguous(), shift.contiguous(), C, HW)
+        fwd = lif_forward_affine(x2, params, spec, spike_fmt="io", return_v_final=False, residual=r2)
+        ctx.save_for_backward(x2, fwd.saved, spec.scale, spec.shift, fwd.residual)
+        ctx.params, ctx.cshape, ctx.C, ctx.HW = params, fwd.shape, C, HW
         ctx.shape = x.shape
         ctx.res_shape = None if residual is None else (residual.shape, residual.dtype)
         return fwd.spikes.reshape(x.shape)
 
     @staticmethod
     def backward(ctx, grad_spikes):
-        fwd = ctx.fwd
+        x2, saved, scale, shift, r2 = ctx.saved_tensors
+        fwd = LIFForward(None, saved, None, x2, None, ctx.params, ctx.cshape)
+        fwd.affine = AffineSpec(scale, shift, ctx.C, ctx.HW)
+        fwd.residual = r2
         T = grad_spikes.shape[0]
-        out = lif_backward_affine(grad_spikes.reshape(T, -1).to(fwd.x.dtype), fwd, return_grad_v_init=False)
-        ctx.fwd = None
+        out = lif_backward_affine(grad_spikes.reshape(T, -1).to(x2.dtype), fwd, return_grad_v_init=False)
         gres = None
         if ctx.res_shape is not None:
             shape, dtype = ctx.res_shape

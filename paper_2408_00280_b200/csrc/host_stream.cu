@@ -61,9 +61,16 @@ bool make_plan(const snn_lif_params* p, const snn_lif_shape* s, int64_t chunk_ne
 
 struct Resources {   // streams / events of one call (created and destroyed inside it)
     cudaStream_t in = nullptr, out = nullptr;
+    cudaStream_t caller = nullptr;   // the caller's kernel stream (its queued chunks read the slots)
     cudaEvent_t start = nullptr;
     cudaEvent_t ready[8] = {}, computed[8] = {}, drained[8] = {};
     ~Resources() {
+        // Every exit -- success or an error half-way through the chunk loop -- first drains
+        // the copies and kernels already queued: they read and write the caller's host
+        // buffers and workspace, which the caller may free as soon as this call returns.
+        if (in) cudaStreamSynchronize(in);
+        if (caller) cudaStreamSynchronize(caller);
+        if (out) cudaStreamSynchronize(out);
         for (int i = 0; i < 8; ++i) {
             if (ready[i]) cudaEventDestroy(ready[i]);
             if (computed[i]) cudaEventDestroy(computed[i]);
@@ -116,6 +123,7 @@ snn_status snn_lif_fwd_bwd_host(const snn_lif_params* p, const snn_lif_shape* s,
 
     cudaStream_t cs = static_cast<cudaStream_t>(stream);
     Resources r;
+    r.caller = cs;
     SNN_CUDA_TRY(cudaStreamCreateWithFlags(&r.in, cudaStreamNonBlocking), "cudaStreamCreate");
     SNN_CUDA_TRY(cudaStreamCreateWithFlags(&r.out, cudaStreamNonBlocking), "cudaStreamCreate");
     SNN_CUDA_TRY(cudaEventCreateWithFlags(&r.start, cudaEventDisableTiming), "cudaEventCreate");
@@ -156,9 +164,9 @@ snn_status snn_lif_fwd_bwd_host(const snn_lif_params* p, const snn_lif_shape* s,
         // the fused kernels on the caller's stream
         SNN_CUDA_TRY(cudaStreamWaitEvent(cs, r.ready[sl], 0), "cudaStreamWaitEvent");
         snn_status st = snn_lif_forward(p, &sh, dx, nullptr, ds, dsaved, nullptr, stream);
-        if (st != SNN_OK) { cudaStreamSynchronize(cs); return st; }
+        if (st != SNN_OK) return st;   // ~Resources drains every queued copy first
         st = snn_lif_backward(p, &sh, dg, dx, nullptr, dsaved, nullptr, dgx, nullptr, stream);
-        if (st != SNN_OK) { cudaStreamSynchronize(cs); return st; }
+        if (st != SNN_OK) return st;
         SNN_CUDA_TRY(cudaEventRecord(r.computed[sl], cs), "cudaEventRecord");
 
         // device -> host

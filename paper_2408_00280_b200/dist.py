@@ -159,67 +159,95 @@ class TimeSplitLIF:
         self.messages_sent = 0
 
     def forward(self, x_local: torch.Tensor, fwd_fn: Callable, *, v_init: Optional[torch.Tensor] = None):
-        """x_local: [T_d, N] (this rank's time segment).  Returns (spikes_local, state,
-        v_final) -- v_final is the layer's final V on the last rank, else None."""
+        """x_local: [T_d, N] (this rank's time segment).  Returns (spikes_local [T_d, N], state,
+        v_final) -- v_final is the layer's final V on the last rank, else None.
+
+        When ``fwd_fn.writes_into`` is set (the CUDA segment functions), the segment's spikes
+        are allocated ONCE here and every chunk writes its column view of them (no per-chunk
+        buffers, no concatenation); otherwise the chunk results are concatenated."""
         T_d, N = x_local.shape
         chunks = neuron_chunks(N, self.n_chunks, self.align)
         dev = x_local.device
         prev, nxt = self.rank - 1, self.rank + 1
-        ctxs, spikes, sends, v_last = [], [], [], []
+        into = getattr(fwd_fn, "writes_into", False)
+        out = fwd_fn.alloc_spikes(x_local) if into else None
+        ctxs, spikes, sends = [], [], []
+        v_final = torch.empty(N, dtype=torch.float32, device=dev) if nxt >= self.k else None
         for (a, b) in chunks:
             if prev >= 0:
                 v_in = torch.empty(b - a, dtype=torch.float32, device=dev)
                 self.t.irecv(v_in, prev).wait()
             else:
                 v_in = None if v_init is None else v_init[a:b].contiguous()
-            ctx, spk, v_out = fwd_fn(x_local[:, a:b], v_in)
+            if into:
+                ctx, spk, v_out = fwd_fn(x_local[:, a:b], v_in, out=out[:, a:b])
+            else:
+                ctx, spk, v_out = fwd_fn(x_local[:, a:b], v_in)
+                spikes.append(spk)
             ctxs.append(ctx)
-            spikes.append(spk)
             if nxt < self.k:
                 sends.append(self.t.isend(v_out, nxt))
                 self.messages_sent += 1
             else:
-                v_last.append(v_out)
+                v_final[a:b] = v_out
         for s in sends:
             s.wait()
-        v_final = torch.cat(v_last) if v_last else None
-        return spikes, SegmentState(ctxs, chunks), v_final
+        if not into:
+            out = torch.cat(spikes, dim=1)
+        return out, SegmentState(ctxs, chunks), v_final
 
     def backward(self, g_local: torch.Tensor, state: SegmentState, bwd_fn: Callable, *,
                  grad_v_final: Optional[torch.Tensor] = None):
-        """g_local: [T_d, N] dL/dS of this segment.  Returns (gx chunks, grad_v_init) --
-        grad_v_init is the layer's dL/dV[-1] on rank 0, else None."""
+        """g_local: [T_d, N] dL/dS of this segment.  Returns (grad_x [T_d, N], grad_v_init) --
+        grad_v_init is the layer's dL/dV[-1] on rank 0, else None.  grad_x is allocated once
+        when ``bwd_fn.writes_into`` is set (chunks write their column views)."""
         dev = g_local.device
+        T_d, N = g_local.shape
         prev, nxt = self.rank - 1, self.rank + 1
-        gxs, sends, g_first = [], [], []
+        into = getattr(bwd_fn, "writes_into", False)
+        out = torch.empty((T_d, N), dtype=g_local.dtype, device=dev) if into else None
+        gxs, sends = [], []
+        g_first = torch.empty(N, dtype=torch.float32, device=dev) if prev < 0 else None
         for (a, b), ctx in zip(state.chunks, state.ctxs):
             if nxt < self.k:
                 g_in = torch.empty(b - a, dtype=torch.float32, device=dev)
                 self.t.irecv(g_in, nxt).wait()
             else:
                 g_in = None if grad_v_final is None else grad_v_final[a:b].contiguous()
-            gx, g_out = bwd_fn(g_local[:, a:b], ctx, g_in)
-            gxs.append(gx)
+            if into:
+                _, g_out = bwd_fn(g_local[:, a:b], ctx, g_in, out=out[:, a:b])
+            else:
+                gx, g_out = bwd_fn(g_local[:, a:b], ctx, g_in)
+                gxs.append(gx)
             if prev >= 0:
                 sends.append(self.t.isend(g_out, prev))
                 self.messages_sent += 1
             else:
-                g_first.append(g_out)
+                g_first[a:b] = g_out
         for s in sends:
             s.wait()
-        return gxs, (torch.cat(g_first) if g_first else None)
+        if not into:
+            out = torch.cat(gxs, dim=1)
+        return out, g_first
 
 
 def lif_segment_fns(params, *, spike_fmt: str = "u8", save_mode: str = "recompute"):
     """(fwd_fn, bwd_fn) running one segment of one neuron chunk through the fused CUDA
-    kernels (C ABI) -- the product compute of TimeSplitLIF."""
-    from .lif import lif_backward, lif_forward
+    kernels (C ABI) -- the per-chunk compute of TimeSplitLIF over a torch.distributed
+    transport.  Both write into column views of segment-wide outputs (``writes_into``):
+    a chunk view x[:, a:b] has row stride N, and so do the views of the [T_d, N] outputs."""
+    from .lif import lif_backward, lif_forward, alloc_spikes
 
-    def fwd_fn(x_chunk, v_in):
-        f = lif_forward(x_chunk, params, v_init=v_in, spike_fmt=spike_fmt, save_mode=save_mode)
+    def fwd_fn(x_chunk, v_in, out=None):
+        f = lif_forward(x_chunk, params, v_init=v_in, spike_fmt=spike_fmt, save_mode=save_mode,
+                        spikes=out)
         return f, f.spikes, f.v_final
 
-    def bwd_fn(g_chunk, ctx, g_in):
-        return lif_backward(g_chunk, ctx, grad_v_final=g_in)
+    def bwd_fn(g_chunk, ctx, g_in, out=None):
+        return lif_backward(g_chunk, ctx, grad_v_final=g_in, grad_x=out)
 
+    # bit-packed spikes have dense [T, ceil(n/32)] rows per call: no column views
+    fwd_fn.writes_into = spike_fmt != "bits"
+    fwd_fn.alloc_spikes = lambda x: alloc_spikes(x, spike_fmt)
+    bwd_fn.writes_into = True
     return fwd_fn, bwd_fn

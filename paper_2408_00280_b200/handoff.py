@@ -24,7 +24,8 @@ import torch
 import torch.distributed as dist
 
 from . import _lib
-from .lif import LIFForward, LIFParams, _DTYPES, _ptr, _stream, alloc_spikes, make_shape
+from .lif import (LIFForward, LIFParams, _check_2d, _like_x, _ptr, _stream, _vec, alloc_spikes,
+                  make_shape)
 
 _cudart = None
 
@@ -178,10 +179,12 @@ def lif_forward_handoff(x: torch.Tensor, params: LIFParams, handoff, *, spike_fm
                         return_v_final: bool = True) -> LIFForward:
     """The local time segment's fused forward; the boundary V arrives / leaves through
     `handoff` inside the kernel (snn_lif_forward_handoff)."""
+    _check_2d("x", x)
     T, N = x.shape
     shape = make_shape(x, spike_fmt, save_mode)
     cp = params.to_c()
-    spikes = alloc_spikes(x, spike_fmt)
+    v_init = _vec("v_init", v_init, N, x.device)
+    spikes = alloc_spikes(x, spike_fmt, shape.ld)   # row stride ld, like x (a column view is fine)
     saved = torch.empty(_lib.snn_lif_saved_bytes(cp, shape) // 4, dtype=torch.float32, device=x.device)
     v_final = torch.empty(N, dtype=torch.float32, device=x.device) if return_v_final else None
     _lib.snn_lif_forward_handoff(cp, shape, _ptr(x), _ptr(v_init), handoff, _ptr(spikes), _ptr(saved),
@@ -193,10 +196,14 @@ def lif_backward_handoff(grad_spikes: torch.Tensor, fwd: LIFForward, handoff, *,
                          grad_v_final: Optional[torch.Tensor] = None, return_grad_v_init: bool = True):
     """The local segment's fused backward; dL/dV arrives from the later segment and the
     segment's grad_v_init leaves to the earlier one through `handoff`."""
-    T, N = fwd.x.shape
-    grad_x = torch.empty_like(fwd.x)
-    gvi = torch.empty(N, dtype=torch.float32, device=fwd.x.device) if return_grad_v_init else None
-    _lib.snn_lif_backward_handoff(fwd.params.to_c(), fwd.shape, _ptr(grad_spikes.contiguous()),
-                                  _ptr(fwd.x), _ptr(fwd.saved), _ptr(grad_v_final), handoff,
+    x = fwd.x
+    T, N = x.shape
+    ld = fwd.shape.ld
+    grad_spikes = _like_x("grad_spikes", grad_spikes, x, ld)        # every operand walks rows of stride ld
+    grad_x = torch.empty((T, ld), dtype=x.dtype, device=x.device)[:, :N]
+    grad_v_final = _vec("grad_v_final", grad_v_final, N, x.device)
+    gvi = torch.empty(N, dtype=torch.float32, device=x.device) if return_grad_v_init else None
+    _lib.snn_lif_backward_handoff(fwd.params.to_c(), fwd.shape, _ptr(grad_spikes),
+                                  _ptr(x), _ptr(fwd.saved), _ptr(grad_v_final), handoff,
                                   _ptr(grad_x), _ptr(gvi), _stream())
     return grad_x, gvi

@@ -130,8 +130,13 @@ def saved_bytes(params: LIFParams, shape: _lib.snn_lif_shape) -> int:
     return _lib.snn_lif_saved_bytes(params.to_c(), shape)
 
 
-def alloc_spikes(x: torch.Tensor, spike_fmt: str) -> torch.Tensor:
+def alloc_spikes(x: torch.Tensor, spike_fmt: str, ld: Optional[int] = None) -> torch.Tensor:
+    """Spike output for x [T, N]: u8 / io rows of stride ``ld`` (default N; the kernels walk
+    every [T, N] operand with x's row stride), bits as dense [T, ceil(N/32)] words."""
     T, N = x.shape
+    if ld is not None and ld != N and spike_fmt != "bits":
+        dt = torch.uint8 if spike_fmt == "u8" else x.dtype
+        return torch.empty((T, ld), dtype=dt, device=x.device)[:, :N]
     if spike_fmt == "u8":
         return torch.empty((T, N), dtype=torch.uint8, device=x.device)
     if spike_fmt == "bits":
@@ -157,13 +162,8 @@ def lif_forward(x: torch.Tensor, params: LIFParams = LIFParams(), *,
     shape, nbytes = _shape_entry(x, spike_fmt, save_mode)
     cp = params.to_c()
     v_init = _vec("v_init", v_init, N, x.device)
-    if spikes is None:
-        if spike_fmt != "bits" and shape.ld != N:
-            # keep the caller's ld for views: allocate [T, ld] and view its first N columns
-            spikes = torch.empty((T, shape.ld), dtype=torch.uint8 if spike_fmt == "u8" else x.dtype,
-                                 device=x.device)[:, :N]
-        else:
-            spikes = alloc_spikes(x, spike_fmt)
+    if spikes is None:   # keep the caller's ld for views: [T, ld] with its first N columns used
+        spikes = alloc_spikes(x, spike_fmt, shape.ld)
     if save_mode != "none" and saved is None:
         saved = torch.empty(nbytes // 4, dtype=torch.float32, device=x.device)
     if return_v_final and v_final is None:
@@ -289,9 +289,7 @@ def lif_forward_affine(x: torch.Tensor, params: LIFParams, affine: AffineSpec, *
         residual = _like_x("residual", residual, x, shape.ld)
     cp = params.to_c()
     v_init = _vec("v_init", v_init, N, x.device)
-    spikes = alloc_spikes(x, spike_fmt)
-    if spike_fmt != "bits" and shape.ld != N:
-        spikes = torch.empty((T, shape.ld), dtype=spikes.dtype, device=x.device)[:, :N]
+    spikes = alloc_spikes(x, spike_fmt, shape.ld)
     saved = torch.empty(_lib.snn_lif_saved_bytes(cp, shape) // 4, dtype=torch.float32, device=x.device)
     v_final = torch.empty(N, dtype=torch.float32, device=x.device) if return_v_final else None
     ca = affine.to_c(residual)
@@ -405,11 +403,7 @@ class LIFPlan:
         self.x, self.params, self.device = x, params, x.device
         self.shape, nbytes = _shape_entry(x, spike_fmt, save_mode)
         self.v_init = _vec("v_init", v_init, N, x.device)
-        if spike_fmt != "bits" and self.shape.ld != N:
-            self.spikes = torch.empty((T, self.shape.ld), dtype=torch.uint8 if spike_fmt == "u8" else x.dtype,
-                                      device=x.device)[:, :N]
-        else:
-            self.spikes = alloc_spikes(x, spike_fmt)
+        self.spikes = alloc_spikes(x, spike_fmt, self.shape.ld)
         self.saved = torch.empty(nbytes // 4, dtype=torch.float32, device=x.device) if save_mode != "none" else None
         self.v_final = torch.empty(N, dtype=torch.float32, device=x.device) if with_v_final else None
         self.grad_spikes = grad_spikes

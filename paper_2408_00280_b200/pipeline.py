@@ -35,13 +35,13 @@ class TimeSplitLIFFunction(torch.autograd.Function):
     def forward(ctx, x_local, ts: TimeSplitLIF, fwd_fn: Callable, bwd_fn: Callable):
         spikes, state, _ = ts.forward(x_local, fwd_fn)
         ctx.ts, ctx.state, ctx.bwd_fn = ts, state, bwd_fn
-        return torch.cat([s.to(x_local.dtype) for s in spikes], dim=1)
+        return spikes.to(x_local.dtype)
 
     @staticmethod
     def backward(ctx, grad_spikes):
-        gxs, _ = ctx.ts.backward(grad_spikes.contiguous(), ctx.state, ctx.bwd_fn)
+        gx, _ = ctx.ts.backward(grad_spikes.contiguous(), ctx.state, ctx.bwd_fn)
         ctx.state = None
-        return torch.cat(gxs, dim=1).to(grad_spikes.dtype), None, None, None
+        return gx.to(grad_spikes.dtype), None, None, None
 
 
 class TimeSplitLIFLayer(torch.nn.Module):

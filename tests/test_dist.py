@@ -132,8 +132,8 @@ def _tsplit_worker(rank, world, port, T, N, n_chunks, out):
     spikes, state, v_final = ts.forward(X, fwd_fn)
     gxs, gvi = ts.backward(G, state, bwd_fn)
     # gather to rank 0 for the check (host logic only)
-    S = torch.cat(spikes, dim=1).float()
-    gX = torch.cat(gxs, dim=1).float()
+    S = spikes.float()
+    gX = gxs.float()
     objs = [None] * world
     dist.all_gather_object(objs, (a, b, S.numpy(), gX.numpy(), ts.messages_sent,
                                   None if v_final is None else v_final.numpy(),

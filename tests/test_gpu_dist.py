@@ -43,7 +43,7 @@ def _worker(rank, world, port, T, N, n_chunks, dtype, out):
     # numpy (pickled by value): a torch CPU tensor put on an mp.Queue is shared through a
     # file-descriptor socket that dies with this process, racing the parent's get().
     np_ = lambda t: None if t is None else t.cpu().view(torch.int16 if t.dtype == torch.bfloat16 else t.dtype).numpy()
-    dist.all_gather_object(objs, (a, b, np_(torch.cat(spikes, 1)), np_(torch.cat(gxs, 1)),
+    dist.all_gather_object(objs, (a, b, np_(spikes), np_(gxs),
                                   np_(v_final), np_(gvi)))
     if rank == 0:
         out.put(objs)
@@ -77,6 +77,18 @@ def test_time_split_bitwise_equals_whole_axis(world, n_chunks, dtype):
     assert np.array_equal(np.concatenate([o[3] for o in objs], 0), as_np(gx))   # bitwise (int16 view for bf16)
     assert np.array_equal(objs[-1][4], as_np(f.v_final))
     assert np.array_equal(objs[0][5], as_np(gvi))
+    # ... and anchored to the oracle directly (not only to the whole-axis CUDA run): the
+    # k-rank result vs the fp64 oracle on the host-regenerated inputs.
+    from parity import oracle_check
+    to_t = lambda a: (torch.from_numpy(a).view(torch.bfloat16).float() if dtype == torch.bfloat16
+                      else torch.from_numpy(a))
+    rep = oracle_check(snn.LIFParams.paper(), snn_synth.normal_tensor(1234, T, N, dtype=dtype),
+                       snn_synth.normal_tensor(4321, T, N, dtype=dtype),
+                       torch.from_numpy(np.concatenate([o[2] for o in objs], 0)),
+                       to_t(np.concatenate([o[3] for o in objs], 0)),
+                       vf_gpu=torch.from_numpy(objs[-1][4]), gvi_gpu=torch.from_numpy(objs[0][5]),
+                       io_bf16=dtype == torch.bfloat16)
+    assert rep.ok, str(rep)
 
 
 def _pipe_worker(rank, world, path, T, out):
@@ -93,11 +105,20 @@ def _pipe_worker(rank, world, path, T, out):
         P.TimeFolded(torch.nn.Flatten()), P.TimeFolded(torch.nn.Linear(16 * 16 * 16, 10))).cuda()
     a, b = D.partition_time(T, world)[rank]
     x = snn_synth.normal_tensor(93, b - a, 4 * 2 * 16 * 16, t_offset=a, device="cuda").reshape(b - a, 4, 2, 16, 16)
+    # the LIF layer's own input / output / gradients on this rank's segment (for the oracle check)
+    seen = {}
+    lif = model[1]
+    lif.register_forward_hook(lambda m, i, o: seen.update(x=i[0].detach().reshape(b - a, -1).cpu().numpy(),
+                                                          s=o.detach().reshape(b - a, -1).cpu().numpy()))
+    lif.register_full_backward_hook(lambda m, gi, go: seen.update(gx=gi[0].detach().reshape(b - a, -1).cpu().numpy(),
+                                                                  gs=go[0].detach().reshape(b - a, -1).cpu().numpy()))
     loss = P.TimeSplitTrainer(model, T).step(x, torch.nn.functional.cross_entropy,
                                             torch.arange(4, device="cuda") % 10)
     grads = [p.grad.detach().cpu().numpy() for p in model.parameters()]
+    segs = [None] * world
+    dist.all_gather_object(segs, (a, seen["x"], seen["s"], seen["gs"], seen["gx"]))
     if rank == 0:
-        out.put((float(loss), grads))
+        out.put((float(loss), grads, sorted(segs, key=lambda q: q[0])))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -117,7 +138,7 @@ def test_conv_snn_time_split_training_step(world):
     ps = [ctx.Process(target=_pipe_worker, args=(r, world, path, T, q)) for r in range(world)]
     for pr in ps:
         pr.start()
-    loss_k, grads_k = q.get(timeout=300)
+    loss_k, grads_k, segs = q.get(timeout=300)
     for pr in ps:
         pr.join(timeout=60)
         assert pr.exitcode == 0
@@ -133,3 +154,10 @@ def test_conv_snn_time_split_training_step(world):
     assert loss_k == pytest.approx(float(loss_1), rel=1e-5)
     for gk, p in zip(grads_k, model.parameters()):
         np.testing.assert_allclose(gk, p.grad.cpu().numpy(), rtol=2e-4, atol=2e-5)
+    # The time-split LIF layer inside the k-rank training step, anchored to the oracle: on its
+    # own (conv-produced) input and incoming gradient, the spikes and dL/dX the k ranks
+    # produced together equal the fp64 oracle's whole-axis answer.
+    from parity import oracle_check
+    cat = lambda i: torch.from_numpy(np.concatenate([sg[i] for sg in segs], 0))
+    rep = oracle_check(snn.LIFParams.paper(), cat(1), cat(3), cat(2), cat(4))
+    assert rep.ok, str(rep)

@@ -18,6 +18,7 @@ import paper_2408_00280_b200 as snn  # noqa: E402
 from paper_2408_00280_b200 import dist as D  # noqa: E402
 from paper_2408_00280_b200 import handoff as HO  # noqa: E402
 import snn_synth  # noqa: E402
+from parity import oracle_check  # noqa: E402
 
 
 def _local_dirs(k, N):
@@ -74,6 +75,11 @@ def test_handoff_segments_in_one_process_bitwise(k, T, N, dtype, save_mode):
         assert torch.equal(gvi, gvi_ref)
         # flags carry the epoch for every block
         assert int(fd[1]["ready"].min()) == epoch and int(bd[0]["ready"].min()) == epoch
+    # anchored to the oracle directly: the k-segment handoff result vs the fp64 oracle
+    rep = oracle_check(p, snn_synth.normal_tensor(61, T, N, dtype=dtype), snn_synth.normal_tensor(62, T, N, dtype=dtype),
+                       torch.cat([q.spikes for q in fwds]).cpu(), torch.cat(gxs).cpu(),
+                       vf_gpu=fwds[-1].v_final.cpu(), gvi_gpu=gvi.cpu(), io_bf16=dtype == torch.bfloat16)
+    assert rep.ok, str(rep)
 
 
 def test_handoff_concurrent_streams_bitwise():
@@ -99,6 +105,10 @@ def test_handoff_concurrent_streams_bitwise():
     torch.cuda.synchronize()
     assert torch.equal(torch.cat([f0.spikes, f1.spikes]), f.spikes)
     assert torch.equal(torch.cat([g0, g1]), gx_ref) and torch.equal(gvi, gvi_ref)
+    rep = oracle_check(p, snn_synth.normal_tensor(71, T, N), snn_synth.normal_tensor(72, T, N),
+                       torch.cat([f0.spikes, f1.spikes]).cpu(), torch.cat([g0, g1]).cpu(),
+                       vf_gpu=f1.v_final.cpu(), gvi_gpu=gvi.cpu())
+    assert rep.ok, str(rep)
 
 
 def test_handoff_requires_tma_path():
@@ -168,6 +178,11 @@ def test_handoff_ipc_processes_bitwise(world):
     f = snn.lif_forward(X, p)
     gx, gvi = snn.lif_backward(G, f)
     torch.cuda.synchronize()
+    rep = oracle_check(p, snn_synth.normal_tensor(81, T, N), snn_synth.normal_tensor(82, T, N),
+                       torch.from_numpy(np.concatenate([o[2][1][0] for o in objs])),
+                       torch.from_numpy(np.concatenate([o[2][1][1] for o in objs])),
+                       vf_gpu=torch.from_numpy(objs[-1][2][1][2]), gvi_gpu=torch.from_numpy(objs[0][2][1][3]))
+    assert rep.ok, str(rep)
     for e in range(2):
         assert np.array_equal(np.concatenate([o[2][e][0] for o in objs]), f.spikes.cpu().numpy())
         assert np.array_equal(np.concatenate([o[2][e][1] for o in objs]), gx.cpu().numpy())

@@ -14,7 +14,7 @@ if not torch.cuda.is_available():
 import paper_2408_00280_b200 as snn  # noqa: E402  (raises if libsnn_lif.so is missing)
 import oracle  # noqa: E402
 import snn_synth  # noqa: E402
-from parity import compare, oracle_params, oracle_run, run_gpu_and_oracle  # noqa: E402
+from parity import compare, oracle_check, oracle_params, oracle_run, run_gpu_and_oracle  # noqa: E402
 
 LIFParams = snn.LIFParams
 PAPER = LIFParams.paper()
@@ -188,11 +188,24 @@ def test_cfg1_full_size_sampled_columns():
 
 # ------------------------------------------------------------------ fault injection
 
-def test_fault_injection_perturbed_k_fails_parity():
-    """a kernel whose k is off by 1e-3 relative must fail parity, naming
-    the first bad element -- the comparator is not vacuous."""
+def _k_perturbed(rel):
+    """Paper params with k = 1 - 1/tau scaled by (1 + rel)."""
+    k = (1.0 - 1.0 / 1.25) * (1.0 + rel)
+    return LIFParams(tau=1.0 / (1.0 - k))
+
+
+@pytest.mark.parametrize("p_bad,what", [
+    (LIFParams(tau=1.25 * (1 + 1e-3)), "tau +1e-3"),
+    (_k_perturbed(1e-4), "k +1e-4 relative"),
+    (_k_perturbed(-1e-4), "k -1e-4 relative"),
+    (LIFParams(alpha=4.0 * (1 + 1e-4)), "alpha +1e-4 relative"),
+    (LIFParams(alpha=4.0 * (1 - 1e-4)), "alpha -1e-4 relative"),
+])
+def test_fault_injection_perturbed_constants_fail_parity(p_bad, what):
+    """a kernel run with k or alpha off by 1e-4 relative (10x the 1e-5 the
+    comparator claims to resolve; the survey's fixture was 1e-3) must fail parity against the
+    oracle of the true parameters, naming the first bad element -- the comparator is not vacuous."""
     T, N = 32, 512
-    p_bad = LIFParams(tau=1.25 * (1 + 1e-3))
     X = snn_synth.normal_tensor(1234, T, N)
     G = snn_synth.normal_tensor(4321, T, N)
     fwd, gX, gvi = _run(p_bad, X.cuda(), G.cuda())
@@ -200,7 +213,12 @@ def test_fault_injection_perturbed_k_fails_parity():
     ref = oracle_run(PAPER, X, G)
     rep = compare(PAPER, ref, ref["gX"], ref["gvi"], fwd.spikes.cpu(), gX.cpu(), vf_gpu=fwd.v_final.cpu(),
                   gvi_gpu=gvi.cpu())
-    assert not rep.ok and rep.failures
+    assert not rep.ok and rep.failures, what
+    # the unperturbed run of the same inputs passes the same comparator
+    fwd, gX, gvi = _run(PAPER, X.cuda(), G.cuda())
+    torch.cuda.synchronize()
+    assert compare(PAPER, ref, ref["gX"], ref["gvi"], fwd.spikes.cpu(), gX.cpu(), vf_gpu=fwd.v_final.cpu(),
+                   gvi_gpu=gvi.cpu()).ok
 
 
 # ------------------------------------------------------------------ both kernel paths
@@ -262,6 +280,11 @@ def test_serial_baseline_equals_fused_bitwise(dtype, mode):
     ldh = (N + 15) // 16 * 16
     assert torch.equal(S, f.spikes) and torch.equal(H, f.saved.view(T, ldh)[:, :N])
     assert torch.equal(vf, f.v_final) and torch.equal(gX, g) and torch.equal(gvi, v)
+    # the serial baseline's own outputs vs the oracle (every H, spike, carry and gradient)
+    rep = oracle_check(p, snn_synth.normal_tensor(51, T, N, dtype=dtype), snn_synth.normal_tensor(52, T, N, dtype=dtype),
+                       S.cpu(), gX.cpu(), H_gpu=H.cpu(), vf_gpu=vf.cpu(), gvi_gpu=gvi.cpu(),
+                       v0=snn_synth.normal_tensor(53, 1, N)[0], io_bf16=dtype == torch.bfloat16)
+    assert_ok(rep)
 
 
 # ------------------------------------------------------------------ randomized (hypothesis)
@@ -269,7 +292,7 @@ def test_serial_baseline_equals_fused_bitwise(dtype, mode):
 from hypothesis import given, settings, strategies as st, HealthCheck  # noqa: E402
 
 
-@settings(max_examples=40, deadline=None, suppress_health_check=list(HealthCheck))
+@settings(max_examples=40, deadline=None, derandomize=True, suppress_health_check=list(HealthCheck))
 @given(T=st.integers(1, 70), N=st.integers(1, 3000), ld_pad=st.sampled_from([0, 0, 0, 1, 8]),
        dtype=st.sampled_from([torch.float32, torch.bfloat16]), mode=st.integers(0, 7),
        decay_input=st.booleans(), save_mode=st.sampled_from(["recompute", "h"]),
@@ -571,7 +594,7 @@ def test_affine_residual_carries_and_formats(spike_fmt):
     assert_ok(rep)
 
 
-@settings(max_examples=30, deadline=None, suppress_health_check=list(HealthCheck))
+@settings(max_examples=30, deadline=None, derandomize=True, suppress_health_check=list(HealthCheck))
 @given(T=st.integers(1, 50), B=st.integers(1, 3), C=st.integers(1, 5), HW=st.sampled_from([8, 16, 24, 40]),
        dtype=st.sampled_from([torch.float32, torch.bfloat16]), mode=st.integers(0, 7),
        decay_input=st.booleans(), residual=st.booleans(), spike_fmt=st.sampled_from(["u8", "bits", "io"]))

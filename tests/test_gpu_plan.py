@@ -96,7 +96,7 @@ def test_affine_plan_equals_direct_calls_bitwise(residual):
 from hypothesis import HealthCheck, given, settings, strategies as st  # noqa: E402
 
 
-@settings(max_examples=25, deadline=None, suppress_health_check=list(HealthCheck))
+@settings(max_examples=25, deadline=None, derandomize=True, suppress_health_check=list(HealthCheck))
 @given(T=st.integers(1, 40), N=st.integers(1, 3000), dtype=st.sampled_from([torch.float32, torch.bfloat16]),
        mode=st.integers(0, 7), decay_input=st.booleans(), v_reset=st.sampled_from([0.0, 0.1]),
        save_mode=st.sampled_from(["recompute", "h"]), spike_fmt=st.sampled_from(["u8", "bits", "io"]))

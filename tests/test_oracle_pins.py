@@ -42,6 +42,20 @@ def test_p1_constant_current_paper_golden():
     assert forward(PAPER, col(0.5, 4))["S"][:, 0].tolist() == g["paper_x0p5_S"]
 
 
+def test_p15_exact_ties_fire():
+    """Eq. 2's ">=": H == V_th exactly must spike (tests/golden/p15)."""
+    g = load_golden("p15_exact_ties.txt")
+    r = forward(CFG0, col(2.0, 4))
+    assert r["H"][:, 0].tolist() == g["cfg0_x2_H"] and r["S"][:, 0].tolist() == g["cfg0_x2_S"]
+    r = forward(CFG0, col(1.0, 4))
+    assert r["H"][:, 0].tolist() == g["cfg0_x1_H"] and r["S"][:, 0].tolist() == g["cfg0_x1_S"]
+    f32 = lambda v: float(np.float32(v))
+    p = OracleParams(tau=f32(1.25), v_th=f32(0.3), v_reset=0.0)   # the fp32 values a kernel gets
+    assert forward(p, col(f32(0.3), 3))["S"][:, 0].tolist() == g["paper_x0p3_S"]
+    x = np.array([[f32(0.3)], [0.0], [0.0]])
+    assert forward(p, x)["S"][:, 0].tolist() == g["paper_x0p3_then0_S"]
+
+
 @pytest.mark.parametrize("X", [1.07, 1.3, 1.61, 2.2, 3.9, 7.3])
 @pytest.mark.parametrize("tau", [1.5, 2.0, 4.0])
 def test_p1_closed_form_period_decay_input(X, tau):
