@@ -49,9 +49,14 @@ def parse():
     ap.add_argument("--sweep", action="store_true",
                     help="cfg1: also time T in {8,32,128,512} (L2 flushed before every launch)")
     ap.add_argument("--chunks", type=int, default=32, help="cfg3 neuron chunks of the wavefront")
-    ap.add_argument("--transport", choices=["handoff", "nccl"], default="handoff",
-                    help="cfg3 boundary exchange: fused in-kernel peer handoff (CUDA IPC over "
-                         "NVLink) or NCCL send/recv between per-chunk launches")
+    ap.add_argument("--transport", choices=["handoff", "nccl"], default="nccl",
+                    help="cfg3 boundary exchange: NCCL send/recv between per-chunk launches inside the "
+                         "C ABI (snn_lif_*_tsplit), or the fused in-kernel peer handoff (CUDA IPC)")
+    ap.add_argument("--tsplit-n", type=int, default=None,
+                    help="neurons of the cfg3 time-split layer (default 2^22; 2^18 with --debug-single-gpu)")
+    ap.add_argument("--tsplit-steps", type=int, default=10,
+                    help="timed steps of the N>1 tsplit sub-record (and its k=1 reference)")
+    ap.add_argument("--no-tsplit", action="store_true", help="N>1: skip the cfg3 time-split sub-record")
     ap.add_argument("--debug-single-gpu", action="store_true",
                     help="test harness only: every rank on cuda:0 with a gloo group (exercises "
                          "the multi-rank code paths on a 1-GPU box; numbers are not bench values)")
@@ -80,6 +85,8 @@ def parse():
     a = ap.parse_args()
     if a.T is None:
         a.T = 1024 if a.workload == "cfg3" else 512
+    if a.tsplit_n is None:
+        a.tsplit_n = (1 << 18) if a.debug_single_gpu else (1 << 22)
     return a
 
 
@@ -616,111 +623,174 @@ def time_serial_baselines(params, X, G, dev, flush, reps=5):
 
 # ----------------------------------------------------------------------------- cfg3 time split
 
-def run_tsplit(args):
-    """BASELINE configs[3]: N = 2^22, T = 1024, the paper's time-segment split over the
-    ranks: rank d owns partition_time(T, k)[d]; the boundary V (forward)
-    and dL/dV (backward) go to the neighbour rank with NCCL send/recv, M neuron chunks
-    form a wavefront (paper_2408_00280_b200/dist.py).  Strong scaling: the total work is
-    fixed.  Also measures T_c (one [N] fp32 boundary hop) and reports Eq. 5's mu."""
+def _debug_nccl_env(rank):
+    """--debug-single-gpu: every rank shares cuda:0, which NCCL refuses ("duplicate GPU"); a
+    distinct NCCL_HOSTID per rank makes the ranks look like separate hosts, connected through
+    the socket transport on loopback.  Test harness only (the numbers are not bench values)."""
+    os.environ.update(NCCL_HOSTID=f"snn-bench-host-{rank}", NCCL_P2P_DISABLE="1", NCCL_SHM_DISABLE="1",
+                      NCCL_IB_DISABLE="1", NCCL_NET="Socket", NCCL_SOCKET_IFNAME="lo", NCCL_NVLS_ENABLE="0")
+
+
+def _timed(step, steps, warmup, dev, world, debug, barrier=True):
+    """Max-over-ranks CUDA-event time (ms) of `steps` calls of step() after `warmup` calls."""
+    import torch
+    import torch.distributed as dist
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    if world > 1 and barrier:
+        dist.barrier()
+    st = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(steps):
+        step()
+    e1.record(st)
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1)
+    if world > 1 and barrier:
+        dist.barrier()
+        ms = max_over_ranks([ms], dev, debug)[0]
+    return ms
+
+
+def tsplit_measure(args, world, rank, dev, N, T, steps, warmup, transport="nccl", with_k1=True):
+    """BASELINE configs[3]: one LIF layer of N neurons over T steps, the paper's time-segment
+    split over the `world` ranks: rank d owns partition_time(T, k)[d] of every
+    neuron, the boundary V (forward) and dL/dV (backward) go to the neighbour rank.
+      transport "nccl":    the C ABI snn_lif_*_tsplit over an snn_comm (NCCL send / recv,
+                           args.chunks neuron chunks in a wavefront);
+      transport "handoff": the fused in-kernel peer handoff (CUDA IPC peer stores + flags).
+    Returns per-step times: T(k) over the ranks, T(1) = the whole axis on one GPU (every rank runs
+    it on its own GPU at the same time; max over ranks), the one-hop boundary time, and Eq. 5
+     evaluated with T_s = T(1) and T_c = 2 hops (forward V + backward dL/dV)."""
     import torch
     import torch.distributed as dist
     import paper_2408_00280_b200 as snn
     import snn_synth
     from paper_2408_00280_b200 import dist as D
+    params = snn.LIFParams.paper()
+    out = {"k": world, "N": N, "T": T, "transport": transport}
+    debug = args.debug_single_gpu
+    # ---- T(1): the whole time axis on one GPU (each rank, concurrently, on its own GPU)
+    if with_k1:
+        X = snn_synth.normal_tensor(1234, T, N, device=dev)
+        G = snn_synth.normal_tensor(4321, T, N, device=dev)
+        f = snn.lif_forward(X, params, return_v_final=False)
+        gx, _ = snn.lif_backward(G, f, return_grad_v_init=False)
 
+        def step1():
+            snn.lif_forward(X, params, spikes=f.spikes, saved=f.saved, return_v_final=False)
+            snn.lif_backward(G, f, grad_x=gx, return_grad_v_init=False)
+        t1 = _timed(step1, steps, warmup, dev, world, debug) / steps
+        out["T1_ms"] = t1
+        del X, G, f, gx
+        torch.cuda.empty_cache()
+    # ---- T(k): the split
+    a, b = D.partition_time(T, world)[rank]
+    X = snn_synth.normal_tensor(1234, b - a, N, t_offset=a, device=dev)
+    G = snn_synth.normal_tensor(4321, b - a, N, t_offset=a, device=dev)
+    comm = ph = None
+    if transport == "nccl":
+        comm = D.NcclComm()
+        ts = D.TimeSplitLIF(rank, world, comm, n_chunks=args.chunks, params=params,
+                            spike_fmt=args.spike_fmt, save_mode=args.save_mode)
+
+        def stepk():
+            spikes, state, _ = ts.forward(X)
+            ts.backward(G, state)
+        out["chunks"] = len(D.neuron_chunks(N, args.chunks, 512))
+        out["pipeline_efficiency"] = D.pipeline_efficiency(out["chunks"], world)
+        out["gpu_launches_per_step"] = 2 * out["chunks"]
+    else:
+        from paper_2408_00280_b200 import handoff as HO
+        ph = HO.PeerHandoff(N)
+
+        def stepk():
+            f = HO.lif_forward_handoff(X, params, ph.forward_handoff(), spike_fmt=args.spike_fmt,
+                                       save_mode=args.save_mode, return_v_final=False)
+            if debug:   # k processes time-share ONE GPU: a spinning receiver may hold it, so separate phases
+                torch.cuda.synchronize(dev)
+                dist.barrier()
+            HO.lif_backward_handoff(G, f, ph.backward_handoff(), return_grad_v_init=False)
+            if debug:
+                torch.cuda.synchronize(dev)
+                dist.barrier()
+        out["chunks"] = None
+        out["pipeline_efficiency"] = 1.0
+        out["gpu_launches_per_step"] = 2
+    with ClockSampler(dev.index) as clk:
+        tk = _timed(stepk, steps, warmup, dev, world, debug) / steps
+    out["Tk_ms"] = tk
+    out["clocks"] = clk.summary()
+    # ---- T_c: one [N] fp32 boundary hop rank 0 -> 1, median of 20 (NCCL process group)
+    hop = None
+    if world > 1 and not debug:
+        buf = torch.empty(N, dtype=torch.float32, device=dev)
+        times = []
+        st = torch.cuda.current_stream(dev)
+        for _ in range(23):
+            dist.barrier()
+            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c0.record(st)
+            if rank == 0:
+                dist.send(buf, 1)
+            elif rank == 1:
+                dist.recv(buf, 0)
+            c1.record(st)
+            torch.cuda.synchronize(dev)
+            times.append(c0.elapsed_time(c1))
+        hop = sorted(times[3:])[len(times[3:]) // 2]
+        hop = max_over_ranks([hop if rank == 1 else 0.0], dev, debug)[0]
+    out["T_c_hop_ms"] = hop
+    if with_k1:
+        out["mu_measured"] = out["T1_ms"] / tk          # T(k=1) / T(k)
+        if hop:
+            Tc = 2.0 * hop                              # forward V hop + backward dL/dV hop per step
+            out["T_c_ms"] = Tc
+            out["mu_model_eq5"] = D.speedup_mu(out["T1_ms"], Tc, world)
+            out["k_opt_eq5"] = D.optimal_k(out["T1_ms"], Tc)
+            out["Ts_over_Tc"] = out["T1_ms"] / Tc
+        out["eq5_inputs"] = "T_s = T(k=1) measured in this run; T_c = 2 one-hop [N] fp32 NCCL transfers"
+    out["neuron_steps_per_s"] = N * T / (tk / 1e3)
+    if comm is not None:
+        comm.close()
+    if ph is not None:
+        ph.close()
+    del X, G
+    torch.cuda.empty_cache()
+    return out
+
+
+def run_tsplit(args):
+    """--workload cfg3: the time-split line itself (strong scaling: the total work is fixed)."""
+    import torch
+    import torch.distributed as dist
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.debug_single_gpu:
         local = 0
+        _debug_nccl_env(rank)
     torch.cuda.set_device(local)
     if world > 1:
         init_group(args, local)
     dev = torch.device("cuda", local)
-    stream = torch.cuda.current_stream(dev)
-    params = snn.LIFParams.paper()
-    T, N = args.T, 1 << 22
-    a, b = D.partition_time(T, world)[rank]
-    X = snn_synth.normal_tensor(1234, b - a, N, t_offset=a, device=dev)
-    G = snn_synth.normal_tensor(4321, b - a, N, t_offset=a, device=dev)
-    ts = D.TimeSplitLIF(rank, world, D.NcclTransport(), n_chunks=args.chunks if world > 1 else 1)
-    fwd_fn, bwd_fn = D.lif_segment_fns(params, spike_fmt=args.spike_fmt, save_mode=args.save_mode)
-    use_handoff = world > 1 and args.transport == "handoff"
-    if use_handoff:
-        from paper_2408_00280_b200 import handoff as HO
-        ph = HO.PeerHandoff(N)
-
-    def step():
-        if use_handoff:   # one fused launch per direction; boundary moves inside the kernels
-            f = HO.lif_forward_handoff(X, params, ph.forward_handoff(), spike_fmt=args.spike_fmt,
-                                       save_mode=args.save_mode, return_v_final=False)
-            if args.debug_single_gpu:
-                # k processes time-share ONE GPU here: a spinning receiver kernel may hold
-                # the GPU while its sender's context waits, so phases are separated (on a
-                # multi-GPU box every rank owns its GPU and the dependency graph is acyclic).
-                torch.cuda.synchronize(dev)
-                dist.barrier()
-            HO.lif_backward_handoff(G, f, ph.backward_handoff(), return_grad_v_init=False)
-            if args.debug_single_gpu:
-                torch.cuda.synchronize(dev)
-                dist.barrier()
-            return
-        spikes, state, vf = ts.forward(X, fwd_fn)
-        ts.backward(G, state, bwd_fn)
-
-    for _ in range(max(3, args.warmup)):
-        step()
-    torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
-    with ClockSampler(dev.index) as clk:
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.steps):
-            step()
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-    ms = e0.elapsed_time(e1)
-    # T_c: one boundary hop of [N] fp32 (rank 0 -> 1), median of 20
-    tc_ms = None
-    if world > 1 and not args.debug_single_gpu:
-        buf = torch.empty(N, dtype=torch.float32, device=dev)
-        times = []
-        for _ in range(23):
-            dist.barrier()
-            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            c0.record(stream)
-            if rank == 0:
-                dist.send(buf, 1)
-            elif rank == 1:
-                dist.recv(buf, 0)
-            c1.record(stream)
-            torch.cuda.synchronize(dev)
-            times.append(c0.elapsed_time(c1))
-        tc_ms = sorted(times[3:])[len(times[3:]) // 2]
-        ms, tc_ms = max_over_ranks([ms, tc_ms if rank == 1 else 0.0], dev, args.debug_single_gpu)
-    value = N * T * args.steps / (ms / 1e3)
+    T, N = args.T, args.tsplit_n
+    rec = tsplit_measure(args, world, rank, dev, N, T, args.steps, max(3, args.warmup),
+                         transport=args.transport if world > 1 else "nccl", with_k1=world > 1)
     if rank == 0:
-        t_seg = ms / args.steps
-        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": max(3, args.warmup), "ms_per_step": t_seg, "higher_is_better": True,
+        ms = rec["Tk_ms"]
+        line = {"metric": METRIC, "value": N * T / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": {"workload": f"BASELINE configs[3]: N=2^22, T={T}, time-segment split k={world}",
-                           "chunks": (None if use_handoff else ts.n_chunks), "spike_fmt": args.spike_fmt,
-                           "save_mode": args.save_mode,
+                "config": {"workload": f"BASELINE configs[3]: N={N}, T={T}, time-segment split k={world}",
+                           "chunks": rec["chunks"], "spike_fmt": args.spike_fmt, "save_mode": args.save_mode,
                            "parallelism": f"time-split k={world}",
                            "l2": "no flush: per-rank inputs exceed the 126 MB L2"},
-                "tsplit": {"k": world, "T_c_ms": tc_ms,
-                           "transport": ("fused peer handoff (per-tile flags over NVLink)" if use_handoff
-                                         else f"NCCL send/recv, {ts.n_chunks} chunks"),
-                           "pipeline_efficiency": (1.0 if use_handoff else D.pipeline_efficiency(ts.n_chunks, world)),
-                           "mu_model_eq5": (D.speedup_mu(world * t_seg, tc_ms, world) if tc_ms else 1.0),
-                           "k_opt_eq5": (D.optimal_k(world * t_seg, tc_ms) if tc_ms else None)},
-                "gpu_launches": (2 if use_handoff else 2 * ts.n_chunks) * args.steps,
-                "clocks": clk.summary()}
+                "tsplit": rec, "gpu_launches": rec["gpu_launches_per_step"] * args.steps,
+                "clocks": rec["clocks"]}
         print(json.dumps(line), flush=True)
-    if use_handoff:
-        ph.close()
     if world > 1:
         dist.destroy_process_group()
 
@@ -771,6 +841,7 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.debug_single_gpu:
         local = 0
+        _debug_nccl_env(rank)
     if world > 1:
         torch.cuda.set_device(local)
         init_group(args, local)
@@ -954,6 +1025,14 @@ def run_ours(args):
                "ms_per_step": round(ems / args.e2e_steps, 3)}
         del hb
 
+    # ---- N > 1: the paper's time-segment split at k = N (BASELINE configs[3]), beside the
+    # weak neuron-shard figure above: T(k), T(k=1) in this same run, mu_measured, Eq. 5.
+    tsplit = None
+    if world > 1 and not args.no_tsplit:
+        del graph, bufs, kern
+        torch.cuda.empty_cache()
+        tsplit = tsplit_measure(args, world, rank, dev, args.tsplit_n, 1024, args.tsplit_steps, 3)
+
     sweep = None
     if args.sweep and args.workload == "cfg1" and rank == 0:
         sweep = run_sweep(args, params, dev, stream)
@@ -984,6 +1063,8 @@ def run_ours(args):
                 "dtype": "bf16" if dt0 == torch.bfloat16 else "f32", "data": "synthetic",
                 "config": cfg, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": 2 * nlaunch * args.steps, "clocks": clk.summary()}
+        if tsplit is not None:
+            line["tsplit"] = tsplit
         if sweep is not None:
             line["sweep"] = sweep
             # context only: the paper's A100 claim for the same comparison
@@ -1001,8 +1082,29 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def relaunch_under_torchrun(args):
+    """`python bench.py --gpus N` (N > 1) outside torchrun: start N ranks on this node with
+    torch.distributed.run (127.0.0.1 rendezvous, NCCL INIT lines on) and exit with its status."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    import subprocess
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     args = parse()
+    world = os.environ.get("WORLD_SIZE")
+    if args.impl == "ours" and args.gpus > 1 and world is None:
+        sys.exit(relaunch_under_torchrun(args))
+    if args.impl == "ours" and world is not None and int(world) != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args)
     elif args.workload == "cfg3":

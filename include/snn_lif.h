@@ -55,7 +55,7 @@
 extern "C" {
 #endif
 
-#define SNN_LIF_ABI_VERSION 2
+#define SNN_LIF_ABI_VERSION 3
 
 typedef enum {
     SNN_OK = 0,
@@ -64,7 +64,7 @@ typedef enum {
     SNN_ERR_MISALIGNED = 3,     /* a pointer is not aligned to its element size          */
     SNN_ERR_UNSUPPORTED = 4,    /* a valid but unimplemented combination                 */
     SNN_ERR_CUDA = 5,           /* the CUDA runtime reported an error at launch          */
-    SNN_ERR_NCCL = 6            /* reserved for the time-split transport                 */
+    SNN_ERR_NCCL = 6            /* NCCL reported an error (time split), or is unavailable */
 } snn_status;
 
 /* dtype of x, grad_spikes, grad_x (and of spikes when spike_fmt == SNN_SPK_IO).
@@ -197,6 +197,65 @@ snn_status snn_lif_backward_handoff(const snn_lif_params* params, const snn_lif_
                                     const void* grad_spikes, const void* x, const void* saved,
                                     const float* grad_v_final, const snn_lif_handoff* handoff,
                                     void* grad_x, float* grad_v_init, void* stream);
+
+/* ---- Time-segment split over NCCL (Eq. 4b
+ * "each GPU handles a time segment, and the boundary membrane state (and, in
+ * backward, the boundary dV gradient) is handed to the next rank", BASELINE north_star (3)).
+ *
+ * An snn_comm wraps an NCCL communicator whose rank order is time order: rank d owns local
+ * time steps [t_d, t_{d+1}) of every neuron of a layer (x is the [T_d, ld] segment).
+ *   snn_nccl_unique_id  writes the 128-byte ncclUniqueId (one rank calls it and ships the
+ *                       bytes to the others, e.g. over torch.distributed).
+ *   snn_comm_create     collective over the nranks processes (blocks until all joined); binds
+ *                       the CUDA device current at the call; connects the neighbour ranks in
+ *                       both directions up front.  *out = NULL on failure.
+ *   snn_comm_destroy    synchronises the comm's stream and frees everything (NULL is a no-op).
+ * NCCL is loaded at run time (the process's libnccl.so.2, else $SNN_NCCL_LIBRARY): without it
+ * these calls return SNN_ERR_NCCL and every other entry point still works.  The comm owns
+ * one CUDA stream, a few events and 16 bytes of device memory -- no layer buffers.
+ *
+ * snn_lif_forward_tsplit: the fused forward of this rank's segment, the neuron axis cut into
+ * n_chunks chunks (boundaries on multiples of 512 neurons; n_chunks is clamped to
+ * ceil(N/512)) processed in the same order on every rank, so the ranks form a wavefront
+ * (efficiency n_chunks / (n_chunks + nranks - 1)).  Per chunk: receive its V [chunk] fp32
+ * from rank-1 into v_in_ws, run the fused forward kernel from it, send the chunk's final V
+ * (v_out_ws) to rank+1.  The kernels run on `stream`; the NCCL send / recv run on the comm's
+ * stream, event-ordered against it and joined back before the call's work on `stream` ends
+ * (capturable into a CUDA graph).  Every rank passes the same params, N, ld, io_dtype,
+ * spike_fmt, save_mode and n_chunks; T may differ (the partition of the time axis).
+ *   x, spikes, saved   as snn_lif_forward over the local segment (saved: snn_lif_saved_bytes
+ *                      of this local shape)
+ *   v_in_ws  [N] fp32  rank > 0: receive buffer (required); rank 0: the layer's v_init, or NULL
+ *   v_out_ws [N] fp32  rank < nranks-1: send buffer (required); last rank: the layer's final V
+ *                      (v_final), or NULL
+ * snn_lif_backward_tsplit: the mirror image -- per chunk receive dL/dV from rank+1 into
+ * g_in_ws, run the fused backward, send grad_v_init (g_out_ws) to rank-1.
+ *   grad_spikes, x, saved, grad_x  as snn_lif_backward over the local segment
+ *   v_in_ws            ignored (the RECOMPUTE checkpoints hold each segment's V[-1]); may be NULL
+ *   g_in_ws  [N] fp32  rank < nranks-1: receive buffer (required); last rank: the layer's
+ *                      grad_v_final, or NULL (0)
+ *   g_out_ws [N] fp32  rank > 0: send buffer (required); rank 0: the layer's grad_v_init, or NULL
+ * The result is bitwise identical to one whole-axis snn_lif_forward / snn_lif_backward on one
+ * GPU (the boundary state travels in fp32, exactly the register state).
+ * With nranks = 1 both calls are the chunked single-GPU kernels.  Errors: as snn_lif_forward
+ * / snn_lif_backward (validated for the whole segment before anything is enqueued), plus
+ * SNN_ERR_INVALID_VALUE for n_chunks < 1 or > N, or a device other than the comm's;
+ * SNN_ERR_NCCL if NCCL fails (work already enqueued for earlier chunks stays enqueued). */
+#define SNN_NCCL_UNIQUE_ID_BYTES 128
+
+typedef struct snn_comm snn_comm;
+
+snn_status snn_nccl_unique_id(void* out /* SNN_NCCL_UNIQUE_ID_BYTES bytes */);
+snn_status snn_comm_create(snn_comm** out, const void* unique_id, int nranks, int rank);
+snn_status snn_comm_destroy(snn_comm* comm);
+snn_status snn_comm_info(const snn_comm* comm, int* nranks, int* rank);
+snn_status snn_lif_forward_tsplit(snn_comm* comm, const snn_lif_params* params, const snn_lif_shape* shape,
+                                  int n_chunks, const void* x, void* spikes, void* saved,
+                                  float* v_in_ws, float* v_out_ws, void* stream);
+snn_status snn_lif_backward_tsplit(snn_comm* comm, const snn_lif_params* params, const snn_lif_shape* shape,
+                                   int n_chunks, const void* grad_spikes, const void* x, const float* v_in_ws,
+                                   const void* saved, void* grad_x, float* g_in_ws, float* g_out_ws,
+                                   void* stream);
 
 /* ---- Producer fusion ("fold the preceding BN affine / residual add into
  * the LIF prologue"): a per-channel affine prologue folded into the LIF input -- the

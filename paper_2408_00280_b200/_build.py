@@ -11,6 +11,17 @@ from concurrent.futures import ThreadPoolExecutor
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
+
+
+def nccl_include() -> str:
+    """nccl.h of the NCCL torch ships (types only: the library dlopens libnccl.so.2 at run time)."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia.nccl")
+    if spec and spec.submodule_search_locations:
+        d = os.path.join(list(spec.submodule_search_locations)[0], "include")
+        if os.path.exists(os.path.join(d, "nccl.h")):
+            return d
+    return "/usr/include"
 OBJ = os.path.join(PKG, "build")
 LIB = os.path.join(PKG, "libsnn_lif.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -47,7 +58,8 @@ def _compile(src: str, verbose: bool) -> str:
     hdr_t = max(os.path.getmtime(h) for h in headers() + [__file__])
     if os.path.exists(obj) and os.path.getmtime(obj) > max(os.path.getmtime(src), hdr_t):
         return obj
-    cmd = [NVCC, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-c", "-o", obj + ".tmp", src]
+    cmd = [NVCC, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-I", nccl_include(), "-c", "-o",
+           obj + ".tmp", src]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.check_call(cmd)
@@ -66,7 +78,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         objs = list(ex.map(lambda s: _compile(s, verbose), sources()))
     tmp = LIB + f".tmp{os.getpid()}"
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs,
-           "-cudart", "shared"]
+           "-cudart", "shared", "-ldl"]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.check_call(cmd)

@@ -33,7 +33,10 @@ EXPORTED_SYMBOLS = (
     "snn_lif_backward_handoff", "snn_lif_forward_affine", "snn_lif_backward_affine",
     "snn_lif_host_workspace_bytes", "snn_lif_fwd_bwd_host", "snn_lif_plan_create", "snn_lif_plan_create_affine",
     "snn_lif_plan_forward", "snn_lif_plan_backward", "snn_lif_plan_destroy",
+    "snn_nccl_unique_id", "snn_comm_create", "snn_comm_destroy", "snn_comm_info",
+    "snn_lif_forward_tsplit", "snn_lif_backward_tsplit",
 )
+SNN_NCCL_UNIQUE_ID_BYTES = 128
 SNN_LIF_HANDOFF_BLOCK = 256
 
 
@@ -55,7 +58,7 @@ class snn_lif_affine(ctypes.Structure):
                 ("HW", ctypes.c_int64), ("residual", ctypes.c_void_p), ("grad_residual", ctypes.c_void_p)]
 
 
-ABI_VERSION = 2   # include/snn_lif.h SNN_LIF_ABI_VERSION these structs mirror
+ABI_VERSION = 3   # include/snn_lif.h SNN_LIF_ABI_VERSION these structs mirror
 
 
 class snn_lif_handoff(ctypes.Structure):
@@ -122,6 +125,19 @@ def _load() -> ctypes.CDLL:
     lib.snn_lif_plan_backward.restype = ctypes.c_int
     lib.snn_lif_plan_destroy.argtypes = [vp]
     lib.snn_lif_plan_destroy.restype = None
+    ci = ctypes.c_int
+    lib.snn_nccl_unique_id.argtypes = [vp]
+    lib.snn_nccl_unique_id.restype = ci
+    lib.snn_comm_create.argtypes = [ctypes.POINTER(ctypes.c_void_p), vp, ci, ci]
+    lib.snn_comm_create.restype = ci
+    lib.snn_comm_destroy.argtypes = [vp]
+    lib.snn_comm_destroy.restype = ci
+    lib.snn_comm_info.argtypes = [vp, ctypes.POINTER(ci), ctypes.POINTER(ci)]
+    lib.snn_comm_info.restype = ci
+    lib.snn_lif_forward_tsplit.argtypes = [vp, P, S, ci, vp, vp, vp, fp, fp, vp]
+    lib.snn_lif_forward_tsplit.restype = ci
+    lib.snn_lif_backward_tsplit.argtypes = [vp, P, S, ci, vp, vp, fp, vp, vp, fp, fp, vp]
+    lib.snn_lif_backward_tsplit.restype = ci
     return lib
 
 
@@ -233,3 +249,34 @@ def snn_lif_plan_create_affine(params, shape, x, v_init, affine, spikes, saved, 
                                          ctypes.byref(affine), spikes, saved, v_final, grad_spikes, grad_v_final,
                                          grad_x, grad_v_init, part_a, part_b, grad_scale, grad_shift))
     return h.value
+
+
+# ---- time split over NCCL (include/snn_lif.h snn_comm_* / snn_lif_*_tsplit)
+
+def snn_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(SNN_NCCL_UNIQUE_ID_BYTES)
+    check(lib.snn_nccl_unique_id(buf))
+    return buf.raw
+
+
+def snn_comm_create(unique_id: bytes, nranks: int, rank: int) -> int:
+    if len(unique_id) != SNN_NCCL_UNIQUE_ID_BYTES:
+        raise ValueError("unique_id must be 128 bytes")
+    h = ctypes.c_void_p()
+    check(lib.snn_comm_create(ctypes.byref(h), ctypes.create_string_buffer(unique_id, len(unique_id)), nranks, rank))
+    return h.value
+
+
+def snn_comm_destroy(comm) -> None:
+    check(lib.snn_comm_destroy(comm))
+
+
+def snn_lif_forward_tsplit(comm, params, shape, n_chunks, x, spikes, saved, v_in_ws, v_out_ws, stream) -> None:
+    check(lib.snn_lif_forward_tsplit(comm, ctypes.byref(params), ctypes.byref(shape), n_chunks, x, spikes, saved,
+                                     v_in_ws, v_out_ws, stream))
+
+
+def snn_lif_backward_tsplit(comm, params, shape, n_chunks, grad_spikes, x, v_in_ws, saved, grad_x, g_in_ws,
+                            g_out_ws, stream) -> None:
+    check(lib.snn_lif_backward_tsplit(comm, ctypes.byref(params), ctypes.byref(shape), n_chunks, grad_spikes, x,
+                                      v_in_ws, saved, grad_x, g_in_ws, g_out_ws, stream))

@@ -124,6 +124,25 @@ snn_status launch_pdl(Kernel k, dim3 grid, dim3 block, cudaStream_t st, const ch
     return launch_kernel(k, grid, block, 0, st, true, what, args...);
 }
 
+// ---- the validated entry points behind the C ABI (snn_lif_api.cu) --------------------
+// A launch over a neuron chunk [a, a + n) of a wider layer passes the chunk's shape and
+// pointers (x + a, spikes + a, ...) plus the whole layer's row strides of the saved state and
+// of bit-packed spike rows (the time split, comm.cu).
+struct ChunkView {
+    int64_t ldh;            // saved-state row stride (floats) of the whole layer
+    int64_t spk_words_ld;   // bit-packed spike row stride (uint32 words) of the whole layer
+};
+snn_status forward_impl(const snn_lif_params* p, const snn_lif_shape* s, const void* x,
+                        const float* v_init, const snn_lif_handoff* handoff, void* spikes, void* saved,
+                        float* v_final, void* stream, const snn_lif_affine* affine = nullptr,
+                        const ChunkView* cv = nullptr);
+snn_status backward_impl(const snn_lif_params* p, const snn_lif_shape* s, const void* grad_spikes,
+                         const void* x, const void* saved, const float* grad_v_final,
+                         const snn_lif_handoff* handoff, void* grad_x, float* grad_v_init, void* stream,
+                         const snn_lif_affine* affine = nullptr, float* part_a = nullptr,
+                         float* part_b = nullptr, const ChunkView* cv = nullptr);
+int64_t saved_row_stride(const snn_lif_shape* s);   // round_up(N, 16)
+
 // ---- launchers (one translation unit each, compiled in parallel) -------------------
 // Generic path: any alignment; `vec` selects the 128-bit vector variant.
 snn_status launch_forward_generic(const snn_lif_shape* s, const snn::FwdArgs& a, bool soft, bool vec,

@@ -77,6 +77,8 @@ struct FwdArgs {
     float* saved;         // SAVE_H: [T, ldh]; RECOMPUTE: [ceil(T/kCkpt), ldh]
     float* v_final;       // [N] or null
     int64_t T, N, ld, ldh, nwords;
+    int64_t spk_words_ld; // row stride (uint32 words) of bit-packed spikes: nwords, or the whole
+                          // layer's when this launch covers a neuron chunk of it (time split)
     LifConsts c;
     Handoff h;            // boundary V from / to the neighbour time segment (TMA path only)
     Affine af;            // input prologue (identity when af.scale == null)
@@ -228,7 +230,7 @@ template <typename IO, int SFMT>
 __device__ __forceinline__ int64_t spike_row_bytes(const FwdArgs& a) {
     if constexpr (SFMT == SPK_U8) return a.ld;
     else if constexpr (SFMT == SPK_IO) return a.ld * (int64_t)sizeof(IO);
-    else return a.nwords * 4;
+    else return a.spk_words_ld * 4;
 }
 
 // One reverse step of Eq. 3 for this thread's VEC neurons: returns gX[t] (io dtype) and

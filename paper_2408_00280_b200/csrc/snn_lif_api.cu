@@ -288,9 +288,13 @@ snn::Affine to_dev(const snn_lif_affine* af) {
     return d;
 }
 
+}  // namespace
+
+namespace snn_host {
+
 snn_status forward_impl(const snn_lif_params* p, const snn_lif_shape* s, const void* x,
                         const float* v_init, const snn_lif_handoff* handoff, void* spikes, void* saved,
-                        float* v_final, void* stream, const snn_lif_affine* affine = nullptr) {
+                        float* v_final, void* stream, const snn_lif_affine* affine, const ChunkView* cv) {
     g_err[0] = 0;
     snn_status st;
     if ((st = check_params(p)) != SNN_OK) return st;
@@ -310,6 +314,8 @@ snn_status forward_impl(const snn_lif_params* p, const snn_lif_shape* s, const v
     a.saved = s->save_mode == SNN_SAVE_NONE ? nullptr : static_cast<float*>(saved);
     a.v_final = v_final;
     a.T = s->T; a.N = s->N; a.ld = s->ld; a.ldh = saved_ld(s); a.nwords = (s->N + 31) / 32;
+    a.spk_words_ld = a.nwords;
+    if (cv) { a.ldh = cv->ldh; a.spk_words_ld = cv->spk_words_ld; }
     a.c = make_consts(p);
     const bool soft = p->reset_mode == SNN_RESET_SOFT;
     cudaStream_t cs = static_cast<cudaStream_t>(stream);
@@ -342,8 +348,8 @@ snn_status forward_impl(const snn_lif_params* p, const snn_lif_shape* s, const v
 snn_status backward_impl(const snn_lif_params* p, const snn_lif_shape* s,
                          const void* grad_spikes, const void* x, const void* saved,
                          const float* grad_v_final, const snn_lif_handoff* handoff, void* grad_x,
-                         float* grad_v_init, void* stream, const snn_lif_affine* affine = nullptr,
-                         float* part_a = nullptr, float* part_b = nullptr) {
+                         float* grad_v_init, void* stream, const snn_lif_affine* affine,
+                         float* part_a, float* part_b, const ChunkView* cv) {
     g_err[0] = 0;
     snn_status st;
     if ((st = check_params(p)) != SNN_OK) return st;
@@ -363,7 +369,7 @@ snn_status backward_impl(const snn_lif_params* p, const snn_lif_shape* s,
     snn::BwdArgs a{};
     a.gS = grad_spikes; a.x = x; a.saved = static_cast<const float*>(saved);
     a.grad_v_final = grad_v_final; a.gX = grad_x; a.grad_v_init = grad_v_init;
-    a.T = s->T; a.N = s->N; a.ld = s->ld; a.ldh = saved_ld(s);
+    a.T = s->T; a.N = s->N; a.ld = s->ld; a.ldh = cv ? cv->ldh : saved_ld(s);
     a.c = make_consts(p);
     int mode = mode_of(p);
     cudaStream_t cs = static_cast<cudaStream_t>(stream);
@@ -414,7 +420,9 @@ snn_status backward_impl(const snn_lif_params* p, const snn_lif_shape* s,
     return launch_backward_generic(s, a, mode, fast, cs);
 }
 
-}  // namespace
+int64_t saved_row_stride(const snn_lif_shape* s) { return saved_ld(s); }
+
+}  // namespace snn_host
 
 extern "C" {
 

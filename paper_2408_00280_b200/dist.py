@@ -106,6 +106,85 @@ class NcclTransport:
         return dist.irecv(t, src, group=self.group)
 
 
+class NcclComm:
+    """The C ABI's NCCL communicator (include/snn_lif.h ``snn_comm``) over the ranks of a
+    torch.distributed group; rank order is time order.  Rank 0 draws the ncclUniqueId and the
+    group broadcasts it (any backend: gloo or NCCL); every rank then joins the communicator
+    on its current CUDA device.  Used as the transport of ``TimeSplitLIF`` it runs the whole
+    segment -- chunked kernels and NCCL send/recv -- inside ``snn_lif_*_tsplit``."""
+
+    def __init__(self, group=None):
+        from . import _lib
+        self._lib = _lib
+        if dist.is_available() and dist.is_initialized():
+            self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        else:
+            self.rank, self.world = 0, 1
+        uid = [_lib.snn_nccl_unique_id() if self.rank == 0 else None]
+        if self.world > 1:
+            src = dist.get_global_rank(group, 0) if group is not None else 0
+            dist.broadcast_object_list(uid, src=src, group=group)
+        self.handle = _lib.snn_comm_create(uid[0], self.world, self.rank)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self._lib.snn_comm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def lif_forward_tsplit(comm: NcclComm, x_local: torch.Tensor, params, *, n_chunks: int = 32,
+                       spike_fmt: str = "u8", save_mode: str = "recompute",
+                       v_init: Optional[torch.Tensor] = None):
+    """This rank's time segment of one LIF layer's fused forward, boundary V through NCCL
+    (snn_lif_forward_tsplit).  x_local: [T_d, N] CUDA.  Returns a LIFForward whose v_final
+    is the layer's final V on the last rank (None elsewhere)."""
+    from . import _lib
+    from .lif import LIFForward, _check_2d, _ptr, _stream, _vec, alloc_spikes, make_shape, saved_bytes
+    _check_2d("x_local", x_local)
+    T_d, N = x_local.shape
+    shape = make_shape(x_local, spike_fmt, save_mode)
+    dev = x_local.device
+    spikes = alloc_spikes(x_local, spike_fmt, shape.ld)
+    saved = (torch.empty(saved_bytes(params, shape) // 4, dtype=torch.float32, device=dev)
+             if save_mode != "none" else None)
+    first, last = comm.rank == 0, comm.rank == comm.world - 1
+    v_in = _vec("v_init", v_init, N, dev) if first else torch.empty(N, dtype=torch.float32, device=dev)
+    v_out = torch.empty(N, dtype=torch.float32, device=dev)
+    _lib.snn_lif_forward_tsplit(comm.handle, params.to_c(), shape, int(n_chunks), _ptr(x_local), _ptr(spikes),
+                                _ptr(saved), _ptr(v_in), _ptr(v_out), _stream(dev))
+    f = LIFForward(spikes, saved, v_out if last else None, x_local, v_in if first else None, params, shape)
+    f.v_in_ws = v_in
+    return f
+
+
+def lif_backward_tsplit(comm: NcclComm, grad_local: torch.Tensor, fwd, *, n_chunks: int = 32,
+                        grad_v_final: Optional[torch.Tensor] = None, grad_x: Optional[torch.Tensor] = None):
+    """This rank's segment of the fused backward, dL/dV through NCCL (snn_lif_backward_tsplit).
+    Returns (grad_x [T_d, N], grad_v_init [N] on rank 0 / None elsewhere)."""
+    from . import _lib
+    from .lif import _like_x, _ptr, _stream, _vec
+    x = fwd.x
+    T_d, N = x.shape
+    dev = x.device
+    ld = fwd.shape.ld
+    grad_local = _like_x("grad_local", grad_local, x, ld)
+    if grad_x is None:
+        grad_x = torch.empty((T_d, ld), dtype=x.dtype, device=dev)[:, :N]
+    first, last = comm.rank == 0, comm.rank == comm.world - 1
+    g_in = _vec("grad_v_final", grad_v_final, N, dev) if last else torch.empty(N, dtype=torch.float32, device=dev)
+    g_out = torch.empty(N, dtype=torch.float32, device=dev)
+    _lib.snn_lif_backward_tsplit(comm.handle, fwd.params.to_c(), fwd.shape, int(n_chunks), _ptr(grad_local),
+                                 _ptr(x), None, _ptr(fwd.saved), _ptr(grad_x), _ptr(g_in), _ptr(g_out),
+                                 _stream(dev))
+    return grad_x, (g_out if first else None)
+
+
 class HostTransport:
     """Stages through host memory with a CPU-capable backend (gloo).  Used by the tests
     to run the protocol with several processes on one GPU or on CPU; not a hot path."""
@@ -153,12 +232,22 @@ class TimeSplitLIF:
     (k-1) per chunk per layer in total.
     """
 
-    def __init__(self, rank: int, k: int, transport, n_chunks: int = 32, align: int = 512):
+    def __init__(self, rank: int, k: int, transport, n_chunks: int = 32, align: int = 512, *,
+                 params=None, spike_fmt: str = "u8", save_mode: str = "recompute"):
+        """transport: ``NcclComm`` (the product: the C ABI runs the whole segment, chunk kernels
+        and NCCL send/recv, in snn_lif_*_tsplit; ``params`` / ``spike_fmt`` / ``save_mode`` then
+        configure it), or any object with isend / irecv (NcclTransport, HostTransport) driving the
+        per-chunk callables given to forward / backward."""
         self.rank, self.k, self.t = rank, k, transport
         self.n_chunks, self.align = n_chunks, align
+        self.params, self.spike_fmt, self.save_mode = params, spike_fmt, save_mode
         self.messages_sent = 0
 
-    def forward(self, x_local: torch.Tensor, fwd_fn: Callable, *, v_init: Optional[torch.Tensor] = None):
+    def _c_abi(self) -> bool:
+        return isinstance(self.t, NcclComm)
+
+    def forward(self, x_local: torch.Tensor, fwd_fn: Optional[Callable] = None, *,
+                v_init: Optional[torch.Tensor] = None):
         """x_local: [T_d, N] (this rank's time segment).  Returns (spikes_local [T_d, N], state,
         v_final) -- v_final is the layer's final V on the last rank, else None.
 
@@ -167,6 +256,11 @@ class TimeSplitLIF:
         buffers, no concatenation); otherwise the chunk results are concatenated."""
         T_d, N = x_local.shape
         chunks = neuron_chunks(N, self.n_chunks, self.align)
+        if self._c_abi():
+            f = lif_forward_tsplit(self.t, x_local, self.params, n_chunks=self.n_chunks, spike_fmt=self.spike_fmt,
+                                   save_mode=self.save_mode, v_init=v_init)
+            self.messages_sent += len(chunks) if self.rank + 1 < self.k else 0
+            return f.spikes, SegmentState([f], chunks), f.v_final
         dev = x_local.device
         prev, nxt = self.rank - 1, self.rank + 1
         into = getattr(fwd_fn, "writes_into", False)
@@ -196,11 +290,16 @@ class TimeSplitLIF:
             out = torch.cat(spikes, dim=1)
         return out, SegmentState(ctxs, chunks), v_final
 
-    def backward(self, g_local: torch.Tensor, state: SegmentState, bwd_fn: Callable, *,
+    def backward(self, g_local: torch.Tensor, state: SegmentState, bwd_fn: Optional[Callable] = None, *,
                  grad_v_final: Optional[torch.Tensor] = None):
         """g_local: [T_d, N] dL/dS of this segment.  Returns (grad_x [T_d, N], grad_v_init) --
         grad_v_init is the layer's dL/dV[-1] on rank 0, else None.  grad_x is allocated once
         when ``bwd_fn.writes_into`` is set (chunks write their column views)."""
+        if self._c_abi():
+            gx, gvi = lif_backward_tsplit(self.t, g_local, state.ctxs[0], n_chunks=self.n_chunks,
+                                          grad_v_final=grad_v_final)
+            self.messages_sent += len(state.chunks) if self.rank > 0 else 0
+            return gx, gvi
         dev = g_local.device
         T_d, N = g_local.shape
         prev, nxt = self.rank - 1, self.rank + 1

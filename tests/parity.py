@@ -11,19 +11,17 @@ compares:
   makes every earlier gX depend on the diverged tail) are excluded and counted.
 * potentials (H, v_final): |gpu - oracle| <= rtol |oracle| + atol, rtol = 1e-5,
   atol = 1e-5 max(1, |V_th|, |V_reset|).
-* gradients (grad_x, grad_v_init): |gpu - oracle| <= rtol * s * G[t] + 4 * sens[t]
-  (+1e-37), where G[t] = |gS[t]| delta[t] + (|a| + |b|) k G[t+1] (G[T] =
-  |grad_v_final|, dV/dH = a + b split into its terms) is the backward recursion run on
-  absolute values -- the standard running bound on the magnitude of every term that
-  enters gX[t], so the test stays relative where the result is a cancellation of larger
-  terms -- and sens[t] is the change of the oracle's gX when H is perturbed by +-2^-21
-  relative (the conditioning of Eq. 3 with respect to the fp32 rounding of H, which the
-  kernel cannot avoid).  rtol = 1e-5 (fp32 outputs) / 1e-2 (bf16 outputs).
-  "Parity" states this reading of "1e-5 relative".
+* gradients (grad_x, grad_v_init): |gpu - oracle| <= rtol * s * G[t] (+1e-37), where
+  G[t] = |gS[t]| delta[t] + (|a| + |b|) k G[t+1] (G[T] = |grad_v_final|, dV/dH = a + b
+  split into its terms) is the backward recursion run on absolute values -- the standard
+  running bound on the magnitude of every term that enters gX[t], so the test stays
+  relative where the result is a cancellation of larger terms.  rtol = 1e-5 (fp32
+  outputs) / 1e-2 (bf16 outputs).  DESIGN.md "Parity" states this reading of "1e-5
+  relative".  (Round 1 also added 4x the oracle's sensitivity to a +-2^-21 perturbation of
+  H; the whole GPU suite passed without it, so it was removed.)
 """
 from __future__ import annotations
 
-import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -33,9 +31,6 @@ import oracle
 import snn_synth
 
 TIE_EPS = 1e-5
-# Weight of the fp32-rounding sensitivity term in the gradient bound (module docstring).
-# PARITY_SENS=0 runs the comparator without it (DESIGN.md "Parity" records that A/B).
-SENS_WEIGHT = float(os.environ.get("PARITY_SENS", "4.0"))
 
 
 def oracle_params(p, smoothed=False) -> "oracle.OracleParams":
@@ -99,18 +94,7 @@ def oracle_run(params, X, G, v0=None, gvf=None):
         g = np.abs(G[t]) * terms["delta"][t] + mag[t] * carry
         bound[t] = s * g
         carry = k * g
-    # (2) sensitivity to the fp32 rounding of H (the kernel's H carries ~1-2 ulp of forward
-    #     rounding): re-run the oracle backward on H perturbed by +-2^-21 relative (kept on
-    #     the same side of V_th) and take the largest change.
-    rng = np.random.default_rng(12345)
-    sens = np.zeros((T, N)); sens_vi = np.zeros(N)
-    for _ in range(2):
-        Hp = ref["H"] * (1.0 + rng.choice([-1.0, 1.0], size=ref["H"].shape) * 2.0 ** -21)
-        Hp = np.where((Hp >= op.v_th) == S, Hp, ref["H"])
-        gXp, gvip = oracle.backward(op, G, Hp, grad_v_final=gvf)
-        sens = np.maximum(sens, np.abs(gXp - gX))
-        sens_vi = np.maximum(sens_vi, np.abs(gvip - gvi))
-    ref.update(gX=gX, gvi=gvi, gX_bound=bound, gvi_bound=carry, gX_sens=sens, gvi_sens=sens_vi)
+    ref.update(gX=gX, gvi=gvi, gX_bound=bound, gvi_bound=carry)
     return ref
 
 
@@ -172,11 +156,11 @@ def compare(params, ref_fwd, ref_gX, ref_gvi, S_gpu, gX_gpu, *, H_gpu=None, vf_g
     if gX_gpu is not None:
         g_rtol = 1e-2 if io_bf16 else 1e-5
         chk("grad_x", gX_gpu, ref_gX, 0.0,
-            g_rtol * ref_fwd["gX_bound"] + SENS_WEIGHT * ref_fwd["gX_sens"] + 1e-37,
+            g_rtol * ref_fwd["gX_bound"] + 1e-37,
             np.broadcast_to(keep[None, :], ref_gX.shape))
         if gvi_gpu is not None and ref_gvi is not None:
             chk("grad_v_init", gvi_gpu, ref_gvi, 0.0,
-                1e-5 * ref_fwd["gvi_bound"] + SENS_WEIGHT * ref_fwd["gvi_sens"] + 1e-37, keep)
+                1e-5 * ref_fwd["gvi_bound"] + 1e-37, keep)
     return rep
 
 

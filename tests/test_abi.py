@@ -35,7 +35,7 @@ def test_every_declared_symbol_is_exported(lib):
 
 
 def test_abi_version_and_status_strings(lib):
-    assert lib.lib.snn_lif_abi_version() == lib.ABI_VERSION == 2
+    assert lib.lib.snn_lif_abi_version() == lib.ABI_VERSION == 3
     assert lib.lib.snn_status_string(0) == b"SNN_OK"
     assert lib.lib.snn_status_string(3) == b"SNN_ERR_MISALIGNED"
 
@@ -111,3 +111,28 @@ def test_plan_validation_before_any_device_work(lib):
     assert lib.lib.snn_lif_plan_forward(None, None) == 2
     assert lib.lib.snn_lif_plan_backward(None, None) == 2
     lib.lib.snn_lif_plan_destroy(None)
+
+
+def test_comm_and_tsplit_validation(lib):
+    """The NCCL time-split entry points validate before touching NCCL or the device."""
+    P, S = ctypes.byref(_p(lib)), ctypes.byref(_s(lib))
+    h = ctypes.c_void_p()
+    uid = ctypes.create_string_buffer(128)
+    assert lib.lib.snn_nccl_unique_id(None) == 2
+    assert lib.lib.snn_comm_create(None, uid, 1, 0) == 2
+    assert lib.lib.snn_comm_create(ctypes.byref(h), None, 1, 0) == 2
+    assert lib.lib.snn_comm_create(ctypes.byref(h), uid, 0, 0) == 1
+    assert lib.lib.snn_comm_create(ctypes.byref(h), uid, 2, 2) == 1
+    assert lib.lib.snn_comm_create(ctypes.byref(h), uid, 2, -1) == 1
+    assert h.value is None
+    assert lib.lib.snn_comm_destroy(None) == 0
+    assert lib.lib.snn_comm_info(None, None, None) == 2
+    assert lib.lib.snn_lif_forward_tsplit(None, P, S, 1, 16, 16, 16, None, None, None) == 2
+    assert lib.lib.snn_lif_backward_tsplit(None, P, S, 1, 16, 16, None, 16, 16, None, None, None) == 2
+    assert b"comm is NULL" in lib.lib.snn_last_error_message()
+
+
+def test_nccl_unique_id_from_the_process_nccl(lib):
+    """snn_nccl_unique_id resolves NCCL at run time (no GPU needed) and returns 128 bytes."""
+    uid = lib.snn_nccl_unique_id()
+    assert len(uid) == 128 and any(uid)

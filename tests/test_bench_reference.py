@@ -32,3 +32,35 @@ def test_reference_arm_other_ranks_exit_quietly():
     out = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1", "--warmup", "3"],
                          cwd=ROOT, capture_output=True, text=True, timeout=600, env=env)
     assert out.returncode == 0 and not _lines(out.stdout)
+
+
+def test_gpus_flag_relaunches_under_torchrun(monkeypatch):
+    """`python bench.py --gpus N` (N > 1) without torchrun re-executes itself as N ranks of
+    torch.distributed.run on 127.0.0.1, forwarding every argument (the driver's N-GPU runs)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    seen = {}
+
+    def fake_call(cmd, env=None):
+        seen["cmd"], seen["env"] = cmd, env
+        return 0
+
+    import subprocess as sp
+    monkeypatch.setattr(sp, "call", fake_call)
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--steps", "7", "--warmup", "3"])
+    args = bench.parse()
+    assert bench.relaunch_under_torchrun(args) == 0
+    cmd = seen["cmd"]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"] and "--nproc-per-node=4" in cmd
+    assert cmd[cmd.index("--master-addr") + 1] == "127.0.0.1"
+    assert cmd[-6:] == ["--gpus", "4", "--steps", "7", "--warmup", "3"]
+    assert seen["env"]["NCCL_DEBUG"] == "INFO"
+    # under torchrun, a --gpus that disagrees with WORLD_SIZE is refused
+    monkeypatch.setenv("WORLD_SIZE", "2")
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4"])
+    import pytest
+    with pytest.raises(SystemExit):
+        bench.main()

@@ -43,12 +43,27 @@ def test_default_line_contract_keys():
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["gpu_launches"] == 10
 
 
-@pytest.mark.parametrize("workload,extra", [("cfg1", ["--T", "32"]), ("cfg3", ["--T", "64"])])
+@pytest.mark.parametrize("workload,extra", [("cfg1", ["--T", "32"]), ("cfg3", ["--T", "64"]),
+                                            ("cfg3", ["--T", "64", "--transport", "handoff"])])
 def test_multirank_paths_under_torchrun(workload, extra):
     d = _run(["--gpus", "2", "--workload", workload, "--steps", "2", "--warmup", "3", "--no-e2e",
               "--debug-single-gpu", *extra], nproc=2, port=29532 if workload == "cfg1" else 29533)
     assert d["n_gpus"] == 2
     assert d["scaling"] == ("weak" if workload == "cfg1" else "strong")
+    ts = d["tsplit"]
+    assert ts["k"] == 2 and ts["Tk_ms"] > 0 and ts["T1_ms"] > 0 and ts["mu_measured"] > 0
+
+
+def test_gpus_flag_self_launches_ranks():
+    """`python bench.py --gpus 2` outside torchrun starts 2 ranks itself; at N > 1 the line
+    carries the cfg3 time-split sub-record (T(k), T(1) of this run, mu_measured) beside the
+    weak neuron-shard value.  (--debug-single-gpu: both ranks on cuda:0; NCCL over loopback.)"""
+    d = _run(["--gpus", "2", "--steps", "2", "--warmup", "3", "--T", "32", "--no-e2e", "--debug-single-gpu",
+              "--tsplit-steps", "2"])
+    assert d["n_gpus"] == 2 and d["scaling"] == "weak"
+    ts = d["tsplit"]
+    assert ts["k"] == 2 and ts["transport"] == "nccl" and ts["mu_measured"] > 0
+    assert ts["chunks"] >= 1 and 0 < ts["pipeline_efficiency"] <= 1
 
 
 def test_affine_and_inference_legs():
