@@ -693,13 +693,14 @@ def tsplit_measure(args, world, rank, dev, N, T, steps, warmup, transport="nccl"
     comm = ph = None
     if transport == "nccl":
         comm = D.NcclComm()
-        ts = D.TimeSplitLIF(rank, world, comm, n_chunks=args.chunks, params=params,
+        # chunks exist for the wavefront between ranks; one rank runs the layer in one launch
+        ts = D.TimeSplitLIF(rank, world, comm, n_chunks=args.chunks if world > 1 else 1, params=params,
                             spike_fmt=args.spike_fmt, save_mode=args.save_mode)
 
         def stepk():
             spikes, state, _ = ts.forward(X)
             ts.backward(G, state)
-        out["chunks"] = len(D.neuron_chunks(N, args.chunks, 512))
+        out["chunks"] = len(D.neuron_chunks(N, ts.n_chunks, 512))
         out["pipeline_efficiency"] = D.pipeline_efficiency(out["chunks"], world)
         out["gpu_launches_per_step"] = 2 * out["chunks"]
     else:

@@ -282,6 +282,34 @@ __device__ __forceinline__ void st_stream(T* p, const Pack<T, VEC>& r) {
     }
 }
 
+// Store VEC elements at p whose address may not be aligned to the pack (rows of an odd
+// row stride or an unaligned view): the widest aligned form, else element by element.
+// `nvalid` < VEC for the ragged group at the end of the neuron range.  The alignment test is
+// uniform across a warp (its lanes' groups are consecutive whole packs of one row).
+template <typename T, int VEC>
+__device__ __forceinline__ void st_any(T* p, const Pack<T, VEC>& r, int nvalid) {
+    if (nvalid >= VEC && (reinterpret_cast<uintptr_t>(p) % sizeof(Pack<T, VEC>)) == 0) {
+        st_stream<T, VEC>(p, r);
+        return;
+    }
+    if constexpr (VEC % 2 == 0 && sizeof(T) * 2 <= 8) {
+        using H = Pack<T, 2>;
+        if (nvalid >= VEC && (reinterpret_cast<uintptr_t>(p) % sizeof(H)) == 0) {
+#pragma unroll
+            for (int i = 0; i < VEC; i += 2) {
+                H h;
+                h.v[0] = r.v[i];
+                h.v[1] = r.v[i + 1];
+                st_stream<T, 2>(p + i, h);
+            }
+            return;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < VEC; ++i)
+        if (i < nvalid) __stcs(p + i, r.v[i]);
+}
+
 // Load VEC elements at p (neuron n0 .. n0+VEC-1); `nvalid` < VEC only for the single
 // ragged group at the end of the neuron range (scalar loads, zeros beyond N).
 template <typename T, int VEC>
