@@ -1,9 +1,10 @@
-// fwd_tma_bf16.cu -- instantiates the persistent TMA forward kernels for __nv_bfloat16 io
+// fwd_tma_bf16.cu -- instantiates the persistent TMA forward kernels for __nv_bfloat16 io, aligned rows
 // (one translation unit per variant family so the library builds in parallel).
 #include "launch_tma.cuh"
 
 namespace snn_host {
-snn_status launch_forward_tma_bf16(const snn_lif_shape* s, const snn::FwdArgs& a, bool soft, cudaStream_t st) {
-    return launch_forward_tma<__nv_bfloat16>(s, a, soft, st);
+snn_status launch_forward_tma_bf16(const snn_lif_shape* s, const snn::FwdArgs& a, bool soft, bool unal, cudaStream_t st) {
+    if (unal) return launch_forward_tma_unal_bf16(s, a, soft, st);
+    return launch_forward_tma<__nv_bfloat16, false>(s, a, soft, st);
 }
 }  // namespace snn_host

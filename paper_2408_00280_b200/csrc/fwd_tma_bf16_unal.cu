@@ -1,0 +1,9 @@
+// fwd_tma_bf16_unal.cu -- the persistent TMA forward kernels for __nv_bfloat16 io rows that are not
+// 16-byte aligned (1-D tensor maps; lif_tma.cuh UNAL).
+#include "launch_tma.cuh"
+
+namespace snn_host {
+snn_status launch_forward_tma_unal_bf16(const snn_lif_shape* s, const snn::FwdArgs& a, bool soft, cudaStream_t st) {
+    return launch_forward_tma<__nv_bfloat16, true>(s, a, soft, st);
+}
+}  // namespace snn_host

@@ -25,6 +25,8 @@ int num_sms();
 // box = box_inner x box_outer elements; out-of-range elements read as zero.
 bool encode_2d(CUtensorMap* m, const void* base, size_t esz, int64_t inner, int64_t outer,
                int64_t ld, int box_inner, int box_outer);
+// 1-D tensor map over `extent` elements from `base` (16-B aligned), boxes of `box` elements.
+bool encode_1d(CUtensorMap* m, const void* base, size_t esz, int64_t extent, int box);
 bool tma_available();
 const char* encode_detail();   // why the last encode_2d on this thread failed
 
@@ -149,11 +151,16 @@ snn_status launch_forward_generic(const snn_lif_shape* s, const snn::FwdArgs& a,
                                   cudaStream_t st);
 snn_status launch_backward_generic(const snn_lif_shape* s, const snn::BwdArgs& a, int mode, bool vec,
                                    cudaStream_t st);
-// TMA path: 16-byte-aligned pointers and rows, N % tma_vec_*(io) == 0.
-snn_status launch_forward_tma_f32(const snn_lif_shape* s, const snn::FwdArgs& a, bool soft, cudaStream_t st);
-snn_status launch_forward_tma_bf16(const snn_lif_shape* s, const snn::FwdArgs& a, bool soft, cudaStream_t st);
-snn_status launch_backward_tma_f32(const snn_lif_shape* s, const snn::BwdArgs& a, int mode, cudaStream_t st);
-snn_status launch_backward_tma_bf16(const snn_lif_shape* s, const snn::BwdArgs& a, int mode, cudaStream_t st);
+// TMA path, any N; unal = the io rows are not 16-B aligned (1-D tensor maps).  The _unal
+// halves live in their own translation units (parallel build).
+snn_status launch_forward_tma_f32(const snn_lif_shape* s, const snn::FwdArgs& a, bool soft, bool unal, cudaStream_t st);
+snn_status launch_forward_tma_bf16(const snn_lif_shape* s, const snn::FwdArgs& a, bool soft, bool unal, cudaStream_t st);
+snn_status launch_backward_tma_f32(const snn_lif_shape* s, const snn::BwdArgs& a, int mode, bool unal, cudaStream_t st);
+snn_status launch_backward_tma_bf16(const snn_lif_shape* s, const snn::BwdArgs& a, int mode, bool unal, cudaStream_t st);
+snn_status launch_forward_tma_unal_f32(const snn_lif_shape* s, const snn::FwdArgs& a, bool soft, cudaStream_t st);
+snn_status launch_forward_tma_unal_bf16(const snn_lif_shape* s, const snn::FwdArgs& a, bool soft, cudaStream_t st);
+snn_status launch_backward_tma_unal_f32(const snn_lif_shape* s, const snn::BwdArgs& a, int mode, cudaStream_t st);
+snn_status launch_backward_tma_unal_bf16(const snn_lif_shape* s, const snn::BwdArgs& a, int mode, cudaStream_t st);
 int tma_vec_forward(int io_dtype);
 // part_a / part_b are scratch: the reduction overwrites some of their entries.
 snn_status launch_affine_reduce(float* part_a, float* part_b, int64_t B, int64_t C,

@@ -1,5 +1,6 @@
 // launch_tma.cuh -- host launchers of the persistent TMA kernels (lif_tma.cuh), templated
-// on the io dtype; instantiated by fwd_tma_{f32,bf16}.cu and bwd_tma_{f32,bf16}.cu.
+// on the io dtype and on UNAL (rows of the io tensors not 16-byte aligned: 1-D tensor maps);
+// instantiated by fwd_tma_{f32,bf16}[_unal].cu and bwd_tma_{f32,bf16}[_unal].cu.
 #pragma once
 
 #include "internal.h"
@@ -27,20 +28,38 @@ template <> struct TmaCfg<__nv_bfloat16> {
     static constexpr int HV = 2, HN = 512, HR = 8, HS = 4;
 };
 
-template <typename IO>
-snn_status launch_forward_tma(const snn_lif_shape* s, const snn::FwdArgs& a, bool soft,
-                              cudaStream_t st) {
+// Tensor map of an io tensor [T, ld] (first N columns) with boxes of box_inner neurons x rows:
+// 2-D when aligned; UNAL: a 1-D map over the flat storage from the pointer aligned down to
+// 16 B (*off = the elements skipped), extent up to the last element of the view.
+template <typename IO, bool UNAL>
+bool encode_io(CUtensorMap* m, const void* base, const snn_lif_shape* s, int box_inner, int rows, int* off) {
+    if constexpr (!UNAL) {
+        *off = 0;
+        return encode_2d(m, base, sizeof(IO), s->N, s->T, s->ld, box_inner, rows);
+    } else {
+        const uintptr_t p = reinterpret_cast<uintptr_t>(base);
+        const uintptr_t al = p & ~uintptr_t(15);
+        *off = (int)((p - al) / sizeof(IO));
+        const int64_t extent = *off + (s->T - 1) * s->ld + s->N;
+        return encode_1d(m, reinterpret_cast<const void*>(al), sizeof(IO), extent, box_inner);
+    }
+}
+
+template <typename IO, bool UNAL>
+snn_status launch_forward_tma(const snn_lif_shape* s, const snn::FwdArgs& a0, bool soft, cudaStream_t st) {
     using C = TmaCfg<IO>;
+    snn::FwdArgs a = a0;
     CUtensorMap tmx, tmr;
     // pro: 0 plain, 1 affine, 2 affine + residual (the residual doubles the stage, so that
     // variant has its own, shallower tile configuration).
     const bool res = a.af.residual != nullptr;
     const int bw = res ? snn::FwdTma<IO, C::FV, C::FN_RES, C::FR, C::FS_RES, 2>::BW
                        : snn::FwdTma<IO, C::FV, C::FN, C::FR, C::FS>::BW;
-    if (!encode_2d(&tmx, a.x, sizeof(IO), s->N, s->T, s->ld, bw, C::FR))
+    if (!encode_io<IO, UNAL>(&tmx, a.x, s, bw, C::FR, &a.x_off))
         return fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled failed for x%s", encode_detail());
     tmr = tmx;
-    if (res && !encode_2d(&tmr, a.af.residual, sizeof(IO), s->N, s->T, s->ld, bw, C::FR))
+    a.r_off = 0;
+    if (res && !encode_io<IO, UNAL>(&tmr, a.af.residual, s, bw, C::FR, &a.r_off))
         return fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled failed for the residual%s", encode_detail());
     auto go = [&](auto sfmt, auto save, auto sft, auto pro) {
         constexpr int P = decltype(pro)::value;
@@ -48,7 +67,7 @@ snn_status launch_forward_tma(const snn_lif_shape* s, const snn::FwdArgs& a, boo
         constexpr int NC = P == 2 ? C::FN_RES : C::FN;
         using K = snn::FwdTma<IO, C::FV, NC, C::FR, NS, P == 2 ? 2 : 1>;
         auto k = snn::lif_forward_tma_kernel<IO, C::FV, decltype(sfmt)::value, decltype(save)::value,
-                                             (bool)decltype(sft)::value, P >= 1, P == 2, NC, C::FR, NS>;
+                                             (bool)decltype(sft)::value, P >= 1, P == 2, NC, C::FR, NS, UNAL>;
         return launch_tiles(k, K::THREADS, K::SMEM, (s->N + K::W - 1) / K::W, (s->T + C::FR - 1) / C::FR,
                             st, "lif_forward_tma_kernel", tmx, tmr, a);
     };
@@ -76,18 +95,20 @@ snn_status launch_forward_tma(const snn_lif_shape* s, const snn::FwdArgs& a, boo
     }
 }
 
-template <typename IO, int MODE>
-snn_status launch_backward_tma_mode(const snn_lif_shape* s, const snn::BwdArgs& a, cudaStream_t st) {
+template <typename IO, int MODE, bool UNAL>
+snn_status launch_backward_tma_mode(const snn_lif_shape* s, const snn::BwdArgs& a0, cudaStream_t st) {
     using C = TmaCfg<IO>;
     static_assert(MODE < 32 || (MODE & 24) == 0, "P0 variants are plain-path only");
+    snn::BwdArgs a = a0;
+    a.x_off = a.g_off = a.r_off = 0;
     if constexpr (MODE < 8) {   // SAVE_H has no affine-gradient or P0 variant (host never asks)
     if (s->save_mode == SNN_SAVE_H) {
         using Cfg = snn::BwdHTma<IO, C::HV, C::HN, C::HR, C::HS>;
         CUtensorMap tmh, tmg;
         if (!encode_2d(&tmh, a.saved, 4, s->N, s->T, a.ldh, Cfg::BW, C::HR) ||
-            !encode_2d(&tmg, a.gS, sizeof(IO), s->N, s->T, s->ld, Cfg::BW, C::HR))
+            !encode_io<IO, UNAL>(&tmg, a.gS, s, Cfg::BW, C::HR, &a.g_off))
             return fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled failed (SAVE_H backward)%s", encode_detail());
-        auto k = snn::lif_backward_saveh_tma_kernel<IO, C::HV, MODE, C::HN, C::HR, C::HS>;
+        auto k = snn::lif_backward_saveh_tma_kernel<IO, C::HV, MODE, C::HN, C::HR, C::HS, UNAL>;
         return launch_tiles(k, Cfg::THREADS, Cfg::SMEM, (s->N + Cfg::W - 1) / Cfg::W,
                             (s->T + C::HR - 1) / C::HR, st, "lif_backward_saveh_tma_kernel", tmh, tmg, a);
     }
@@ -97,54 +118,53 @@ snn_status launch_backward_tma_mode(const snn_lif_shape* s, const snn::BwdArgs& 
     using Cfg = snn::BwdRecTma<IO, C::RV, C::RN, NS, RES>;
     const int64_t nch = (s->T + snn::kCkpt - 1) / snn::kCkpt;
     CUtensorMap tmx, tmg, tmck, tmr;
-    if (!encode_2d(&tmx, a.x, sizeof(IO), s->N, s->T, s->ld, Cfg::BW, snn::kCkpt) ||
-        !encode_2d(&tmg, a.gS, sizeof(IO), s->N, s->T, s->ld, Cfg::BW, snn::kCkpt) ||
+    if (!encode_io<IO, UNAL>(&tmx, a.x, s, Cfg::BW, snn::kCkpt, &a.x_off) ||
+        !encode_io<IO, UNAL>(&tmg, a.gS, s, Cfg::BW, snn::kCkpt, &a.g_off) ||
         !encode_2d(&tmck, a.saved, 4, s->N, nch, a.ldh, Cfg::BW, 1))
         return fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled failed (RECOMPUTE backward)%s", encode_detail());
     tmr = tmx;
-    if (RES && !encode_2d(&tmr, a.af.residual, sizeof(IO), s->N, s->T, s->ld, Cfg::BW, snn::kCkpt))
+    if (RES && !encode_io<IO, UNAL>(&tmr, a.af.residual, s, Cfg::BW, snn::kCkpt, &a.r_off))
         return fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled failed for the residual%s", encode_detail());
-    auto k = snn::lif_backward_recompute_tma_kernel<IO, C::RV, MODE, C::RN, NS>;
+    auto k = snn::lif_backward_recompute_tma_kernel<IO, C::RV, MODE, C::RN, NS, UNAL>;
     return launch_tiles(k, Cfg::THREADS, Cfg::SMEM, (s->N + Cfg::W - 1) / Cfg::W, nch, st,
                         "lif_backward_recompute_tma_kernel", tmx, tmg, tmck, tmr, a);
 }
 
-template <typename IO>
-snn_status launch_backward_tma(const snn_lif_shape* s, const snn::BwdArgs& a, int mode,
-                               cudaStream_t st) {
+template <typename IO, bool UNAL>
+snn_status launch_backward_tma(const snn_lif_shape* s, const snn::BwdArgs& a, int mode, cudaStream_t st) {
     switch (mode & 63) {
-        case 0: return launch_backward_tma_mode<IO, 0>(s, a, st);
-        case 1: return launch_backward_tma_mode<IO, 1>(s, a, st);
-        case 2: return launch_backward_tma_mode<IO, 2>(s, a, st);
-        case 3: return launch_backward_tma_mode<IO, 3>(s, a, st);
-        case 4: return launch_backward_tma_mode<IO, 4>(s, a, st);
-        case 5: return launch_backward_tma_mode<IO, 5>(s, a, st);
-        case 6: return launch_backward_tma_mode<IO, 6>(s, a, st);
-        case 7: return launch_backward_tma_mode<IO, 7>(s, a, st);
-        case 8: return launch_backward_tma_mode<IO, 8>(s, a, st);
-        case 9: return launch_backward_tma_mode<IO, 9>(s, a, st);
-        case 10: return launch_backward_tma_mode<IO, 10>(s, a, st);
-        case 11: return launch_backward_tma_mode<IO, 11>(s, a, st);
-        case 12: return launch_backward_tma_mode<IO, 12>(s, a, st);
-        case 13: return launch_backward_tma_mode<IO, 13>(s, a, st);
-        case 14: return launch_backward_tma_mode<IO, 14>(s, a, st);
-        case 15: return launch_backward_tma_mode<IO, 15>(s, a, st);
-        case 24: return launch_backward_tma_mode<IO, 24>(s, a, st);
-        case 25: return launch_backward_tma_mode<IO, 25>(s, a, st);
-        case 26: return launch_backward_tma_mode<IO, 26>(s, a, st);
-        case 27: return launch_backward_tma_mode<IO, 27>(s, a, st);
-        case 28: return launch_backward_tma_mode<IO, 28>(s, a, st);
-        case 29: return launch_backward_tma_mode<IO, 29>(s, a, st);
-        case 30: return launch_backward_tma_mode<IO, 30>(s, a, st);
-        case 31: return launch_backward_tma_mode<IO, 31>(s, a, st);
-        case 32: return launch_backward_tma_mode<IO, 32>(s, a, st);
-        case 33: return launch_backward_tma_mode<IO, 33>(s, a, st);
-        case 34: return launch_backward_tma_mode<IO, 34>(s, a, st);
-        case 35: return launch_backward_tma_mode<IO, 35>(s, a, st);
-        case 36: return launch_backward_tma_mode<IO, 36>(s, a, st);
-        case 37: return launch_backward_tma_mode<IO, 37>(s, a, st);
-        case 38: return launch_backward_tma_mode<IO, 38>(s, a, st);
-        case 39: return launch_backward_tma_mode<IO, 39>(s, a, st);
+        case 0: return launch_backward_tma_mode<IO, 0, UNAL>(s, a, st);
+        case 1: return launch_backward_tma_mode<IO, 1, UNAL>(s, a, st);
+        case 2: return launch_backward_tma_mode<IO, 2, UNAL>(s, a, st);
+        case 3: return launch_backward_tma_mode<IO, 3, UNAL>(s, a, st);
+        case 4: return launch_backward_tma_mode<IO, 4, UNAL>(s, a, st);
+        case 5: return launch_backward_tma_mode<IO, 5, UNAL>(s, a, st);
+        case 6: return launch_backward_tma_mode<IO, 6, UNAL>(s, a, st);
+        case 7: return launch_backward_tma_mode<IO, 7, UNAL>(s, a, st);
+        case 8: return launch_backward_tma_mode<IO, 8, UNAL>(s, a, st);
+        case 9: return launch_backward_tma_mode<IO, 9, UNAL>(s, a, st);
+        case 10: return launch_backward_tma_mode<IO, 10, UNAL>(s, a, st);
+        case 11: return launch_backward_tma_mode<IO, 11, UNAL>(s, a, st);
+        case 12: return launch_backward_tma_mode<IO, 12, UNAL>(s, a, st);
+        case 13: return launch_backward_tma_mode<IO, 13, UNAL>(s, a, st);
+        case 14: return launch_backward_tma_mode<IO, 14, UNAL>(s, a, st);
+        case 15: return launch_backward_tma_mode<IO, 15, UNAL>(s, a, st);
+        case 24: return launch_backward_tma_mode<IO, 24, UNAL>(s, a, st);
+        case 25: return launch_backward_tma_mode<IO, 25, UNAL>(s, a, st);
+        case 26: return launch_backward_tma_mode<IO, 26, UNAL>(s, a, st);
+        case 27: return launch_backward_tma_mode<IO, 27, UNAL>(s, a, st);
+        case 28: return launch_backward_tma_mode<IO, 28, UNAL>(s, a, st);
+        case 29: return launch_backward_tma_mode<IO, 29, UNAL>(s, a, st);
+        case 30: return launch_backward_tma_mode<IO, 30, UNAL>(s, a, st);
+        case 31: return launch_backward_tma_mode<IO, 31, UNAL>(s, a, st);
+        case 32: return launch_backward_tma_mode<IO, 32, UNAL>(s, a, st);
+        case 33: return launch_backward_tma_mode<IO, 33, UNAL>(s, a, st);
+        case 34: return launch_backward_tma_mode<IO, 34, UNAL>(s, a, st);
+        case 35: return launch_backward_tma_mode<IO, 35, UNAL>(s, a, st);
+        case 36: return launch_backward_tma_mode<IO, 36, UNAL>(s, a, st);
+        case 37: return launch_backward_tma_mode<IO, 37, UNAL>(s, a, st);
+        case 38: return launch_backward_tma_mode<IO, 38, UNAL>(s, a, st);
+        case 39: return launch_backward_tma_mode<IO, 39, UNAL>(s, a, st);
         default: return fail(SNN_ERR_UNSUPPORTED, "backward variant %d (residual without affine)", mode);
     }
 }

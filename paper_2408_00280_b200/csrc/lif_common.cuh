@@ -310,6 +310,17 @@ __device__ __forceinline__ void st_any(T* p, const Pack<T, VEC>& r, int nvalid) 
         if (i < nvalid) __stcs(p + i, r.v[i]);
 }
 
+// Load VEC elements at p of any alignment (zeros beyond nvalid): the pack load when p is
+// pack-aligned and the group full, else element by element.
+template <typename T, int VEC>
+__device__ __forceinline__ Pack<T, VEC> ld_any(const T* p, int nvalid) {
+    if (nvalid >= VEC && (reinterpret_cast<uintptr_t>(p) % sizeof(Pack<T, VEC>)) == 0) return ld_stream<T, VEC>(p);
+    Pack<T, VEC> r;
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) r.v[i] = (i < nvalid) ? p[i] : from_f32<T>(0.0f);
+    return r;
+}
+
 // Load VEC elements at p (neuron n0 .. n0+VEC-1); `nvalid` < VEC only for the single
 // ragged group at the end of the neuron range (scalar loads, zeros beyond N).
 template <typename T, int VEC>

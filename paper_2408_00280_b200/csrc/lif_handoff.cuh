@@ -49,29 +49,27 @@ __device__ __forceinline__ void consumers_sync() {
 
 // Tile start: the boundary state of this lane's VEC neurons from the previous rank.
 template <int VEC>
-__device__ __forceinline__ void handoff_recv(const Handoff& h, int64_t N, int64_t n0, bool valid,
+__device__ __forceinline__ void handoff_recv(const Handoff& h, int64_t N, int64_t n0, int nvalid,
                                              float (&out)[VEC]) {
     const int lane = threadIdx.x & 31;
     if (lane == 0 && n0 < N) wait_flag_ge(h.recv_ready + n0 / kHandoffBlock, h.epoch);   // warp inside one block
     __syncwarp();
-    if (valid) {
 #pragma unroll
-        for (int i = 0; i < VEC; ++i) out[i] = __ldcv(h.recv_state + n0 + i);   // bypass stale L1
-    }
+    for (int i = 0; i < VEC; ++i)
+        if (i < nvalid) out[i] = __ldcv(h.recv_state + n0 + i);   // bypass stale L1
 }
 
 // Tile end: publish this tile's carry-out to the next rank and acknowledge the receive.
 template <int VEC, int NCONS>
 __device__ __forceinline__ void handoff_send(const Handoff& h, int tile, int W, int64_t N, int64_t n0,
-                                             bool valid, const float (&val)[VEC]) {
+                                             int nvalid, const float (&val)[VEC]) {
     const int lane = threadIdx.x & 31;
     if (h.send_state != nullptr) {
         if (lane == 0 && n0 < N) wait_flag_ge(h.send_ack + n0 / kHandoffBlock, h.epoch - 1);
         __syncwarp();
-        if (valid) {
 #pragma unroll
-            for (int i = 0; i < VEC; ++i) h.send_state[n0 + i] = val[i];
-        }
+        for (int i = 0; i < VEC; ++i)
+            if (i < nvalid) h.send_state[n0 + i] = val[i];
     }
     consumers_sync<NCONS>();   // every consumer's stores (and receive loads) are done
     if (threadIdx.x == 32) {   // first consumer thread

@@ -79,6 +79,8 @@ struct FwdArgs {
     int64_t T, N, ld, ldh, nwords;
     int64_t spk_words_ld; // row stride (uint32 words) of bit-packed spikes: nwords, or the whole
                           // layer's when this launch covers a neuron chunk of it (time split)
+    int x_off, r_off;     // unaligned TMA path: element offset of x / residual from their 1-D
+                          // tensor maps' (16-byte aligned) base
     LifConsts c;
     Handoff h;            // boundary V from / to the neighbour time segment (TMA path only)
     Affine af;            // input prologue (identity when af.scale == null)
@@ -92,6 +94,7 @@ struct BwdArgs {
     void* gX;                   // [T, ld] IO
     float* grad_v_init;         // [N] or null
     int64_t T, N, ld, ldh;
+    int x_off, g_off, r_off;    // unaligned TMA path: element offsets of x / gS / residual
     LifConsts c;
     Handoff h;                  // boundary dL/dV from / to the neighbour segment (TMA path only)
     Affine af;                  // input prologue + its per-neuron gradient partials
@@ -202,7 +205,8 @@ __device__ __forceinline__ void store_spike_bits(uint32_t* row, int64_t g, unsig
 
 // Store one time row's spikes.  `row` = spikes + t*ld (U8/IO) or words + t*nwords (BITS).
 // Every lane of the warp must call this (BITS uses warp shuffles).
-template <typename IO, int VEC, int SFMT>
+// UNAL: the row may not be pack-aligned (odd row stride / unaligned view): st_any.
+template <typename IO, int VEC, int SFMT, bool UNAL = false>
 __device__ __forceinline__ void store_spikes(void* row, int64_t g, int64_t n0, unsigned bits,
                                              int nvalid, int64_t nwords) {
     bits &= (nvalid >= VEC) ? ((VEC == 32) ? kFull : ((1u << VEC) - 1u)) : ((1u << nvalid) - 1u);
@@ -211,14 +215,16 @@ __device__ __forceinline__ void store_spikes(void* row, int64_t g, int64_t n0, u
             Pack<uint8_t, VEC> sp;
 #pragma unroll
             for (int i = 0; i < VEC; ++i) sp.v[i] = (uint8_t)((bits >> i) & 1u);
-            st_group<uint8_t, VEC>(reinterpret_cast<uint8_t*>(row) + n0, sp, nvalid);
+            if constexpr (UNAL) st_any<uint8_t, VEC>(reinterpret_cast<uint8_t*>(row) + n0, sp, nvalid);
+            else st_group<uint8_t, VEC>(reinterpret_cast<uint8_t*>(row) + n0, sp, nvalid);
         }
     } else if constexpr (SFMT == SPK_IO) {
         if (nvalid > 0) {
             Pack<IO, VEC> sp;
 #pragma unroll
             for (int i = 0; i < VEC; ++i) sp.v[i] = from_f32<IO>(((bits >> i) & 1u) ? 1.0f : 0.0f);
-            st_group<IO, VEC>(reinterpret_cast<IO*>(row) + n0, sp, nvalid);
+            if constexpr (UNAL) st_any<IO, VEC>(reinterpret_cast<IO*>(row) + n0, sp, nvalid);
+            else st_group<IO, VEC>(reinterpret_cast<IO*>(row) + n0, sp, nvalid);
         }
     } else {
         store_spike_bits<VEC>(reinterpret_cast<uint32_t*>(row), g, bits, nwords);

@@ -18,7 +18,15 @@
 //    the recurrence in registers and store outputs straight to HBM with coalesced
 //    streaming stores, then release the ring slot (one mbarrier arrive per warp).
 //  * Ragged T (not a multiple of the row block) and a ragged last tile are handled by the
-//    TMA's zero fill; consumers do not store past T / N.  Host guarantees N % VEC == 0.
+//    TMA's zero fill; consumers do not store past T / N.  A ragged last VEC group (N not a
+//    multiple of VEC) stores element by element.
+//  * UNAL (unaligned) variants: a 2-D tensor map needs 16-byte row strides and a 16-byte
+//    aligned base; an odd row stride (e.g. a contiguous [T, N] with N % 4 != 0 in fp32) or an
+//    unaligned column view cannot have one.  Those tensors get a 1-D tensor map over the
+//    flat [T, ld] storage (base aligned down to 16 B, the offset folded into the
+//    coordinates): the producer issues one 1-D box per (row, 256-neuron box) -- same smem
+//    layout, same bytes, more instructions -- and consumers store with the widest aligned
+//    form per row (st_any).  Everything else is the aligned kernel.
 //
 // Smem layout of one tensor's row-block: NB boxes of [rows][BW] (BW = min(W, 256)).
 #pragma once
@@ -72,12 +80,13 @@ __device__ __forceinline__ void init_barriers(Barriers<S>* b, uint32_t consumer_
 // `depth` (1..kMaxClc) steal requests are kept in flight, so with short tiles (few ring
 // stages, e.g. T = 8) the next tiles are known before the current one is issued; with
 // long tiles depth = 1 avoids hoarding work near the end.  Each tile is `nstages` ring
-// stages; `issue(stage_ptr, tile, j, bar)` issues the TMA loads of stage j.  Ends with a
-// tile = -1 sentinel stage; every outstanding request is drained before returning (its
-// response is an async smem write) and a late success is still processed.
-template <int S, int STAGE_BYTES, typename Issue>
+// stages; `bytes(j)` is stage j's transaction byte count and `issue(stage_ptr, tile, j, bar)`
+// issues its TMA loads.  Ends with a tile = -1 sentinel stage; every outstanding request is
+// drained before returning (its response is an async smem write) and a late success is still
+// processed.
+template <int S, int STAGE_BYTES, typename Bytes, typename Issue>
 __device__ __forceinline__ void produce(unsigned char* smem, Barriers<S>* bar, int64_t nstages,
-                                        int depth, Issue issue) {
+                                        int depth, Bytes bytes, Issue issue) {
     uint32_t k = 0;
     uint32_t phases = 0;   // bit i = parity of CLC slot i (a bit set, not an array: no local memory)
     int issued = 0, consumed = 0;
@@ -89,7 +98,7 @@ __device__ __forceinline__ void produce(unsigned char* smem, Barriers<S>* bar, i
             const int s = k % S;
             mbar_wait(&bar->empty[s], ((k / S) & 1) ^ 1);
             bar->tile[s] = tile;
-            mbar_arrive_expect_tx(&bar->full[s], STAGE_BYTES);
+            mbar_arrive_expect_tx(&bar->full[s], bytes(j));
             issue(smem + s * STAGE_BYTES, tile, j, &bar->full[s]);
         }
         tile = -1;
@@ -123,6 +132,69 @@ __device__ __forceinline__ int box_off(int nt, int r) {
     return ((nt / BW) * ROWS + r) * BW + (nt % BW);
 }
 
+// Load one [NB][ROWS][BW] region (rows t0 .. t0 + rows - 1 of tile columns c0 ..) into dst.
+// UNAL = false: NB 2-D boxes (rows past T zero-filled by the TMA).  UNAL = true: one 1-D box
+// per (box, row) of the flat [T, ld] tensor whose 1-D map starts `off` elements before the
+// tensor; only the `rows` valid rows are loaded (region_bytes counts the same).
+template <typename IO, int BW, int ROWS, int NB, bool UNAL>
+__device__ __forceinline__ void load_region(unsigned char* dst, const void* tm, int64_t c0, int64_t t0, int rows,
+                                            int64_t ld, int off, uint64_t* fb, uint64_t pol) {
+    constexpr int BOX = BW * ROWS * (int)sizeof(IO);
+    if constexpr (!UNAL) {
+#pragma unroll
+        for (int b = 0; b < NB; ++b) tma_load_2d(dst + b * BOX, tm, (int)(c0 + b * BW), (int)t0, fb, pol);
+    } else {   // (one issuing thread: a rolled loop keeps its registers low)
+        int64_t row = off + t0 * ld + c0;
+#pragma unroll 1
+        for (int r = 0; r < rows; ++r, row += ld) {
+#pragma unroll
+            for (int b = 0; b < NB; ++b)
+                tma_load_1d(dst + b * BOX + r * BW * (int)sizeof(IO), tm, (int)(row + b * BW), fb, pol);
+        }
+    }
+}
+template <typename IO, int BW, int ROWS, int NB, bool UNAL>
+__device__ __forceinline__ uint32_t region_bytes(int rows) {
+    return (uint32_t)NB * BW * (UNAL ? rows : ROWS) * (uint32_t)sizeof(IO);
+}
+
+// Store a consumer's VEC outputs of one row: the plain streaming pack store on the aligned
+// path, the widest aligned form on the unaligned one; a ragged last group (nvalid < VEC)
+// element by element either way (a pack store would spill into the neighbouring columns).
+template <bool UNAL, typename T, int VEC>
+__device__ __forceinline__ void st_out(T* p, const Pack<T, VEC>& r, int nvalid) {
+    if constexpr (UNAL) {
+        st_any<T, VEC>(p, r, nvalid);
+    } else if (nvalid >= VEC) {
+        st_stream<T, VEC>(p, r);
+    } else {
+#pragma unroll
+        for (int i = 0; i < VEC; ++i)
+            if (i < nvalid) __stcs(p + i, r.v[i]);
+    }
+}
+
+// [N] fp32 vectors (carries, partials): any alignment, ragged last group.
+template <int VEC>
+__device__ __forceinline__ void load_vec(const float* p, int nvalid, float (&out)[VEC]) {
+    const Pack<float, VEC> v = ld_any<float, VEC>(p, nvalid);
+#pragma unroll
+    for (int i = 0; i < VEC; ++i)
+        if (i < nvalid) out[i] = v.v[i];
+}
+template <int VEC>
+__device__ __forceinline__ void store_vec(float* p, int nvalid, const float (&in)[VEC]) {
+    Pack<float, VEC> v;
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) v.v[i] = in[i];
+    st_any<float, VEC>(p, v, nvalid);
+}
+
+__device__ __forceinline__ int group_valid(int64_t n0, int64_t N, int vec) {
+    const int64_t r = N - n0;
+    return r <= 0 ? 0 : (r >= vec ? vec : (int)r);
+}
+
 // ------------------------------------------------------------------------------------
 // Forward.  Stage = R time rows of a W-neuron tile.  Warp 0 lane 0 = producer;
 // warps 1..NCONS/32 = consumers, each lane owning VEC neurons.
@@ -140,7 +212,8 @@ struct FwdTma {
     static_assert(W % BW == 0 && BW % VEC == 0, "tile geometry");
 };
 
-template <typename IO, int VEC, int SFMT, int SAVE, bool SOFT, bool AFF, bool RES, int NCONS, int R, int S>
+template <typename IO, int VEC, int SFMT, int SAVE, bool SOFT, bool AFF, bool RES, int NCONS, int R, int S,
+          bool UNAL>
 __global__ void __launch_bounds__(NCONS + 32)
 lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmr,
                        const FwdArgs a, const int clc_depth) {
@@ -161,15 +234,17 @@ lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_con
             tma_prefetch_desc(&tmx);
             if constexpr (RES) tma_prefetch_desc(&tmr);
             const uint64_t pol = policy_evict_first();
-            produce<S, Cfg::STAGE_BYTES>(smem, bar, nrb, clc_depth, [&](unsigned char* stg, int tile, int64_t rb, uint64_t* fb) {
-#pragma unroll
-                for (int b = 0; b < NB; ++b) {
-                    tma_load_2d(stg + b * Cfg::BOX_BYTES, &tmx, tile * W + b * BW, (int)(rb * R), fb, pol);
+            auto rows_of = [&](int64_t rb) { return (int)min((int64_t)R, T - rb * R); };
+            produce<S, Cfg::STAGE_BYTES>(
+                smem, bar, nrb, clc_depth,
+                [&](int64_t rb) { return (RES ? 2u : 1u) * region_bytes<IO, BW, R, NB, UNAL>(rows_of(rb)); },
+                [&](unsigned char* stg, int tile, int64_t rb, uint64_t* fb) {
+                    load_region<IO, BW, R, NB, UNAL>(stg, &tmx, (int64_t)tile * W, rb * R, rows_of(rb), a.ld, a.x_off,
+                                                     fb, pol);
                     if constexpr (RES)
-                        tma_load_2d(stg + Cfg::R_OFF + b * Cfg::BOX_BYTES, &tmr, tile * W + b * BW,
-                                    (int)(rb * R), fb, pol);
-                }
-            });
+                        load_region<IO, BW, R, NB, UNAL>(stg + Cfg::R_OFF, &tmr, (int64_t)tile * W, rb * R, rows_of(rb),
+                                                         a.ld, a.r_off, fb, pol);
+                });
         }
         return;
     }
@@ -188,17 +263,15 @@ lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_con
         if (tile < 0) break;
         const int64_t g = (int64_t)tile * NCONS + ct;
         const int64_t n0 = g * VEC;
-        const int nvalid = n0 < N ? VEC : 0;
+        const int nvalid = group_valid(n0, N, VEC);
         const bool tile_full = (int64_t)(tile + 1) * W <= N;   // uniform across the CTA
         float V[VEC];
 #pragma unroll
         for (int i = 0; i < VEC; ++i) V[i] = c.v_reset;
         if (a.h.recv_state != nullptr) {            // segment boundary from the previous rank
-            handoff_recv<VEC>(a.h, N, n0, nvalid > 0, V);
+            handoff_recv<VEC>(a.h, N, n0, nvalid, V);
         } else if (a.v_init != nullptr && nvalid > 0) {
-            const Pack<float, VEC> v0 = ld_stream<float, VEC>(a.v_init + n0);
-#pragma unroll
-            for (int i = 0; i < VEC; ++i) V[i] = v0.v[i];
+            load_vec<VEC>(a.v_init + n0, nvalid, V);
         }
         const AffCoef<VEC> co = load_affine<VEC, AFF>(a.af, n0, nvalid);
         unsigned char* spk_row = reinterpret_cast<unsigned char*>(a.spikes);
@@ -225,7 +298,8 @@ lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_con
                         rv = *reinterpret_cast<const Pack<IO, VEC>*>(
                             reinterpret_cast<const IO*>(smem + s * Cfg::STAGE_BYTES + Cfg::R_OFF) + xoff + r * BW);
                     if constexpr (SAVE == SAVE_RECOMPUTE) {
-                        // checkpoint the V entering step t when t % kCkpt == 0
+                        // checkpoint the V entering step t when t % kCkpt == 0 (the saved rows are
+                        // padded to 16 floats: a ragged group's pack store stays inside its row)
                         const int64_t t = rb * R + r;
                         if ((t % kCkpt) == 0 && nv > 0) {
                             Pack<float, VEC> ck;
@@ -240,7 +314,7 @@ lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_con
                         if (nv > 0) st_stream<float, VEC>(h_row, hp);
                         h_row += a.ldh;
                     }
-                    store_spikes<IO, VEC, SFMT>(spk_row, g, n0, bits, nv, a.nwords);
+                    store_spikes<IO, VEC, SFMT, UNAL>(spk_row, g, n0, bits, nv, a.nwords);
                     spk_row += spk_step;
                 }
             }
@@ -250,13 +324,8 @@ lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_con
             if (lane == 0) mbar_arrive(&bar->empty[s]);
         }
         if (a.h.send_state != nullptr || a.h.recv_ack != nullptr)   // uniform across the CTA
-            handoff_send<VEC, NCONS>(a.h, tile, W, N, n0, nvalid > 0, V);
-        if (a.v_final != nullptr && nvalid > 0) {
-            Pack<float, VEC> vf;
-#pragma unroll
-            for (int i = 0; i < VEC; ++i) vf.v[i] = V[i];
-            st_stream<float, VEC>(a.v_final + n0, vf);
-        }
+            handoff_send<VEC, NCONS>(a.h, tile, W, N, n0, nvalid, V);
+        if (a.v_final != nullptr && nvalid > 0) store_vec<VEC>(a.v_final + n0, nvalid, V);
     }
 }
 
@@ -285,10 +354,10 @@ struct BwdRecTma {
 // Reverse walk over rows [0, rows) of one chunk.  h = recomputed H; gsm = gS rows in smem;
 // gxp = gX at the chunk's LAST row, walked backwards by ldb bytes.
 // RES: grp = dL/dR at the chunk's last row, walked like gxp.
-template <typename IO, int VEC, int MODE, int BW, int ROWS_MAX>
+template <typename IO, int VEC, int MODE, int BW, int ROWS_MAX, bool UNAL>
 __device__ __forceinline__ void bwd_chunk(const LifConsts& c, float (&gV)[VEC],
                                           const float (&h)[ROWS_MAX][VEC], const IO* gsm,
-                                          IO* gxp, int64_t ldb, int rows, bool valid,
+                                          IO* gxp, int64_t ldb, int rows, int nvalid,
                                           const AffCoef<VEC>& co, const IO* xs, float* pa, float* pb,
                                           IO* grp = nullptr) {
 #pragma unroll
@@ -302,10 +371,10 @@ __device__ __forceinline__ void bwd_chunk(const LifConsts& c, float (&gV)[VEC],
             } else {
                 out = bwd_step<IO, VEC, MODE>(c, gV, h[j], gv);
             }
-            if (valid) st_stream<IO, VEC>(gxp, out);
+            if (nvalid > 0) st_out<UNAL>(gxp, out, nvalid);
             gxp = step_bytes(gxp, -ldb);
             if constexpr (Mode<MODE>::RES) {
-                if (valid) st_stream<IO, VEC>(grp, outr);
+                if (nvalid > 0) st_out<UNAL>(grp, outr, nvalid);
                 grp = step_bytes(grp, -ldb);
             }
         }
@@ -313,15 +382,16 @@ __device__ __forceinline__ void bwd_chunk(const LifConsts& c, float (&gV)[VEC],
 }
 
 // Partial chunk (rows < ROWS_MAX, or a ragged last tile): every row of the ROWS_MAX block is
-// computed unconditionally -- rows past T were zero-filled by the TMA, so their arithmetic
-// is finite and independent of the carried gV until the select -- and only the carry update
-// (a select on the uniform `act`) and the stores are conditional.  One basic block per chunk
-// lets the compiler interleave the rows' independent surrogate math, which a per-row branch
-// (the old guarded loop) serialised: T=10 cost as much as T=16.  gx0 / gr0 = row 0 of the chunk.
-template <typename IO, int VEC, int MODE, int BW, int ROWS_MAX>
+// computed unconditionally -- rows past T were zero-filled by the TMA (or hold a previous
+// stage's values on the unaligned path), so their arithmetic stays independent of the carried
+// gV until the select -- and only the carry update (a select on the uniform `act`) and the
+// stores are conditional.  One basic block per chunk lets the compiler interleave the rows'
+// independent surrogate math, which a per-row branch (the old guarded loop) serialised: T=10
+// cost as much as T=16.  gx0 / gr0 = row 0 of the chunk.
+template <typename IO, int VEC, int MODE, int BW, int ROWS_MAX, bool UNAL>
 __device__ __forceinline__ void bwd_chunk_masked(const LifConsts& c, float (&gV)[VEC],
                                                  const float (&h)[kCkpt][VEC], const IO* gsm,
-                                                 IO* gx0, int64_t ldb, int rows, bool valid,
+                                                 IO* gx0, int64_t ldb, int rows, int nvalid,
                                                  const AffCoef<VEC>& co, const IO* xs, float* pa, float* pb,
                                                  IO* gr0 = nullptr) {
 #pragma unroll
@@ -343,9 +413,9 @@ __device__ __forceinline__ void bwd_chunk_masked(const LifConsts& c, float (&gV)
             gV[i] = act ? g2[i] : gV[i];
             if constexpr (Mode<MODE>::AFF) { pa[i] = act ? pa2[i] : pa[i]; pb[i] = act ? pb2[i] : pb[i]; }
         }
-        if (act && valid) {
-            st_stream<IO, VEC>(step_bytes(gx0, j * ldb), out);
-            if constexpr (Mode<MODE>::RES) st_stream<IO, VEC>(step_bytes(gr0, j * ldb), outr);
+        if (act && nvalid > 0) {
+            st_out<UNAL>(step_bytes(gx0, j * ldb), out, nvalid);
+            if constexpr (Mode<MODE>::RES) st_out<UNAL>(step_bytes(gr0, j * ldb), outr, nvalid);
         }
     }
 }
@@ -366,7 +436,7 @@ __device__ __forceinline__ void recompute_chunk(const LifConsts& c, float (&V)[V
     }
 }
 
-template <typename IO, int VEC, int MODE, int NCONS, int S>
+template <typename IO, int VEC, int MODE, int NCONS, int S, bool UNAL>
 __global__ void __launch_bounds__(NCONS + 32)
 lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
                                   const __grid_constant__ CUtensorMap tmg,
@@ -391,18 +461,32 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
             tma_prefetch_desc(&tmx); tma_prefetch_desc(&tmg); tma_prefetch_desc(&tmck);
             if constexpr (RES) tma_prefetch_desc(&tmr);
             const uint64_t pol = policy_evict_first();
-            produce<S, Cfg::STAGE_BYTES>(smem, bar, nch, clc_depth, [&](unsigned char* stg, int tile, int64_t j, uint64_t* fb) {
-                const int ch = (int)(nch - 1 - j);
+            auto rows_of = [&](int64_t j) {
+                const int64_t ch = nch - 1 - j;
+                return (int)min((int64_t)kCkpt, T - ch * kCkpt);
+            };
+            produce<S, Cfg::STAGE_BYTES>(
+                smem, bar, nch, clc_depth,
+                [&](int64_t j) {
+                    return (uint32_t)Cfg::NIN * region_bytes<IO, BW, kCkpt, NB, UNAL>(rows_of(j)) +
+                           (uint32_t)(NB * Cfg::CK_BOX_BYTES);
+                },
+                [&](unsigned char* stg, int tile, int64_t j, uint64_t* fb) {
+                    const int64_t ch = nch - 1 - j;
+                    const int rows = rows_of(j);
+                    const int64_t c0 = (int64_t)tile * W;
 #pragma unroll
-                for (int b = 0; b < NB; ++b) {
-                    const int c0 = tile * W + b * BW;
-                    tma_load_2d(stg + Cfg::CK_OFF + b * Cfg::CK_BOX_BYTES, &tmck, c0, ch, fb, pol);
-                    tma_load_2d(stg + Cfg::X_OFF + b * Cfg::BOX_BYTES, &tmx, c0, ch * kCkpt, fb, pol);
-                    tma_load_2d(stg + Cfg::G_OFF + b * Cfg::BOX_BYTES, &tmg, c0, ch * kCkpt, fb, pol);
+                    for (int b = 0; b < NB; ++b)   // checkpoints: the saved rows are always 16-B aligned
+                        tma_load_2d(stg + Cfg::CK_OFF + b * Cfg::CK_BOX_BYTES, &tmck, (int)(c0 + b * BW), (int)ch, fb,
+                                    pol);
+                    load_region<IO, BW, kCkpt, NB, UNAL>(stg + Cfg::X_OFF, &tmx, c0, ch * kCkpt, rows, ld, a.x_off, fb,
+                                                         pol);
+                    load_region<IO, BW, kCkpt, NB, UNAL>(stg + Cfg::G_OFF, &tmg, c0, ch * kCkpt, rows, ld, a.g_off, fb,
+                                                         pol);
                     if constexpr (RES)
-                        tma_load_2d(stg + Cfg::R_OFF + b * Cfg::BOX_BYTES, &tmr, c0, ch * kCkpt, fb, pol);
-                }
-            });
+                        load_region<IO, BW, kCkpt, NB, UNAL>(stg + Cfg::R_OFF, &tmr, c0, ch * kCkpt, rows, ld, a.r_off,
+                                                             fb, pol);
+                });
         }
         return;
     }
@@ -423,9 +507,9 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
         const int tile = bar->tile[s];
         if (tile < 0) break;
         const int64_t n0 = (int64_t)tile * W + nt;
-        const bool valid = n0 < N;   // N % VEC == 0 on this path
+        const int nvalid = group_valid(n0, N, VEC);
         const bool tile_full = (int64_t)(tile + 1) * W <= N;   // uniform across the CTA
-        const AffCoef<VEC> co = load_affine<VEC, Mode<MODE>::AFF>(a.af, n0, valid ? VEC : 0);
+        const AffCoef<VEC> co = load_affine<VEC, Mode<MODE>::AFF>(a.af, n0, nvalid);
         float pa[VEC], pb[VEC];
 #pragma unroll
         for (int i = 0; i < VEC; ++i) pa[i] = pb[i] = 0.0f;
@@ -433,11 +517,9 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
 #pragma unroll
         for (int i = 0; i < VEC; ++i) gV[i] = 0.0f;
         if (a.h.recv_state != nullptr) {            // dL/dV from the later segment's rank
-            handoff_recv<VEC>(a.h, N, n0, valid, gV);
-        } else if (a.grad_v_final != nullptr && valid) {
-            const Pack<float, VEC> g0 = ld_stream<float, VEC>(a.grad_v_final + n0);
-#pragma unroll
-            for (int i = 0; i < VEC; ++i) gV[i] = g0.v[i];
+            handoff_recv<VEC>(a.h, N, n0, nvalid, gV);
+        } else if (a.grad_v_final != nullptr && nvalid > 0) {
+            load_vec<VEC>(a.grad_v_final + n0, nvalid, gV);
         }
         for (int64_t ch = nch - 1; ch >= 0; --ch, ++k) {
             if (ch < nch - 1) {
@@ -464,49 +546,41 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
             }
             if (rows == kCkpt && tile_full) {   // full chunk of a full tile: guard-free code
                 recompute_chunk<IO, VEC, MODE, BW>(c, V, h, xs, kCkpt, co, rs);
-                bwd_chunk<IO, VEC, MODE, BW, kCkpt>(c, gV, h, gsm, gxp, ldb, kCkpt, true, co, xs, pa, pb, grp);
+                bwd_chunk<IO, VEC, MODE, BW, kCkpt, UNAL>(c, gV, h, gsm, gxp, ldb, kCkpt, VEC, co, xs, pa, pb, grp);
             } else if (rows == kCkpt / 2 && tile_full) {   // half chunk (T % 16 == 8, e.g. T = 8): guard-free too
                 constexpr int HR = kCkpt / 2;
                 recompute_chunk<IO, VEC, MODE, BW, HR>(c, V, h, xs, HR, co, rs);
-                bwd_chunk<IO, VEC, MODE, BW, HR>(c, gV, reinterpret_cast<const float(&)[HR][VEC]>(h), gsm, gxp, ldb,
-                                                 HR, true, co, xs, pa, pb, grp);
+                bwd_chunk<IO, VEC, MODE, BW, HR, UNAL>(c, gV, reinterpret_cast<const float(&)[HR][VEC]>(h), gsm, gxp,
+                                                       ldb, HR, VEC, co, xs, pa, pb, grp);
             } else {                            // partial chunk or ragged tile: masked rows
                 IO* gx0 = gx + t0 * ld + n0;
                 IO* gr0 = RES ? reinterpret_cast<IO*>(a.af.grad_residual) + t0 * ld + n0 : nullptr;
                 if (rows <= kCkpt / 4) {
                     recompute_chunk<IO, VEC, MODE, BW, kCkpt / 4>(c, V, h, xs, kCkpt / 4, co, rs);
-                    bwd_chunk_masked<IO, VEC, MODE, BW, kCkpt / 4>(c, gV, h, gsm, gx0, ldb, rows, valid, co, xs,
-                                                                   pa, pb, gr0);
+                    bwd_chunk_masked<IO, VEC, MODE, BW, kCkpt / 4, UNAL>(c, gV, h, gsm, gx0, ldb, rows, nvalid, co,
+                                                                         xs, pa, pb, gr0);
                 } else if (rows <= kCkpt / 2) {
                     recompute_chunk<IO, VEC, MODE, BW, kCkpt / 2>(c, V, h, xs, kCkpt / 2, co, rs);
-                    bwd_chunk_masked<IO, VEC, MODE, BW, kCkpt / 2>(c, gV, h, gsm, gx0, ldb, rows, valid, co, xs,
-                                                                   pa, pb, gr0);
+                    bwd_chunk_masked<IO, VEC, MODE, BW, kCkpt / 2, UNAL>(c, gV, h, gsm, gx0, ldb, rows, nvalid, co,
+                                                                         xs, pa, pb, gr0);
                 } else {
                     recompute_chunk<IO, VEC, MODE, BW>(c, V, h, xs, kCkpt, co, rs);
-                    bwd_chunk_masked<IO, VEC, MODE, BW, kCkpt>(c, gV, h, gsm, gx0, ldb, rows, valid, co, xs,
-                                                               pa, pb, gr0);
+                    bwd_chunk_masked<IO, VEC, MODE, BW, kCkpt, UNAL>(c, gV, h, gsm, gx0, ldb, rows, nvalid, co, xs,
+                                                                     pa, pb, gr0);
                 }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&bar->empty[s]);
         }
         if (a.h.send_state != nullptr || a.h.recv_ack != nullptr)   // uniform across the CTA
-            handoff_send<VEC, NCONS>(a.h, tile, W, N, n0, valid, gV);
+            handoff_send<VEC, NCONS>(a.h, tile, W, N, n0, nvalid, gV);
         if constexpr (Mode<MODE>::AFF) {
-            if (valid) {
-                Pack<float, VEC> qa, qb;
-#pragma unroll
-                for (int i = 0; i < VEC; ++i) { qa.v[i] = pa[i]; qb.v[i] = pb[i]; }
-                st_stream<float, VEC>(a.af.part_a + n0, qa);
-                st_stream<float, VEC>(a.af.part_b + n0, qb);
+            if (nvalid > 0) {
+                store_vec<VEC>(a.af.part_a + n0, nvalid, pa);
+                store_vec<VEC>(a.af.part_b + n0, nvalid, pb);
             }
         }
-        if (a.grad_v_init != nullptr && valid) {
-            Pack<float, VEC> gi;
-#pragma unroll
-            for (int i = 0; i < VEC; ++i) gi.v[i] = gV[i];
-            st_stream<float, VEC>(a.grad_v_init + n0, gi);
-        }
+        if (a.grad_v_init != nullptr && nvalid > 0) store_vec<VEC>(a.grad_v_init + n0, nvalid, gV);
     }
 }
 
@@ -526,7 +600,7 @@ struct BwdHTma {
     static_assert(W % BW == 0 && BW % VEC == 0 && STAGE_BYTES % 128 == 0, "tile geometry");
 };
 
-template <typename IO, int VEC, int MODE, int NCONS, int R, int S>
+template <typename IO, int VEC, int MODE, int NCONS, int R, int S, bool UNAL>
 __global__ void __launch_bounds__(NCONS + 32)
 lif_backward_saveh_tma_kernel(const __grid_constant__ CUtensorMap tmh,
                               const __grid_constant__ CUtensorMap tmg, const BwdArgs a,
@@ -546,15 +620,22 @@ lif_backward_saveh_tma_kernel(const __grid_constant__ CUtensorMap tmh,
         if (lane == 0) {
             tma_prefetch_desc(&tmh); tma_prefetch_desc(&tmg);
             const uint64_t pol = policy_evict_first();
-            produce<S, Cfg::STAGE_BYTES>(smem, bar, nrb, clc_depth, [&](unsigned char* stg, int tile, int64_t j, uint64_t* fb) {
-                const int rb = (int)(nrb - 1 - j);
+            auto rows_of = [&](int64_t j) {
+                const int64_t rb = nrb - 1 - j;
+                return (int)min((int64_t)R, T - rb * R);
+            };
+            produce<S, Cfg::STAGE_BYTES>(
+                smem, bar, nrb, clc_depth,
+                [&](int64_t j) { return (uint32_t)(NB * Cfg::HBOX) + region_bytes<IO, BW, R, NB, UNAL>(rows_of(j)); },
+                [&](unsigned char* stg, int tile, int64_t j, uint64_t* fb) {
+                    const int64_t rb = nrb - 1 - j;
+                    const int64_t c0 = (int64_t)tile * W;
 #pragma unroll
-                for (int b = 0; b < NB; ++b) {
-                    const int c0 = tile * W + b * BW;
-                    tma_load_2d(stg + b * Cfg::HBOX, &tmh, c0, rb * R, fb, pol);
-                    tma_load_2d(stg + Cfg::G_OFF + b * Cfg::GBOX, &tmg, c0, rb * R, fb, pol);
-                }
-            });
+                    for (int b = 0; b < NB; ++b)   // H: the saved rows are always 16-B aligned
+                        tma_load_2d(stg + b * Cfg::HBOX, &tmh, (int)(c0 + b * BW), (int)(rb * R), fb, pol);
+                    load_region<IO, BW, R, NB, UNAL>(stg + Cfg::G_OFF, &tmg, c0, rb * R, rows_of(j), ld, a.g_off, fb,
+                                                     pol);
+                });
         }
         return;
     }
@@ -573,17 +654,15 @@ lif_backward_saveh_tma_kernel(const __grid_constant__ CUtensorMap tmh,
         const int tile = bar->tile[s];
         if (tile < 0) break;
         const int64_t n0 = (int64_t)tile * W + nt;
-        const bool valid = n0 < N;
+        const int nvalid = group_valid(n0, N, VEC);
         const bool tile_full = (int64_t)(tile + 1) * W <= N;   // uniform across the CTA
         float gV[VEC];
 #pragma unroll
         for (int i = 0; i < VEC; ++i) gV[i] = 0.0f;
         if (a.h.recv_state != nullptr) {            // dL/dV from the later segment's rank
-            handoff_recv<VEC>(a.h, N, n0, valid, gV);
-        } else if (a.grad_v_final != nullptr && valid) {
-            const Pack<float, VEC> g0 = ld_stream<float, VEC>(a.grad_v_final + n0);
-#pragma unroll
-            for (int i = 0; i < VEC; ++i) gV[i] = g0.v[i];
+            handoff_recv<VEC>(a.h, N, n0, nvalid, gV);
+        } else if (a.grad_v_final != nullptr && nvalid > 0) {
+            load_vec<VEC>(a.grad_v_final + n0, nvalid, gV);
         }
         for (int64_t rb = nrb - 1; rb >= 0; --rb, ++k) {
             if (rb < nrb - 1) {
@@ -596,13 +675,14 @@ lif_backward_saveh_tma_kernel(const __grid_constant__ CUtensorMap tmh,
             const IO* gsm = reinterpret_cast<const IO*>(stg + Cfg::G_OFF) + roff;
             IO* gxp = gx + (rb * R + rows - 1) * ld + n0;
             auto walk = [&](auto full) {
+                constexpr bool F = decltype(full)::value;
 #pragma unroll
                 for (int r = R - 1; r >= 0; --r) {
-                    if (decltype(full)::value || r < rows) {
+                    if (F || r < rows) {
                         const Pack<float, VEC> hv = *reinterpret_cast<const Pack<float, VEC>*>(hs + r * BW);
                         const Pack<IO, VEC> gv = *reinterpret_cast<const Pack<IO, VEC>*>(gsm + r * BW);
                         const Pack<IO, VEC> out = bwd_step<IO, VEC, MODE>(c, gV, hv.v, gv);
-                        if (decltype(full)::value || valid) st_stream<IO, VEC>(gxp, out);
+                        if (F || nvalid > 0) st_out<UNAL>(gxp, out, F ? VEC : nvalid);
                         gxp = step_bytes(gxp, -ldb);
                     }
                 }
@@ -613,13 +693,8 @@ lif_backward_saveh_tma_kernel(const __grid_constant__ CUtensorMap tmh,
             if (lane == 0) mbar_arrive(&bar->empty[s]);
         }
         if (a.h.send_state != nullptr || a.h.recv_ack != nullptr)   // uniform across the CTA
-            handoff_send<VEC, NCONS>(a.h, tile, W, N, n0, valid, gV);
-        if (a.grad_v_init != nullptr && valid) {
-            Pack<float, VEC> gi;
-#pragma unroll
-            for (int i = 0; i < VEC; ++i) gi.v[i] = gV[i];
-            st_stream<float, VEC>(a.grad_v_init + n0, gi);
-        }
+            handoff_send<VEC, NCONS>(a.h, tile, W, N, n0, nvalid, gV);
+        if (a.grad_v_init != nullptr && nvalid > 0) store_vec<VEC>(a.grad_v_init + n0, nvalid, gV);
     }
 }
 

@@ -115,6 +115,29 @@ bool encode_2d(CUtensorMap* m, const void* base, size_t esz, int64_t inner, int6
     return r == CUDA_SUCCESS;
 }
 
+bool encode_1d(CUtensorMap* m, const void* base, size_t esz, int64_t extent, int box) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return false;
+    const CUtensorMapDataType dt = esz == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                            : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+    const cuuint64_t dims[1] = {(cuuint64_t)extent};
+    const cuuint32_t boxd[1] = {(cuuint32_t)box};
+    const cuuint32_t estr[1] = {1};
+    auto encode = [&] {
+        return fn(m, dt, 1, const_cast<void*>(base), dims, nullptr, boxd, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    };
+    CUresult r = encode();
+    if (r == CUDA_ERROR_INVALID_CONTEXT) {
+        cudaFree(nullptr);
+        r = encode();
+    }
+    if (r != CUDA_SUCCESS)
+        snprintf(g_enc, sizeof(g_enc), " [CUresult %d: 1-D base %p extent %lld box %d]", (int)r, base,
+                 (long long)extent, box);
+    return r == CUDA_SUCCESS;
+}
+
 const char* encode_detail() { return g_enc; }
 
 int cached_occupancy(const void* k, int threads, int smem, int (*prep)(const void*, int, int)) {
@@ -209,18 +232,24 @@ int64_t saved_rows(const snn_lif_shape* s) {
     return 0;
 }
 
-// TMA path: 16-byte-aligned base pointers, rows a multiple of 16 B (tensor-map strides),
-// N a multiple of the kernel's lane group, int32 coordinates.  SNN_LIF_NO_TMA=1 forces the
-// generic kernels (used by tests to cover both paths).
-bool tma_ok(const snn_lif_shape* s, int vec, std::initializer_list<const void*> ptrs) {
+// Which kernel family runs (SNN_LIF_NO_TMA=1 forces the generic kernels: tests cover both).
+// The TMA kernels take every shape: rows of the io tensors ([T, ld]: x, grad_spikes, grad_x,
+// spikes, residual) that are 16-B aligned with a 16-B row stride get 2-D tensor maps (ALIGNED);
+// otherwise (odd ld, an unaligned column view) 1-D maps over the flat storage (UNALIGNED), whose
+// int32 element coordinates bound T*ld.  [N] vectors and the saved state need no alignment
+// beyond their element (saved: 16 B, validated).
+enum class Path { GENERIC, ALIGNED, UNALIGNED };
+Path tma_path(const snn_lif_shape* s, std::initializer_list<const void*> rows) {
     const char* e = std::getenv("SNN_LIF_NO_TMA");
-    if ((e && e[0] == '1') || !tma_available()) return false;
+    if ((e && e[0] == '1') || !tma_available()) return Path::GENERIC;
+    if (s->N > INT32_MAX || s->T > INT32_MAX) return Path::GENERIC;
     const int64_t q = 16 / (int64_t)io_size(s->io_dtype);
-    if (s->ld % q != 0 || s->N % vec != 0) return false;
-    if (s->N > INT32_MAX || s->T > INT32_MAX) return false;
-    for (const void* p : ptrs)
-        if (p && !aligned(p, 16)) return false;
-    return true;
+    bool al = s->ld % q == 0;
+    for (const void* p : rows)
+        if (p && !aligned(p, 16)) al = false;
+    if (al) return Path::ALIGNED;
+    if (s->T > (INT32_MAX - 16) / s->ld) return Path::GENERIC;   // 1-D coordinates are int32
+    return Path::UNALIGNED;
 }
 
 }  // namespace
@@ -331,13 +360,16 @@ snn_status forward_impl(const snn_lif_params* p, const snn_lif_shape* s, const v
             return fail(SNN_ERR_UNSUPPORTED, "the residual prologue needs save_mode SAVE_RECOMPUTE or SAVE_NONE");
     }
 
-    if (tma_ok(s, tma_vec_forward(s->io_dtype), {x, v_init, v_final, a.saved, spikes, res}))
-        return s->io_dtype == SNN_BF16 ? launch_forward_tma_bf16(s, a, soft, cs)
-                                       : launch_forward_tma_f32(s, a, soft, cs);
+    const Path path = tma_path(s, {x, s->spike_fmt == SNN_SPK_BITS ? nullptr : spikes, res});
+    if (path != Path::GENERIC)
+        return s->io_dtype == SNN_BF16 ? launch_forward_tma_bf16(s, a, soft, path == Path::UNALIGNED, cs)
+                                       : launch_forward_tma_f32(s, a, soft, path == Path::UNALIGNED, cs);
     if (res)
-        return fail(SNN_ERR_UNSUPPORTED, "the residual prologue needs the TMA path (16-B aligned rows, "
-                                         "N a multiple of %d)", tma_vec_forward(s->io_dtype));
-    if (handoff) return fail(SNN_ERR_UNSUPPORTED, "the fused handoff needs the TMA path (aligned rows)");
+        return fail(SNN_ERR_UNSUPPORTED, "the residual prologue runs on the TMA kernels only (SNN_LIF_NO_TMA "
+                                         "is set, or T*ld exceeds int32 coordinates with unaligned rows)");
+    if (handoff)
+        return fail(SNN_ERR_UNSUPPORTED, "the fused handoff runs on the TMA kernels only (SNN_LIF_NO_TMA is "
+                                         "set, or T*ld exceeds int32 coordinates with unaligned rows)");
     const int vec = 4;   // bf16 and fp32: 4 neurons per thread (bf16 x 8 measured 5% slower, fp32 x 2 2x slower)
     bool fast = (s->ld % vec) == 0 && aligned(x, 16) && (!v_init || aligned(v_init, 16)) &&
                 (!v_final || aligned(v_final, 16));
@@ -398,20 +430,21 @@ snn_status backward_impl(const snn_lif_params* p, const snn_lif_shape* s,
     const void* res = (mode & 16) ? affine->residual : nullptr;
     void* gres = (mode & 16) ? affine->grad_residual : nullptr;
 
-    if (tma_ok(s, tma_vec_backward(s->io_dtype),
-               {grad_spikes, grad_x, s->save_mode == SNN_SAVE_RECOMPUTE ? x : nullptr, saved,
-                grad_v_final, grad_v_init, res, gres})) {
+    const Path path = tma_path(s, {grad_spikes, grad_x, s->save_mode == SNN_SAVE_RECOMPUTE ? x : nullptr, res, gres});
+    if (path != Path::GENERIC) {
         // paper-mode constants on the plain RECOMPUTE path: the P0 variants (lif_common.cuh
         // Mode::P0; the SAVE_H kernel has no P0 instantiation)
         const int tmode = (mode < 8 && s->save_mode == SNN_SAVE_RECOMPUTE && !p->decay_input &&
                            p->v_reset == 0.0f) ? (mode | 32) : mode;
-        return s->io_dtype == SNN_BF16 ? launch_backward_tma_bf16(s, a, tmode, cs)
-                                       : launch_backward_tma_f32(s, a, tmode, cs);
+        return s->io_dtype == SNN_BF16 ? launch_backward_tma_bf16(s, a, tmode, path == Path::UNALIGNED, cs)
+                                       : launch_backward_tma_f32(s, a, tmode, path == Path::UNALIGNED, cs);
     }
     if (res)
-        return fail(SNN_ERR_UNSUPPORTED, "the residual prologue needs the TMA path (16-B aligned rows, "
-                                         "N a multiple of %d)", tma_vec_backward(s->io_dtype));
-    if (handoff) return fail(SNN_ERR_UNSUPPORTED, "the fused handoff needs the TMA path (aligned rows)");
+        return fail(SNN_ERR_UNSUPPORTED, "the residual prologue runs on the TMA kernels only (SNN_LIF_NO_TMA "
+                                         "is set, or T*ld exceeds int32 coordinates with unaligned rows)");
+    if (handoff)
+        return fail(SNN_ERR_UNSUPPORTED, "the fused handoff runs on the TMA kernels only (SNN_LIF_NO_TMA is "
+                                         "set, or T*ld exceeds int32 coordinates with unaligned rows)");
     const int vec = 2;   // bf16 and fp32: 2 neurons per thread (bf16 x 4 held too many registers)
     const bool fast = (s->ld % vec) == 0 && aligned(grad_spikes, 16) && aligned(grad_x, 16) &&
                       (!x || s->save_mode != SNN_SAVE_RECOMPUTE || aligned(x, 16)) &&

@@ -111,12 +111,30 @@ def test_handoff_concurrent_streams_bitwise():
     assert rep.ok, str(rep)
 
 
-def test_handoff_requires_tma_path():
+@pytest.mark.parametrize("N,view", [(4099, False), (3, False), (2050, True)])
+def test_handoff_ragged_and_unaligned_rows(N, view):
+    """The fused handoff on shapes the round-1 TMA path refused: a ragged N (odd row stride:
+    1-D tensor maps, element-wise stores) and an unaligned column view x[:, 1:] of a wider
+    tensor.  Bitwise = whole axis, and = the oracle."""
     p = snn.LIFParams.paper()
-    X = torch.zeros(4, 3, device="cuda")          # N % 4 != 0 -> generic path
-    fd, _ = _local_dirs(2, 3)
-    with pytest.raises(RuntimeError, match="SNN_ERR_UNSUPPORTED"):
-        HO.lif_forward_handoff(X, p, _fwd_h(fd, 0, 2, 1))
+    T, k = 40, 2
+    Xw = snn_synth.normal_tensor(91, T, N + 1 if view else N, device="cuda")
+    Gw = snn_synth.normal_tensor(92, T, N + 1 if view else N, device="cuda")
+    X, G = (Xw[:, 1:], Gw[:, 1:]) if view else (Xw, Gw)
+    f = snn.lif_forward(X, p)
+    gx_ref, gvi_ref = snn.lif_backward(G, f)
+    segs = D.partition_time(T, k)
+    fd, bd = _local_dirs(k, N)
+    fwds = [HO.lif_forward_handoff(X[a:b], p, _fwd_h(fd, d, k, 1)) for d, (a, b) in enumerate(segs)]
+    g1, _ = HO.lif_backward_handoff(G[segs[1][0]:], fwds[1], _bwd_h(bd, 1, k, 1))
+    g0, gvi = HO.lif_backward_handoff(G[: segs[0][1]], fwds[0], _bwd_h(bd, 0, k, 1))
+    torch.cuda.synchronize()
+    S = torch.cat([q.spikes for q in fwds])
+    assert torch.equal(S, f.spikes) and torch.equal(fwds[-1].v_final, f.v_final)
+    assert torch.equal(torch.cat([g0, g1]), gx_ref) and torch.equal(gvi, gvi_ref)
+    rep = oracle_check(p, X.cpu(), G.cpu(), S.cpu(), torch.cat([g0, g1]).cpu(), vf_gpu=fwds[-1].v_final.cpu(),
+                       gvi_gpu=gvi.cpu())
+    assert rep.ok, str(rep)
 
 
 # ------------------------------------------------------------------ k processes, CUDA IPC

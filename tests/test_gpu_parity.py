@@ -530,14 +530,72 @@ def test_affine_residual_zero_equals_affine_path_bitwise():
     assert torch.equal(g2[0], g2[4])    # scale 1: dL/dX == dL/dR
 
 
-def test_affine_residual_needs_tma_path():
-    """The residual prologue runs only on the TMA path: a ragged N reports SNN_ERR_UNSUPPORTED
-    (no silent fallback)."""
-    T, C, HW = 8, 3, 7            # N = 21: not a multiple of the lane group
-    X = torch.randn(T, C * HW, device="cuda")
-    af = snn.AffineSpec(torch.ones(C, device="cuda"), torch.zeros(C, device="cuda"), C, HW)
-    with pytest.raises(RuntimeError, match="UNSUPPORTED"):
-        snn.lif_forward_affine(X, PAPER, af, residual=torch.zeros_like(X))
+@pytest.mark.parametrize("T,B,C,HW,dtype", [(8, 1, 3, 7, torch.float32), (19, 3, 5, 13, torch.float32),
+                                            (21, 2, 3, 11, torch.bfloat16)])
+def test_affine_residual_ragged_rows(T, B, C, HW, dtype):
+    """The residual prologue on ragged N (odd row strides: the unaligned TMA kernels; round 1
+    returned SNN_ERR_UNSUPPORTED here) vs the oracle, all outputs."""
+    N = B * C * HW
+    X, G, sc, sh = _affine_case(PAPER, T, B, C, HW, dtype, 501 + N)
+    R = snn_synth.normal_tensor(601 + N, T, N, std=0.5, dtype=dtype)
+    af = snn.AffineSpec(sc.cuda(), sh.cuda(), C, HW)
+    f = snn.lif_forward_affine(X.cuda(), PAPER, af, residual=R.cuda())
+    gx, gvi, gsc, gsh, gres = snn.lif_backward_affine(G.cuda(), f)
+    torch.cuda.synchronize()
+    Xp = oracle.affine_input(X.double().numpy(), sc.double().numpy(), sh.double().numpy(), C, HW,
+                             residual=R.double().numpy())
+    ref = oracle_run(PAPER, Xp, G)
+    bf = dtype == torch.bfloat16
+    rep = compare(PAPER, ref, ref["gX"], ref["gvi"], f.spikes.cpu(), gres.cpu(), vf_gpu=f.v_final.cpu(),
+                  gvi_gpu=gvi.cpu(), io_bf16=bf)
+    assert_ok(rep)
+    rgx, rgs, rgb = oracle.affine_grads(X.double().numpy(), ref["gX"], sc.double().numpy(), C, HW)
+    cidx = (np.arange(N) // HW) % C
+    ref_scaled = dict(ref)
+    ref_scaled["gX_bound"] = ref["gX_bound"] * np.abs(sc.double().numpy())[cidx][None, :]
+    assert_ok(compare(PAPER, ref_scaled, rgx, ref["gvi"], f.spikes.cpu(), gx.cpu(), io_bf16=bf))
+    bnd = ref["gX_bound"]
+    tol_s = np.zeros(C); tol_b = np.zeros(C)
+    np.add.at(tol_s, cidx, (bnd * np.abs(X.double().numpy())).sum(0)); np.add.at(tol_b, cidx, bnd.sum(0))
+    rtol = 1e-2 if bf else 1e-5
+    assert np.all(np.abs(gsc.cpu().numpy() - rgs) <= rtol * tol_s + 1e-30)
+    assert np.all(np.abs(gsh.cpu().numpy() - rgb) <= rtol * tol_b + 1e-30)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("mode", range(8))
+@pytest.mark.parametrize("case", ["ragged_N", "unaligned_view"])
+def test_unaligned_tma_equals_generic_bitwise(monkeypatch, dtype, mode, case):
+    """Rows the 2-D tensor maps cannot describe -- a contiguous ragged N (odd row stride) and a
+    column view starting at an odd element -- run on the unaligned TMA kernels (1-D maps); they
+    must equal the generic kernels bitwise (all 8 modes, both save modes, carries) and the oracle."""
+    p = LIFParams(tau=1.5, v_th=0.6, v_reset=-0.1, surrogate=("atan" if mode & 1 else "sigmoid"),
+                  reset=("soft" if mode & 2 else "hard"), detach_reset=bool(mode & 4),
+                  decay_input=bool(mode & 1))
+    T, N = 37, 3071
+    if case == "ragged_N":
+        X = snn_synth.normal_tensor(41, T, N, dtype=dtype).cuda()
+        G = snn_synth.normal_tensor(42, T, N, dtype=dtype).cuda()
+    else:
+        X = snn_synth.normal_tensor(41, T, N + 3, dtype=dtype).cuda()[:, 3:]
+        G = snn_synth.normal_tensor(42, T, N + 3, dtype=dtype).cuda()[:, 3:]
+    v0 = snn_synth.normal_tensor(43, 1, N)[0].cuda()
+    outs = []
+    for no_tma in ("0", "1"):
+        monkeypatch.setenv("SNN_LIF_NO_TMA", no_tma)
+        for sm in ("recompute", "h"):
+            for fmt in ("u8", "bits"):
+                f, g, v = _run(p, X, G, fmt, sm, v0=v0, gvf=v0)
+                torch.cuda.synchronize()
+                outs.append((f.spikes.clone(), f.v_final.clone(), g.clone(), v.clone()))
+    monkeypatch.delenv("SNN_LIF_NO_TMA")
+    half = len(outs) // 2
+    for o_tma, o_gen in zip(outs[:half], outs[half:]):
+        for a_, b_ in zip(o_tma, o_gen):
+            assert torch.equal(a_, b_)
+    rep = oracle_check(p, X.cpu(), G.cpu(), outs[0][0].cpu(), outs[0][2].cpu(), vf_gpu=outs[0][1].cpu(),
+                       gvi_gpu=outs[0][3].cpu(), v0=v0.cpu(), gvf=v0.cpu(), io_bf16=dtype == torch.bfloat16)
+    assert_ok(rep)
 
 
 def test_affine_lif_layer_residual_matches_unfused_autograd():

@@ -28,6 +28,10 @@ CASES = {
               ("bf16", 16, 1 << 21), ("f32", 64, 1 << 22)],
     "ragged": [("f32", 4, 1 << 21), ("f32", 10, 1 << 21), ("f32", 16, 1 << 21), ("f32", 20, 1 << 21),
                ("f32", 32, 1 << 21), ("bf16", 10, 1 << 22), ("bf16", 16, 1 << 22)],
+    # unaligned rows (1-D tensor-map TMA kernels) vs the aligned shape: (dtype, T, N[, view offset])
+    "unal": [("f32", 512, 1 << 20), ("f32", 512, (1 << 20) + 1), ("f32", 512, (1 << 20) + 2),
+             ("f32", 512, (1 << 20) + 3), ("f32", 512, 1 << 20, 1), ("bf16", 64, 1 << 22),
+             ("bf16", 64, (1 << 22) + 1), ("bf16", 64, 1 << 22, 3)],
     "small": [("bf16", 16, 1 << 14), ("bf16", 16, 1 << 16), ("bf16", 16, 1 << 18), ("bf16", 1, 1 << 14),
               ("f32", 16, 1 << 18), ("f32", 1, 1 << 14)],
 }
@@ -57,11 +61,12 @@ def alg_bytes(dt, T, N, save_mode="recompute"):
 SAVE_MODE = "recompute"
 
 
-def time_case(dt, T, N, reps):
+def time_case(dt, T, N, reps, off=0):
+    """off > 0: x / grad_spikes are column views [:, off:] of [T, N + off] tensors (unaligned rows)."""
     dtype = torch.float32 if dt == "f32" else torch.bfloat16
     p = snn.LIFParams.paper()
-    xs = [snn_synth.normal_tensor(1234 + i, T, N, device="cuda", dtype=dtype) for i in range(2)]
-    gs = [snn_synth.normal_tensor(4321 + i, T, N, device="cuda", dtype=dtype) for i in range(2)]
+    xs = [snn_synth.normal_tensor(1234 + i, T, N + off, device="cuda", dtype=dtype)[:, off:] for i in range(2)]
+    gs = [snn_synth.normal_tensor(4321 + i, T, N + off, device="cuda", dtype=dtype)[:, off:] for i in range(2)]
     st = torch.cuda.current_stream()
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(reps)]
     for i in range(3):
@@ -81,7 +86,7 @@ def time_case(dt, T, N, reps):
     tf = sorted(e[0].elapsed_time(e[1]) for e in ev)[reps // 2]
     tb = sorted(e[2].elapsed_time(e[3]) for e in ev)[reps // 2]
     bf, bb = alg_bytes(dt, T, N)
-    print(f"{dt:5s} T={T:4d} N={N:9d}  fwd {tf * 1e3:8.1f} us {bf / tf / 1e6:7.0f} GB/s   "
+    print(f"{dt:5s} T={T:4d} N={N:9d}{f' view+{off}' if off else ''}  fwd {tf * 1e3:8.1f} us {bf / tf / 1e6:7.0f} GB/s   "
           f"bwd {tb * 1e3:8.1f} us {bb / tb / 1e6:7.0f} GB/s", flush=True)
     return tf, tb
 
@@ -97,8 +102,8 @@ def main():
     torch.cuda.set_device(0)
     time_null(a.reps)
     for c in a.cases.split(","):
-        for dt, T, N in CASES[c]:
-            time_case(dt, T, N, a.reps)
+        for case in CASES[c]:
+            time_case(*case[:3], a.reps, *case[3:])
 
 
 if __name__ == "__main__":
