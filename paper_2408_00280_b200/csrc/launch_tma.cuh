@@ -1,5 +1,5 @@
 // launch_tma.cuh -- host launchers of the persistent TMA kernels (lif_tma.cuh), templated
-// on the io dtype and on UNAL (rows of the io tensors not 16-byte aligned: 1-D tensor maps);
+// on the io dtype and on UNAL (rows of the io tensors not 16-byte aligned: flat tensor maps);
 // instantiated by fwd_tma_{f32,bf16}[_unal].cu and bwd_tma_{f32,bf16}[_unal].cu.
 #pragma once
 
@@ -29,8 +29,8 @@ template <> struct TmaCfg<__nv_bfloat16> {
 };
 
 // Tensor map of an io tensor [T, ld] (first N columns) with boxes of box_inner neurons x rows:
-// 2-D when aligned; UNAL: a 1-D map over the flat storage from the pointer aligned down to
-// 16 B (*off = the elements skipped), extent up to the last element of the view.
+// 2-D when aligned; UNAL: a flat (one-row) map over the storage from the pointer aligned down
+// to 16 B (*off = the elements skipped), extent up to the last element of the view.
 template <typename IO, bool UNAL>
 bool encode_io(CUtensorMap* m, const void* base, const snn_lif_shape* s, int box_inner, int rows, int* off) {
     if constexpr (!UNAL) {

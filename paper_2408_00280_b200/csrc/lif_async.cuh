@@ -80,18 +80,6 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, int c0,
         : "memory");
 }
 
-// 1-D TMA tile load: `box` consecutive elements starting at element coordinate c0 of a 1-D
-// tensor map.  Used for rows whose address is not 16-byte aligned (odd row strides, unaligned
-// column views): a 2-D map needs 16-byte row strides, a 1-D box may start at any element.
-__device__ __forceinline__ void tma_load_1d(void* dst, const void* tmap, int c0, uint64_t* bar,
-                                            uint64_t policy) {
-    asm volatile(
-        "cp.async.bulk.tensor.1d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-        ".L2::cache_hint [%0], [%1, {%2}], [%3], %4;" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(smem_u32(bar)), "l"(policy)
-        : "memory");
-}
-
 __device__ __forceinline__ void tma_prefetch_desc(const void* tmap) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
 }

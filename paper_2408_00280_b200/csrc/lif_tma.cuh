@@ -22,9 +22,9 @@
 //    multiple of VEC) stores element by element.
 //  * UNAL (unaligned) variants: a 2-D tensor map needs 16-byte row strides and a 16-byte
 //    aligned base; an odd row stride (e.g. a contiguous [T, N] with N % 4 != 0 in fp32) or an
-//    unaligned column view cannot have one.  Those tensors get a 1-D tensor map over the
-//    flat [T, ld] storage (base aligned down to 16 B, the offset folded into the
-//    coordinates): the producer issues one 1-D box per (row, 256-neuron box) -- same smem
+//    unaligned column view cannot have one.  Those tensors get a flat tensor map -- one row of
+//    the whole [T, ld] storage (base aligned down to 16 B, the offset folded into the
+//    coordinates): the producer issues one box per (time row, 256-neuron box) -- same smem
 //    layout, same bytes, more instructions -- and consumers store with the widest aligned
 //    form per row (st_any).  Everything else is the aligned kernel.
 //
@@ -133,9 +133,9 @@ __device__ __forceinline__ int box_off(int nt, int r) {
 }
 
 // Load one [NB][ROWS][BW] region (rows t0 .. t0 + rows - 1 of tile columns c0 ..) into dst.
-// UNAL = false: NB 2-D boxes (rows past T zero-filled by the TMA).  UNAL = true: one 1-D box
-// per (box, row) of the flat [T, ld] tensor whose 1-D map starts `off` elements before the
-// tensor; only the `rows` valid rows are loaded (region_bytes counts the same).
+// UNAL = false: NB 2-D boxes (rows past T zero-filled by the TMA).  UNAL = true: one box per
+// (box, time row) of the flat [T, ld] storage, whose one-row map starts `off` elements before
+// the tensor; only the `rows` valid rows are loaded (region_bytes counts the same).
 template <typename IO, int BW, int ROWS, int NB, bool UNAL>
 __device__ __forceinline__ void load_region(unsigned char* dst, const void* tm, int64_t c0, int64_t t0, int rows,
                                             int64_t ld, int off, uint64_t* fb, uint64_t pol) {
@@ -149,7 +149,7 @@ __device__ __forceinline__ void load_region(unsigned char* dst, const void* tm, 
         for (int r = 0; r < rows; ++r, row += ld) {
 #pragma unroll
             for (int b = 0; b < NB; ++b)
-                tma_load_1d(dst + b * BOX + r * BW * (int)sizeof(IO), tm, (int)(row + b * BW), fb, pol);
+                tma_load_2d(dst + b * BOX + r * BW * (int)sizeof(IO), tm, (int)(row + b * BW), 0, fb, pol);
         }
     }
 }

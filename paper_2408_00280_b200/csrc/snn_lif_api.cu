@@ -120,11 +120,14 @@ bool encode_1d(CUtensorMap* m, const void* base, size_t esz, int64_t extent, int
     if (!fn) return false;
     const CUtensorMapDataType dt = esz == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
                                             : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
-    const cuuint64_t dims[1] = {(cuuint64_t)extent};
-    const cuuint32_t boxd[1] = {(cuuint32_t)box};
-    const cuuint32_t estr[1] = {1};
+    // Written as a one-row 2-D map {extent, 1} (row stride rounded up to 16 B): the loads are the
+    // ordinary 2-D tile loads at row 0, and the encode needs no rank-1 special case.
+    const cuuint64_t dims[2] = {(cuuint64_t)extent, 1};
+    const cuuint64_t strides[1] = {(cuuint64_t)((extent * (int64_t)esz + 15) / 16 * 16)};
+    const cuuint32_t boxd[2] = {(cuuint32_t)box, 1};
+    const cuuint32_t estr[2] = {1, 1};
     auto encode = [&] {
-        return fn(m, dt, 1, const_cast<void*>(base), dims, nullptr, boxd, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        return fn(m, dt, 2, const_cast<void*>(base), dims, strides, boxd, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     };
     CUresult r = encode();
