@@ -21,12 +21,15 @@
 //    TMA's zero fill; consumers do not store past T / N.  A ragged last VEC group (N not a
 //    multiple of VEC) stores element by element.
 //  * UNAL (unaligned) variants: a 2-D tensor map needs 16-byte row strides and a 16-byte
-//    aligned base; an odd row stride (e.g. a contiguous [T, N] with N % 4 != 0 in fp32) or an
-//    unaligned column view cannot have one.  Those tensors get a flat tensor map -- one row of
-//    the whole [T, ld] storage (base aligned down to 16 B, the offset folded into the
-//    coordinates): the producer issues one box per (time row, 256-neuron box) -- same smem
-//    layout, same bytes, more instructions -- and consumers store with the widest aligned
-//    form per row (st_any).  Everything else is the aligned kernel.
+//    aligned base, and a TMA box must start on a 16-byte boundary; an odd row stride (e.g. a
+//    contiguous [T, N] with N % 4 != 0 in fp32) or an unaligned column view breaks both.  Those
+//    tensors get a flat tensor map -- one row over the whole [T, ld] storage, base aligned down
+//    to 16 B.  Per time row the producer loads the tile's span aligned DOWN to 16 B: the tile's
+//    256-neuron boxes plus one 16-byte tail box (smem rows [NB*BW + 16 B, padded to 128 B]);
+//    the row's element shift m (0..3 fp32, 0..7 bf16) is read past by the consumers, with
+//    pack loads when m keeps the pack aligned and element loads otherwise, and they store with
+//    the widest aligned form per row (st_any).  ~3% more smem and bytes than the aligned
+//    kernel; everything else is the same code.
 //
 // Smem layout of one tensor's row-block: NB boxes of [rows][BW] (BW = min(W, 256)).
 #pragma once
@@ -132,30 +135,83 @@ __device__ __forceinline__ int box_off(int nt, int r) {
     return ((nt / BW) * ROWS + r) * BW + (nt % BW);
 }
 
-// Load one [NB][ROWS][BW] region (rows t0 .. t0 + rows - 1 of tile columns c0 ..) into dst.
-// UNAL = false: NB 2-D boxes (rows past T zero-filled by the TMA).  UNAL = true: one box per
-// (box, time row) of the flat [T, ld] storage, whose one-row map starts `off` elements before
-// the tensor; only the `rows` valid rows are loaded (region_bytes counts the same).
+// One io tensor's rows of a stage.  Aligned: NB 2-D boxes, smem [NB][ROWS][BW] (rows past T
+// zero-filled by the TMA).  UNAL: per time row, the tile span [c0, c0 + NB*BW) of the flat
+// storage shifted down to a 16-byte boundary -- NB boxes of BW elements plus one Q-element tail
+// box (Q = 16 B) -- into smem row r at r * RP (RP = NB*BW*esz + 128 B: the tail box and the next
+// row stay 128-B aligned); only the `rows` valid rows are loaded (tx_bytes counts the same).
 template <typename IO, int BW, int ROWS, int NB, bool UNAL>
-__device__ __forceinline__ void load_region(unsigned char* dst, const void* tm, int64_t c0, int64_t t0, int rows,
-                                            int64_t ld, int off, uint64_t* fb, uint64_t pol) {
-    constexpr int BOX = BW * ROWS * (int)sizeof(IO);
-    if constexpr (!UNAL) {
-#pragma unroll
-        for (int b = 0; b < NB; ++b) tma_load_2d(dst + b * BOX, tm, (int)(c0 + b * BW), (int)t0, fb, pol);
-    } else {   // (one issuing thread: a rolled loop keeps its registers low)
-        int64_t row = off + t0 * ld + c0;
-#pragma unroll 1
-        for (int r = 0; r < rows; ++r, row += ld) {
+struct Region {
+    static constexpr int Q = 16 / (int)sizeof(IO);
+    static constexpr int RP = NB * BW * (int)sizeof(IO) + 128;   // UNAL smem row pitch (bytes)
+    static constexpr int RPE = RP / (int)sizeof(IO);
+    static constexpr int BYTES = UNAL ? ROWS * RP : NB * BW * ROWS * (int)sizeof(IO);
+
+    __device__ static __forceinline__ uint32_t tx_bytes(int rows) {
+        return UNAL ? (uint32_t)rows * (uint32_t)(NB * BW + Q) * (uint32_t)sizeof(IO)
+                    : (uint32_t)(NB * BW * ROWS) * (uint32_t)sizeof(IO);
+    }
+    // rows t0 .. t0 + rows - 1 of tile columns c0 .. (off: elements between the flat map's base
+    // and the tensor's first element)
+    __device__ static __forceinline__ void load(unsigned char* dst, const void* tm, const void* tm_tail, int64_t c0,
+                                                int64_t t0, int rows, int64_t ld, int off, uint64_t* fb,
+                                                uint64_t pol) {
+        if constexpr (!UNAL) {
 #pragma unroll
             for (int b = 0; b < NB; ++b)
-                tma_load_2d(dst + b * BOX + r * BW * (int)sizeof(IO), tm, (int)(row + b * BW), 0, fb, pol);
+                tma_load_2d(dst + b * BW * ROWS * (int)sizeof(IO), tm, (int)(c0 + b * BW), (int)t0, fb, pol);
+        } else {   // (one issuing thread: a rolled loop keeps its registers low)
+            int64_t e = off + t0 * ld + c0;
+#pragma unroll 1
+            for (int r = 0; r < rows; ++r, e += ld) {
+                const int e0 = (int)(e & ~(int64_t)(Q - 1));
+                unsigned char* d = dst + r * RP;
+#pragma unroll
+                for (int b = 0; b < NB; ++b) tma_load_2d(d + b * BW * (int)sizeof(IO), tm, e0 + b * BW, 0, fb, pol);
+                tma_load_2d(d + NB * BW * (int)sizeof(IO), tm_tail, e0 + NB * BW, 0, fb, pol);
+            }
         }
     }
-}
-template <typename IO, int BW, int ROWS, int NB, bool UNAL>
-__device__ __forceinline__ uint32_t region_bytes(int rows) {
-    return (uint32_t)NB * BW * (UNAL ? rows : ROWS) * (uint32_t)sizeof(IO);
+};
+
+// A consumer lane's view of one tensor's rows in a stage: src(j) = the lane's VEC elements of
+// row j.  Aligned: box layout, pack loads.  UNAL: row-major with the row's element shift
+// m_j = (m0 + j*dm) mod Q (m0 = the first row's, dm = ld mod Q); pack loads where the shift keeps
+// the pack aligned, element loads otherwise (a warp-uniform choice per row).
+template <typename IO, int VEC, int BW, int RPE, bool UNAL>
+struct RowSrc {
+    const IO* p;   // aligned: the lane's element of row 0 (box layout); UNAL: row 0 base + lane offset
+    int m0, dm;
+    __device__ __forceinline__ Pack<IO, VEC> operator()(int j) const {
+        if constexpr (!UNAL) {
+            return *reinterpret_cast<const Pack<IO, VEC>*>(p + j * BW);
+        } else {
+            constexpr int Q = 16 / (int)sizeof(IO);
+            const IO* q = p + j * RPE + ((m0 + j * dm) & (Q - 1));
+            if ((smem_u32(q) % sizeof(Pack<IO, VEC>)) == 0) return *reinterpret_cast<const Pack<IO, VEC>*>(q);
+            Pack<IO, VEC> r;
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) r.v[i] = q[i];
+            return r;
+        }
+    }
+};
+
+// The lane's RowSrc for rows starting at time t0 of a region at `base` (stage smem).
+template <typename IO, int VEC, int BW, int ROWS, int NB, bool UNAL>
+__device__ __forceinline__ RowSrc<IO, VEC, BW, Region<IO, BW, ROWS, NB, UNAL>::RPE, UNAL>
+row_src(const unsigned char* base, int nt, int64_t t0, int64_t ld, int off) {
+    constexpr int Q = 16 / (int)sizeof(IO);
+    RowSrc<IO, VEC, BW, Region<IO, BW, ROWS, NB, UNAL>::RPE, UNAL> s;
+    if constexpr (!UNAL) {
+        s.p = reinterpret_cast<const IO*>(base) + ((nt / BW) * ROWS) * BW + (nt % BW);
+        s.m0 = s.dm = 0;
+    } else {
+        s.p = reinterpret_cast<const IO*>(base) + nt;
+        s.m0 = (int)((off + t0 * ld) & (Q - 1));
+        s.dm = (int)(ld & (Q - 1));
+    }
+    return s;
 }
 
 // Store a consumer's VEC outputs of one row: the plain streaming pack store on the aligned
@@ -199,14 +255,14 @@ __device__ __forceinline__ int group_valid(int64_t n0, int64_t N, int vec) {
 // Forward.  Stage = R time rows of a W-neuron tile.  Warp 0 lane 0 = producer;
 // warps 1..NCONS/32 = consumers, each lane owning VEC neurons.
 // NIN = 2: the stage also holds the residual rows R at R_OFF.
-template <typename IO, int VEC, int NCONS, int R, int S, int NIN = 1>
+template <typename IO, int VEC, int NCONS, int R, int S, int NIN = 1, bool UNAL = false>
 struct FwdTma {
     static constexpr int W = NCONS * VEC;
     static constexpr int BW = W < 256 ? W : 256;
     static constexpr int NB = W / BW;
-    static constexpr int BOX_BYTES = BW * R * (int)sizeof(IO);
-    static constexpr int R_OFF = NB * BOX_BYTES;
-    static constexpr int STAGE_BYTES = NIN * NB * BOX_BYTES;
+    using Reg = Region<IO, BW, R, NB, UNAL>;
+    static constexpr int R_OFF = Reg::BYTES;
+    static constexpr int STAGE_BYTES = NIN * Reg::BYTES;
     static constexpr int SMEM = S * STAGE_BYTES + (int)sizeof(Barriers<S>) + kAlignSlack;
     static constexpr int THREADS = NCONS + 32;
     static_assert(W % BW == 0 && BW % VEC == 0, "tile geometry");
@@ -215,10 +271,12 @@ struct FwdTma {
 template <typename IO, int VEC, int SFMT, int SAVE, bool SOFT, bool AFF, bool RES, int NCONS, int R, int S,
           bool UNAL>
 __global__ void __launch_bounds__(NCONS + 32)
-lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmr,
+lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmx_tail,
+                       const __grid_constant__ CUtensorMap tmr, const __grid_constant__ CUtensorMap tmr_tail,
                        const FwdArgs a, const int clc_depth) {
     static_assert(!RES || AFF, "the residual prologue rides on the affine one");
-    using Cfg = FwdTma<IO, VEC, NCONS, R, S, RES ? 2 : 1>;
+    using Cfg = FwdTma<IO, VEC, NCONS, R, S, RES ? 2 : 1, UNAL>;
+    using Reg = typename Cfg::Reg;
     constexpr int W = Cfg::W, BW = Cfg::BW, NB = Cfg::NB;
     unsigned char* smem = smem_base();
     auto* bar = reinterpret_cast<Barriers<S>*>(smem + S * Cfg::STAGE_BYTES);
@@ -237,13 +295,12 @@ lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_con
             auto rows_of = [&](int64_t rb) { return (int)min((int64_t)R, T - rb * R); };
             produce<S, Cfg::STAGE_BYTES>(
                 smem, bar, nrb, clc_depth,
-                [&](int64_t rb) { return (RES ? 2u : 1u) * region_bytes<IO, BW, R, NB, UNAL>(rows_of(rb)); },
+                [&](int64_t rb) { return (RES ? 2u : 1u) * Reg::tx_bytes(rows_of(rb)); },
                 [&](unsigned char* stg, int tile, int64_t rb, uint64_t* fb) {
-                    load_region<IO, BW, R, NB, UNAL>(stg, &tmx, (int64_t)tile * W, rb * R, rows_of(rb), a.ld, a.x_off,
-                                                     fb, pol);
+                    Reg::load(stg, &tmx, &tmx_tail, (int64_t)tile * W, rb * R, rows_of(rb), a.ld, a.x_off, fb, pol);
                     if constexpr (RES)
-                        load_region<IO, BW, R, NB, UNAL>(stg + Cfg::R_OFF, &tmr, (int64_t)tile * W, rb * R, rows_of(rb),
-                                                         a.ld, a.r_off, fb, pol);
+                        Reg::load(stg + Cfg::R_OFF, &tmr, &tmr_tail, (int64_t)tile * W, rb * R, rows_of(rb), a.ld,
+                                  a.r_off, fb, pol);
                 });
         }
         return;
@@ -253,7 +310,6 @@ lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_con
     LifConsts c = a.c;
     pin(c);
     const int ct = threadIdx.x - 32;
-    const int xoff = box_off<VEC, BW, R>(ct * VEC, 0);
     const int64_t spk_step = spike_row_bytes<IO, SFMT>(a);
     uint32_t k = 0;
     while (true) {
@@ -282,7 +338,9 @@ lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_con
                 mbar_wait(&bar->full[s], (k / S) & 1);
             }
             const int rows = (int)min((int64_t)R, T - rb * R);
-            const IO* xs = reinterpret_cast<const IO*>(smem + s * Cfg::STAGE_BYTES) + xoff;
+            const unsigned char* stg = smem + s * Cfg::STAGE_BYTES;
+            const auto xs = row_src<IO, VEC, BW, R, NB, UNAL>(stg, ct * VEC, rb * R, a.ld, a.x_off);
+            const auto rsrc = row_src<IO, VEC, BW, R, NB, UNAL>(stg + Cfg::R_OFF, ct * VEC, rb * R, a.ld, a.r_off);
             // F: a full stage of a full tile (guard-free).  A partial stage keeps per-row guards:
             // unlike the backward (bwd_chunk_masked), masking every row here measured slower
             // (bf16 T=10: 31 -> 39 us), the forward's V chain being serial anyway.
@@ -292,11 +350,9 @@ lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_con
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 if (F || r < rows) {
-                    const Pack<IO, VEC> xv = *reinterpret_cast<const Pack<IO, VEC>*>(xs + r * BW);
+                    const Pack<IO, VEC> xv = xs(r);
                     Pack<IO, VEC> rv;
-                    if constexpr (RES)
-                        rv = *reinterpret_cast<const Pack<IO, VEC>*>(
-                            reinterpret_cast<const IO*>(smem + s * Cfg::STAGE_BYTES + Cfg::R_OFF) + xoff + r * BW);
+                    if constexpr (RES) rv = rsrc(r);
                     if constexpr (SAVE == SAVE_RECOMPUTE) {
                         // checkpoint the V entering step t when t % kCkpt == 0 (the saved rows are
                         // padded to 16 floats: a ragged group's pack store stays inside its row)
@@ -333,19 +389,19 @@ lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_con
 // Backward, RECOMPUTE.  Stage = one kCkpt-step chunk of the tile: x rows, gS rows and the
 // chunk's entry-V checkpoint row.  Chunks of a tile are streamed last-first.
 // RES: the stage also holds the chunk's residual rows at R_OFF.
-template <typename IO, int VEC, int NCONS, int S, bool RES = false>
+template <typename IO, int VEC, int NCONS, int S, bool RES = false, bool UNAL = false>
 struct BwdRecTma {
     static constexpr int W = NCONS * VEC;
     static constexpr int BW = W < 256 ? W : 256;
     static constexpr int NB = W / BW;
-    static constexpr int BOX_BYTES = BW * kCkpt * (int)sizeof(IO);
+    using Reg = Region<IO, BW, kCkpt, NB, UNAL>;
     static constexpr int CK_BOX_BYTES = BW * 4;
     static constexpr int NIN = RES ? 3 : 2;
     static constexpr int X_OFF = 0;
-    static constexpr int G_OFF = NB * BOX_BYTES;
-    static constexpr int R_OFF = 2 * NB * BOX_BYTES;
-    static constexpr int CK_OFF = NIN * NB * BOX_BYTES;
-    static constexpr int STAGE_BYTES = NIN * NB * BOX_BYTES + NB * CK_BOX_BYTES;
+    static constexpr int G_OFF = Reg::BYTES;
+    static constexpr int R_OFF = 2 * Reg::BYTES;
+    static constexpr int CK_OFF = NIN * Reg::BYTES;
+    static constexpr int STAGE_BYTES = NIN * Reg::BYTES + NB * CK_BOX_BYTES;
     static constexpr int SMEM = S * STAGE_BYTES + (int)sizeof(Barriers<S>) + kAlignSlack;
     static constexpr int THREADS = NCONS + 32;
     static_assert(W % BW == 0 && BW % VEC == 0 && STAGE_BYTES % 128 == 0, "tile geometry");
@@ -354,19 +410,19 @@ struct BwdRecTma {
 // Reverse walk over rows [0, rows) of one chunk.  h = recomputed H; gsm = gS rows in smem;
 // gxp = gX at the chunk's LAST row, walked backwards by ldb bytes.
 // RES: grp = dL/dR at the chunk's last row, walked like gxp.
-template <typename IO, int VEC, int MODE, int BW, int ROWS_MAX, bool UNAL>
+template <typename IO, int VEC, int MODE, int ROWS_MAX, bool UNAL, typename GS, typename XS>
 __device__ __forceinline__ void bwd_chunk(const LifConsts& c, float (&gV)[VEC],
-                                          const float (&h)[ROWS_MAX][VEC], const IO* gsm,
+                                          const float (&h)[ROWS_MAX][VEC], const GS& gsm,
                                           IO* gxp, int64_t ldb, int rows, int nvalid,
-                                          const AffCoef<VEC>& co, const IO* xs, float* pa, float* pb,
+                                          const AffCoef<VEC>& co, const XS& xs, float* pa, float* pb,
                                           IO* grp = nullptr) {
 #pragma unroll
     for (int j = ROWS_MAX - 1; j >= 0; --j) {
         if (j < rows) {
-            const Pack<IO, VEC> gv = *reinterpret_cast<const Pack<IO, VEC>*>(gsm + j * BW);
+            const Pack<IO, VEC> gv = gsm(j);
             Pack<IO, VEC> out, outr;
             if constexpr (Mode<MODE>::AFF) {
-                const Pack<IO, VEC> xr = *reinterpret_cast<const Pack<IO, VEC>*>(xs + j * BW);
+                const Pack<IO, VEC> xr = xs(j);
                 out = bwd_step<IO, VEC, MODE, true>(c, gV, h[j], gv, &co, &xr, pa, pb, &outr);
             } else {
                 out = bwd_step<IO, VEC, MODE>(c, gV, h[j], gv);
@@ -388,22 +444,22 @@ __device__ __forceinline__ void bwd_chunk(const LifConsts& c, float (&gV)[VEC],
 // stores are conditional.  One basic block per chunk lets the compiler interleave the rows'
 // independent surrogate math, which a per-row branch (the old guarded loop) serialised: T=10
 // cost as much as T=16.  gx0 / gr0 = row 0 of the chunk.
-template <typename IO, int VEC, int MODE, int BW, int ROWS_MAX, bool UNAL>
+template <typename IO, int VEC, int MODE, int ROWS_MAX, bool UNAL, typename GS, typename XS>
 __device__ __forceinline__ void bwd_chunk_masked(const LifConsts& c, float (&gV)[VEC],
-                                                 const float (&h)[kCkpt][VEC], const IO* gsm,
+                                                 const float (&h)[kCkpt][VEC], const GS& gsm,
                                                  IO* gx0, int64_t ldb, int rows, int nvalid,
-                                                 const AffCoef<VEC>& co, const IO* xs, float* pa, float* pb,
+                                                 const AffCoef<VEC>& co, const XS& xs, float* pa, float* pb,
                                                  IO* gr0 = nullptr) {
 #pragma unroll
     for (int j = ROWS_MAX - 1; j >= 0; --j) {
         const bool act = j < rows;   // uniform across the CTA
-        const Pack<IO, VEC> gv = *reinterpret_cast<const Pack<IO, VEC>*>(gsm + j * BW);
+        const Pack<IO, VEC> gv = gsm(j);
         Pack<IO, VEC> out, outr;
         float g2[VEC], pa2[VEC], pb2[VEC];
 #pragma unroll
         for (int i = 0; i < VEC; ++i) { g2[i] = gV[i]; pa2[i] = pa[i]; pb2[i] = pb[i]; }
         if constexpr (Mode<MODE>::AFF) {
-            const Pack<IO, VEC> xr = *reinterpret_cast<const Pack<IO, VEC>*>(xs + j * BW);
+            const Pack<IO, VEC> xr = xs(j);
             out = bwd_step<IO, VEC, MODE, true>(c, g2, h[j], gv, &co, &xr, pa2, pb2, &outr);
         } else {
             out = bwd_step<IO, VEC, MODE>(c, g2, h[j], gv);
@@ -420,16 +476,16 @@ __device__ __forceinline__ void bwd_chunk_masked(const LifConsts& c, float (&gV)
     }
 }
 
-template <typename IO, int VEC, int MODE, int BW, int ROWS_MAX = kCkpt>
+template <typename IO, int VEC, int MODE, int ROWS_MAX, typename XS>
 __device__ __forceinline__ void recompute_chunk(const LifConsts& c, float (&V)[VEC],
-                                                float (&h)[kCkpt][VEC], const IO* xs, int rows,
-                                                const AffCoef<VEC>& co, const IO* rs = nullptr) {
+                                                float (&h)[kCkpt][VEC], const XS& xs, int rows,
+                                                const AffCoef<VEC>& co, const XS& rs) {
 #pragma unroll
     for (int j = 0; j < ROWS_MAX; ++j) {
         if (j < rows) {
-            const Pack<IO, VEC> xv = *reinterpret_cast<const Pack<IO, VEC>*>(xs + j * BW);
+            const Pack<IO, VEC> xv = xs(j);
             Pack<IO, VEC> rv;
-            if constexpr (Mode<MODE>::RES) rv = *reinterpret_cast<const Pack<IO, VEC>*>(rs + j * BW);
+            if constexpr (Mode<MODE>::RES) rv = rs(j);
             fwd_recompute_step<Mode<MODE>::SOFT, Mode<MODE>::AFF, Mode<MODE>::RES, Mode<MODE>::P0>(c, V, xv, h[j],
                                                                                                co, &rv);
         }
@@ -441,11 +497,15 @@ __global__ void __launch_bounds__(NCONS + 32)
 lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
                                   const __grid_constant__ CUtensorMap tmg,
                                   const __grid_constant__ CUtensorMap tmck,
-                                  const __grid_constant__ CUtensorMap tmr, const BwdArgs a,
+                                  const __grid_constant__ CUtensorMap tmr,
+                                  const __grid_constant__ CUtensorMap tmx_tail,
+                                  const __grid_constant__ CUtensorMap tmg_tail,
+                                  const __grid_constant__ CUtensorMap tmr_tail, const BwdArgs a,
                                   const int clc_depth) {
     constexpr bool RES = Mode<MODE>::RES;
     static_assert(!RES || Mode<MODE>::AFF, "the residual prologue rides on the affine one");
-    using Cfg = BwdRecTma<IO, VEC, NCONS, S, RES>;
+    using Cfg = BwdRecTma<IO, VEC, NCONS, S, RES, UNAL>;
+    using Reg = typename Cfg::Reg;
     constexpr int W = Cfg::W, BW = Cfg::BW, NB = Cfg::NB;
     unsigned char* smem = smem_base();
     auto* bar = reinterpret_cast<Barriers<S>*>(smem + S * Cfg::STAGE_BYTES);
@@ -467,10 +527,7 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
             };
             produce<S, Cfg::STAGE_BYTES>(
                 smem, bar, nch, clc_depth,
-                [&](int64_t j) {
-                    return (uint32_t)Cfg::NIN * region_bytes<IO, BW, kCkpt, NB, UNAL>(rows_of(j)) +
-                           (uint32_t)(NB * Cfg::CK_BOX_BYTES);
-                },
+                [&](int64_t j) { return (uint32_t)Cfg::NIN * Reg::tx_bytes(rows_of(j)) + (uint32_t)(NB * Cfg::CK_BOX_BYTES); },
                 [&](unsigned char* stg, int tile, int64_t j, uint64_t* fb) {
                     const int64_t ch = nch - 1 - j;
                     const int rows = rows_of(j);
@@ -479,13 +536,10 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
                     for (int b = 0; b < NB; ++b)   // checkpoints: the saved rows are always 16-B aligned
                         tma_load_2d(stg + Cfg::CK_OFF + b * Cfg::CK_BOX_BYTES, &tmck, (int)(c0 + b * BW), (int)ch, fb,
                                     pol);
-                    load_region<IO, BW, kCkpt, NB, UNAL>(stg + Cfg::X_OFF, &tmx, c0, ch * kCkpt, rows, ld, a.x_off, fb,
-                                                         pol);
-                    load_region<IO, BW, kCkpt, NB, UNAL>(stg + Cfg::G_OFF, &tmg, c0, ch * kCkpt, rows, ld, a.g_off, fb,
-                                                         pol);
+                    Reg::load(stg + Cfg::X_OFF, &tmx, &tmx_tail, c0, ch * kCkpt, rows, ld, a.x_off, fb, pol);
+                    Reg::load(stg + Cfg::G_OFF, &tmg, &tmg_tail, c0, ch * kCkpt, rows, ld, a.g_off, fb, pol);
                     if constexpr (RES)
-                        load_region<IO, BW, kCkpt, NB, UNAL>(stg + Cfg::R_OFF, &tmr, c0, ch * kCkpt, rows, ld, a.r_off,
-                                                             fb, pol);
+                        Reg::load(stg + Cfg::R_OFF, &tmr, &tmr_tail, c0, ch * kCkpt, rows, ld, a.r_off, fb, pol);
                 });
         }
         return;
@@ -496,7 +550,6 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
     pin(c);
     const int ct = threadIdx.x - 32;
     const int nt = ct * VEC;
-    const int roff = box_off<VEC, BW, kCkpt>(nt, 0);
     const int ckoff = box_off<VEC, BW, 1>(nt, 0);
     IO* gx = reinterpret_cast<IO*>(a.gX);
     const int64_t ldb = ld * (int64_t)sizeof(IO);
@@ -529,8 +582,9 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
             const int64_t t0 = ch * kCkpt;
             const int rows = (int)min((int64_t)kCkpt, T - t0);
             const unsigned char* stg = smem + s * Cfg::STAGE_BYTES;
-            const IO* xs = reinterpret_cast<const IO*>(stg + Cfg::X_OFF) + roff;
-            const IO* gsm = reinterpret_cast<const IO*>(stg + Cfg::G_OFF) + roff;
+            const auto xs = row_src<IO, VEC, BW, kCkpt, NB, UNAL>(stg + Cfg::X_OFF, nt, t0, ld, a.x_off);
+            const auto gsm = row_src<IO, VEC, BW, kCkpt, NB, UNAL>(stg + Cfg::G_OFF, nt, t0, ld, a.g_off);
+            const auto rs = row_src<IO, VEC, BW, kCkpt, NB, UNAL>(stg + Cfg::R_OFF, nt, t0, ld, a.r_off);
             const Pack<float, VEC> v0 =
                 *reinterpret_cast<const Pack<float, VEC>*>(reinterpret_cast<const float*>(stg + Cfg::CK_OFF) + ckoff);
             float V[VEC];
@@ -538,35 +592,31 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
             for (int i = 0; i < VEC; ++i) V[i] = v0.v[i];
             float h[kCkpt][VEC];
             IO* gxp = gx + (t0 + rows - 1) * ld + n0;
-            const IO* rs = nullptr;
             IO* grp = nullptr;
-            if constexpr (RES) {
-                rs = reinterpret_cast<const IO*>(stg + Cfg::R_OFF) + roff;
-                grp = reinterpret_cast<IO*>(a.af.grad_residual) + (t0 + rows - 1) * ld + n0;
-            }
+            if constexpr (RES) grp = reinterpret_cast<IO*>(a.af.grad_residual) + (t0 + rows - 1) * ld + n0;
             if (rows == kCkpt && tile_full) {   // full chunk of a full tile: guard-free code
-                recompute_chunk<IO, VEC, MODE, BW>(c, V, h, xs, kCkpt, co, rs);
-                bwd_chunk<IO, VEC, MODE, BW, kCkpt, UNAL>(c, gV, h, gsm, gxp, ldb, kCkpt, VEC, co, xs, pa, pb, grp);
+                recompute_chunk<IO, VEC, MODE, kCkpt>(c, V, h, xs, kCkpt, co, rs);
+                bwd_chunk<IO, VEC, MODE, kCkpt, UNAL>(c, gV, h, gsm, gxp, ldb, kCkpt, VEC, co, xs, pa, pb, grp);
             } else if (rows == kCkpt / 2 && tile_full) {   // half chunk (T % 16 == 8, e.g. T = 8): guard-free too
                 constexpr int HR = kCkpt / 2;
-                recompute_chunk<IO, VEC, MODE, BW, HR>(c, V, h, xs, HR, co, rs);
-                bwd_chunk<IO, VEC, MODE, BW, HR, UNAL>(c, gV, reinterpret_cast<const float(&)[HR][VEC]>(h), gsm, gxp,
-                                                       ldb, HR, VEC, co, xs, pa, pb, grp);
+                recompute_chunk<IO, VEC, MODE, HR>(c, V, h, xs, HR, co, rs);
+                bwd_chunk<IO, VEC, MODE, HR, UNAL>(c, gV, reinterpret_cast<const float(&)[HR][VEC]>(h), gsm, gxp, ldb,
+                                                   HR, VEC, co, xs, pa, pb, grp);
             } else {                            // partial chunk or ragged tile: masked rows
                 IO* gx0 = gx + t0 * ld + n0;
                 IO* gr0 = RES ? reinterpret_cast<IO*>(a.af.grad_residual) + t0 * ld + n0 : nullptr;
                 if (rows <= kCkpt / 4) {
-                    recompute_chunk<IO, VEC, MODE, BW, kCkpt / 4>(c, V, h, xs, kCkpt / 4, co, rs);
-                    bwd_chunk_masked<IO, VEC, MODE, BW, kCkpt / 4, UNAL>(c, gV, h, gsm, gx0, ldb, rows, nvalid, co,
-                                                                         xs, pa, pb, gr0);
+                    recompute_chunk<IO, VEC, MODE, kCkpt / 4>(c, V, h, xs, kCkpt / 4, co, rs);
+                    bwd_chunk_masked<IO, VEC, MODE, kCkpt / 4, UNAL>(c, gV, h, gsm, gx0, ldb, rows, nvalid, co, xs, pa,
+                                                                     pb, gr0);
                 } else if (rows <= kCkpt / 2) {
-                    recompute_chunk<IO, VEC, MODE, BW, kCkpt / 2>(c, V, h, xs, kCkpt / 2, co, rs);
-                    bwd_chunk_masked<IO, VEC, MODE, BW, kCkpt / 2, UNAL>(c, gV, h, gsm, gx0, ldb, rows, nvalid, co,
-                                                                         xs, pa, pb, gr0);
+                    recompute_chunk<IO, VEC, MODE, kCkpt / 2>(c, V, h, xs, kCkpt / 2, co, rs);
+                    bwd_chunk_masked<IO, VEC, MODE, kCkpt / 2, UNAL>(c, gV, h, gsm, gx0, ldb, rows, nvalid, co, xs, pa,
+                                                                     pb, gr0);
                 } else {
-                    recompute_chunk<IO, VEC, MODE, BW>(c, V, h, xs, kCkpt, co, rs);
-                    bwd_chunk_masked<IO, VEC, MODE, BW, kCkpt, UNAL>(c, gV, h, gsm, gx0, ldb, rows, nvalid, co, xs,
-                                                                     pa, pb, gr0);
+                    recompute_chunk<IO, VEC, MODE, kCkpt>(c, V, h, xs, kCkpt, co, rs);
+                    bwd_chunk_masked<IO, VEC, MODE, kCkpt, UNAL>(c, gV, h, gsm, gx0, ldb, rows, nvalid, co, xs, pa, pb,
+                                                                 gr0);
                 }
             }
             __syncwarp();
@@ -586,15 +636,15 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
 
 // ------------------------------------------------------------------------------------
 // Backward, SAVE_H.  Stage = R time rows of H (fp32) and gS; row blocks streamed last-first.
-template <typename IO, int VEC, int NCONS, int R, int S>
+template <typename IO, int VEC, int NCONS, int R, int S, bool UNAL = false>
 struct BwdHTma {
     static constexpr int W = NCONS * VEC;
     static constexpr int BW = W < 256 ? W : 256;
     static constexpr int NB = W / BW;
     static constexpr int HBOX = BW * R * 4;
-    static constexpr int GBOX = BW * R * (int)sizeof(IO);
+    using Reg = Region<IO, BW, R, NB, UNAL>;
     static constexpr int G_OFF = NB * HBOX;
-    static constexpr int STAGE_BYTES = NB * (HBOX + GBOX);
+    static constexpr int STAGE_BYTES = NB * HBOX + Reg::BYTES;
     static constexpr int SMEM = S * STAGE_BYTES + (int)sizeof(Barriers<S>) + kAlignSlack;
     static constexpr int THREADS = NCONS + 32;
     static_assert(W % BW == 0 && BW % VEC == 0 && STAGE_BYTES % 128 == 0, "tile geometry");
@@ -603,9 +653,11 @@ struct BwdHTma {
 template <typename IO, int VEC, int MODE, int NCONS, int R, int S, bool UNAL>
 __global__ void __launch_bounds__(NCONS + 32)
 lif_backward_saveh_tma_kernel(const __grid_constant__ CUtensorMap tmh,
-                              const __grid_constant__ CUtensorMap tmg, const BwdArgs a,
+                              const __grid_constant__ CUtensorMap tmg,
+                              const __grid_constant__ CUtensorMap tmg_tail, const BwdArgs a,
                               const int clc_depth) {
-    using Cfg = BwdHTma<IO, VEC, NCONS, R, S>;
+    using Cfg = BwdHTma<IO, VEC, NCONS, R, S, UNAL>;
+    using Reg = typename Cfg::Reg;
     constexpr int W = Cfg::W, BW = Cfg::BW, NB = Cfg::NB;
     unsigned char* smem = smem_base();
     auto* bar = reinterpret_cast<Barriers<S>*>(smem + S * Cfg::STAGE_BYTES);
@@ -626,15 +678,14 @@ lif_backward_saveh_tma_kernel(const __grid_constant__ CUtensorMap tmh,
             };
             produce<S, Cfg::STAGE_BYTES>(
                 smem, bar, nrb, clc_depth,
-                [&](int64_t j) { return (uint32_t)(NB * Cfg::HBOX) + region_bytes<IO, BW, R, NB, UNAL>(rows_of(j)); },
+                [&](int64_t j) { return (uint32_t)(NB * Cfg::HBOX) + Reg::tx_bytes(rows_of(j)); },
                 [&](unsigned char* stg, int tile, int64_t j, uint64_t* fb) {
                     const int64_t rb = nrb - 1 - j;
                     const int64_t c0 = (int64_t)tile * W;
 #pragma unroll
                     for (int b = 0; b < NB; ++b)   // H: the saved rows are always 16-B aligned
                         tma_load_2d(stg + b * Cfg::HBOX, &tmh, (int)(c0 + b * BW), (int)(rb * R), fb, pol);
-                    load_region<IO, BW, R, NB, UNAL>(stg + Cfg::G_OFF, &tmg, c0, rb * R, rows_of(j), ld, a.g_off, fb,
-                                                     pol);
+                    Reg::load(stg + Cfg::G_OFF, &tmg, &tmg_tail, c0, rb * R, rows_of(j), ld, a.g_off, fb, pol);
                 });
         }
         return;
@@ -672,7 +723,7 @@ lif_backward_saveh_tma_kernel(const __grid_constant__ CUtensorMap tmh,
             const int rows = (int)min((int64_t)R, T - rb * R);
             const unsigned char* stg = smem + s * Cfg::STAGE_BYTES;
             const float* hs = reinterpret_cast<const float*>(stg) + roff;
-            const IO* gsm = reinterpret_cast<const IO*>(stg + Cfg::G_OFF) + roff;
+            const auto gsm = row_src<IO, VEC, BW, R, NB, UNAL>(stg + Cfg::G_OFF, nt, rb * R, ld, a.g_off);
             IO* gxp = gx + (rb * R + rows - 1) * ld + n0;
             auto walk = [&](auto full) {
                 constexpr bool F = decltype(full)::value;
@@ -680,7 +731,7 @@ lif_backward_saveh_tma_kernel(const __grid_constant__ CUtensorMap tmh,
                 for (int r = R - 1; r >= 0; --r) {
                     if (F || r < rows) {
                         const Pack<float, VEC> hv = *reinterpret_cast<const Pack<float, VEC>*>(hs + r * BW);
-                        const Pack<IO, VEC> gv = *reinterpret_cast<const Pack<IO, VEC>*>(gsm + r * BW);
+                        const Pack<IO, VEC> gv = gsm(r);
                         const Pack<IO, VEC> out = bwd_step<IO, VEC, MODE>(c, gV, hv.v, gv);
                         if (F || nvalid > 0) st_out<UNAL>(gxp, out, F ? VEC : nvalid);
                         gxp = step_bytes(gxp, -ldb);
