@@ -87,21 +87,31 @@ __device__ __forceinline__ void init_barriers(Barriers<S>* b, uint32_t consumer_
 // issues its TMA loads.  Ends with a tile = -1 sentinel stage; every outstanding request is
 // drained before returning (its response is an async smem write) and a late success is still
 // processed.
-template <int S, int STAGE_BYTES, typename Bytes, typename Issue>
+// WARP = false: run by one thread.  WARP = true: run by the whole producer warp in lockstep --
+// every lane waits and tracks the same state, lane 0 alone writes the stage metadata, arms the
+// barriers and sends the steal requests, and `issue` is called on every lane (the unaligned
+// kernels spread their per-row TMA loads over the lanes: one thread issues ~one UTMALDG per
+// 50 ns, too few for rows that each need their own loads).
+template <int S, int STAGE_BYTES, bool WARP = false, typename Bytes, typename Issue>
 __device__ __forceinline__ void produce(unsigned char* smem, Barriers<S>* bar, int64_t nstages,
                                         int depth, Bytes bytes, Issue issue) {
+    const bool leader = !WARP || (threadIdx.x & 31) == 0;
     uint32_t k = 0;
     uint32_t phases = 0;   // bit i = parity of CLC slot i (a bit set, not an array: no local memory)
     int issued = 0, consumed = 0;
     bool stop = false;
-    for (int i = 0; i < depth; ++i, ++issued) clc_request(&bar->clc[i]);
+    for (int i = 0; i < depth; ++i, ++issued)
+        if (leader) clc_request(&bar->clc[i]);
     int tile = (int)blockIdx.x;
     while (true) {
         for (int64_t j = 0; j < nstages; ++j, ++k) {
             const int s = k % S;
             mbar_wait(&bar->empty[s], ((k / S) & 1) ^ 1);
-            bar->tile[s] = tile;
-            mbar_arrive_expect_tx(&bar->full[s], bytes(j));
+            if (leader) {
+                bar->tile[s] = tile;
+                mbar_arrive_expect_tx(&bar->full[s], bytes(j));
+            }
+            if constexpr (WARP) __syncwarp();
             issue(smem + s * STAGE_BYTES, tile, j, &bar->full[s]);
         }
         tile = -1;
@@ -113,17 +123,22 @@ __device__ __forceinline__ void produce(unsigned char* smem, Barriers<S>* bar, i
             ++consumed;
             if (r >= 0) {
                 tile = r;
-                if (!stop) { clc_request(&bar->clc[i]); ++issued; }
+                if (!stop) {
+                    if (leader) clc_request(&bar->clc[i]);
+                    ++issued;
+                }
                 break;
             }
             stop = true;   // no CTA pending: issue no more requests, drain the rest
         }
         if (tile < 0) {
-            pdl_trigger();   // nothing left to steal: let the next kernel start filling SMs
+            if (leader) pdl_trigger();   // nothing left to steal: let the next kernel start filling SMs
             const int s = k % S;
             mbar_wait(&bar->empty[s], ((k / S) & 1) ^ 1);
-            bar->tile[s] = -1;
-            mbar_arrive(&bar->full[s]);
+            if (leader) {
+                bar->tile[s] = -1;
+                mbar_arrive(&bar->full[s]);
+            }
             return;
         }
     }
@@ -152,18 +167,20 @@ struct Region {
                     : (uint32_t)(NB * BW * ROWS) * (uint32_t)sizeof(IO);
     }
     // rows t0 .. t0 + rows - 1 of tile columns c0 .. (off: elements between the flat map's base
-    // and the tensor's first element)
+    // and the tensor's first element).  Aligned: called by one thread.  UNAL: called by every lane
+    // of the producer warp; lane (r + lane0) % 32 issues row r's loads.
     __device__ static __forceinline__ void load(unsigned char* dst, const void* tm, const void* tm_tail, int64_t c0,
                                                 int64_t t0, int rows, int64_t ld, int off, uint64_t* fb,
-                                                uint64_t pol) {
+                                                uint64_t pol, int lane0 = 0) {
         if constexpr (!UNAL) {
 #pragma unroll
             for (int b = 0; b < NB; ++b)
                 tma_load_2d(dst + b * BW * ROWS * (int)sizeof(IO), tm, (int)(c0 + b * BW), (int)t0, fb, pol);
-        } else {   // (one issuing thread: a rolled loop keeps its registers low)
-            int64_t e = off + t0 * ld + c0;
+        } else {
+            const int lane = threadIdx.x & 31;
 #pragma unroll 1
-            for (int r = 0; r < rows; ++r, e += ld) {
+            for (int r = (lane - lane0) & 31; r < rows; r += 32) {
+                const int64_t e = off + (t0 + r) * ld + c0;
                 const int e0 = (int)(e & ~(int64_t)(Q - 1));
                 unsigned char* d = dst + r * RP;
 #pragma unroll
@@ -287,20 +304,22 @@ lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_con
     const int64_t nrb = (T + R - 1) / R;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-    if (warp == 0) {  // ---------------- producer
-        if (lane == 0) {
-            tma_prefetch_desc(&tmx);
-            if constexpr (RES) tma_prefetch_desc(&tmr);
+    if (warp == 0) {  // ---------------- producer (one lane; the whole warp for unaligned rows)
+        if (UNAL || lane == 0) {
+            if (lane == 0) {
+                tma_prefetch_desc(&tmx);
+                if constexpr (RES) tma_prefetch_desc(&tmr);
+            }
             const uint64_t pol = policy_evict_first();
             auto rows_of = [&](int64_t rb) { return (int)min((int64_t)R, T - rb * R); };
-            produce<S, Cfg::STAGE_BYTES>(
+            produce<S, Cfg::STAGE_BYTES, UNAL>(
                 smem, bar, nrb, clc_depth,
                 [&](int64_t rb) { return (RES ? 2u : 1u) * Reg::tx_bytes(rows_of(rb)); },
                 [&](unsigned char* stg, int tile, int64_t rb, uint64_t* fb) {
                     Reg::load(stg, &tmx, &tmx_tail, (int64_t)tile * W, rb * R, rows_of(rb), a.ld, a.x_off, fb, pol);
                     if constexpr (RES)
                         Reg::load(stg + Cfg::R_OFF, &tmr, &tmr_tail, (int64_t)tile * W, rb * R, rows_of(rb), a.ld,
-                                  a.r_off, fb, pol);
+                                  a.r_off, fb, pol, R);
                 });
         }
         return;
@@ -516,30 +535,35 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
     const int64_t nch = (T + kCkpt - 1) / kCkpt;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-    if (warp == 0) {  // ---------------- producer: chunks of a tile, last first
-        if (lane == 0) {
-            tma_prefetch_desc(&tmx); tma_prefetch_desc(&tmg); tma_prefetch_desc(&tmck);
-            if constexpr (RES) tma_prefetch_desc(&tmr);
+    if (warp == 0) {  // ---------------- producer: chunks of a tile, last first (whole warp if unaligned)
+        if (UNAL || lane == 0) {
+            if (lane == 0) {
+                tma_prefetch_desc(&tmx); tma_prefetch_desc(&tmg); tma_prefetch_desc(&tmck);
+                if constexpr (RES) tma_prefetch_desc(&tmr);
+            }
             const uint64_t pol = policy_evict_first();
             auto rows_of = [&](int64_t j) {
                 const int64_t ch = nch - 1 - j;
                 return (int)min((int64_t)kCkpt, T - ch * kCkpt);
             };
-            produce<S, Cfg::STAGE_BYTES>(
+            produce<S, Cfg::STAGE_BYTES, UNAL>(
                 smem, bar, nch, clc_depth,
                 [&](int64_t j) { return (uint32_t)Cfg::NIN * Reg::tx_bytes(rows_of(j)) + (uint32_t)(NB * Cfg::CK_BOX_BYTES); },
                 [&](unsigned char* stg, int tile, int64_t j, uint64_t* fb) {
                     const int64_t ch = nch - 1 - j;
                     const int rows = rows_of(j);
                     const int64_t c0 = (int64_t)tile * W;
+                    if (lane == 0) {
 #pragma unroll
-                    for (int b = 0; b < NB; ++b)   // checkpoints: the saved rows are always 16-B aligned
-                        tma_load_2d(stg + Cfg::CK_OFF + b * Cfg::CK_BOX_BYTES, &tmck, (int)(c0 + b * BW), (int)ch, fb,
-                                    pol);
+                        for (int b = 0; b < NB; ++b)   // checkpoints: the saved rows are always 16-B aligned
+                            tma_load_2d(stg + Cfg::CK_OFF + b * Cfg::CK_BOX_BYTES, &tmck, (int)(c0 + b * BW), (int)ch,
+                                        fb, pol);
+                    }
                     Reg::load(stg + Cfg::X_OFF, &tmx, &tmx_tail, c0, ch * kCkpt, rows, ld, a.x_off, fb, pol);
-                    Reg::load(stg + Cfg::G_OFF, &tmg, &tmg_tail, c0, ch * kCkpt, rows, ld, a.g_off, fb, pol);
+                    Reg::load(stg + Cfg::G_OFF, &tmg, &tmg_tail, c0, ch * kCkpt, rows, ld, a.g_off, fb, pol, kCkpt);
                     if constexpr (RES)
-                        Reg::load(stg + Cfg::R_OFF, &tmr, &tmr_tail, c0, ch * kCkpt, rows, ld, a.r_off, fb, pol);
+                        Reg::load(stg + Cfg::R_OFF, &tmr, &tmr_tail, c0, ch * kCkpt, rows, ld, a.r_off, fb, pol,
+                                  2 * kCkpt);
                 });
         }
         return;
@@ -668,23 +692,25 @@ lif_backward_saveh_tma_kernel(const __grid_constant__ CUtensorMap tmh,
     const int64_t nrb = (T + R - 1) / R;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-    if (warp == 0) {
-        if (lane == 0) {
-            tma_prefetch_desc(&tmh); tma_prefetch_desc(&tmg);
+    if (warp == 0) {   // producer (whole warp if unaligned)
+        if (UNAL || lane == 0) {
+            if (lane == 0) { tma_prefetch_desc(&tmh); tma_prefetch_desc(&tmg); }
             const uint64_t pol = policy_evict_first();
             auto rows_of = [&](int64_t j) {
                 const int64_t rb = nrb - 1 - j;
                 return (int)min((int64_t)R, T - rb * R);
             };
-            produce<S, Cfg::STAGE_BYTES>(
+            produce<S, Cfg::STAGE_BYTES, UNAL>(
                 smem, bar, nrb, clc_depth,
                 [&](int64_t j) { return (uint32_t)(NB * Cfg::HBOX) + Reg::tx_bytes(rows_of(j)); },
                 [&](unsigned char* stg, int tile, int64_t j, uint64_t* fb) {
                     const int64_t rb = nrb - 1 - j;
                     const int64_t c0 = (int64_t)tile * W;
+                    if (lane == 0) {
 #pragma unroll
-                    for (int b = 0; b < NB; ++b)   // H: the saved rows are always 16-B aligned
-                        tma_load_2d(stg + b * Cfg::HBOX, &tmh, (int)(c0 + b * BW), (int)(rb * R), fb, pol);
+                        for (int b = 0; b < NB; ++b)   // H: the saved rows are always 16-B aligned
+                            tma_load_2d(stg + b * Cfg::HBOX, &tmh, (int)(c0 + b * BW), (int)(rb * R), fb, pol);
+                    }
                     Reg::load(stg + Cfg::G_OFF, &tmg, &tmg_tail, c0, rb * R, rows_of(j), ld, a.g_off, fb, pol);
                 });
         }
