@@ -25,9 +25,6 @@ int num_sms();
 // box = box_inner x box_outer elements; out-of-range elements read as zero.
 bool encode_2d(CUtensorMap* m, const void* base, size_t esz, int64_t inner, int64_t outer,
                int64_t ld, int box_inner, int box_outer);
-// Flat ("1-D") tensor map over `extent` elements from `base` (16-B aligned), boxes of `box`
-// elements: a one-row 2-D map, loaded with 2-D tile loads at row 0.
-bool encode_1d(CUtensorMap* m, const void* base, size_t esz, int64_t extent, int box);
 bool tma_available();
 const char* encode_detail();   // why the last encode_2d on this thread failed
 

@@ -6,6 +6,8 @@
 #include "internal.h"
 #include "lif_tma.cuh"
 
+#include <cstring>
+
 namespace snn_host {
 
 // Tile configurations: VEC neurons per consumer lane x NCONS
@@ -28,25 +30,17 @@ template <> struct TmaCfg<__nv_bfloat16> {
     static constexpr int HV = 2, HN = 512, HR = 8, HS = 4;
 };
 
-// Tensor maps of an io tensor [T, ld] (first N columns) with boxes of box_inner neurons x rows:
-// 2-D when aligned (*tail = *m, unused); UNAL: flat (one-row) maps over the storage from the
-// pointer aligned down to 16 B (*off = the elements skipped), extent up to the last element of
-// the view -- *m with box_inner-element boxes, *tail with one 16-byte box (lif_tma.cuh Region).
+// Tensor map of an io tensor [T, ld] (first N columns) with boxes of box_inner neurons x rows,
+// and the element offset of its first element from 16 B below it (*off).  UNAL: no map -- the
+// kernels copy those rows with 1-D bulk copies (lif_tma.cuh Region); *m is zeroed.
 template <typename IO, bool UNAL>
-bool encode_io(CUtensorMap* m, CUtensorMap* tail, const void* base, const snn_lif_shape* s, int box_inner, int rows,
-               int* off) {
+bool encode_io(CUtensorMap* m, const void* base, const snn_lif_shape* s, int box_inner, int rows, int* off) {
+    *off = (int)((reinterpret_cast<uintptr_t>(base) & 15u) / sizeof(IO));
     if constexpr (!UNAL) {
-        *off = 0;
-        const bool ok = encode_2d(m, base, sizeof(IO), s->N, s->T, s->ld, box_inner, rows);
-        *tail = *m;
-        return ok;
+        return encode_2d(m, base, sizeof(IO), s->N, s->T, s->ld, box_inner, rows);
     } else {
-        const uintptr_t p = reinterpret_cast<uintptr_t>(base);
-        const uintptr_t al = p & ~uintptr_t(15);
-        *off = (int)((p - al) / sizeof(IO));
-        const int64_t extent = *off + (s->T - 1) * s->ld + s->N;
-        return encode_1d(m, reinterpret_cast<const void*>(al), sizeof(IO), extent, box_inner) &&
-               encode_1d(tail, reinterpret_cast<const void*>(al), sizeof(IO), extent, 16 / (int)sizeof(IO));
+        std::memset(m, 0, sizeof(*m));
+        return true;
     }
 }
 
@@ -54,18 +48,17 @@ template <typename IO, bool UNAL>
 snn_status launch_forward_tma(const snn_lif_shape* s, const snn::FwdArgs& a0, bool soft, cudaStream_t st) {
     using C = TmaCfg<IO>;
     snn::FwdArgs a = a0;
-    CUtensorMap tmx, tmx_t, tmr, tmr_t;
+    CUtensorMap tmx, tmr;
     // pro: 0 plain, 1 affine, 2 affine + residual (the residual doubles the stage, so that
     // variant has its own, shallower tile configuration).
     const bool res = a.af.residual != nullptr;
     const int bw = res ? snn::FwdTma<IO, C::FV, C::FN_RES, C::FR, C::FS_RES, 2>::BW
                        : snn::FwdTma<IO, C::FV, C::FN, C::FR, C::FS>::BW;
-    if (!encode_io<IO, UNAL>(&tmx, &tmx_t, a.x, s, bw, C::FR, &a.x_off))
+    if (!encode_io<IO, UNAL>(&tmx, a.x, s, bw, C::FR, &a.x_off))
         return fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled failed for x%s", encode_detail());
     tmr = tmx;
-    tmr_t = tmx_t;
     a.r_off = 0;
-    if (res && !encode_io<IO, UNAL>(&tmr, &tmr_t, a.af.residual, s, bw, C::FR, &a.r_off))
+    if (res && !encode_io<IO, UNAL>(&tmr, a.af.residual, s, bw, C::FR, &a.r_off))
         return fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled failed for the residual%s", encode_detail());
     auto go = [&](auto sfmt, auto save, auto sft, auto pro) {
         constexpr int P = decltype(pro)::value;
@@ -75,7 +68,7 @@ snn_status launch_forward_tma(const snn_lif_shape* s, const snn::FwdArgs& a0, bo
         auto k = snn::lif_forward_tma_kernel<IO, C::FV, decltype(sfmt)::value, decltype(save)::value,
                                              (bool)decltype(sft)::value, P >= 1, P == 2, NC, C::FR, NS, UNAL>;
         return launch_tiles(k, K::THREADS, K::SMEM, (s->N + K::W - 1) / K::W, (s->T + C::FR - 1) / C::FR,
-                            st, "lif_forward_tma_kernel", tmx, tmx_t, tmr, tmr_t, a);
+                            st, "lif_forward_tma_kernel", tmx, tmr, a);
     };
     auto by_aff = [&](auto sfmt, auto save, auto sft) {
         if (a.af.scale == nullptr) return go(sfmt, save, sft, IC<0>{});
@@ -110,31 +103,30 @@ snn_status launch_backward_tma_mode(const snn_lif_shape* s, const snn::BwdArgs& 
     if constexpr (MODE < 8) {   // SAVE_H has no affine-gradient or P0 variant (host never asks)
     if (s->save_mode == SNN_SAVE_H) {
         using Cfg = snn::BwdHTma<IO, C::HV, C::HN, C::HR, C::HS, UNAL>;
-        CUtensorMap tmh, tmg, tmg_t;
+        CUtensorMap tmh, tmg;
         if (!encode_2d(&tmh, a.saved, 4, s->N, s->T, a.ldh, Cfg::BW, C::HR) ||
-            !encode_io<IO, UNAL>(&tmg, &tmg_t, a.gS, s, Cfg::BW, C::HR, &a.g_off))
+            !encode_io<IO, UNAL>(&tmg, a.gS, s, Cfg::BW, C::HR, &a.g_off))
             return fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled failed (SAVE_H backward)%s", encode_detail());
         auto k = snn::lif_backward_saveh_tma_kernel<IO, C::HV, MODE, C::HN, C::HR, C::HS, UNAL>;
         return launch_tiles(k, Cfg::THREADS, Cfg::SMEM, (s->N + Cfg::W - 1) / Cfg::W,
-                            (s->T + C::HR - 1) / C::HR, st, "lif_backward_saveh_tma_kernel", tmh, tmg, tmg_t, a);
+                            (s->T + C::HR - 1) / C::HR, st, "lif_backward_saveh_tma_kernel", tmh, tmg, a);
     }
     }
     constexpr bool RES = snn::Mode<MODE>::RES;
     constexpr int NS = RES ? C::RS_RES : C::RS;
     using Cfg = snn::BwdRecTma<IO, C::RV, C::RN, NS, RES, UNAL>;
     const int64_t nch = (s->T + snn::kCkpt - 1) / snn::kCkpt;
-    CUtensorMap tmx, tmg, tmck, tmr, tmx_t, tmg_t, tmr_t;
-    if (!encode_io<IO, UNAL>(&tmx, &tmx_t, a.x, s, Cfg::BW, snn::kCkpt, &a.x_off) ||
-        !encode_io<IO, UNAL>(&tmg, &tmg_t, a.gS, s, Cfg::BW, snn::kCkpt, &a.g_off) ||
+    CUtensorMap tmx, tmg, tmck, tmr;
+    if (!encode_io<IO, UNAL>(&tmx, a.x, s, Cfg::BW, snn::kCkpt, &a.x_off) ||
+        !encode_io<IO, UNAL>(&tmg, a.gS, s, Cfg::BW, snn::kCkpt, &a.g_off) ||
         !encode_2d(&tmck, a.saved, 4, s->N, nch, a.ldh, Cfg::BW, 1))
         return fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled failed (RECOMPUTE backward)%s", encode_detail());
     tmr = tmx;
-    tmr_t = tmx_t;
-    if (RES && !encode_io<IO, UNAL>(&tmr, &tmr_t, a.af.residual, s, Cfg::BW, snn::kCkpt, &a.r_off))
+    if (RES && !encode_io<IO, UNAL>(&tmr, a.af.residual, s, Cfg::BW, snn::kCkpt, &a.r_off))
         return fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled failed for the residual%s", encode_detail());
     auto k = snn::lif_backward_recompute_tma_kernel<IO, C::RV, MODE, C::RN, NS, UNAL>;
     return launch_tiles(k, Cfg::THREADS, Cfg::SMEM, (s->N + Cfg::W - 1) / Cfg::W, nch, st,
-                        "lif_backward_recompute_tma_kernel", tmx, tmg, tmck, tmr, tmx_t, tmg_t, tmr_t, a);
+                        "lif_backward_recompute_tma_kernel", tmx, tmg, tmck, tmr, a);
 }
 
 template <typename IO, bool UNAL>

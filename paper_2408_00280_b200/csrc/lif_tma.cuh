@@ -83,7 +83,7 @@ __device__ __forceinline__ void init_barriers(Barriers<S>* b, uint32_t consumer_
 // `depth` (1..kMaxClc) steal requests are kept in flight, so with short tiles (few ring
 // stages, e.g. T = 8) the next tiles are known before the current one is issued; with
 // long tiles depth = 1 avoids hoarding work near the end.  Each tile is `nstages` ring
-// stages; `bytes(j)` is stage j's transaction byte count and `issue(stage_ptr, tile, j, bar)`
+// stages; `bytes(tile, j)` is stage j's transaction byte count and `issue(stage_ptr, tile, j, bar)`
 // issues its TMA loads.  Ends with a tile = -1 sentinel stage; every outstanding request is
 // drained before returning (its response is an async smem write) and a late success is still
 // processed.
@@ -109,7 +109,7 @@ __device__ __forceinline__ void produce(unsigned char* smem, Barriers<S>* bar, i
             mbar_wait(&bar->empty[s], ((k / S) & 1) ^ 1);
             if (leader) {
                 bar->tile[s] = tile;
-                mbar_arrive_expect_tx(&bar->full[s], bytes(j));
+                mbar_arrive_expect_tx(&bar->full[s], bytes(tile, j));
             }
             if constexpr (WARP) __syncwarp();
             issue(smem + s * STAGE_BYTES, tile, j, &bar->full[s]);
@@ -150,28 +150,53 @@ __device__ __forceinline__ int box_off(int nt, int r) {
     return ((nt / BW) * ROWS + r) * BW + (nt % BW);
 }
 
-// One io tensor's rows of a stage.  Aligned: NB 2-D boxes, smem [NB][ROWS][BW] (rows past T
-// zero-filled by the TMA).  UNAL: per time row, the tile span [c0, c0 + NB*BW) of the flat
-// storage shifted down to a 16-byte boundary -- NB boxes of BW elements plus one Q-element tail
-// box (Q = 16 B) -- into smem row r at r * RP (RP = NB*BW*esz + 128 B: the tail box and the next
-// row stay 128-B aligned); only the `rows` valid rows are loaded (tx_bytes counts the same).
+// One io tensor's rows of a stage.  Aligned: NB 2-D tensor-map boxes, smem [NB][ROWS][BW]
+// (rows past T zero-filled by the TMA).  UNAL: per time row ONE 1-D bulk copy
+// (cp.async.bulk, UBLKCP) of the tile span [c0, c0 + W) of that row shifted down to a 16-byte
+// boundary, W*esz + 16 bytes (truncated at the view's last 16-byte chunk, which holds its last
+// element: nothing past the allocation is read), into smem row r at r * RP (RP = W*esz + 128 B,
+// 128-B aligned rows); only the `rows` valid rows are loaded (tx_bytes counts the same).
 template <typename IO, int BW, int ROWS, int NB, bool UNAL>
 struct Region {
     static constexpr int Q = 16 / (int)sizeof(IO);
-    static constexpr int RP = NB * BW * (int)sizeof(IO) + 128;   // UNAL smem row pitch (bytes)
+    static constexpr int WB = NB * BW * (int)sizeof(IO);          // tile span bytes
+    static constexpr int RP = WB + 128;                           // UNAL smem row pitch (bytes)
     static constexpr int RPE = RP / (int)sizeof(IO);
-    static constexpr int BYTES = UNAL ? ROWS * RP : NB * BW * ROWS * (int)sizeof(IO);
+    static constexpr int BYTES = UNAL ? ROWS * RP : WB * ROWS;
 
-    __device__ static __forceinline__ uint32_t tx_bytes(int rows) {
-        return UNAL ? (uint32_t)rows * (uint32_t)(NB * BW + Q) * (uint32_t)sizeof(IO)
-                    : (uint32_t)(NB * BW * ROWS) * (uint32_t)sizeof(IO);
+    // The flat extent of an io view x [T, ld] (first N columns): its aligned-down base and the
+    // end of the 16-byte chunk holding its last element.
+    struct Flat {
+        uintptr_t x;     // the view's first element
+        uintptr_t end;   // round_up(address past its last element, 16)
+    };
+    __device__ static __forceinline__ Flat flat(const void* x, int64_t T, int64_t N, int64_t ld) {
+        const uintptr_t a = reinterpret_cast<uintptr_t>(x);
+        return Flat{a, (a + (uintptr_t)(((T - 1) * ld + N) * (int64_t)sizeof(IO)) + 15) & ~uintptr_t(15)};
     }
-    // rows t0 .. t0 + rows - 1 of tile columns c0 .. (off: elements between the flat map's base
-    // and the tensor's first element).  Aligned: called by one thread.  UNAL: called by every lane
-    // of the producer warp; lane (r + lane0) % 32 issues row r's loads.
-    __device__ static __forceinline__ void load(unsigned char* dst, const void* tm, const void* tm_tail, int64_t c0,
-                                                int64_t t0, int rows, int64_t ld, int off, uint64_t* fb,
-                                                uint64_t pol, int lane0 = 0) {
+    // UNAL: source address and byte count of time row t's copy.
+    __device__ static __forceinline__ uint32_t row_copy(const Flat& f, int64_t t, int64_t c0, int64_t ld,
+                                                        uintptr_t* src) {
+        const uintptr_t s = (f.x + (uintptr_t)((t * ld + c0) * (int64_t)sizeof(IO))) & ~uintptr_t(15);
+        *src = s;
+        const uintptr_t lim = f.end - s;
+        return (uint32_t)(lim < (uintptr_t)(WB + 16) ? lim : (uintptr_t)(WB + 16));
+    }
+    __device__ static __forceinline__ uint32_t tx_bytes(const Flat& f, int64_t t0, int rows, int64_t c0, int64_t ld) {
+        if constexpr (!UNAL) {
+            return (uint32_t)(WB * ROWS);
+        } else {
+            uint32_t b = 0;
+            uintptr_t src;
+            for (int r = 0; r < rows; ++r) b += row_copy(f, t0 + r, c0, ld, &src);
+            return b;
+        }
+    }
+    // rows t0 .. t0 + rows - 1 of tile columns c0 ..  Aligned: one thread, tensor map tm.
+    // UNAL: every lane of the producer warp; lane (r + lane0) % 32 copies row r.
+    __device__ static __forceinline__ void load(unsigned char* dst, const void* tm, const Flat& f, int64_t c0,
+                                                int64_t t0, int rows, int64_t ld, uint64_t* fb, uint64_t pol,
+                                                int lane0 = 0) {
         if constexpr (!UNAL) {
 #pragma unroll
             for (int b = 0; b < NB; ++b)
@@ -180,12 +205,9 @@ struct Region {
             const int lane = threadIdx.x & 31;
 #pragma unroll 1
             for (int r = (lane - lane0) & 31; r < rows; r += 32) {
-                const int64_t e = off + (t0 + r) * ld + c0;
-                const int e0 = (int)(e & ~(int64_t)(Q - 1));
-                unsigned char* d = dst + r * RP;
-#pragma unroll
-                for (int b = 0; b < NB; ++b) tma_load_2d(d + b * BW * (int)sizeof(IO), tm, e0 + b * BW, 0, fb, pol);
-                tma_load_2d(d + NB * BW * (int)sizeof(IO), tm_tail, e0 + NB * BW, 0, fb, pol);
+                uintptr_t src;
+                const uint32_t n = row_copy(f, t0 + r, c0, ld, &src);
+                bulk_g2s(dst + r * RP, reinterpret_cast<const void*>(src), n, fb, pol);
             }
         }
     }
@@ -288,8 +310,7 @@ struct FwdTma {
 template <typename IO, int VEC, int SFMT, int SAVE, bool SOFT, bool AFF, bool RES, int NCONS, int R, int S,
           bool UNAL>
 __global__ void __launch_bounds__(NCONS + 32)
-lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmx_tail,
-                       const __grid_constant__ CUtensorMap tmr, const __grid_constant__ CUtensorMap tmr_tail,
+lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmr,
                        const FwdArgs a, const int clc_depth) {
     static_assert(!RES || AFF, "the residual prologue rides on the affine one");
     using Cfg = FwdTma<IO, VEC, NCONS, R, S, RES ? 2 : 1, UNAL>;
@@ -311,15 +332,21 @@ lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_con
                 if constexpr (RES) tma_prefetch_desc(&tmr);
             }
             const uint64_t pol = policy_evict_first();
+            const auto fx = Reg::flat(a.x, T, N, a.ld);
+            const auto fr = Reg::flat(a.af.residual, T, N, a.ld);
             auto rows_of = [&](int64_t rb) { return (int)min((int64_t)R, T - rb * R); };
             produce<S, Cfg::STAGE_BYTES, UNAL>(
                 smem, bar, nrb, clc_depth,
-                [&](int64_t rb) { return (RES ? 2u : 1u) * Reg::tx_bytes(rows_of(rb)); },
+                [&](int tile, int64_t rb) {
+                    const int64_t c0 = (int64_t)tile * W;
+                    uint32_t b = Reg::tx_bytes(fx, rb * R, rows_of(rb), c0, a.ld);
+                    if constexpr (RES) b += Reg::tx_bytes(fr, rb * R, rows_of(rb), c0, a.ld);
+                    return b;
+                },
                 [&](unsigned char* stg, int tile, int64_t rb, uint64_t* fb) {
-                    Reg::load(stg, &tmx, &tmx_tail, (int64_t)tile * W, rb * R, rows_of(rb), a.ld, a.x_off, fb, pol);
+                    Reg::load(stg, &tmx, fx, (int64_t)tile * W, rb * R, rows_of(rb), a.ld, fb, pol);
                     if constexpr (RES)
-                        Reg::load(stg + Cfg::R_OFF, &tmr, &tmr_tail, (int64_t)tile * W, rb * R, rows_of(rb), a.ld,
-                                  a.r_off, fb, pol, R);
+                        Reg::load(stg + Cfg::R_OFF, &tmr, fr, (int64_t)tile * W, rb * R, rows_of(rb), a.ld, fb, pol, R);
                 });
         }
         return;
@@ -516,10 +543,7 @@ __global__ void __launch_bounds__(NCONS + 32)
 lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
                                   const __grid_constant__ CUtensorMap tmg,
                                   const __grid_constant__ CUtensorMap tmck,
-                                  const __grid_constant__ CUtensorMap tmr,
-                                  const __grid_constant__ CUtensorMap tmx_tail,
-                                  const __grid_constant__ CUtensorMap tmg_tail,
-                                  const __grid_constant__ CUtensorMap tmr_tail, const BwdArgs a,
+                                  const __grid_constant__ CUtensorMap tmr, const BwdArgs a,
                                   const int clc_depth) {
     constexpr bool RES = Mode<MODE>::RES;
     static_assert(!RES || Mode<MODE>::AFF, "the residual prologue rides on the affine one");
@@ -546,9 +570,18 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
                 const int64_t ch = nch - 1 - j;
                 return (int)min((int64_t)kCkpt, T - ch * kCkpt);
             };
+            const auto fx = Reg::flat(a.x, T, N, ld);
+            const auto fg = Reg::flat(a.gS, T, N, ld);
+            const auto fr = Reg::flat(a.af.residual, T, N, ld);
             produce<S, Cfg::STAGE_BYTES, UNAL>(
                 smem, bar, nch, clc_depth,
-                [&](int64_t j) { return (uint32_t)Cfg::NIN * Reg::tx_bytes(rows_of(j)) + (uint32_t)(NB * Cfg::CK_BOX_BYTES); },
+                [&](int tile, int64_t j) {
+                    const int64_t t0 = (nch - 1 - j) * kCkpt, c0 = (int64_t)tile * W;
+                    uint32_t b = (uint32_t)(NB * Cfg::CK_BOX_BYTES) + Reg::tx_bytes(fx, t0, rows_of(j), c0, ld) +
+                                 Reg::tx_bytes(fg, t0, rows_of(j), c0, ld);
+                    if constexpr (RES) b += Reg::tx_bytes(fr, t0, rows_of(j), c0, ld);
+                    return b;
+                },
                 [&](unsigned char* stg, int tile, int64_t j, uint64_t* fb) {
                     const int64_t ch = nch - 1 - j;
                     const int rows = rows_of(j);
@@ -559,11 +592,9 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
                             tma_load_2d(stg + Cfg::CK_OFF + b * Cfg::CK_BOX_BYTES, &tmck, (int)(c0 + b * BW), (int)ch,
                                         fb, pol);
                     }
-                    Reg::load(stg + Cfg::X_OFF, &tmx, &tmx_tail, c0, ch * kCkpt, rows, ld, a.x_off, fb, pol);
-                    Reg::load(stg + Cfg::G_OFF, &tmg, &tmg_tail, c0, ch * kCkpt, rows, ld, a.g_off, fb, pol, kCkpt);
-                    if constexpr (RES)
-                        Reg::load(stg + Cfg::R_OFF, &tmr, &tmr_tail, c0, ch * kCkpt, rows, ld, a.r_off, fb, pol,
-                                  2 * kCkpt);
+                    Reg::load(stg + Cfg::X_OFF, &tmx, fx, c0, ch * kCkpt, rows, ld, fb, pol);
+                    Reg::load(stg + Cfg::G_OFF, &tmg, fg, c0, ch * kCkpt, rows, ld, fb, pol, kCkpt);
+                    if constexpr (RES) Reg::load(stg + Cfg::R_OFF, &tmr, fr, c0, ch * kCkpt, rows, ld, fb, pol, 2 * kCkpt);
                 });
         }
         return;
@@ -677,8 +708,7 @@ struct BwdHTma {
 template <typename IO, int VEC, int MODE, int NCONS, int R, int S, bool UNAL>
 __global__ void __launch_bounds__(NCONS + 32)
 lif_backward_saveh_tma_kernel(const __grid_constant__ CUtensorMap tmh,
-                              const __grid_constant__ CUtensorMap tmg,
-                              const __grid_constant__ CUtensorMap tmg_tail, const BwdArgs a,
+                              const __grid_constant__ CUtensorMap tmg, const BwdArgs a,
                               const int clc_depth) {
     using Cfg = BwdHTma<IO, VEC, NCONS, R, S, UNAL>;
     using Reg = typename Cfg::Reg;
@@ -700,9 +730,13 @@ lif_backward_saveh_tma_kernel(const __grid_constant__ CUtensorMap tmh,
                 const int64_t rb = nrb - 1 - j;
                 return (int)min((int64_t)R, T - rb * R);
             };
+            const auto fg = Reg::flat(a.gS, T, N, ld);
             produce<S, Cfg::STAGE_BYTES, UNAL>(
                 smem, bar, nrb, clc_depth,
-                [&](int64_t j) { return (uint32_t)(NB * Cfg::HBOX) + Reg::tx_bytes(rows_of(j)); },
+                [&](int tile, int64_t j) {
+                    return (uint32_t)(NB * Cfg::HBOX) +
+                           Reg::tx_bytes(fg, (nrb - 1 - j) * R, rows_of(j), (int64_t)tile * W, ld);
+                },
                 [&](unsigned char* stg, int tile, int64_t j, uint64_t* fb) {
                     const int64_t rb = nrb - 1 - j;
                     const int64_t c0 = (int64_t)tile * W;
@@ -711,7 +745,7 @@ lif_backward_saveh_tma_kernel(const __grid_constant__ CUtensorMap tmh,
                         for (int b = 0; b < NB; ++b)   // H: the saved rows are always 16-B aligned
                             tma_load_2d(stg + b * Cfg::HBOX, &tmh, (int)(c0 + b * BW), (int)(rb * R), fb, pol);
                     }
-                    Reg::load(stg + Cfg::G_OFF, &tmg, &tmg_tail, c0, rb * R, rows_of(j), ld, a.g_off, fb, pol);
+                    Reg::load(stg + Cfg::G_OFF, &tmg, fg, c0, rb * R, rows_of(j), ld, fb, pol);
                 });
         }
         return;

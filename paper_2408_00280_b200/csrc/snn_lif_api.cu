@@ -115,32 +115,6 @@ bool encode_2d(CUtensorMap* m, const void* base, size_t esz, int64_t inner, int6
     return r == CUDA_SUCCESS;
 }
 
-bool encode_1d(CUtensorMap* m, const void* base, size_t esz, int64_t extent, int box) {
-    EncodeTiledFn fn = encode_fn();
-    if (!fn) return false;
-    const CUtensorMapDataType dt = esz == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
-                                            : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
-    // Written as a one-row 2-D map {extent, 1} (row stride rounded up to 16 B): the loads are the
-    // ordinary 2-D tile loads at row 0, and the encode needs no rank-1 special case.
-    const cuuint64_t dims[2] = {(cuuint64_t)extent, 1};
-    const cuuint64_t strides[1] = {(cuuint64_t)((extent * (int64_t)esz + 15) / 16 * 16)};
-    const cuuint32_t boxd[2] = {(cuuint32_t)box, 1};
-    const cuuint32_t estr[2] = {1, 1};
-    auto encode = [&] {
-        return fn(m, dt, 2, const_cast<void*>(base), dims, strides, boxd, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    };
-    CUresult r = encode();
-    if (r == CUDA_ERROR_INVALID_CONTEXT) {
-        cudaFree(nullptr);
-        r = encode();
-    }
-    if (r != CUDA_SUCCESS)
-        snprintf(g_enc, sizeof(g_enc), " [CUresult %d: 1-D base %p extent %lld box %d]", (int)r, base,
-                 (long long)extent, box);
-    return r == CUDA_SUCCESS;
-}
-
 const char* encode_detail() { return g_enc; }
 
 int cached_occupancy(const void* k, int threads, int smem, int (*prep)(const void*, int, int)) {
