@@ -79,6 +79,36 @@ affine_finish_kernel(const float* __restrict__ part_a, const float* __restrict__
     }
 }
 
+// Per-channel sums of the segment partials the TMA backward wrote (affine_tile_segments):
+// channel c owns segments ((b C + c) HW) / G + p, b < B, p < P = HW / G.  One CTA per channel:
+// thread i sums flat (b, p) indices i, i + 256, ... in order, then a fixed shuffle tree and
+// warp 0 adds the 8 warp partials in order -- deterministic.
+__global__ void __launch_bounds__(256)
+affine_segment_finish_kernel(const float* __restrict__ seg_a, const float* __restrict__ seg_b, int64_t B,
+                             int64_t C, int64_t P, float* __restrict__ grad_scale, float* __restrict__ grad_shift) {
+    pdl_wait();
+    const int64_t c = blockIdx.x;
+    float ta = 0.0f, tb = 0.0f;
+    for (int64_t i = threadIdx.x; i < B * P; i += blockDim.x) {
+        const int64_t s = ((i / P) * C + c) * P + i % P;
+        ta = __fadd_rn(ta, seg_a[s]);
+        tb = __fadd_rn(tb, seg_b[s]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        ta = __fadd_rn(ta, __shfl_xor_sync(0xffffffffu, ta, o));
+        tb = __fadd_rn(tb, __shfl_xor_sync(0xffffffffu, tb, o));
+    }
+    __shared__ float sa[8], sb[8];
+    if ((threadIdx.x & 31) == 0) { sa[threadIdx.x >> 5] = ta; sb[threadIdx.x >> 5] = tb; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < 8; ++w) { sa[0] = __fadd_rn(sa[0], sa[w]); sb[0] = __fadd_rn(sb[0], sb[w]); }
+        grad_scale[c] = sa[0];
+        grad_shift[c] = sb[0];
+    }
+}
+
 }  // namespace snn
 
 namespace snn_host {
@@ -128,6 +158,13 @@ snn_status launch_backward_generic(const snn_lif_shape* s, const snn::BwdArgs& a
     if (s->io_dtype == SNN_BF16)
         return vec ? go<__nv_bfloat16, 2>(s, a, mode, st) : go<__nv_bfloat16, 1>(s, a, mode, st);
     return vec ? go<float, 2>(s, a, mode, st) : go<float, 1>(s, a, mode, st);
+}
+
+snn_status launch_affine_segment_finish(const float* seg_a, const float* seg_b, int64_t B, int64_t C, int64_t HW,
+                                        int G, float* grad_scale, float* grad_shift, cudaStream_t st) {
+    if (C > INT32_MAX) return fail(SNN_ERR_INVALID_VALUE, "affine: too many channels");
+    return launch_pdl(snn::affine_segment_finish_kernel, dim3((unsigned)C), dim3(256), st,
+                      "affine_segment_finish_kernel", seg_a, seg_b, B, C, (int64_t)(HW / G), grad_scale, grad_shift);
 }
 
 snn_status launch_affine_reduce(float* part_a, float* part_b, int64_t B, int64_t C, int64_t HW,

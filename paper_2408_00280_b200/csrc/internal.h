@@ -140,7 +140,8 @@ snn_status backward_impl(const snn_lif_params* p, const snn_lif_shape* s, const 
                          const void* x, const void* saved, const float* grad_v_final,
                          const snn_lif_handoff* handoff, void* grad_x, float* grad_v_init, void* stream,
                          const snn_lif_affine* affine = nullptr, float* part_a = nullptr,
-                         float* part_b = nullptr, const ChunkView* cv = nullptr);
+                         float* part_b = nullptr, const ChunkView* cv = nullptr, int* seg_out = nullptr);
+int affine_segment(int64_t HW);
 int64_t saved_row_stride(const snn_lif_shape* s);   // round_up(N, 16)
 
 // ---- launchers (one translation unit each, compiled in parallel) -------------------
@@ -160,6 +161,9 @@ snn_status launch_forward_tma_unal_bf16(const snn_lif_shape* s, const snn::FwdAr
 snn_status launch_backward_tma_unal_f32(const snn_lif_shape* s, const snn::BwdArgs& a, int mode, cudaStream_t st);
 snn_status launch_backward_tma_unal_bf16(const snn_lif_shape* s, const snn::BwdArgs& a, int mode, cudaStream_t st);
 int tma_vec_forward(int io_dtype);
+// Channel sums of the per-tile segment partials of the fused affine backward (G neurons each).
+snn_status launch_affine_segment_finish(const float* seg_a, const float* seg_b, int64_t B, int64_t C, int64_t HW,
+                                        int G, float* grad_scale, float* grad_shift, cudaStream_t st);
 // part_a / part_b are scratch: the reduction overwrites some of their entries.
 snn_status launch_affine_reduce(float* part_a, float* part_b, int64_t B, int64_t C,
                                 int64_t HW, float* grad_scale, float* grad_shift, cudaStream_t st);

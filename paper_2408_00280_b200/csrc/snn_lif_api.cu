@@ -358,7 +358,8 @@ snn_status backward_impl(const snn_lif_params* p, const snn_lif_shape* s,
                          const void* grad_spikes, const void* x, const void* saved,
                          const float* grad_v_final, const snn_lif_handoff* handoff, void* grad_x,
                          float* grad_v_init, void* stream, const snn_lif_affine* affine,
-                         float* part_a, float* part_b, const ChunkView* cv) {
+                         float* part_a, float* part_b, const ChunkView* cv, int* seg_out) {
+    if (seg_out) *seg_out = 0;
     g_err[0] = 0;
     snn_status st;
     if ((st = check_params(p)) != SNN_OK) return st;
@@ -395,6 +396,7 @@ snn_status backward_impl(const snn_lif_params* p, const snn_lif_shape* s,
         a.af = to_dev(affine);
         a.af.part_a = part_a;
         a.af.part_b = part_b;
+        a.af.seg = 0;   // set below when the TMA kernels fold the channel reduction in
         mode |= 8;
         if ((affine->residual == nullptr) != (affine->grad_residual == nullptr))
             return fail(SNN_ERR_NULL_POINTER, "residual and grad_residual go together");
@@ -413,6 +415,7 @@ snn_status backward_impl(const snn_lif_params* p, const snn_lif_shape* s,
         // Mode::P0; the SAVE_H kernel has no P0 instantiation)
         const int tmode = (mode < 8 && s->save_mode == SNN_SAVE_RECOMPUTE && !p->decay_input &&
                            p->v_reset == 0.0f) ? (mode | 32) : mode;
+        if (affine && seg_out) a.af.seg = *seg_out = affine_segment(affine->HW);
         return s->io_dtype == SNN_BF16 ? launch_backward_tma_bf16(s, a, tmode, path == Path::UNALIGNED, cs)
                                        : launch_backward_tma_f32(s, a, tmode, path == Path::UNALIGNED, cs);
     }
@@ -431,6 +434,15 @@ snn_status backward_impl(const snn_lif_params* p, const snn_lif_shape* s,
 }
 
 int64_t saved_row_stride(const snn_lif_shape* s) { return saved_ld(s); }
+
+// Segment length of the affine reduction folded into the TMA backward's tile epilogue
+// (lif_kernels.cuh affine_tile_segments): G = min(HW, 512) when it divides both the 512-neuron
+// tile and the channel block of HW neurons (HW a power of two >= 2, or a multiple of 512);
+// 0 = the per-neuron partials + two-pass reduction.
+int affine_segment(int64_t HW) {
+    if (HW >= snn::kSegTile) return HW % snn::kSegTile == 0 ? snn::kSegTile : 0;
+    return (HW >= 2 && (HW & (HW - 1)) == 0) ? (int)HW : 0;
+}
 
 }  // namespace snn_host
 
@@ -464,9 +476,13 @@ snn_status snn_lif_backward_affine(const snn_lif_params* p, const snn_lif_shape*
                                    float* grad_scale, float* grad_shift, void* stream) {
     if (!af) return fail(SNN_ERR_NULL_POINTER, "affine is NULL");
     if (!grad_scale || !grad_shift) return fail(SNN_ERR_NULL_POINTER, "grad_scale / grad_shift is NULL");
+    int seg = 0;
     snn_status st = backward_impl(p, s, grad_spikes, x, saved, grad_v_final, nullptr, grad_x, grad_v_init,
-                                  stream, af, part_a, part_b);
+                                  stream, af, part_a, part_b, nullptr, &seg);
     if (st != SNN_OK) return st;
+    if (seg > 0)   // the backward already reduced each tile into channel segments: one tiny finish
+        return launch_affine_segment_finish(part_a, part_b, s->N / (af->C * af->HW), af->C, af->HW, seg,
+                                            grad_scale, grad_shift, static_cast<cudaStream_t>(stream));
     return launch_affine_reduce(part_a, part_b, s->N / (af->C * af->HW), af->C, af->HW, grad_scale,
                                 grad_shift, static_cast<cudaStream_t>(stream));
 }

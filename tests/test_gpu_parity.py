@@ -720,3 +720,36 @@ def test_cfg4_stem_with_bn_and_residual_full_size_sampled():
     rep = compare(PAPER, ref_scaled, ref["gX"] * a[None, :], ref["gvi"], f.spikes[:, ci].cpu(),
                   gx[:, ci].cpu(), col_ids=cols)
     assert_ok(rep)
+
+
+@pytest.mark.parametrize("HW,B,C,dtype", [(2, 8, 33, torch.float32), (32, 4, 5, torch.float32),
+                                          (128, 3, 3, torch.bfloat16), (512, 2, 3, torch.float32),
+                                          (2048, 2, 2, torch.float32), (64, 5, 7, torch.bfloat16)])
+def test_affine_reduction_folded_into_backward(HW, B, C, dtype):
+    """HW a power of two (or a multiple of 512): the TMA backward reduces its tile's partials into
+    channel segments in the epilogue and one finish kernel sums them (no per-neuron partials, no
+    two-pass reduction).  Parity of dscale / dshift with the oracle, bitwise determinism run to
+    run, every segment shape (lanes per segment 1 .. 256, several warps per segment, ragged last
+    tile)."""
+    T = 21
+    N = B * C * HW
+    X, G, sc, sh = _affine_case(PAPER, T, B, C, HW, dtype, 701 + HW)
+    af = snn.AffineSpec(sc.cuda(), sh.cuda(), C, HW)
+    outs = []
+    for _ in range(2):
+        f = snn.lif_forward_affine(X.cuda(), PAPER, af)
+        outs.append(snn.lif_backward_affine(G.cuda(), f))
+        torch.cuda.synchronize()
+    for a_, b_ in zip(*outs):
+        assert torch.equal(a_, b_)
+    gx, gvi, gsc, gsh = outs[0]
+    Xp = oracle.affine_input(X.double().numpy(), sc.double().numpy(), sh.double().numpy(), C, HW)
+    ref = oracle_run(PAPER, Xp, G)
+    rgx, rgs, rgb = oracle.affine_grads(X.double().numpy(), ref["gX"], sc.double().numpy(), C, HW)
+    cidx = (np.arange(N) // HW) % C
+    bnd = ref["gX_bound"]
+    tol_s = np.zeros(C); tol_b = np.zeros(C)
+    np.add.at(tol_s, cidx, (bnd * np.abs(X.double().numpy())).sum(0)); np.add.at(tol_b, cidx, bnd.sum(0))
+    rtol = 1e-2 if dtype == torch.bfloat16 else 1e-5
+    assert np.all(np.abs(gsc.cpu().numpy() - rgs) <= rtol * tol_s + 1e-30)
+    assert np.all(np.abs(gsh.cpu().numpy() - rgb) <= rtol * tol_b + 1e-30)
