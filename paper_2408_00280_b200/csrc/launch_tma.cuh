@@ -97,7 +97,6 @@ snn_status launch_forward_tma(const snn_lif_shape* s, const snn::FwdArgs& a0, bo
 template <typename IO, int MODE, bool UNAL>
 snn_status launch_backward_tma_mode(const snn_lif_shape* s, const snn::BwdArgs& a0, cudaStream_t st) {
     using C = TmaCfg<IO>;
-    static_assert(MODE < 32 || (MODE & 24) == 0, "P0 variants are plain-path only");
     snn::BwdArgs a = a0;
     a.x_off = a.g_off = a.r_off = 0;
     if constexpr (MODE < 8) {   // SAVE_H has no affine-gradient or P0 variant (host never asks)
@@ -164,6 +163,22 @@ snn_status launch_backward_tma(const snn_lif_shape* s, const snn::BwdArgs& a, in
         case 37: return launch_backward_tma_mode<IO, 37, UNAL>(s, a, st);
         case 38: return launch_backward_tma_mode<IO, 38, UNAL>(s, a, st);
         case 39: return launch_backward_tma_mode<IO, 39, UNAL>(s, a, st);
+        case 40: return launch_backward_tma_mode<IO, 40, UNAL>(s, a, st);
+        case 41: return launch_backward_tma_mode<IO, 41, UNAL>(s, a, st);
+        case 42: return launch_backward_tma_mode<IO, 42, UNAL>(s, a, st);
+        case 43: return launch_backward_tma_mode<IO, 43, UNAL>(s, a, st);
+        case 44: return launch_backward_tma_mode<IO, 44, UNAL>(s, a, st);
+        case 45: return launch_backward_tma_mode<IO, 45, UNAL>(s, a, st);
+        case 46: return launch_backward_tma_mode<IO, 46, UNAL>(s, a, st);
+        case 47: return launch_backward_tma_mode<IO, 47, UNAL>(s, a, st);
+        case 56: return launch_backward_tma_mode<IO, 56, UNAL>(s, a, st);
+        case 57: return launch_backward_tma_mode<IO, 57, UNAL>(s, a, st);
+        case 58: return launch_backward_tma_mode<IO, 58, UNAL>(s, a, st);
+        case 59: return launch_backward_tma_mode<IO, 59, UNAL>(s, a, st);
+        case 60: return launch_backward_tma_mode<IO, 60, UNAL>(s, a, st);
+        case 61: return launch_backward_tma_mode<IO, 61, UNAL>(s, a, st);
+        case 62: return launch_backward_tma_mode<IO, 62, UNAL>(s, a, st);
+        case 63: return launch_backward_tma_mode<IO, 63, UNAL>(s, a, st);
         default: return fail(SNN_ERR_UNSUPPORTED, "backward variant %d (residual without affine)", mode);
     }
 }

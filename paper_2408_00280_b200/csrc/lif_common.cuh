@@ -44,7 +44,8 @@ struct Mode {
     static constexpr bool RES = (MODE & 16) != 0;  // + residual add (implies AFF; TMA path only)
     // Paper-mode constants (decay_input = 0, V_reset = 0: s = 1, c0 = 0): the charge is
     // fma(k, V, X) and gX = gH -- the same values up to the sign of a zero (fma(1, -0, +0) is
-    // +0), two fewer paired ops per backward step.  Plain TMA path only.
+    // +0), two fewer paired ops per backward step.  TMA RECOMPUTE backward (plain / affine /
+    // residual).
     static constexpr bool P0 = (MODE & 32) != 0;
 };
 

@@ -411,10 +411,10 @@ snn_status backward_impl(const snn_lif_params* p, const snn_lif_shape* s,
 
     const Path path = tma_path(s, {grad_spikes, grad_x, s->save_mode == SNN_SAVE_RECOMPUTE ? x : nullptr, res, gres});
     if (path != Path::GENERIC) {
-        // paper-mode constants on the plain RECOMPUTE path: the P0 variants (lif_common.cuh
-        // Mode::P0; the SAVE_H kernel has no P0 instantiation)
-        const int tmode = (mode < 8 && s->save_mode == SNN_SAVE_RECOMPUTE && !p->decay_input &&
-                           p->v_reset == 0.0f) ? (mode | 32) : mode;
+        // paper-mode constants on the RECOMPUTE path (plain, affine, residual): the P0 variants
+        // (lif_common.cuh Mode::P0; the SAVE_H kernel has no P0 instantiation)
+        const int tmode = (s->save_mode == SNN_SAVE_RECOMPUTE && !p->decay_input && p->v_reset == 0.0f)
+                              ? (mode | 32) : mode;
         if (affine && seg_out) a.af.seg = *seg_out = affine_segment(affine->HW);
         return s->io_dtype == SNN_BF16 ? launch_backward_tma_bf16(s, a, tmode, path == Path::UNALIGNED, cs)
                                        : launch_backward_tma_f32(s, a, tmode, path == Path::UNALIGNED, cs);
