@@ -79,7 +79,7 @@ affine_finish_kernel(const float* __restrict__ part_a, const float* __restrict__
     }
 }
 
-// Per-channel sums of the segment partials the TMA backward wrote (affine_tile_segments):
+// Per-channel sums of the segment partials the TMA backward wrote (affine_warp_segments):
 // channel c owns segments ((b C + c) HW) / G + p, b < B, p < P = HW / G.  One CTA per channel:
 // thread i sums flat (b, p) indices i, i + 256, ... in order, then a fixed shuffle tree and
 // warp 0 adds the 8 warp partials in order -- deterministic.

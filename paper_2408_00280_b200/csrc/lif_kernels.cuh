@@ -45,7 +45,7 @@ struct Affine {
     float* part_a;        // [N] backward output (per-neuron sum over t) or null
     float* part_b;        // [N]
     int seg;              // > 0: the backward reduces the partials itself into segments of `seg`
-                          // neurons (affine_tile_segments) written to part_a/b[n / seg]; 0: per neuron
+                          // neurons (affine_warp_segments) written to part_a/b[n / seg]; 0: per neuron
     const void* residual; // [T, ld] IO shortcut R added to the input (X' = a X + b + R) or null
     void* grad_residual;  // [T, ld] IO backward output dL/dR = dL/dX' (iff residual)
 };
@@ -103,51 +103,31 @@ struct BwdArgs {
 };
 
 // ------------------------------------------------------------------------------------
-// Affine gradients folded into the backward's tile epilogue: the per-neuron
-// partials of a 512-neuron tile (NCONS = 256 threads x VEC = 2 neurons) are summed over
-// segments of G consecutive neurons -- G = min(HW, 512), so a segment never crosses a
-// (sample, channel) block of HW neurons -- in a fixed order (lane pair, xor-shuffle tree inside
-// G/2 lanes, then warp partials in order through smem), and segment s is written to
-// seg_a/b[s].  Deterministic run to run, and identical wherever it is called (the TMA
-// backward's epilogue, the generic path's affine_segment_kernel).  `sync` synchronises the
-// NCONS threads; ct = thread index among them; red = NCONS/32 x 2 floats of smem.
-constexpr int kSegTile = 512;
-template <int NCONS, int VEC, typename Sync>
-__device__ __forceinline__ void affine_tile_segments(const float (&pa)[VEC], const float (&pb)[VEC], int nvalid,
-                                                     int64_t tile_n0, int ct, int G, int64_t nseg, float* seg_a,
-                                                     float* seg_b, float* red, Sync sync) {
-    static_assert(NCONS * VEC == kSegTile, "segment tile geometry");
+// Affine gradients folded into the backward's tile epilogue: a warp's
+// per-neuron partials (32 lanes x VEC = 2 neurons) are summed over segments of G consecutive
+// neurons -- G = min(HW, 64) with G | HW, so a segment never crosses a (sample, channel) block of
+// HW neurons and never leaves its warp -- in a fixed order (the lane's pair, then an xor-shuffle
+// tree inside G/2 lanes); the segment starting at neuron n is written to seg_a/b[n / G].  No
+// cross-warp synchronisation (the tile epilogue stays asynchronous between warps); the channel
+// totals are summed by affine_segment_finish_kernel.  Deterministic run to run.
+constexpr int kSegMax = 64;
+template <int VEC>
+__device__ __forceinline__ void affine_warp_segments(const float (&pa)[VEC], const float (&pb)[VEC], int nvalid,
+                                                     int64_t n0, int G, int64_t nseg, float* seg_a, float* seg_b) {
+    static_assert(VEC * 32 == kSegMax, "a warp covers one 64-neuron segment");
     float a = 0.0f, b = 0.0f;
 #pragma unroll
     for (int i = 0; i < VEC; ++i)
         if (i < nvalid) { a = __fadd_rn(a, pa[i]); b = __fadd_rn(b, pb[i]); }
-    const int L = G / VEC;                     // lanes per segment (>= 1)
-    const int LW = L < 32 ? L : 32;
-    for (int o = 1; o < LW; o <<= 1) {
+    const int L = G / VEC;                     // lanes per segment, 1 .. 32
+    for (int o = 1; o < L; o <<= 1) {
         a = __fadd_rn(a, __shfl_xor_sync(0xffffffffu, a, o));
         b = __fadd_rn(b, __shfl_xor_sync(0xffffffffu, b, o));
     }
-    const int lane = ct & 31, warp = ct >> 5;
-    if (L <= 32) {
-        if ((lane % L) == 0) {
-            const int64_t sidx = (tile_n0 + (int64_t)ct * VEC) / G;
-            if (sidx < nseg) { seg_a[sidx] = a; seg_b[sidx] = b; }
-        }
-        return;
+    if (((threadIdx.x & 31) % L) == 0) {
+        const int64_t sidx = n0 / G;
+        if (sidx < nseg) { seg_a[sidx] = a; seg_b[sidx] = b; }
     }
-    if (lane == 0) { red[warp] = a; red[NCONS / 32 + warp] = b; }
-    sync();
-    const int wps = L / 32;                    // warps per segment
-    if (ct < kSegTile / G) {
-        float ta = red[ct * wps], tb = red[NCONS / 32 + ct * wps];
-        for (int w = 1; w < wps; ++w) {
-            ta = __fadd_rn(ta, red[ct * wps + w]);
-            tb = __fadd_rn(tb, red[NCONS / 32 + ct * wps + w]);
-        }
-        const int64_t sidx = tile_n0 / G + ct;
-        if (sidx < nseg) { seg_a[sidx] = ta; seg_b[sidx] = tb; }
-    }
-    sync();                                    // red[] is reused by the next tile
 }
 
 // ------------------------------------------------------------------------------------

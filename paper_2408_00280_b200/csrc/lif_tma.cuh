@@ -51,7 +51,6 @@ struct Barriers {
     uint64_t empty[S];   // consumers -> producer: stage released (one arrive per warp)
     int tile[S];         // tile index the stage belongs to; -1 = no more work
     ClcSlot clc[4];      // cluster-launch-control response slots (work stealing)
-    float red[16];       // consumer-warp partials of the affine segment sums (<= 8 warps x 2)
 };
 
 constexpr int kMaxClc = 4;
@@ -682,10 +681,8 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
             handoff_send<VEC, NCONS>(a.h, tile, W, N, n0, nvalid, gV);
         if constexpr (Mode<MODE>::AFF) {
             if (a.af.seg > 0) {   // uniform: fold the per-channel reduction into the tile epilogue
-                if constexpr (W == kSegTile)
-                    affine_tile_segments<NCONS, VEC>(pa, pb, nvalid, (int64_t)tile * W, ct, a.af.seg, N / a.af.seg,
-                                                     a.af.part_a, a.af.part_b, bar->red,
-                                                     [] { consumers_sync<NCONS>(); });
+                if constexpr (VEC * 32 == kSegMax)
+                    affine_warp_segments<VEC>(pa, pb, nvalid, n0, a.af.seg, N / a.af.seg, a.af.part_a, a.af.part_b);
             } else if (nvalid > 0) {
                 store_vec<VEC>(a.af.part_a + n0, nvalid, pa);
                 store_vec<VEC>(a.af.part_b + n0, nvalid, pb);

@@ -436,11 +436,11 @@ snn_status backward_impl(const snn_lif_params* p, const snn_lif_shape* s,
 int64_t saved_row_stride(const snn_lif_shape* s) { return saved_ld(s); }
 
 // Segment length of the affine reduction folded into the TMA backward's tile epilogue
-// (lif_kernels.cuh affine_tile_segments): G = min(HW, 512) when it divides both the 512-neuron
-// tile and the channel block of HW neurons (HW a power of two >= 2, or a multiple of 512);
-// 0 = the per-neuron partials + two-pass reduction.
+// (lif_kernels.cuh affine_warp_segments): G = min(HW, 64) when it divides the channel block of
+// HW neurons (HW a multiple of 64, or a power of two >= 2); 0 = the per-neuron partials + the
+// two-pass reduction.
 int affine_segment(int64_t HW) {
-    if (HW >= snn::kSegTile) return HW % snn::kSegTile == 0 ? snn::kSegTile : 0;
+    if (HW >= snn::kSegMax) return HW % snn::kSegMax == 0 ? snn::kSegMax : 0;
     return (HW >= 2 && (HW & (HW - 1)) == 0) ? (int)HW : 0;
 }
 

@@ -722,15 +722,15 @@ def test_cfg4_stem_with_bn_and_residual_full_size_sampled():
     assert_ok(rep)
 
 
-@pytest.mark.parametrize("HW,B,C,dtype", [(2, 8, 33, torch.float32), (32, 4, 5, torch.float32),
+@pytest.mark.parametrize("HW,B,C,dtype", [(2, 8, 33, torch.float32), (32, 4, 5, torch.float32), (192, 3, 2, torch.float32),
                                           (128, 3, 3, torch.bfloat16), (512, 2, 3, torch.float32),
                                           (2048, 2, 2, torch.float32), (64, 5, 7, torch.bfloat16)])
 def test_affine_reduction_folded_into_backward(HW, B, C, dtype):
-    """HW a power of two (or a multiple of 512): the TMA backward reduces its tile's partials into
-    channel segments in the epilogue and one finish kernel sums them (no per-neuron partials, no
-    two-pass reduction).  Parity of dscale / dshift with the oracle, bitwise determinism run to
-    run, every segment shape (lanes per segment 1 .. 256, several warps per segment, ragged last
-    tile)."""
+    """HW a power of two or a multiple of 64: the TMA backward reduces each warp's partials into
+    channel segments of min(HW, 64) neurons in its tile epilogue and one finish kernel sums them
+    (no per-neuron partials, no two-pass reduction).  Parity of dscale / dshift with the oracle,
+    bitwise determinism run to run, every segment shape (1 .. 32 lanes per segment, HW = 192 =
+    3 x 64, a ragged last tile)."""
     T = 21
     N = B * C * HW
     X, G, sc, sh = _affine_case(PAPER, T, B, C, HW, dtype, 701 + HW)
