@@ -3,8 +3,9 @@
 #include "launch_tma.cuh"
 
 namespace snn_host {
-snn_status launch_forward_tma_bf16(const snn_lif_shape* s, const snn::FwdArgs& a, bool soft, bool unal, cudaStream_t st) {
-    if (unal) return launch_forward_tma_unal_bf16(s, a, soft, st);
-    return launch_forward_tma<__nv_bfloat16, false>(s, a, soft, st);
+snn_status launch_forward_tma_bf16(const snn_lif_shape* s, const snn::FwdArgs& a, bool soft, bool p0, bool unal,
+                                  cudaStream_t st) {
+    if (unal) return launch_forward_tma_unal_bf16(s, a, soft, p0, st);
+    return launch_forward_tma<__nv_bfloat16, false>(s, a, soft, p0, st);
 }
 }  // namespace snn_host

@@ -3,7 +3,8 @@
 #include "launch_tma.cuh"
 
 namespace snn_host {
-snn_status launch_forward_tma_unal_bf16(const snn_lif_shape* s, const snn::FwdArgs& a, bool soft, cudaStream_t st) {
-    return launch_forward_tma<__nv_bfloat16, true>(s, a, soft, st);
+snn_status launch_forward_tma_unal_bf16(const snn_lif_shape* s, const snn::FwdArgs& a, bool soft, bool p0,
+                                       cudaStream_t st) {
+    return launch_forward_tma<__nv_bfloat16, true>(s, a, soft, p0, st);
 }
 }  // namespace snn_host

@@ -152,12 +152,17 @@ snn_status launch_backward_generic(const snn_lif_shape* s, const snn::BwdArgs& a
                                    cudaStream_t st);
 // TMA path, any N; unal = the io rows are not 16-B aligned (1-D tensor maps).  The _unal
 // halves live in their own translation units (parallel build).
-snn_status launch_forward_tma_f32(const snn_lif_shape* s, const snn::FwdArgs& a, bool soft, bool unal, cudaStream_t st);
-snn_status launch_forward_tma_bf16(const snn_lif_shape* s, const snn::FwdArgs& a, bool soft, bool unal, cudaStream_t st);
+// p0: paper-mode constants (decay_input = 0, V_reset = 0) -- the prologue variants' short charge.
+snn_status launch_forward_tma_f32(const snn_lif_shape* s, const snn::FwdArgs& a, bool soft, bool p0, bool unal,
+                                  cudaStream_t st);
+snn_status launch_forward_tma_bf16(const snn_lif_shape* s, const snn::FwdArgs& a, bool soft, bool p0, bool unal,
+                                   cudaStream_t st);
 snn_status launch_backward_tma_f32(const snn_lif_shape* s, const snn::BwdArgs& a, int mode, bool unal, cudaStream_t st);
 snn_status launch_backward_tma_bf16(const snn_lif_shape* s, const snn::BwdArgs& a, int mode, bool unal, cudaStream_t st);
-snn_status launch_forward_tma_unal_f32(const snn_lif_shape* s, const snn::FwdArgs& a, bool soft, cudaStream_t st);
-snn_status launch_forward_tma_unal_bf16(const snn_lif_shape* s, const snn::FwdArgs& a, bool soft, cudaStream_t st);
+snn_status launch_forward_tma_unal_f32(const snn_lif_shape* s, const snn::FwdArgs& a, bool soft, bool p0,
+                                       cudaStream_t st);
+snn_status launch_forward_tma_unal_bf16(const snn_lif_shape* s, const snn::FwdArgs& a, bool soft, bool p0,
+                                        cudaStream_t st);
 snn_status launch_backward_tma_unal_f32(const snn_lif_shape* s, const snn::BwdArgs& a, int mode, cudaStream_t st);
 snn_status launch_backward_tma_unal_bf16(const snn_lif_shape* s, const snn::BwdArgs& a, int mode, cudaStream_t st);
 int tma_vec_forward(int io_dtype);

@@ -44,8 +44,10 @@ bool encode_io(CUtensorMap* m, const void* base, const snn_lif_shape* s, int box
     }
 }
 
+// p0: paper-mode constants (s = 1, c0 = 0); used by the prologue variants only (for the plain
+// forward the shorter charge measured no difference).
 template <typename IO, bool UNAL>
-snn_status launch_forward_tma(const snn_lif_shape* s, const snn::FwdArgs& a0, bool soft, cudaStream_t st) {
+snn_status launch_forward_tma(const snn_lif_shape* s, const snn::FwdArgs& a0, bool soft, bool p0, cudaStream_t st) {
     using C = TmaCfg<IO>;
     snn::FwdArgs a = a0;
     CUtensorMap tmx, tmr;
@@ -60,22 +62,24 @@ snn_status launch_forward_tma(const snn_lif_shape* s, const snn::FwdArgs& a0, bo
     a.r_off = 0;
     if (res && !encode_io<IO, UNAL>(&tmr, a.af.residual, s, bw, C::FR, &a.r_off))
         return fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled failed for the residual%s", encode_detail());
-    auto go = [&](auto sfmt, auto save, auto sft, auto pro) {
+    auto go = [&](auto sfmt, auto save, auto sft, auto pro, auto pz) {
         constexpr int P = decltype(pro)::value;
         constexpr int NS = P == 2 ? C::FS_RES : C::FS;
         constexpr int NC = P == 2 ? C::FN_RES : C::FN;
         using K = snn::FwdTma<IO, C::FV, NC, C::FR, NS, P == 2 ? 2 : 1, UNAL>;
         auto k = snn::lif_forward_tma_kernel<IO, C::FV, decltype(sfmt)::value, decltype(save)::value,
-                                             (bool)decltype(sft)::value, P >= 1, P == 2, NC, C::FR, NS, UNAL>;
+                                             (bool)decltype(sft)::value, P >= 1, P == 2, NC, C::FR, NS, UNAL,
+                                             (bool)decltype(pz)::value>;
         return launch_tiles(k, K::THREADS, K::SMEM, (s->N + K::W - 1) / K::W, (s->T + C::FR - 1) / C::FR,
                             st, "lif_forward_tma_kernel", tmx, tmr, a);
     };
     auto by_aff = [&](auto sfmt, auto save, auto sft) {
-        if (a.af.scale == nullptr) return go(sfmt, save, sft, IC<0>{});
-        if (a.af.residual == nullptr) return go(sfmt, save, sft, IC<1>{});
+        if (a.af.scale == nullptr) return go(sfmt, save, sft, IC<0>{}, IC<0>{});
+        if (a.af.residual == nullptr)
+            return p0 ? go(sfmt, save, sft, IC<1>{}, IC<1>{}) : go(sfmt, save, sft, IC<1>{}, IC<0>{});
         if constexpr (decltype(save)::value == snn::SAVE_H)   // host rejects SAVE_H + residual
             return fail(SNN_ERR_UNSUPPORTED, "the residual prologue needs SAVE_RECOMPUTE or SAVE_NONE");
-        else return go(sfmt, save, sft, IC<2>{});
+        else return p0 ? go(sfmt, save, sft, IC<2>{}, IC<1>{}) : go(sfmt, save, sft, IC<2>{}, IC<0>{});
     };
     auto by_soft = [&](auto sfmt, auto save) {
         return soft ? by_aff(sfmt, save, IC<1>{}) : by_aff(sfmt, save, IC<0>{});

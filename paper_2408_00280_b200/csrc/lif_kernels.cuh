@@ -55,18 +55,36 @@ struct AffCoef {
     float a[VEC], b[VEC];
 };
 
-// AFF = false: the prologue is compiled out (the coefficients are never read).
+// AFF = false: the prologue is compiled out (the coefficients are never read).  One division
+// per group (32-bit when the indices fit): the channel of n0 + i follows by stepping hw.
 template <int VEC, bool AFF>
 __device__ __forceinline__ AffCoef<VEC> load_affine(const Affine& af, int64_t n0, int nvalid) {
     AffCoef<VEC> co;
 #pragma unroll
-    for (int i = 0; i < VEC; ++i) {
-        co.a[i] = 1.0f;
-        co.b[i] = 0.0f;
-        if (AFF && i < nvalid) {
-            const int64_t ch = ((n0 + i) / af.HW) % af.C;
-            co.a[i] = __ldg(af.scale + ch);
-            co.b[i] = __ldg(af.shift + ch);
+    for (int i = 0; i < VEC; ++i) { co.a[i] = 1.0f; co.b[i] = 0.0f; }
+    if constexpr (AFF) {
+        if (nvalid <= 0) return co;
+        int64_t blk, hw;
+        if (n0 + VEC <= (int64_t)UINT32_MAX && af.HW <= (int64_t)UINT32_MAX) {
+            const uint32_t q = (uint32_t)n0 / (uint32_t)af.HW;
+            blk = q;
+            hw = (uint32_t)n0 - q * (uint32_t)af.HW;
+        } else {
+            blk = n0 / af.HW;
+            hw = n0 - blk * af.HW;
+        }
+        int64_t ch = (af.C <= (int64_t)UINT32_MAX && blk <= (int64_t)UINT32_MAX)
+                         ? (int64_t)((uint32_t)blk % (uint32_t)af.C) : blk % af.C;
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) {
+            if (i > 0 && ++hw == af.HW) {
+                hw = 0;
+                if (++ch == af.C) ch = 0;
+            }
+            if (i < nvalid) {
+                co.a[i] = __ldg(af.scale + ch);
+                co.b[i] = __ldg(af.shift + ch);
+            }
         }
     }
     return co;
@@ -154,7 +172,8 @@ __device__ __forceinline__ float input1(const AffCoef<VEC>& co, const Pack<IO, V
     return X;
 }
 
-template <bool SOFT, bool AFF, bool RES = false, typename IO, int VEC>
+// P0 (paper-mode constants, s = 1, c0 = 0): the charge is fma(k, V, X) (Mode::P0).
+template <bool SOFT, bool AFF, bool RES = false, bool P0 = false, typename IO, int VEC>
 __device__ __forceinline__ unsigned fwd_compute(const LifConsts& c, float (&V)[VEC],
                                                 const Pack<IO, VEC>& xv, Pack<float, VEC>& hp,
                                                 const AffCoef<VEC>& co,
@@ -164,7 +183,7 @@ __device__ __forceinline__ unsigned fwd_compute(const LifConsts& c, float (&V)[V
 #pragma unroll
         for (int i = 0; i < VEC; i += 2) {
             const F2 X2 = input2<AFF, RES>(co, xv, i, rv);
-            const F2 H2 = lif_charge2(c, f2(V[i], V[i + 1]), X2);
+            const F2 H2 = lif_charge2<P0>(c, f2(V[i], V[i + 1]), X2);
             const float Ha = lo(H2), Hb = hi(H2);
             const bool Sa = lif_fire(c, Ha), Sb = lif_fire(c, Hb);
             V[i] = lif_reset<SOFT>(c, Ha, Sa);

@@ -308,7 +308,7 @@ struct FwdTma {
 };
 
 template <typename IO, int VEC, int SFMT, int SAVE, bool SOFT, bool AFF, bool RES, int NCONS, int R, int S,
-          bool UNAL>
+          bool UNAL, bool P0 = false>
 __global__ void __launch_bounds__(NCONS + 32)
 lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmr,
                        const FwdArgs a, const int clc_depth) {
@@ -411,7 +411,7 @@ lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_con
                         }
                     }
                     Pack<float, VEC> hp;
-                    const unsigned bits = fwd_compute<SOFT, AFF, RES>(c, V, xv, hp, co, &rv);
+                    const unsigned bits = fwd_compute<SOFT, AFF, RES, P0>(c, V, xv, hp, co, &rv);
                     if constexpr (SAVE == SAVE_H) {
                         if (nv > 0) st_stream<float, VEC>(h_row, hp);
                         h_row += a.ldh;

@@ -338,9 +338,10 @@ snn_status forward_impl(const snn_lif_params* p, const snn_lif_shape* s, const v
     }
 
     const Path path = tma_path(s, {x, s->spike_fmt == SNN_SPK_BITS ? nullptr : spikes, res});
+    const bool p0 = !p->decay_input && p->v_reset == 0.0f;   // paper-mode constants (Mode::P0)
     if (path != Path::GENERIC)
-        return s->io_dtype == SNN_BF16 ? launch_forward_tma_bf16(s, a, soft, path == Path::UNALIGNED, cs)
-                                       : launch_forward_tma_f32(s, a, soft, path == Path::UNALIGNED, cs);
+        return s->io_dtype == SNN_BF16 ? launch_forward_tma_bf16(s, a, soft, p0, path == Path::UNALIGNED, cs)
+                                       : launch_forward_tma_f32(s, a, soft, p0, path == Path::UNALIGNED, cs);
     if (res)
         return fail(SNN_ERR_UNSUPPORTED, "the residual prologue runs on the TMA kernels only (SNN_LIF_NO_TMA "
                                          "is set, or T*ld exceeds int32 coordinates with unaligned rows)");
