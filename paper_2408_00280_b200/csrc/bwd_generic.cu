@@ -87,6 +87,7 @@ __global__ void __launch_bounds__(256)
 affine_segment_finish_kernel(const float* __restrict__ seg_a, const float* __restrict__ seg_b, int64_t B,
                              int64_t C, int64_t P, float* __restrict__ grad_scale, float* __restrict__ grad_shift) {
     pdl_wait();
+    pdl_trigger();   // tiny: let the next kernel's launch and prologue overlap this one
     const int64_t c = blockIdx.x;
     float ta = 0.0f, tb = 0.0f;
     for (int64_t i = threadIdx.x; i < B * P; i += blockDim.x) {
