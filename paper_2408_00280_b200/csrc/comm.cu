@@ -286,7 +286,10 @@ snn_status tsplit_loop(snn_comm* c, int64_t N, int M, int dir, float* in, float*
         int64_t a, b;
         chunk_range(N, M, m, &a, &b);
         if (has_from) SNN_CUDA_OK(cudaStreamWaitEvent(st, c->recv_ev[m], 0), "cudaStreamWaitEvent");
-        if ((s = launch(m, a, b, has_from)) != SNN_OK) return s;
+        {
+            NvtxRange chunk("tsplit chunk");
+            if ((s = launch(m, a, b, has_from)) != SNN_OK) return s;
+        }
         SNN_CUDA_OK(cudaEventRecord(c->done_ev[m], st), "cudaEventRecord");
         SNN_CUDA_OK(cudaStreamWaitEvent(c->cs, c->done_ev[m], 0), "cudaStreamWaitEvent");
         // chunk m's boundary out, and the next chunk's boundary in, as one NCCL group
@@ -342,6 +345,7 @@ extern "C" {
 snn_status snn_lif_forward_tsplit(snn_comm* c, const snn_lif_params* p, const snn_lif_shape* s,
                                   int n_chunks, const void* x, void* spikes, void* saved,
                                   float* v_in_ws, float* v_out_ws, void* stream) {
+    NvtxRange range("snn_lif_forward_tsplit");
     snn_status st;
     if ((st = tsplit_common_checks(c, s, n_chunks)) != SNN_OK) return st;
     const bool first = c->rank == 0, last = c->rank == c->nranks - 1;
@@ -372,6 +376,7 @@ snn_status snn_lif_backward_tsplit(snn_comm* c, const snn_lif_params* p, const s
                                    const float* v_in_ws, const void* saved, void* grad_x,
                                    float* g_in_ws, float* g_out_ws, void* stream) {
     (void)v_in_ws;   // the RECOMPUTE checkpoints already hold each segment's V[-1]
+    NvtxRange range("snn_lif_backward_tsplit");
     snn_status st;
     if ((st = tsplit_common_checks(c, s, n_chunks)) != SNN_OK) return st;
     const bool first = c->rank == 0, last = c->rank == c->nranks - 1;

@@ -121,6 +121,7 @@ snn_status snn_lif_fwd_bwd_host(const snn_lif_params* p, const snn_lif_shape* s,
     if (reinterpret_cast<uintptr_t>(workspace) % kAlign != 0)
         return fail(SNN_ERR_MISALIGNED, "workspace must be 256-byte aligned");
 
+    NvtxRange range("snn_lif_fwd_bwd_host");
     cudaStream_t cs = static_cast<cudaStream_t>(stream);
     Resources r;
     r.caller = cs;

@@ -4,6 +4,7 @@
 
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <memory>
@@ -14,6 +15,16 @@
 #include "lif_kernels.cuh"
 
 namespace snn_host {
+
+// NVTX range over a C-ABI call (forward / backward / time-split chunks show up as
+// named ranges in an Nsight timeline).  Header-only NVTX v3: without an attached tool a push /
+// pop is a null function-pointer check.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // Thread-local error detail (snn_last_error_message) + status.
 snn_status fail(snn_status st, const char* fmt, ...) __attribute__((format(printf, 2, 3)));

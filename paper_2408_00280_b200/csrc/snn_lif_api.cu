@@ -452,6 +452,7 @@ extern "C" {
 snn_status snn_lif_forward(const snn_lif_params* p, const snn_lif_shape* s, const void* x,
                            const float* v_init, void* spikes, void* saved, float* v_final,
                            void* stream) {
+    NvtxRange r("snn_lif_forward");
     return forward_impl(p, s, x, v_init, nullptr, spikes, saved, v_final, stream);
 }
 
@@ -460,6 +461,7 @@ snn_status snn_lif_backward(const snn_lif_params* p, const snn_lif_shape* s,
                             const void* saved, const float* grad_v_final, void* grad_x,
                             float* grad_v_init, void* stream) {
     (void)v_init;  // the RECOMPUTE checkpoints already hold V[-1]
+    NvtxRange r("snn_lif_backward");
     return backward_impl(p, s, grad_spikes, x, saved, grad_v_final, nullptr, grad_x, grad_v_init, stream);
 }
 
@@ -467,6 +469,7 @@ snn_status snn_lif_forward_affine(const snn_lif_params* p, const snn_lif_shape* 
                                   const float* v_init, const snn_lif_affine* af, void* spikes,
                                   void* saved, float* v_final, void* stream) {
     if (!af) return fail(SNN_ERR_NULL_POINTER, "affine is NULL");
+    NvtxRange r("snn_lif_forward_affine");
     return forward_impl(p, s, x, v_init, nullptr, spikes, saved, v_final, stream, af);
 }
 
@@ -477,6 +480,7 @@ snn_status snn_lif_backward_affine(const snn_lif_params* p, const snn_lif_shape*
                                    float* grad_scale, float* grad_shift, void* stream) {
     if (!af) return fail(SNN_ERR_NULL_POINTER, "affine is NULL");
     if (!grad_scale || !grad_shift) return fail(SNN_ERR_NULL_POINTER, "grad_scale / grad_shift is NULL");
+    NvtxRange r("snn_lif_backward_affine");
     int seg = 0;
     snn_status st = backward_impl(p, s, grad_spikes, x, saved, grad_v_final, nullptr, grad_x, grad_v_init,
                                   stream, af, part_a, part_b, nullptr, &seg);
@@ -496,6 +500,7 @@ snn_status snn_lif_forward_handoff(const snn_lif_params* p, const snn_lif_shape*
                                    const float* v_init, const snn_lif_handoff* h, void* spikes,
                                    void* saved, float* v_final, void* stream) {
     if (!h) return fail(SNN_ERR_NULL_POINTER, "handoff is NULL");
+    NvtxRange r("snn_lif_forward_handoff");
     return forward_impl(p, s, x, v_init, h, spikes, saved, v_final, stream);
 }
 
@@ -504,6 +509,7 @@ snn_status snn_lif_backward_handoff(const snn_lif_params* p, const snn_lif_shape
                                     const float* grad_v_final, const snn_lif_handoff* h, void* grad_x,
                                     float* grad_v_init, void* stream) {
     if (!h) return fail(SNN_ERR_NULL_POINTER, "handoff is NULL");
+    NvtxRange r("snn_lif_backward_handoff");
     return backward_impl(p, s, grad_spikes, x, saved, grad_v_final, h, grad_x, grad_v_init, stream);
 }
 

@@ -113,6 +113,17 @@ def launches(args):
                      f"{(sum(b) / len(b) / 1e9 if b else float('nan')):.3f} GB |")
     with open(args.out, "w") as f:
         f.write("\n".join(lines) + "\n")
+    if args.traffic_key:   # mean DRAM bytes per launch of the matching kernels (bench roofline.traffic)
+        per = []
+        for name, m in agg.items():
+            if re.search(args.kernel, name):
+                per += [x + y for x, y in zip(m.get("dram__bytes_read.sum", []), m.get("dram__bytes_write.sum", []))]
+        if per:
+            path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+            db = json.load(open(path)) if os.path.exists(path) else {}
+            db[args.traffic_key] = sum(per) / len(per)
+            with open(path, "w") as f:
+                json.dump(db, f, indent=1, sort_keys=True)
     print(open(args.out).read())
 
 
