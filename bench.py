@@ -58,8 +58,9 @@ def parse():
                     help="timed steps of the N>1 tsplit sub-record (and its k=1 reference)")
     ap.add_argument("--no-tsplit", action="store_true", help="N>1: skip the cfg3 time-split sub-record")
     ap.add_argument("--debug-single-gpu", action="store_true",
-                    help="test harness only: every rank on cuda:0 with a gloo group (exercises "
-                         "the multi-rank code paths on a 1-GPU box; numbers are not bench values)")
+                    help="test harness only: every rank on cuda:0, NCCL between them over its socket "
+                         "transport (exercises the multi-rank code paths on a 1-GPU box; numbers "
+                         "are not bench values)")
     ap.add_argument("--serial", action="store_true",
                     help="with --sweep: also time the paper's serial baselines (Fig. 3 / Fig. 5)")
     ap.add_argument("--prologue", action="store_true",
@@ -196,19 +197,19 @@ def workload_config(args, world, layers):
 # ----------------------------------------------------------------------------- helpers
 
 def init_group(args, local):
+    """The NCCL process group, also under --debug-single-gpu (every rank on cuda:0: NCCL then
+    runs over its socket transport because _debug_nccl_env gave each rank its own host id), so
+    the harness exercises the production code path, device placement aside."""
     import torch
     import torch.distributed as dist
-    if args.debug_single_gpu:
-        dist.init_process_group("gloo")
-    else:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
 
-def max_over_ranks(vals, dev, debug):
-    """MAX all-reduce of a few floats (NCCL on the GPU box; gloo/CPU in the debug harness)."""
+def max_over_ranks(vals, dev, debug=False):
+    """MAX all-reduce of a few floats over the NCCL process group."""
     import torch
     import torch.distributed as dist
-    t = torch.tensor(vals, dtype=torch.float64, device="cpu" if debug else dev)
+    t = torch.tensor(vals, dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return [float(v) for v in t.tolist()]
 
@@ -340,7 +341,8 @@ class OracleSample:
 def run_sweep(args, params, dev, stream):
     """BASELINE configs[1]: N = 2^20, T in {8, 32, 128, 512}.  Each fwd / bwd launch is
     timed alone with CUDA events; an L2 flush (a 512 MiB memset, outside the events)
-    precedes every launch so small-T working sets are not served from the 126 MB L2."""
+    precedes every launch so small-T working sets are not served from the 126 MB L2.
+    `stream`: the same layer timed like the main line (sweep_stream)."""
     import torch
     import paper_2408_00280_b200 as snn
     import snn_synth
@@ -396,7 +398,55 @@ def run_sweep(args, params, dev, stream):
             out[-1]["speedup_vs_serial_cuda"] = round(serial["cuda_ms"] / (mf + mb), 2)
             out[-1]["speedup_vs_serial_torch"] = round(serial["torch_ms"] / (mf + mb), 2)
         del X, G, f, gx, g
+        out[-1]["stream"] = sweep_stream(args, params, dev, T, N)
     return out
+
+
+def sweep_stream(args, params, dev, T, N, steps=20):
+    """The same layer timed like the main bench line instead of launch by launch: K steps
+    (fwd on batch i, bwd of the previous step's batch) captured as one graph, CUDA events only
+    around the whole region, B input batches rotating so the inputs of the K steps (>= 4x the
+    126 MB L2) are never served from L2.  No flush kernel between launches: consecutive LIF
+    kernels overlap their launch with the predecessor's tail (programmatic dependent launch)."""
+    import torch
+    import paper_2408_00280_b200 as snn
+    import snn_synth
+    per = 2 * T * N * 4
+    nb = max(2, min(8, -(-(512 << 20) // per)))
+    bat = []
+    for i in range(nb):
+        X = snn_synth.normal_tensor(1234 + i, T, N, device=dev)
+        G = snn_synth.normal_tensor(4321 + i, T, N, device=dev)
+        f = snn.lif_forward(X, params, spike_fmt=args.spike_fmt, save_mode=args.save_mode, return_v_final=False)
+        bat.append((X, G, f))
+    gx = torch.empty_like(bat[0][0])
+
+    def step(j):
+        X, _, f = bat[j % nb]
+        snn.lif_forward(X, params, spike_fmt=args.spike_fmt, save_mode=args.save_mode, spikes=f.spikes,
+                        saved=f.saved, return_v_final=False)
+        _, G, fp = bat[(j - 1) % nb]
+        snn.lif_backward(G, fp, grad_x=gx, return_grad_v_init=False)
+
+    for j in range(3):
+        step(j)
+    torch.cuda.synchronize(dev)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for j in range(steps):
+            step(j)
+    g.replay()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    g.replay()
+    e1.record()
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / steps
+    bf, bb = bytes_per_neuron_step(4, args.spike_fmt, args.save_mode, T)
+    del g, bat, gx
+    return {"ms_per_step": round(ms, 4), "neuron_steps_per_s": T * N / (ms / 1e3),
+            "fwdbwd_GBps": round((bf + bb) * T * N / (ms / 1e3) / 1e9, 1), "batches": nb}
 
 
 def run_inference(args, params, dev):
@@ -726,7 +776,7 @@ def tsplit_measure(args, world, rank, dev, N, T, steps, warmup, transport="nccl"
     out["clocks"] = clk.summary()
     # ---- T_c: one [N] fp32 boundary hop rank 0 -> 1, median of 20 (NCCL process group)
     hop = None
-    if world > 1 and not debug:
+    if world > 1:
         buf = torch.empty(N, dtype=torch.float32, device=dev)
         times = []
         st = torch.cuda.current_stream(dev)

@@ -23,9 +23,16 @@ def _rendezvous_file():
     return path
 
 
-def _worker(rank, world, port, T, N, n_chunks, dtype, out):
+def _worker(rank, world, port, T, N, n_chunks, dtype, out, backend="gloo"):
     # file-based rendezvous: no TCP port to race for between consecutive tests
-    dist.init_process_group("gloo", init_method=f"file://{port}", rank=rank, world_size=world)
+    if backend == "nccl":   # two ranks on one GPU: distinct NCCL host ids -> socket transport
+        os.environ.update(NCCL_HOSTID=f"snn-dist-host-{rank}", NCCL_P2P_DISABLE="1", NCCL_SHM_DISABLE="1",
+                          NCCL_IB_DISABLE="1", NCCL_NET="Socket", NCCL_SOCKET_IFNAME="lo", NCCL_NVLS_ENABLE="0")
+        torch.cuda.set_device(0)
+        dist.init_process_group("nccl", init_method=f"file://{port}", rank=rank, world_size=world,
+                                device_id=torch.device("cuda", 0))
+    else:
+        dist.init_process_group("gloo", init_method=f"file://{port}", rank=rank, world_size=world)
     torch.cuda.set_device(0)
     import paper_2408_00280_b200 as snn
     from paper_2408_00280_b200 import dist as D
@@ -34,7 +41,8 @@ def _worker(rank, world, port, T, N, n_chunks, dtype, out):
     a, b = D.partition_time(T, world)[rank]
     X = snn_synth.normal_tensor(1234, b - a, N, t_offset=a, dtype=dtype, device="cuda")
     G = snn_synth.normal_tensor(4321, b - a, N, t_offset=a, dtype=dtype, device="cuda")
-    ts = D.TimeSplitLIF(rank, world, D.HostTransport(), n_chunks=n_chunks)
+    transport = D.NcclTransport() if backend == "nccl" else D.HostTransport()
+    ts = D.TimeSplitLIF(rank, world, transport, n_chunks=n_chunks)
     fwd_fn, bwd_fn = D.lif_segment_fns(p)
     spikes, state, v_final = ts.forward(X, fwd_fn)
     gxs, gvi = ts.backward(G, state, bwd_fn)
@@ -51,22 +59,30 @@ def _worker(rank, world, port, T, N, n_chunks, dtype, out):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,n_chunks,dtype", [(2, 4, torch.float32), (4, 3, torch.float32),
-                                                  (3, 2, torch.bfloat16)])
-def test_time_split_bitwise_equals_whole_axis(world, n_chunks, dtype):
+@pytest.mark.parametrize("world,n_chunks,dtype,backend", [(2, 4, torch.float32, "gloo"), (4, 3, torch.float32, "gloo"),
+                                                          (3, 2, torch.bfloat16, "gloo"), (2, 3, torch.float32, "nccl")])
+def test_time_split_bitwise_equals_whole_axis(world, n_chunks, dtype, backend):
+    """backend "nccl": the NcclTransport (torch.distributed isend / irecv over NCCL) between two
+    ranks on this one GPU (distinct NCCL host ids, socket transport)."""
     import paper_2408_00280_b200 as snn
     import snn_synth
     T, N = 70, 4096
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _rendezvous_file()
-    ps = [ctx.Process(target=_worker, args=(r, world, port, T, N, n_chunks, dtype, q)) for r in range(world)]
+    ps = [ctx.Process(target=_worker, args=(r, world, port, T, N, n_chunks, dtype, q, backend), daemon=True)
+          for r in range(world)]
     for p in ps:
         p.start()
-    objs = sorted(q.get(timeout=300), key=lambda o: o[0])
-    for p in ps:
-        p.join(timeout=60)
-        assert p.exitcode == 0
+    try:
+        objs = sorted(q.get(timeout=300), key=lambda o: o[0])
+        for p in ps:
+            p.join(timeout=60)
+            assert p.exitcode == 0
+    finally:
+        for p in ps:
+            if p.is_alive():
+                p.kill()
     X = snn_synth.normal_tensor(1234, T, N, dtype=dtype, device="cuda")
     G = snn_synth.normal_tensor(4321, T, N, dtype=dtype, device="cuda")
     f = snn.lif_forward(X, snn.LIFParams.paper())
