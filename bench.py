@@ -404,10 +404,11 @@ def run_sweep(args, params, dev, stream):
 
 def sweep_stream(args, params, dev, T, N, steps=20):
     """The same layer timed like the main bench line instead of launch by launch: K steps
-    (fwd on batch i, bwd of the previous step's batch) captured as one graph, CUDA events only
-    around the whole region, B input batches rotating so the inputs of the K steps (>= 4x the
-    126 MB L2) are never served from L2.  No flush kernel between launches: consecutive LIF
-    kernels overlap their launch with the predecessor's tail (programmatic dependent launch)."""
+    (fwd on batch j, bwd of batch j - B/2) captured as one graph, CUDA events only around the
+    whole region, B input batches rotating (>= 4x the 126 MB L2 in total) so that between a
+    batch's forward and its backward at least ~B/2 steps of other traffic pass through L2 and
+    neither kernel reads the other's residue.  No flush kernel between launches: consecutive
+    LIF kernels overlap their launch with the predecessor's tail (programmatic dependent launch)."""
     import torch
     import paper_2408_00280_b200 as snn
     import snn_synth
@@ -425,7 +426,7 @@ def sweep_stream(args, params, dev, T, N, steps=20):
         X, _, f = bat[j % nb]
         snn.lif_forward(X, params, spike_fmt=args.spike_fmt, save_mode=args.save_mode, spikes=f.spikes,
                         saved=f.saved, return_v_final=False)
-        _, G, fp = bat[(j - 1) % nb]
+        _, G, fp = bat[(j - nb // 2) % nb]
         snn.lif_backward(G, fp, grad_x=gx, return_grad_v_init=False)
 
     for j in range(3):
