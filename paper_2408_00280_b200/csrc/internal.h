@@ -7,6 +7,7 @@
 #include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <memory>
 #include <type_traits>
 #include <vector>
@@ -64,6 +65,16 @@ void record_arg(RecordedLaunch& r, const P& v) {
     r.arg_store.push_back(std::move(p));
 }
 
+// SNN_LIF_NO_PDL=1: launch without programmatic dependent launch (A/B measurements only; the
+// kernels' griddepcontrol instructions are no-ops then).
+inline bool pdl_disabled() {
+    static const bool off = [] {
+        const char* e = std::getenv("SNN_LIF_NO_PDL");
+        return e && e[0] == '1';
+    }();
+    return off;
+}
+
 // Launch kernel `k` (PDL attribute when `pdl`), or record it when a Recorder is installed.
 template <typename... Params, typename... Args>
 snn_status launch_kernel(void (*k)(Params...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
@@ -86,7 +97,7 @@ snn_status launch_kernel(void (*k)(Params...), dim3 grid, dim3 block, size_t sme
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL (lif_async.cuh)
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = pdl ? 1 : 0;
+    cfg.numAttrs = pdl && !pdl_disabled() ? 1 : 0;
     const cudaError_t e = cudaLaunchKernelEx(&cfg, k, static_cast<Params>(args)...);
     if (e != cudaSuccess) return fail(SNN_ERR_CUDA, "%s launch failed: %s", what, cudaGetErrorString(e));
     return launch_status(what);
