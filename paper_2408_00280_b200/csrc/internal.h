@@ -121,8 +121,20 @@ int prepare(Kernel k, int threads, int smem) {
 int cached_occupancy(const void* k, int threads, int smem, int (*prep)(const void*, int, int));
 
 // Tile launch: one CTA per tile; resident CTAs steal the tiles of pending CTAs through
-// cluster launch control (lif_tma.cuh), so the grid behaves persistently.  Short tiles
-// (few ring stages: small T) keep up to 4 steal requests in flight.
+// cluster launch control (lif_tma.cuh), so the grid behaves persistently, with one steal
+// request in flight.  Short tiles (<= 8 ring stages) L2-prefetch the CTA's own first ring
+// stages before griddepcontrol.wait (hides the first DRAM round trip behind the predecessor's
+// tail; measured +4% on cfg2, but -3% sustained at T = 512, so long tiles do not).
+// Environment overrides (A/B timing, tools/trace_timeline.py): SNN_LIF_CLC_DEPTH (requests
+// in flight, 1..4), SNN_LIF_PREFETCH (0: never prefetch; >0: prefetch tiles of up to that
+// many stages).
+struct SchedKnobs {
+    int max_depth = 1;
+    int prefetch_max_stages = 8;
+    int prefetch_hint = 0;
+};
+const SchedKnobs& sched_knobs();
+
 template <typename Kernel, typename... Args>
 snn_status launch_tiles(Kernel k, int threads, int smem, int64_t ntiles, int64_t stages_per_tile,
                         cudaStream_t st, const char* what, const Args&... args) {
@@ -130,12 +142,17 @@ snn_status launch_tiles(Kernel k, int threads, int smem, int64_t ntiles, int64_t
         return prepare(reinterpret_cast<Kernel>(const_cast<void*>(kk)), t, sm);
     });
     if (ntiles > INT32_MAX) return fail(SNN_ERR_INVALID_VALUE, "too many tiles");
+    const SchedKnobs& kn = sched_knobs();
+    const int64_t resident = (int64_t)occ * num_sms();
+    snn::Sched sc;
     // Steal requests in flight: none when every CTA is resident from the start (nothing can
     // ever be pending, and a CTA would only wait for the failed responses before exiting).
-    const int depth = ntiles <= (int64_t)occ * num_sms()
-                          ? 0
-                          : (int)std::max<int64_t>(1, std::min<int64_t>(4, (8 + stages_per_tile - 1) / stages_per_tile));
-    return launch_kernel(k, dim3((unsigned)ntiles), dim3(threads), (size_t)smem, st, true, what, args..., depth);
+    sc.depth = ntiles <= resident
+                   ? 0
+                   : (int)std::max<int64_t>(1, std::min<int64_t>(kn.max_depth, (8 + stages_per_tile - 1) / stages_per_tile));
+    sc.prefetch = stages_per_tile <= kn.prefetch_max_stages ? 1 << 20 : 0;
+    sc.pf_hint = kn.prefetch_hint;
+    return launch_kernel(k, dim3((unsigned)ntiles), dim3(threads), (size_t)smem, st, true, what, args..., sc);
 }
 
 // Plain launch with programmatic dependent launch allowed: the kernel must call pdl_wait()

@@ -12,20 +12,46 @@ namespace snn_host {
 
 // Tile configurations: VEC neurons per consumer lane x NCONS
 // consumer threads = W-neuron tile; R rows per stage; S stages in the smem ring.
+// The SNN_{F32,BF16}_{FN,FS,RN,RS} macros exist for A/B builds of other tile geometries
+// (tools/variant_build.py); the product build takes the defaults.
+#ifndef SNN_F32_FN
+#define SNN_F32_FN 256
+#endif
+#ifndef SNN_F32_FS
+#define SNN_F32_FS 3
+#endif
+#ifndef SNN_F32_RN
+#define SNN_F32_RN 256
+#endif
+#ifndef SNN_F32_RS
+#define SNN_F32_RS 3
+#endif
+#ifndef SNN_BF16_FN
+#define SNN_BF16_FN 128
+#endif
+#ifndef SNN_BF16_FS
+#define SNN_BF16_FS 6
+#endif
+#ifndef SNN_BF16_RN
+#define SNN_BF16_RN 256
+#endif
+#ifndef SNN_BF16_RS
+#define SNN_BF16_RS 3
+#endif
 template <typename IO> struct TmaCfg;
 template <> struct TmaCfg<float> {
     // forward: 1024-neuron tiles, 8 consumer warps, 32 KB stages x 3, 2 CTAs/SM (measured 5%
     // faster at T=512 than 512-neuron tiles with 4 warps and 16 KB x 6 stages)
-    static constexpr int FV = 4, FN = 256, FR = 8, FS = 3;
+    static constexpr int FV = 4, FN = SNN_F32_FN, FR = 8, FS = SNN_F32_FS;
     static constexpr int FN_RES = 128, FS_RES = 3;           // + residual rows: 32 KB stages
-    static constexpr int RV = 2, RN = 256, RS = 3;           // backward RECOMPUTE: 66 KB chunks, FFMA2 pairs
+    static constexpr int RV = 2, RN = SNN_F32_RN, RS = SNN_F32_RS;   // backward RECOMPUTE: 66 KB chunks, FFMA2 pairs
     static constexpr int RS_RES = 2;                         // + residual rows: 99 KB chunks
     static constexpr int HV = 2, HN = 256, HR = 8, HS = 6;   // backward SAVE_H: 32 KB stages
 };
 template <> struct TmaCfg<__nv_bfloat16> {
-    static constexpr int FV = 8, FN = 128, FR = 8, FS = 6;   // (8 warps x 2048-neuron tiles: slower on mid layers)
+    static constexpr int FV = 8, FN = SNN_BF16_FN, FR = 8, FS = SNN_BF16_FS;   // (8 warps x 2048-neuron tiles: slower on mid layers)
     static constexpr int FN_RES = 128, FS_RES = 3;
-    static constexpr int RV = 2, RN = 256, RS = 3;           // 34 KB chunks, 2 CTAs/SM (VEC 4 x 128 lanes measured 6% slower at T=16)
+    static constexpr int RV = 2, RN = SNN_BF16_RN, RS = SNN_BF16_RS;   // 34 KB chunks, 2 CTAs/SM (VEC 4 x 128 lanes measured 6% slower at T=16)
     static constexpr int RS_RES = 2;                         // + residual rows: 51 KB chunks
     static constexpr int HV = 2, HN = 512, HR = 8, HS = 4;
 };

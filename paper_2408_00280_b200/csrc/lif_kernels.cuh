@@ -90,6 +90,13 @@ __device__ __forceinline__ AffCoef<VEC> load_affine(const Affine& af, int64_t n0
     return co;
 }
 
+// Work distribution of a launch (host: launch_tiles).
+struct Sched {
+    int depth;      // steal requests kept in flight, 1..kMaxClc (0: the whole grid is resident)
+    int prefetch;   // ring stages of the CTA's own tile to L2-prefetch before griddepcontrol.wait
+    int pf_hint;    // 1: the prefetch carries the evict-first L2 policy of the loads
+};
+
 struct FwdArgs {
     const void* x;        // [T, ld] IO
     const float* v_init;  // [N] or null
@@ -104,6 +111,9 @@ struct FwdArgs {
     LifConsts c;
     Handoff h;            // boundary V from / to the neighbour time segment (TMA path only)
     Affine af;            // input prologue (identity when af.scale == null)
+#ifdef SNN_TRACE
+    void* trace;          // TraceBuf (trace.cuh)
+#endif
 };
 
 struct BwdArgs {
@@ -118,6 +128,9 @@ struct BwdArgs {
     LifConsts c;
     Handoff h;                  // boundary dL/dV from / to the neighbour segment (TMA path only)
     Affine af;                  // input prologue + its per-neuron gradient partials
+#ifdef SNN_TRACE
+    void* trace;                // TraceBuf (trace.cuh)
+#endif
 };
 
 // ------------------------------------------------------------------------------------

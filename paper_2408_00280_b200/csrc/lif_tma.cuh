@@ -41,8 +41,15 @@
 #include "lif_async.cuh"
 #include "lif_handoff.cuh"
 #include "lif_kernels.cuh"
+#include "trace.cuh"
 
 namespace snn {
+
+#ifdef SNN_TRACE
+#define SNN_TRACE_BUF(a) ((a).trace)
+#else
+#define SNN_TRACE_BUF(a) nullptr
+#endif
 
 // Shared-memory control block of a ring with S stages.
 template <int S>
@@ -79,14 +86,15 @@ __device__ __forceinline__ void init_barriers(Barriers<S>* b, uint32_t consumer_
 }
 
 // Producer skeleton shared by the kernels.  The CTA processes its own tile (blockIdx.x)
-// first, then tiles of pending CTAs it cancels through cluster launch control.  Up to
-// `depth` (1..kMaxClc) steal requests are kept in flight, so with short tiles (few ring
-// stages, e.g. T = 8) the next tiles are known before the current one is issued; with
-// long tiles depth = 1 avoids hoarding work near the end.  Each tile is `nstages` ring
-// stages; `bytes(tile, j)` is stage j's transaction byte count and `issue(stage_ptr, tile, j, bar)`
+// first, then tiles of pending CTAs it cancels through cluster launch control.  sc.depth
+// (1..kMaxClc) steal requests are kept in flight; the default is one: more lets a CTA hoard
+// tiles it cannot start yet while others run dry at the end of the grid (r2, per-CTA
+// timelines of tools/trace_timeline.py: the last CTA ended 4-5 us after the median one at
+// depth 4, ~2 us at depth 1; cfg2 +4%).  Each tile is `nstages` ring stages;
+// `bytes(tile, j)` is stage j's transaction byte count and `issue(stage_ptr, tile, j, bar)`
 // issues its TMA loads.  Ends with a tile = -1 sentinel stage; every outstanding request is
 // drained before returning (its response is an async smem write) and a late success is still
-// processed.
+// processed.  Request number q lives in slot q % depth (each slot has at most one in flight).
 // WARP = false: run by one thread.  WARP = true: run by the whole producer warp in lockstep --
 // every lane waits and tracks the same state, lane 0 alone writes the stage metadata, arms the
 // barriers and sends the steal requests, and `issue` is called on every lane (the unaligned
@@ -94,8 +102,9 @@ __device__ __forceinline__ void init_barriers(Barriers<S>* b, uint32_t consumer_
 // 50 ns, too few for rows that each need their own loads).
 template <int S, int STAGE_BYTES, bool WARP = false, typename Bytes, typename Issue>
 __device__ __forceinline__ void produce(unsigned char* smem, Barriers<S>* bar, int64_t nstages,
-                                        int depth, Bytes bytes, Issue issue) {
+                                        const Sched& sc, Bytes bytes, Issue issue) {
     const bool leader = !WARP || (threadIdx.x & 31) == 0;
+    const int depth = sc.depth;
     uint32_t k = 0;
     uint32_t phases = 0;   // bit i = parity of CLC slot i (a bit set, not an array: no local memory)
     int issued = 0, consumed = 0;
@@ -124,7 +133,7 @@ __device__ __forceinline__ void produce(unsigned char* smem, Barriers<S>* bar, i
             if (r >= 0) {
                 tile = r;
                 if (!stop) {
-                    if (leader) clc_request(&bar->clc[i]);
+                    if (leader) clc_request(&bar->clc[issued % depth]);
                     ++issued;
                 }
                 break;
@@ -311,32 +320,47 @@ template <typename IO, int VEC, int SFMT, int SAVE, bool SOFT, bool AFF, bool RE
           bool UNAL, bool P0 = false>
 __global__ void __launch_bounds__(NCONS + 32)
 lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmr,
-                       const FwdArgs a, const int clc_depth) {
+                       const FwdArgs a, const Sched sc) {
     static_assert(!RES || AFF, "the residual prologue rides on the affine one");
     using Cfg = FwdTma<IO, VEC, NCONS, R, S, RES ? 2 : 1, UNAL>;
     using Reg = typename Cfg::Reg;
     constexpr int W = Cfg::W, BW = Cfg::BW, NB = Cfg::NB;
     unsigned char* smem = smem_base();
     auto* bar = reinterpret_cast<Barriers<S>*>(smem + S * Cfg::STAGE_BYTES);
+    TraceCta tr;
+    tr.entry();
     init_barriers<S>(bar, NCONS / 32);
-    pdl_wait();   // predecessor complete before any global-memory access
-
     const int64_t T = a.T, N = a.N;
     const int64_t nrb = (T + R - 1) / R;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {   // before the wait: kernel-parameter descriptors, L2 prefetch of the own tile
+        const uint64_t pfpol = policy_evict_first();
+        auto pf2d = [&](const CUtensorMap* m, int c0_, int c1_) {
+            if (sc.pf_hint) tma_prefetch_2d(m, c0_, c1_, pfpol); else tma_prefetch_2d(m, c0_, c1_);
+        };
+        tma_prefetch_desc(&tmx);
+        if constexpr (RES) tma_prefetch_desc(&tmr);
+        if constexpr (!UNAL) {
+            const int c0 = (int)blockIdx.x * W;
+            for (int j = 0; j < sc.prefetch && j < S && j < nrb; ++j)
+#pragma unroll
+                for (int b = 0; b < NB; ++b) {
+                    pf2d(&tmx, c0 + b * BW, j * R);
+                    if constexpr (RES) pf2d(&tmr, c0 + b * BW, j * R);
+                }
+        }
+    }
+    pdl_wait();   // predecessor complete before any global-memory access
+    tr.waited();
 
     if (warp == 0) {  // ---------------- producer (one lane; the whole warp for unaligned rows)
         if (UNAL || lane == 0) {
-            if (lane == 0) {
-                tma_prefetch_desc(&tmx);
-                if constexpr (RES) tma_prefetch_desc(&tmr);
-            }
             const uint64_t pol = policy_evict_first();
             const auto fx = Reg::flat(a.x, T, N, a.ld);
             const auto fr = Reg::flat(a.af.residual, T, N, a.ld);
             auto rows_of = [&](int64_t rb) { return (int)min((int64_t)R, T - rb * R); };
             produce<S, Cfg::STAGE_BYTES, UNAL>(
-                smem, bar, nrb, clc_depth,
+                smem, bar, nrb, sc,
                 [&](int tile, int64_t rb) {
                     const int64_t c0 = (int64_t)tile * W;
                     uint32_t b = Reg::tx_bytes(fx, rb * R, rows_of(rb), c0, a.ld);
@@ -363,6 +387,8 @@ lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_con
         mbar_wait(&bar->full[s], (k / S) & 1);
         const int tile = bar->tile[s];
         if (tile < 0) break;
+        tr.stage();
+        tr.tile();
         const int64_t g = (int64_t)tile * NCONS + ct;
         const int64_t n0 = g * VEC;
         const int nvalid = group_valid(n0, N, VEC);
@@ -429,6 +455,7 @@ lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_con
             handoff_send<VEC, NCONS>(a.h, tile, W, N, n0, nvalid, V);
         if (a.v_final != nullptr && nvalid > 0) store_vec<VEC>(a.v_final + n0, nvalid, V);
     }
+    if (warp == 1) tr.done(SNN_TRACE_BUF(a), 1u, T, N);
 }
 
 // ------------------------------------------------------------------------------------
@@ -544,7 +571,7 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
                                   const __grid_constant__ CUtensorMap tmg,
                                   const __grid_constant__ CUtensorMap tmck,
                                   const __grid_constant__ CUtensorMap tmr, const BwdArgs a,
-                                  const int clc_depth) {
+                                  const Sched sc) {
     constexpr bool RES = Mode<MODE>::RES;
     static_assert(!RES || Mode<MODE>::AFF, "the residual prologue rides on the affine one");
     using Cfg = BwdRecTma<IO, VEC, NCONS, S, RES, UNAL>;
@@ -552,19 +579,38 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
     constexpr int W = Cfg::W, BW = Cfg::BW, NB = Cfg::NB;
     unsigned char* smem = smem_base();
     auto* bar = reinterpret_cast<Barriers<S>*>(smem + S * Cfg::STAGE_BYTES);
+    TraceCta tr;
+    tr.entry();
     init_barriers<S>(bar, NCONS / 32);
-    pdl_wait();   // predecessor complete before any global-memory access
-
     const int64_t T = a.T, N = a.N, ld = a.ld;
     const int64_t nch = (T + kCkpt - 1) / kCkpt;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {   // before the wait: kernel-parameter descriptors, L2 prefetch of the own tile
+        const uint64_t pfpol = policy_evict_first();
+        auto pf2d = [&](const CUtensorMap* m, int c0_, int c1_) {
+            if (sc.pf_hint) tma_prefetch_2d(m, c0_, c1_, pfpol); else tma_prefetch_2d(m, c0_, c1_);
+        };
+        tma_prefetch_desc(&tmx); tma_prefetch_desc(&tmg); tma_prefetch_desc(&tmck);
+        if constexpr (RES) tma_prefetch_desc(&tmr);
+        const int c0 = (int)blockIdx.x * W;
+        for (int j = 0; j < sc.prefetch && j < S && j < nch; ++j) {
+            const int ch = (int)nch - 1 - j;
+#pragma unroll
+            for (int b = 0; b < NB; ++b) {
+                pf2d(&tmck, c0 + b * BW, ch);
+                if constexpr (!UNAL) {
+                    pf2d(&tmx, c0 + b * BW, ch * kCkpt);
+                    pf2d(&tmg, c0 + b * BW, ch * kCkpt);
+                    if constexpr (RES) pf2d(&tmr, c0 + b * BW, ch * kCkpt);
+                }
+            }
+        }
+    }
+    pdl_wait();   // predecessor complete before any global-memory access
+    tr.waited();
 
     if (warp == 0) {  // ---------------- producer: chunks of a tile, last first (whole warp if unaligned)
         if (UNAL || lane == 0) {
-            if (lane == 0) {
-                tma_prefetch_desc(&tmx); tma_prefetch_desc(&tmg); tma_prefetch_desc(&tmck);
-                if constexpr (RES) tma_prefetch_desc(&tmr);
-            }
             const uint64_t pol = policy_evict_first();
             auto rows_of = [&](int64_t j) {
                 const int64_t ch = nch - 1 - j;
@@ -574,7 +620,7 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
             const auto fg = Reg::flat(a.gS, T, N, ld);
             const auto fr = Reg::flat(a.af.residual, T, N, ld);
             produce<S, Cfg::STAGE_BYTES, UNAL>(
-                smem, bar, nch, clc_depth,
+                smem, bar, nch, sc,
                 [&](int tile, int64_t j) {
                     const int64_t t0 = (nch - 1 - j) * kCkpt, c0 = (int64_t)tile * W;
                     uint32_t b = (uint32_t)(NB * Cfg::CK_BOX_BYTES) + Reg::tx_bytes(fx, t0, rows_of(j), c0, ld) +
@@ -614,6 +660,8 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
         mbar_wait(&bar->full[s], (k / S) & 1);
         const int tile = bar->tile[s];
         if (tile < 0) break;
+        tr.stage();
+        tr.tile();
         const int64_t n0 = (int64_t)tile * W + nt;
         const int nvalid = group_valid(n0, N, VEC);
         const bool tile_full = (int64_t)(tile + 1) * W <= N;   // uniform across the CTA
@@ -690,6 +738,7 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
         }
         if (a.grad_v_init != nullptr && nvalid > 0) store_vec<VEC>(a.grad_v_init + n0, nvalid, gV);
     }
+    if (warp == 1) tr.done(SNN_TRACE_BUF(a), 2u, T, N);
 }
 
 // ------------------------------------------------------------------------------------
@@ -712,22 +761,39 @@ template <typename IO, int VEC, int MODE, int NCONS, int R, int S, bool UNAL>
 __global__ void __launch_bounds__(NCONS + 32)
 lif_backward_saveh_tma_kernel(const __grid_constant__ CUtensorMap tmh,
                               const __grid_constant__ CUtensorMap tmg, const BwdArgs a,
-                              const int clc_depth) {
+                              const Sched sc) {
     using Cfg = BwdHTma<IO, VEC, NCONS, R, S, UNAL>;
     using Reg = typename Cfg::Reg;
     constexpr int W = Cfg::W, BW = Cfg::BW, NB = Cfg::NB;
     unsigned char* smem = smem_base();
     auto* bar = reinterpret_cast<Barriers<S>*>(smem + S * Cfg::STAGE_BYTES);
+    TraceCta tr;
+    tr.entry();
     init_barriers<S>(bar, NCONS / 32);
-    pdl_wait();   // predecessor complete before any global-memory access
-
     const int64_t T = a.T, N = a.N, ld = a.ld;
     const int64_t nrb = (T + R - 1) / R;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {   // before the wait: kernel-parameter descriptors, L2 prefetch of the own tile
+        const uint64_t pfpol = policy_evict_first();
+        auto pf2d = [&](const CUtensorMap* m, int c0_, int c1_) {
+            if (sc.pf_hint) tma_prefetch_2d(m, c0_, c1_, pfpol); else tma_prefetch_2d(m, c0_, c1_);
+        };
+        tma_prefetch_desc(&tmh); tma_prefetch_desc(&tmg);
+        const int c0 = (int)blockIdx.x * W;
+        for (int j = 0; j < sc.prefetch && j < S && j < nrb; ++j) {
+            const int rb = (int)nrb - 1 - j;
+#pragma unroll
+            for (int b = 0; b < NB; ++b) {
+                pf2d(&tmh, c0 + b * BW, rb * R);
+                if constexpr (!UNAL) pf2d(&tmg, c0 + b * BW, rb * R);
+            }
+        }
+    }
+    pdl_wait();   // predecessor complete before any global-memory access
+    tr.waited();
 
     if (warp == 0) {   // producer (whole warp if unaligned)
         if (UNAL || lane == 0) {
-            if (lane == 0) { tma_prefetch_desc(&tmh); tma_prefetch_desc(&tmg); }
             const uint64_t pol = policy_evict_first();
             auto rows_of = [&](int64_t j) {
                 const int64_t rb = nrb - 1 - j;
@@ -735,7 +801,7 @@ lif_backward_saveh_tma_kernel(const __grid_constant__ CUtensorMap tmh,
             };
             const auto fg = Reg::flat(a.gS, T, N, ld);
             produce<S, Cfg::STAGE_BYTES, UNAL>(
-                smem, bar, nrb, clc_depth,
+                smem, bar, nrb, sc,
                 [&](int tile, int64_t j) {
                     return (uint32_t)(NB * Cfg::HBOX) +
                            Reg::tx_bytes(fg, (nrb - 1 - j) * R, rows_of(j), (int64_t)tile * W, ld);
@@ -767,6 +833,8 @@ lif_backward_saveh_tma_kernel(const __grid_constant__ CUtensorMap tmh,
         mbar_wait(&bar->full[s], (k / S) & 1);
         const int tile = bar->tile[s];
         if (tile < 0) break;
+        tr.stage();
+        tr.tile();
         const int64_t n0 = (int64_t)tile * W + nt;
         const int nvalid = group_valid(n0, N, VEC);
         const bool tile_full = (int64_t)(tile + 1) * W <= N;   // uniform across the CTA
@@ -810,6 +878,7 @@ lif_backward_saveh_tma_kernel(const __grid_constant__ CUtensorMap tmh,
             handoff_send<VEC, NCONS>(a.h, tile, W, N, n0, nvalid, gV);
         if (a.grad_v_init != nullptr && nvalid > 0) store_vec<VEC>(a.grad_v_init + n0, nvalid, gV);
     }
+    if (warp == 1) tr.done(SNN_TRACE_BUF(a), 3u, T, N);
 }
 
 }  // namespace snn

@@ -3,6 +3,7 @@
 // The library never allocates, frees or synchronises.
 #include <cmath>
 #include <cstdarg>
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -12,6 +13,7 @@
 #include <utility>
 
 #include "internal.h"
+#include "trace.cuh"
 #include "lif_handoff.cuh"
 
 namespace snn_host {
@@ -54,6 +56,21 @@ snn_status launch_status(const char* what) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(SNN_ERR_CUDA, "%s launch failed: %s", what, cudaGetErrorString(e));
     return SNN_OK;
+}
+
+const SchedKnobs& sched_knobs() {
+    static const SchedKnobs k = [] {
+        SchedKnobs r;
+        auto env = [](const char* n, int* v) {
+            if (const char* e = std::getenv(n)) *v = std::atoi(e);
+        };
+        env("SNN_LIF_CLC_DEPTH", &r.max_depth);
+        env("SNN_LIF_PREFETCH", &r.prefetch_max_stages);
+        env("SNN_LIF_PREFETCH_HINT", &r.prefetch_hint);
+        r.max_depth = std::max(1, std::min(r.max_depth, 4));
+        return r;
+    }();
+    return k;
 }
 
 int num_sms() {
@@ -298,6 +315,30 @@ snn::Affine to_dev(const snn_lif_affine* af) {
 
 namespace snn_host {
 
+#ifdef SNN_TRACE
+// Trace builds only (trace.cuh): one device buffer of per-CTA records, allocated on first use.
+static void* trace_buf() {
+    static void* buf = nullptr;
+    if (!buf && cudaMalloc(&buf, sizeof(snn::TraceBuf)) == cudaSuccess) cudaMemset(buf, 0, 64);
+    return buf;
+}
+extern "C" int snn_trace_read(void* host, int max_records) {
+    void* b = trace_buf();
+    unsigned int n = 0;
+    if (!b || cudaDeviceSynchronize() != cudaSuccess ||
+        cudaMemcpy(&n, b, sizeof(n), cudaMemcpyDeviceToHost) != cudaSuccess)
+        return -1;
+    if (n > (unsigned)snn::kTraceRecords) n = snn::kTraceRecords;
+    if ((int)n > max_records) n = (unsigned)max_records;
+    if (n && cudaMemcpy(host, static_cast<char*>(b) + offsetof(snn::TraceBuf, rec), n * sizeof(snn::TraceRec),
+                        cudaMemcpyDeviceToHost) != cudaSuccess)
+        return -1;
+    cudaMemset(b, 0, 64);
+    cudaDeviceSynchronize();
+    return (int)n;
+}
+#endif
+
 snn_status forward_impl(const snn_lif_params* p, const snn_lif_shape* s, const void* x,
                         const float* v_init, const snn_lif_handoff* handoff, void* spikes, void* saved,
                         float* v_final, void* stream, const snn_lif_affine* affine, const ChunkView* cv) {
@@ -322,6 +363,9 @@ snn_status forward_impl(const snn_lif_params* p, const snn_lif_shape* s, const v
     a.T = s->T; a.N = s->N; a.ld = s->ld; a.ldh = saved_ld(s); a.nwords = (s->N + 31) / 32;
     a.spk_words_ld = a.nwords;
     if (cv) { a.ldh = cv->ldh; a.spk_words_ld = cv->spk_words_ld; }
+#ifdef SNN_TRACE
+    a.trace = trace_buf();
+#endif
     a.c = make_consts(p);
     const bool soft = p->reset_mode == SNN_RESET_SOFT;
     cudaStream_t cs = static_cast<cudaStream_t>(stream);
@@ -381,6 +425,9 @@ snn_status backward_impl(const snn_lif_params* p, const snn_lif_shape* s,
     a.gS = grad_spikes; a.x = x; a.saved = static_cast<const float*>(saved);
     a.grad_v_final = grad_v_final; a.gX = grad_x; a.grad_v_init = grad_v_init;
     a.T = s->T; a.N = s->N; a.ld = s->ld; a.ldh = cv ? cv->ldh : saved_ld(s);
+#ifdef SNN_TRACE
+    a.trace = trace_buf();
+#endif
     a.c = make_consts(p);
     int mode = mode_of(p);
     cudaStream_t cs = static_cast<cudaStream_t>(stream);
