@@ -122,15 +122,16 @@ int cached_occupancy(const void* k, int threads, int smem, int (*prep)(const voi
 
 // Tile launch: one CTA per tile; resident CTAs steal the tiles of pending CTAs through
 // cluster launch control (lif_tma.cuh), so the grid behaves persistently, with one steal
-// request in flight.  Short tiles (<= 8 ring stages) L2-prefetch the CTA's own first ring
+// request in flight.  Short tiles (<= 4 ring stages) L2-prefetch the CTA's own first ring
 // stages before griddepcontrol.wait (hides the first DRAM round trip behind the predecessor's
-// tail; measured +4% on cfg2, but -3% sustained at T = 512, so long tiles do not).
+// tail; measured +4% on cfg2, but -3% sustained when tiles of 8 or more stages do, T >= 128;
+// an evict-first hint on the prefetch does not change that).
 // Environment overrides (A/B timing, tools/trace_timeline.py): SNN_LIF_CLC_DEPTH (requests
 // in flight, 1..4), SNN_LIF_PREFETCH (0: never prefetch; >0: prefetch tiles of up to that
 // many stages).
 struct SchedKnobs {
     int max_depth = 1;
-    int prefetch_max_stages = 8;
+    int prefetch_max_stages = 4;
     int prefetch_hint = 0;
 };
 const SchedKnobs& sched_knobs();

@@ -388,7 +388,7 @@ lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_con
         const int tile = bar->tile[s];
         if (tile < 0) break;
         tr.stage();
-        tr.tile();
+        tr.tile(tile);
         const int64_t g = (int64_t)tile * NCONS + ct;
         const int64_t n0 = g * VEC;
         const int nvalid = group_valid(n0, N, VEC);
@@ -661,7 +661,7 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
         const int tile = bar->tile[s];
         if (tile < 0) break;
         tr.stage();
-        tr.tile();
+        tr.tile(tile);
         const int64_t n0 = (int64_t)tile * W + nt;
         const int nvalid = group_valid(n0, N, VEC);
         const bool tile_full = (int64_t)(tile + 1) * W <= N;   // uniform across the CTA
@@ -834,7 +834,7 @@ lif_backward_saveh_tma_kernel(const __grid_constant__ CUtensorMap tmh,
         const int tile = bar->tile[s];
         if (tile < 0) break;
         tr.stage();
-        tr.tile();
+        tr.tile(tile);
         const int64_t n0 = (int64_t)tile * W + nt;
         const int nvalid = group_valid(n0, N, VEC);
         const bool tile_full = (int64_t)(tile + 1) * W <= N;   // uniform across the CTA

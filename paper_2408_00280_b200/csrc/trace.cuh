@@ -17,6 +17,7 @@ struct TraceRec {
     uint32_t kind, grid, smid, tiles;
     int64_t T, N;
     uint64_t t_entry, t_wait, t_first, t_end;
+    int32_t first_stolen, last_tile;   // tile indices: the first taken over from a pending CTA, the last run
 };
 struct TraceBuf {   // device memory, allocated by snn_trace_read's first call
     unsigned int count, pad[15];
@@ -36,12 +37,17 @@ __device__ __forceinline__ uint32_t smid() {
 struct TraceCta {
     uint64_t t_entry = 0, t_wait = 0, t_first = 0;
     uint32_t tiles = 0;
+    int32_t first_stolen = -1, last_tile = -1;
     __device__ __forceinline__ void entry() { t_entry = gtimer(); }
     __device__ __forceinline__ void waited() { t_wait = gtimer(); }
     __device__ __forceinline__ void stage() {
         if (t_first == 0) t_first = gtimer();
     }
-    __device__ __forceinline__ void tile() { ++tiles; }
+    __device__ __forceinline__ void tile(int t) {
+        if (tiles == 1) first_stolen = t;
+        last_tile = t;
+        ++tiles;
+    }
     // first consumer warp, lane 0
     __device__ __forceinline__ void done(void* buf, uint32_t kind, int64_t T, int64_t N) {
         if ((threadIdx.x & 31) != 0 || buf == nullptr) return;
@@ -52,6 +58,7 @@ struct TraceCta {
         r.kind = kind; r.grid = gridDim.x; r.smid = smid(); r.tiles = tiles;
         r.T = T; r.N = N;
         r.t_entry = t_entry; r.t_wait = t_wait; r.t_first = t_first; r.t_end = gtimer();
+        r.first_stolen = first_stolen; r.last_tile = last_tile;
         b->rec[i] = r;
     }
 };
@@ -60,7 +67,7 @@ struct TraceCta {
     __device__ __forceinline__ void entry() {}
     __device__ __forceinline__ void waited() {}
     __device__ __forceinline__ void stage() {}
-    __device__ __forceinline__ void tile() {}
+    __device__ __forceinline__ void tile(int) {}
     __device__ __forceinline__ void done(void*, uint32_t, int64_t, int64_t) {}
 };
 #endif

@@ -23,8 +23,10 @@ from paper_2408_00280_b200 import _lib  # noqa: E402
 import snn_synth  # noqa: E402
 
 REC = np.dtype([("kind", "<u4"), ("grid", "<u4"), ("smid", "<u4"), ("tiles", "<u4"), ("T", "<i8"), ("N", "<i8"),
-                ("t_entry", "<u8"), ("t_wait", "<u8"), ("t_first", "<u8"), ("t_end", "<u8")])
+                ("t_entry", "<u8"), ("t_wait", "<u8"), ("t_first", "<u8"), ("t_end", "<u8"),
+                ("first_stolen", "<i4"), ("last_tile", "<i4")])
 KIND = {1: "fwd", 2: "bwd", 3: "bwdH"}
+ORDER = False
 
 
 def read_trace():
@@ -71,6 +73,13 @@ def report(recs, title):
               f"{us(np.median(a['t_first'])):9.2f} {us(np.median(a['t_end'])):8.2f} {us(end):8.2f} "
               f"{(int(end) - int(ent)) / 1e3:7.2f} {gap} {gbs:6.0f}")
         prev_end = int(end)
+        if ORDER and grid > len(a):
+            # steal order: first stolen tile of each CTA (sorted by time it was taken ~ entry order),
+            # and the tiles that finished last
+            fs = np.sort(a["first_stolen"][a["first_stolen"] >= 0])
+            late = a[np.argsort(a["t_end"])[-8:]]
+            print(f"        first stolen tiles: min {fs.min() if len(fs) else -1} max {fs.max() if len(fs) else -1}; "
+                  f"last 8 CTAs to end ran tiles {list(late['last_tile'])} (grid {grid})")
 
 
 def k_is_bf16(T, N):
@@ -130,7 +139,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--scenario", default="cfg2")
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--order", action="store_true", help="also print which tiles were stolen first / ran last")
     a = ap.parse_args()
+    global ORDER
+    ORDER = a.order
     torch.cuda.set_device(0)
     for s in a.scenario.split(","):
         scenario(s, a.reps)
