@@ -132,7 +132,6 @@ int cached_occupancy(const void* k, int threads, int smem, int (*prep)(const voi
 struct SchedKnobs {
     int max_depth = 1;
     int prefetch_max_stages = 4;
-    int prefetch_hint = 0;
 };
 const SchedKnobs& sched_knobs();
 
@@ -152,7 +151,6 @@ snn_status launch_tiles(Kernel k, int threads, int smem, int64_t ntiles, int64_t
                    ? 0
                    : (int)std::max<int64_t>(1, std::min<int64_t>(kn.max_depth, (8 + stages_per_tile - 1) / stages_per_tile));
     sc.prefetch = stages_per_tile <= kn.prefetch_max_stages ? 1 << 20 : 0;
-    sc.pf_hint = kn.prefetch_hint;
     return launch_kernel(k, dim3((unsigned)ntiles), dim3(threads), (size_t)smem, st, true, what, args..., sc);
 }
 

@@ -91,12 +91,6 @@ __device__ __forceinline__ void tma_prefetch_2d(const void* tmap, int c0, int c1
                  "r"(c0), "r"(c1)
                  : "memory");
 }
-__device__ __forceinline__ void tma_prefetch_2d(const void* tmap, int c0, int c1, uint64_t policy) {
-    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile.L2::cache_hint [%0, {%1, %2}], %3;" ::"l"(
-                     reinterpret_cast<uint64_t>(tmap)),
-                 "r"(c0), "r"(c1), "l"(policy)
-                 : "memory");
-}
 
 __device__ __forceinline__ void tma_prefetch_desc(const void* tmap) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");

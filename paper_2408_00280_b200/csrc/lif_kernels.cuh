@@ -94,7 +94,6 @@ __device__ __forceinline__ AffCoef<VEC> load_affine(const Affine& af, int64_t n0
 struct Sched {
     int depth;      // steal requests kept in flight, 1..kMaxClc (0: the whole grid is resident)
     int prefetch;   // ring stages of the CTA's own tile to L2-prefetch before griddepcontrol.wait
-    int pf_hint;    // 1: the prefetch carries the evict-first L2 policy of the loads
 };
 
 struct FwdArgs {

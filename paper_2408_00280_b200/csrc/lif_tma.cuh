@@ -334,10 +334,6 @@ lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_con
     const int64_t nrb = (T + R - 1) / R;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {   // before the wait: kernel-parameter descriptors, L2 prefetch of the own tile
-        const uint64_t pfpol = policy_evict_first();
-        auto pf2d = [&](const CUtensorMap* m, int c0_, int c1_) {
-            if (sc.pf_hint) tma_prefetch_2d(m, c0_, c1_, pfpol); else tma_prefetch_2d(m, c0_, c1_);
-        };
         tma_prefetch_desc(&tmx);
         if constexpr (RES) tma_prefetch_desc(&tmr);
         if constexpr (!UNAL) {
@@ -345,8 +341,8 @@ lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_con
             for (int j = 0; j < sc.prefetch && j < S && j < nrb; ++j)
 #pragma unroll
                 for (int b = 0; b < NB; ++b) {
-                    pf2d(&tmx, c0 + b * BW, j * R);
-                    if constexpr (RES) pf2d(&tmr, c0 + b * BW, j * R);
+                    tma_prefetch_2d(&tmx, c0 + b * BW, j * R);
+                    if constexpr (RES) tma_prefetch_2d(&tmr, c0 + b * BW, j * R);
                 }
         }
     }
@@ -586,10 +582,6 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
     const int64_t nch = (T + kCkpt - 1) / kCkpt;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {   // before the wait: kernel-parameter descriptors, L2 prefetch of the own tile
-        const uint64_t pfpol = policy_evict_first();
-        auto pf2d = [&](const CUtensorMap* m, int c0_, int c1_) {
-            if (sc.pf_hint) tma_prefetch_2d(m, c0_, c1_, pfpol); else tma_prefetch_2d(m, c0_, c1_);
-        };
         tma_prefetch_desc(&tmx); tma_prefetch_desc(&tmg); tma_prefetch_desc(&tmck);
         if constexpr (RES) tma_prefetch_desc(&tmr);
         const int c0 = (int)blockIdx.x * W;
@@ -597,11 +589,11 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
             const int ch = (int)nch - 1 - j;
 #pragma unroll
             for (int b = 0; b < NB; ++b) {
-                pf2d(&tmck, c0 + b * BW, ch);
+                tma_prefetch_2d(&tmck, c0 + b * BW, ch);
                 if constexpr (!UNAL) {
-                    pf2d(&tmx, c0 + b * BW, ch * kCkpt);
-                    pf2d(&tmg, c0 + b * BW, ch * kCkpt);
-                    if constexpr (RES) pf2d(&tmr, c0 + b * BW, ch * kCkpt);
+                    tma_prefetch_2d(&tmx, c0 + b * BW, ch * kCkpt);
+                    tma_prefetch_2d(&tmg, c0 + b * BW, ch * kCkpt);
+                    if constexpr (RES) tma_prefetch_2d(&tmr, c0 + b * BW, ch * kCkpt);
                 }
             }
         }
@@ -774,18 +766,14 @@ lif_backward_saveh_tma_kernel(const __grid_constant__ CUtensorMap tmh,
     const int64_t nrb = (T + R - 1) / R;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {   // before the wait: kernel-parameter descriptors, L2 prefetch of the own tile
-        const uint64_t pfpol = policy_evict_first();
-        auto pf2d = [&](const CUtensorMap* m, int c0_, int c1_) {
-            if (sc.pf_hint) tma_prefetch_2d(m, c0_, c1_, pfpol); else tma_prefetch_2d(m, c0_, c1_);
-        };
         tma_prefetch_desc(&tmh); tma_prefetch_desc(&tmg);
         const int c0 = (int)blockIdx.x * W;
         for (int j = 0; j < sc.prefetch && j < S && j < nrb; ++j) {
             const int rb = (int)nrb - 1 - j;
 #pragma unroll
             for (int b = 0; b < NB; ++b) {
-                pf2d(&tmh, c0 + b * BW, rb * R);
-                if constexpr (!UNAL) pf2d(&tmg, c0 + b * BW, rb * R);
+                tma_prefetch_2d(&tmh, c0 + b * BW, rb * R);
+                if constexpr (!UNAL) tma_prefetch_2d(&tmg, c0 + b * BW, rb * R);
             }
         }
     }
