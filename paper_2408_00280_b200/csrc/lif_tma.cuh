@@ -163,13 +163,15 @@ __device__ __forceinline__ int box_off(int nt, int r) {
 // (rows past T zero-filled by the TMA).  UNAL: per time row ONE 1-D bulk copy
 // (cp.async.bulk, UBLKCP) of the tile span [c0, c0 + W) of that row shifted down to a 16-byte
 // boundary, W*esz + 16 bytes (truncated at the view's last 16-byte chunk, which holds its last
-// element: nothing past the allocation is read), into smem row r at r * RP (RP = W*esz + 128 B,
+// element: nothing past the allocation is read), into smem row r at r * RP (RP = W*esz + 16 B,
 // 128-B aligned rows); only the `rows` valid rows are loaded (tx_bytes counts the same).
 template <typename IO, int BW, int ROWS, int NB, bool UNAL>
 struct Region {
     static constexpr int Q = 16 / (int)sizeof(IO);
     static constexpr int WB = NB * BW * (int)sizeof(IO);          // tile span bytes
-    static constexpr int RP = WB + 128;                           // UNAL smem row pitch (bytes)
+    // UNAL smem row pitch: 16-B aligned rows (the bulk-copy destination rule).  (r2: was + 128 B,
+    // which pushed the bf16 backward's 3-stage ring past two CTAs per SM: 45% of aligned speed.)
+    static constexpr int RP = WB + 16;
     static constexpr int RPE = RP / (int)sizeof(IO);
     static constexpr int BYTES = UNAL ? ROWS * RP : WB * ROWS;
 
@@ -222,6 +224,36 @@ struct Region {
     }
 };
 
+// VEC elements from shared memory at q of any element alignment, with the widest loads the
+// address allows (16 / 8 / 4 bytes; element loads only for 2-byte-aligned bf16).  The choice
+// is warp-uniform: every lane's q has the same misalignment.
+template <typename IO, int VEC>
+__device__ __forceinline__ Pack<IO, VEC> lds_widest(const IO* q) {
+    constexpr int B = (int)sizeof(Pack<IO, VEC>);
+    const uint32_t a = smem_u32(q);
+    Pack<IO, VEC> r;
+    if (a % B == 0) return *reinterpret_cast<const Pack<IO, VEC>*>(q);
+    if constexpr (B >= 16) {
+        if (a % 8 == 0) {
+#pragma unroll
+            for (int i = 0; i < B / 8; ++i)
+                reinterpret_cast<uint2*>(&r)[i] = reinterpret_cast<const uint2*>(q)[i];
+            return r;
+        }
+    }
+    if constexpr (B >= 8) {
+        if (a % 4 == 0) {
+#pragma unroll
+            for (int i = 0; i < B / 4; ++i)
+                reinterpret_cast<uint32_t*>(&r)[i] = reinterpret_cast<const uint32_t*>(q)[i];
+            return r;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) r.v[i] = q[i];
+    return r;
+}
+
 // A consumer lane's view of one tensor's rows in a stage: src(j) = the lane's VEC elements of
 // row j.  Aligned: box layout, pack loads.  UNAL: row-major with the row's element shift
 // m_j = (m0 + j*dm) mod Q (m0 = the first row's, dm = ld mod Q); pack loads where the shift keeps
@@ -236,11 +268,7 @@ struct RowSrc {
         } else {
             constexpr int Q = 16 / (int)sizeof(IO);
             const IO* q = p + j * RPE + ((m0 + j * dm) & (Q - 1));
-            if ((smem_u32(q) % sizeof(Pack<IO, VEC>)) == 0) return *reinterpret_cast<const Pack<IO, VEC>*>(q);
-            Pack<IO, VEC> r;
-#pragma unroll
-            for (int i = 0; i < VEC; ++i) r.v[i] = q[i];
-            return r;
+            return lds_widest<IO, VEC>(q);
         }
     }
 };
@@ -438,6 +466,8 @@ lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_con
                         if (nv > 0) st_stream<float, VEC>(h_row, hp);
                         h_row += a.ldh;
                     }
+                    // (r2: a warp-cooperative funnel-shift store of unaligned u8 rows -- one aligned word
+                    // per lane instead of byte stores -- measured 10-20% slower; not used)
                     store_spikes<IO, VEC, SFMT, UNAL>(spk_row, g, n0, bits, nv, a.nwords);
                     spk_row += spk_step;
                 }
