@@ -49,9 +49,10 @@ def parse():
     ap.add_argument("--sweep", action="store_true",
                     help="cfg1: also time T in {8,32,128,512} (L2 flushed before every launch)")
     ap.add_argument("--chunks", type=int, default=32, help="cfg3 neuron chunks of the wavefront")
-    ap.add_argument("--transport", choices=["handoff", "nccl"], default="nccl",
+    ap.add_argument("--transport", choices=["handoff", "handoff-nccl", "nccl"], default="nccl",
                     help="cfg3 boundary exchange: NCCL send/recv between per-chunk launches inside the "
-                         "C ABI (snn_lif_*_tsplit), or the fused in-kernel peer handoff (CUDA IPC)")
+                         "C ABI (snn_lif_*_tsplit), or the fused in-kernel peer handoff with peers from "
+                         "CUDA IPC (handoff) or from NCCL symmetric windows (handoff-nccl)")
     ap.add_argument("--tsplit-n", type=int, default=None,
                     help="neurons of the cfg3 time-split layer (default 2^22; 2^18 with --debug-single-gpu)")
     ap.add_argument("--tsplit-steps", type=int, default=10,
@@ -711,7 +712,9 @@ def tsplit_measure(args, world, rank, dev, N, T, steps, warmup, transport="nccl"
     neuron, the boundary V (forward) and dL/dV (backward) go to the neighbour rank.
       transport "nccl":    the C ABI snn_lif_*_tsplit over an snn_comm (NCCL send / recv,
                            args.chunks neuron chunks in a wavefront);
-      transport "handoff": the fused in-kernel peer handoff (CUDA IPC peer stores + flags).
+      transport "handoff": the fused in-kernel peer handoff (CUDA IPC peer stores + flags);
+      transport "handoff-nccl": the same kernels, buffers and peer pointers from an NCCL
+                           symmetric window on an snn_comm (snn_handoff_window_*).
     Returns per-step times: T(k) over the ranks, T(1) = the whole axis on one GPU (every rank runs
     it on its own GPU at the same time; max over ranks), the one-hop boundary time, and Eq. 5
      evaluated with T_s = T(1) and T_c = 2 hops (forward V + backward dL/dV)."""
@@ -756,7 +759,11 @@ def tsplit_measure(args, world, rank, dev, N, T, steps, warmup, transport="nccl"
         out["gpu_launches_per_step"] = 2 * out["chunks"]
     else:
         from paper_2408_00280_b200 import handoff as HO
-        ph = HO.PeerHandoff(N)
+        if transport == "handoff-nccl":
+            comm = D.NcclComm()
+            ph = HO.WindowHandoff(comm, N)
+        else:
+            ph = HO.PeerHandoff(N)
 
         def stepk():
             f = HO.lif_forward_handoff(X, params, ph.forward_handoff(), spike_fmt=args.spike_fmt,
@@ -805,10 +812,10 @@ def tsplit_measure(args, world, rank, dev, N, T, steps, warmup, transport="nccl"
             out["Ts_over_Tc"] = out["T1_ms"] / Tc
         out["eq5_inputs"] = "T_s = T(k=1) measured in this run; T_c = 2 one-hop [N] fp32 NCCL transfers"
     out["neuron_steps_per_s"] = N * T / (tk / 1e3)
-    if comm is not None:
-        comm.close()
     if ph is not None:
         ph.close()
+    if comm is not None:
+        comm.close()
     del X, G
     torch.cuda.empty_cache()
     return out

@@ -257,6 +257,36 @@ snn_status snn_lif_backward_tsplit(snn_comm* comm, const snn_lif_params* params,
                                    const void* saved, void* grad_x, float* g_in_ws, float* g_out_ws,
                                    void* stream);
 
+/* ---- The fused boundary handoff over NCCL symmetric windows (PAPER.md:252
+ * "inter-GPU communication enables cross-device operator fusion and data exchange along the
+ * temporal dimension").  The buffers and peer pointers that snn_lif_forward_handoff /
+ * snn_lif_backward_handoff need, taken from an snn_comm instead of CUDA IPC: each rank
+ * allocates one buffer with ncclMemAlloc holding the receive side of both directions (state
+ * [N] fp32, ready and ack flags [snn_lif_handoff_blocks(N)] int32, per direction) and
+ * registers it as a symmetric window (ncclCommWindowRegister, NCCL_WIN_COLL_SYMMETRIC); the
+ * neighbours' buffers are then ordinary load/store addresses of this process
+ * (ncclGetPeerPointer over the communicator's LSA team -- NVLink / P2P peers of one node).
+ *   snn_handoff_window_create  collective over the comm's ranks; N = neurons of the layer
+ *                              (the same on every rank); zeroes the buffers and returns once
+ *                              every rank has.  SNN_ERR_UNSUPPORTED when a time neighbour is
+ *                              not a load/store peer (another node, or no P2P path) or the
+ *                              process's NCCL has no window API; SNN_ERR_NCCL on NCCL errors.
+ *   snn_handoff_window_next    fills *handoff for this rank's next call in `direction`
+ *                              (0 forward: V from rank-1, to rank+1; 1 backward: dL/dV from
+ *                              rank+1, to rank-1) with epoch = 1, 2, ... per direction; pass
+ *                              it to the matching snn_lif_*_handoff call.  Every rank makes
+ *                              the same sequence of calls.
+ *   snn_handoff_window_pointer the base of this rank's buffer (which = 0) or of its previous
+ *                              (-1) / next (+1) neighbour's as mapped here (NULL without one).
+ *   snn_handoff_window_destroy synchronises the comm's stream, deregisters and frees
+ *                              (collective; NULL is a no-op).  Destroy windows before their comm. */
+typedef struct snn_handoff_window snn_handoff_window;
+
+snn_status snn_handoff_window_create(snn_comm* comm, int64_t N, snn_handoff_window** out);
+snn_status snn_handoff_window_next(snn_handoff_window* window, int direction, snn_lif_handoff* handoff);
+snn_status snn_handoff_window_pointer(const snn_handoff_window* window, int which, void** ptr);
+snn_status snn_handoff_window_destroy(snn_handoff_window* window);
+
 /* ---- Producer fusion ("fold the preceding BN affine / residual add into
  * the LIF prologue"): a per-channel affine prologue folded into the LIF input -- the
  * layer's current is X' = scale[c] X + shift[c] (+ R) with c = (n / HW) % C, e.g. the

@@ -35,6 +35,8 @@ EXPORTED_SYMBOLS = (
     "snn_lif_plan_forward", "snn_lif_plan_backward", "snn_lif_plan_destroy",
     "snn_nccl_unique_id", "snn_comm_create", "snn_comm_destroy", "snn_comm_info",
     "snn_lif_forward_tsplit", "snn_lif_backward_tsplit",
+    "snn_handoff_window_create", "snn_handoff_window_next", "snn_handoff_window_pointer",
+    "snn_handoff_window_destroy",
 )
 SNN_NCCL_UNIQUE_ID_BYTES = 128
 SNN_LIF_HANDOFF_BLOCK = 256
@@ -138,6 +140,14 @@ def _load() -> ctypes.CDLL:
     lib.snn_lif_forward_tsplit.restype = ci
     lib.snn_lif_backward_tsplit.argtypes = [vp, P, S, ci, vp, vp, fp, vp, vp, fp, fp, vp]
     lib.snn_lif_backward_tsplit.restype = ci
+    lib.snn_handoff_window_create.argtypes = [vp, i64, ctypes.POINTER(ctypes.c_void_p)]
+    lib.snn_handoff_window_create.restype = ci
+    lib.snn_handoff_window_next.argtypes = [vp, ci, Hp]
+    lib.snn_handoff_window_next.restype = ci
+    lib.snn_handoff_window_pointer.argtypes = [vp, ci, ctypes.POINTER(ctypes.c_void_p)]
+    lib.snn_handoff_window_pointer.restype = ci
+    lib.snn_handoff_window_destroy.argtypes = [vp]
+    lib.snn_handoff_window_destroy.restype = ci
     return lib
 
 
@@ -280,3 +290,27 @@ def snn_lif_backward_tsplit(comm, params, shape, n_chunks, grad_spikes, x, v_in_
                             g_out_ws, stream) -> None:
     check(lib.snn_lif_backward_tsplit(comm, ctypes.byref(params), ctypes.byref(shape), n_chunks, grad_spikes, x,
                                       v_in_ws, saved, grad_x, g_in_ws, g_out_ws, stream))
+
+
+# ---- fused handoff over NCCL symmetric windows (include/snn_lif.h snn_handoff_window_*)
+
+def snn_handoff_window_create(comm, N: int) -> int:
+    h = ctypes.c_void_p()
+    check(lib.snn_handoff_window_create(comm, N, ctypes.byref(h)))
+    return h.value
+
+
+def snn_handoff_window_next(window, direction: int) -> snn_lif_handoff:
+    h = snn_lif_handoff()
+    check(lib.snn_handoff_window_next(window, direction, ctypes.byref(h)))
+    return h
+
+
+def snn_handoff_window_pointer(window, which: int) -> int:
+    p = ctypes.c_void_p()
+    check(lib.snn_handoff_window_pointer(window, which, ctypes.byref(p)))
+    return p.value or 0
+
+
+def snn_handoff_window_destroy(window) -> None:
+    check(lib.snn_handoff_window_destroy(window))

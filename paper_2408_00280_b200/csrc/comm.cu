@@ -26,6 +26,7 @@
 #include <vector>
 
 #include <nccl.h>
+#include <nccl_device.h>   // ncclWindow_t, ncclGetPeerPointer (the symmetric-window handoff below)
 
 #include "internal.h"
 
@@ -46,11 +47,20 @@ struct NcclApi {
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
+    // symmetric memory windows (NCCL >= 2.27; optional: the window handoff needs them)
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*MemAlloc)(void**, size_t) = nullptr;
+    ncclResult_t (*MemFree)(void*) = nullptr;
+    ncclResult_t (*CommWindowRegister)(ncclComm_t, void*, size_t, ncclWindow_t*, int) = nullptr;
+    ncclResult_t (*CommWindowDeregister)(ncclComm_t, ncclWindow_t) = nullptr;
+    ncclTeam_t (*TeamLsa)(ncclComm_t) = nullptr;
+    bool windows = false;
 };
 
 // libnccl.so.2: the copy already in the process (torch's) if any, else $SNN_NCCL_LIBRARY, else
 // the loader's search path.
-const NcclApi& nccl() {
+const NcclApi& nccl_api() {
     static NcclApi api;
     static std::once_flag once;
     std::call_once(once, [] {
@@ -77,6 +87,15 @@ const NcclApi& nccl() {
         SNN_NCCL_SYM(GroupEnd, "ncclGroupEnd")
         SNN_NCCL_SYM(GetErrorString, "ncclGetErrorString")
 #undef SNN_NCCL_SYM
+        api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
+        api.MemAlloc = reinterpret_cast<decltype(api.MemAlloc)>(sym("ncclMemAlloc"));
+        api.MemFree = reinterpret_cast<decltype(api.MemFree)>(sym("ncclMemFree"));
+        api.CommWindowRegister = reinterpret_cast<decltype(api.CommWindowRegister)>(sym("ncclCommWindowRegister"));
+        api.CommWindowDeregister =
+            reinterpret_cast<decltype(api.CommWindowDeregister)>(sym("ncclCommWindowDeregister"));
+        api.TeamLsa = reinterpret_cast<decltype(api.TeamLsa)>(sym("ncclTeamLsa"));
+        api.windows = api.AllReduce && api.MemAlloc && api.MemFree && api.CommWindowRegister &&
+                      api.CommWindowDeregister && api.TeamLsa;
         api.GetVersion(&api.version);
         api.ok = true;
     });
@@ -103,7 +122,7 @@ namespace {
     do {                                                                                           \
         const ncclResult_t r_ = (expr);                                                            \
         if (r_ != ncclSuccess)                                                                     \
-            return fail(SNN_ERR_NCCL, "%s: %s", what, nccl().GetErrorString(r_));                   \
+            return fail(SNN_ERR_NCCL, "%s: %s", what, nccl_api().GetErrorString(r_));                   \
     } while (0)
 #define SNN_CUDA_OK(expr, what)                                                                    \
     do {                                                                                           \
@@ -161,7 +180,7 @@ extern "C" {
 
 snn_status snn_nccl_unique_id(void* out) {
     if (!out) return fail(SNN_ERR_NULL_POINTER, "out is NULL");
-    const NcclApi& api = nccl();
+    const NcclApi& api = nccl_api();
     if (!api.ok) return fail(SNN_ERR_NCCL, "%s", api.why);
     ncclUniqueId id;
     SNN_NCCL_TRY(api.GetUniqueId(&id), "ncclGetUniqueId");
@@ -176,7 +195,7 @@ snn_status snn_comm_create(snn_comm** out, const void* unique_id, int nranks, in
     if (!unique_id) return fail(SNN_ERR_NULL_POINTER, "unique_id is NULL");
     if (nranks < 1 || rank < 0 || rank >= nranks)
         return fail(SNN_ERR_INVALID_VALUE, "need 0 <= rank < nranks (rank=%d nranks=%d)", rank, nranks);
-    const NcclApi& api = nccl();
+    const NcclApi& api = nccl_api();
     if (!api.ok) return fail(SNN_ERR_NCCL, "%s", api.why);
     auto c = std::make_unique<snn_comm>();
     c->nranks = nranks;
@@ -226,8 +245,8 @@ snn_status snn_comm_destroy(snn_comm* c) {
     snn_status st = SNN_OK;
     if (c->cs) cudaStreamSynchronize(c->cs);
     if (c->comm) {
-        const ncclResult_t r = nccl().CommDestroy(c->comm);
-        if (r != ncclSuccess) st = fail(SNN_ERR_NCCL, "ncclCommDestroy: %s", nccl().GetErrorString(r));
+        const ncclResult_t r = nccl_api().CommDestroy(c->comm);
+        if (r != ncclSuccess) st = fail(SNN_ERR_NCCL, "ncclCommDestroy: %s", nccl_api().GetErrorString(r));
     }
     for (auto ev : c->recv_ev) cudaEventDestroy(ev);
     for (auto ev : c->done_ev) cudaEventDestroy(ev);
@@ -257,7 +276,7 @@ namespace {
 template <typename Launch>
 snn_status tsplit_loop(snn_comm* c, int64_t N, int M, int dir, float* in, float* out, cudaStream_t st,
                        Launch launch) {
-    const NcclApi& api = nccl();
+    const NcclApi& api = nccl_api();
     const int from = c->rank - dir, to = c->rank + dir;
     const bool has_from = c->nranks > 1 && from >= 0 && from < c->nranks;
     const bool has_to = c->nranks > 1 && to >= 0 && to < c->nranks;
@@ -334,7 +353,7 @@ snn_status tsplit_common_checks(snn_comm* c, const snn_lif_shape* s, int n_chunk
     if (!s) return fail(SNN_ERR_NULL_POINTER, "shape is NULL");
     if (n_chunks < 1) return fail(SNN_ERR_INVALID_VALUE, "n_chunks=%d must be >= 1", n_chunks);
     if (n_chunks > s->N) return fail(SNN_ERR_INVALID_VALUE, "n_chunks=%d > N=%lld", n_chunks, (long long)s->N);
-    if (c->nranks > 1 && !nccl().ok) return fail(SNN_ERR_NCCL, "%s", nccl().why);
+    if (c->nranks > 1 && !nccl_api().ok) return fail(SNN_ERR_NCCL, "%s", nccl_api().why);
     return SNN_OK;
 }
 
@@ -399,6 +418,172 @@ snn_status snn_lif_backward_tsplit(snn_comm* c, const snn_lif_params* p, const s
                              col(grad_x, a, esz), g_out_ws ? g_out_ws + a : nullptr, stream, nullptr, nullptr,
                              nullptr, &cv);
     });
+}
+
+}  // extern "C"
+
+// ---- the fused boundary handoff over NCCL symmetric windows -------------
+// Every rank allocates one buffer with ncclMemAlloc holding the receive sides of both
+// directions -- [fwd state N f32 | fwd ready nblk | fwd ack nblk | bwd state N f32 | bwd ready
+// nblk | bwd ack nblk], each part 256-B aligned, identical offsets on every rank -- and
+// registers it as a symmetric window on the snn_comm's communicator.  The neighbours' parts are
+// then plain load/store addresses of this process (ncclGetPeerPointer: the LSA team's flat
+// mapping over NVLink), handed to the kernels' existing snn_lif_handoff struct: the kernels
+// store each tile's carry-out straight into the neighbour's buffer and release its flag, as
+// with CUDA IPC (lif_handoff.cuh), but the peers come from the NCCL communicator.
+
+struct snn_handoff_window {
+    snn_comm* comm = nullptr;
+    void* buf = nullptr;
+    size_t bytes = 0;
+    ncclWindow_t win = nullptr;
+    int64_t N = 0, nblk = 0;
+    size_t off[6] = {};
+    char* local = nullptr;
+    char* prev = nullptr;   // rank-1's buffer (NULL on rank 0)
+    char* next = nullptr;   // rank+1's buffer (NULL on the last rank)
+    int epoch[2] = {0, 0};
+};
+
+namespace snn_window {
+__global__ void window_peer_ptrs(ncclWindow_t w, int p0, int p1, void** out) {
+    out[0] = p0 >= 0 ? ncclGetPeerPointer(w, 0, p0) : nullptr;
+    out[1] = p1 >= 0 ? ncclGetPeerPointer(w, 0, p1) : nullptr;
+}
+}  // namespace snn_window
+
+namespace {
+
+size_t round256(size_t b) { return (b + 255) & ~size_t(255); }
+
+void window_free(snn_handoff_window* w) {
+    const NcclApi& api = nccl_api();
+    if (w->win) api.CommWindowDeregister(w->comm->comm, w->win);
+    if (w->buf) api.MemFree(w->buf);
+    delete w;
+}
+
+}  // namespace
+
+extern "C" {
+
+snn_status snn_handoff_window_create(snn_comm* c, int64_t N, snn_handoff_window** out) {
+    NvtxRange range("snn_handoff_window_create");
+    if (!out) return fail(SNN_ERR_NULL_POINTER, "out is NULL");
+    *out = nullptr;
+    snn_status st;
+    if ((st = check_comm(c)) != SNN_OK) return st;
+    if (N < 1) return fail(SNN_ERR_INVALID_VALUE, "N=%lld must be >= 1", (long long)N);
+    const NcclApi& api = nccl_api();
+    if (!api.ok) return fail(SNN_ERR_NCCL, "%s", api.why);
+    if (!api.windows) return fail(SNN_ERR_UNSUPPORTED, "libnccl.so.2 (version %d) has no symmetric-window API", api.version);
+    // every neighbour must be a load/store peer (the LSA team: same node, NVLink / P2P)
+    const ncclTeam_t lsa = api.TeamLsa(c->comm);
+    for (int peer : {c->rank - 1, c->rank + 1}) {
+        if (peer < 0 || peer >= c->nranks) continue;
+        const int i = lsa.rank + (peer - c->rank);
+        if (lsa.stride != 1 || i < 0 || i >= lsa.nRanks)
+            return fail(SNN_ERR_UNSUPPORTED,
+                        "rank %d is not a load/store peer of rank %d (LSA team of %d ranks): use the NCCL "
+                        "send/recv split (snn_lif_*_tsplit) or CUDA IPC peers",
+                        peer, c->rank, lsa.nRanks);
+    }
+    auto w = new snn_handoff_window();
+    w->comm = c;
+    w->N = N;
+    w->nblk = (N + SNN_LIF_HANDOFF_BLOCK - 1) / SNN_LIF_HANDOFF_BLOCK;
+    const size_t part[6] = {round256(4 * (size_t)N), round256(4 * (size_t)w->nblk), round256(4 * (size_t)w->nblk),
+                            round256(4 * (size_t)N), round256(4 * (size_t)w->nblk), round256(4 * (size_t)w->nblk)};
+    for (int i = 0; i < 6; ++i) {
+        w->off[i] = w->bytes;
+        w->bytes += part[i];
+    }
+    w->bytes = (w->bytes + NCCL_WIN_REQUIRED_ALIGNMENT - 1) / NCCL_WIN_REQUIRED_ALIGNMENT * NCCL_WIN_REQUIRED_ALIGNMENT;
+    ncclResult_t r = api.MemAlloc(&w->buf, w->bytes);
+    if (r == ncclSuccess) r = api.CommWindowRegister(c->comm, w->buf, w->bytes, &w->win, NCCL_WIN_COLL_SYMMETRIC);
+    if (r != ncclSuccess) {
+        window_free(w);
+        return fail(SNN_ERR_NCCL, "symmetric window (ncclMemAlloc / ncclCommWindowRegister): %s", api.GetErrorString(r));
+    }
+    void** ptrs = nullptr;
+    cudaError_t e = cudaMemsetAsync(w->buf, 0, w->bytes, c->cs);
+    if (e == cudaSuccess) e = cudaMalloc(&ptrs, 2 * sizeof(void*));
+    if (e == cudaSuccess) {
+        snn_window::window_peer_ptrs<<<1, 1, 0, c->cs>>>(w->win, c->rank > 0 ? c->rank - 1 : -1,
+                                             c->rank + 1 < c->nranks ? c->rank + 1 : -1, ptrs);
+        e = cudaGetLastError();
+    }
+    void* host[2] = {nullptr, nullptr};
+    if (e == cudaSuccess) e = cudaMemcpyAsync(host, ptrs, sizeof(host), cudaMemcpyDeviceToHost, c->cs);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->cs);
+    if (ptrs) cudaFree(ptrs);
+    if (e != cudaSuccess) {
+        window_free(w);
+        return fail(SNN_ERR_CUDA, "symmetric window setup: %s", cudaGetErrorString(e));
+    }
+    w->local = static_cast<char*>(w->buf);
+    w->prev = static_cast<char*>(host[0]);
+    w->next = static_cast<char*>(host[1]);
+    // every rank's buffer is zeroed before any rank's kernel can publish into it
+    if (c->nranks > 1) {
+        r = api.AllReduce(c->scratch, c->scratch, 1, ncclFloat32, ncclSum, c->comm, c->cs);
+        if (r != ncclSuccess) {
+            window_free(w);
+            return fail(SNN_ERR_NCCL, "window barrier: %s", api.GetErrorString(r));
+        }
+        e = cudaStreamSynchronize(c->cs);
+        if (e != cudaSuccess) {
+            window_free(w);
+            return fail(SNN_ERR_CUDA, "window barrier: %s", cudaGetErrorString(e));
+        }
+    }
+    *out = w;
+    return SNN_OK;
+}
+
+snn_status snn_handoff_window_next(snn_handoff_window* w, int direction, snn_lif_handoff* h) {
+    if (!w || !h) return fail(SNN_ERR_NULL_POINTER, "window or handoff is NULL");
+    if (direction != 0 && direction != 1) return fail(SNN_ERR_INVALID_VALUE, "direction %d: 0 forward, 1 backward", direction);
+    std::memset(h, 0, sizeof(*h));
+    h->epoch = ++w->epoch[direction];
+    // forward (0): receive V from rank-1 into my fwd part, send into rank+1's fwd part;
+    // backward (1): receive dL/dV from rank+1 into my bwd part, send into rank-1's bwd part.
+    const size_t st = direction == 0 ? w->off[0] : w->off[3], rd = direction == 0 ? w->off[1] : w->off[4],
+                 ak = direction == 0 ? w->off[2] : w->off[5];
+    char* from = direction == 0 ? w->prev : w->next;
+    char* to = direction == 0 ? w->next : w->prev;
+    if (from) {
+        h->recv_state = reinterpret_cast<const float*>(w->local + st);
+        h->recv_ready = reinterpret_cast<const int*>(w->local + rd);
+        h->recv_ack = reinterpret_cast<int*>(from + ak);   // the sender's ack flags
+    }
+    if (to) {
+        h->send_state = reinterpret_cast<float*>(to + st);
+        h->send_ready = reinterpret_cast<int*>(to + rd);
+        h->send_ack = reinterpret_cast<const int*>(w->local + ak);
+    }
+    return SNN_OK;
+}
+
+snn_status snn_handoff_window_pointer(const snn_handoff_window* w, int which, void** ptr) {
+    if (!w || !ptr) return fail(SNN_ERR_NULL_POINTER, "window or ptr is NULL");
+    if (which < -1 || which > 1) return fail(SNN_ERR_INVALID_VALUE, "which=%d: -1 previous, 0 own, 1 next", which);
+    *ptr = which < 0 ? w->prev : which > 0 ? w->next : w->local;
+    return SNN_OK;
+}
+
+snn_status snn_handoff_window_destroy(snn_handoff_window* w) {
+    if (!w) return SNN_OK;
+    snn_comm* c = w->comm;
+    snn_status st = SNN_OK;
+    cudaDeviceSynchronize();   // this rank's kernels are done with every buffer they touch
+    if (c->nranks > 1) {       // ... and every other rank's too, before anything is freed
+        const ncclResult_t r = nccl_api().AllReduce(c->scratch, c->scratch, 1, ncclFloat32, ncclSum, c->comm, c->cs);
+        if (r != ncclSuccess) st = fail(SNN_ERR_NCCL, "window barrier: %s", nccl_api().GetErrorString(r));
+        cudaStreamSynchronize(c->cs);
+    }
+    window_free(w);
+    return st;
 }
 
 }  // extern "C"

@@ -13,7 +13,9 @@ Buffers (per rank, per direction): recv_state [N] fp32, recv_ready / send_ack fl
 [ceil(N/256)] int32, allocated with cudaMalloc so their CUDA IPC handles map the whole
 allocation.  ``PeerHandoff`` exchanges the handles over a torch.distributed group (gloo
 or NCCL) and opens the neighbours' buffers (cudaIpcOpenMemHandle: NVLink peer mappings
-on a multi-GPU box; the same device works too, which the tests use).
+on a multi-GPU box; the same device works too, which the tests use).  ``WindowHandoff``
+takes the buffers and peer mappings from the NCCL communicator of the time split instead
+(symmetric memory windows).
 """
 from __future__ import annotations
 
@@ -172,6 +174,37 @@ class PeerHandoff:
         dist.barrier(group=group)
         self.fwd.free()
         self.bwd.free()
+
+
+class WindowHandoff:
+    """The same boundary buffers and neighbour pointers as ``PeerHandoff``, taken from an
+    NCCL communicator instead of CUDA IPC (include/snn_lif.h snn_handoff_window_*): every
+    rank's receive buffers live in one ncclMemAlloc allocation registered as a symmetric
+    window on ``comm`` (a ``dist.NcclComm``, rank order = time order), and the neighbours'
+    buffers are addressed through the window's LSA mapping (NVLink peers of one node).  Raises
+    RuntimeError (SNN_ERR_UNSUPPORTED) when a time neighbour is not a load/store peer.
+    Collective: every rank constructs it with the same N."""
+
+    def __init__(self, comm, N: int):
+        self.comm = comm
+        self.N = N
+        self.rank, self.world = comm.rank, comm.world
+        self.handle = _lib.snn_handoff_window_create(comm.handle, N)
+
+    def forward_handoff(self):
+        return _lib.snn_handoff_window_next(self.handle, 0)
+
+    def backward_handoff(self):
+        return _lib.snn_handoff_window_next(self.handle, 1)
+
+    def pointer(self, which: int) -> int:
+        """Base address of this rank's buffer (0) or its neighbour's (-1 / +1) as mapped here."""
+        return _lib.snn_handoff_window_pointer(self.handle, which)
+
+    def close(self, group=None):
+        if getattr(self, "handle", None):
+            _lib.snn_handoff_window_destroy(self.handle)
+            self.handle = None
 
 
 def lif_forward_handoff(x: torch.Tensor, params: LIFParams, handoff, *, spike_fmt: str = "u8",

@@ -132,6 +132,18 @@ def test_comm_and_tsplit_validation(lib):
     assert b"comm is NULL" in lib.lib.snn_last_error_message()
 
 
+def test_handoff_window_validation(lib):
+    """The NCCL-window handoff entry points validate their handles before any NCCL or device work."""
+    h = ctypes.c_void_p()
+    assert lib.lib.snn_handoff_window_create(None, 1024, ctypes.byref(h)) == 2
+    assert lib.lib.snn_handoff_window_create(None, 1024, None) == 2
+    assert h.value is None
+    ho = lib.snn_lif_handoff()
+    assert lib.lib.snn_handoff_window_next(None, 0, ctypes.byref(ho)) == 2
+    assert lib.lib.snn_handoff_window_pointer(None, 0, ctypes.byref(h)) == 2
+    assert lib.lib.snn_handoff_window_destroy(None) == 0
+
+
 def test_nccl_unique_id_from_the_process_nccl(lib):
     """snn_nccl_unique_id resolves NCCL at run time (no GPU needed) and returns 128 bytes."""
     uid = lib.snn_nccl_unique_id()

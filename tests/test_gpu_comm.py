@@ -65,6 +65,36 @@ def test_tsplit_validation_errors(comm1):
         D.lif_forward_tsplit(comm1, X, snn.LIFParams(tau=0.5))
 
 
+def test_window_handoff_single_rank_equals_plain_and_oracle(comm1):
+    """SURVEY 8(f) f1 over NCCL symmetric windows (snn_handoff_window_*): a 1-rank
+    communicator registers its window (ncclMemAlloc + ncclCommWindowRegister), has no time
+    neighbour, and its handoff calls are the plain fused kernels -- bitwise equal to
+    snn_lif_forward / snn_lif_backward and to the oracle, over two epochs."""
+    from paper_2408_00280_b200 import handoff as HO
+    T, N = 24, 4099
+    X = snn_synth.normal_tensor(1234, T, N, device="cuda")
+    G = snn_synth.normal_tensor(4321, T, N, device="cuda")
+    w = HO.WindowHandoff(comm1, N)
+    try:
+        assert w.pointer(0) != 0 and w.pointer(-1) == 0 and w.pointer(1) == 0
+        for epoch in (1, 2):
+            hf, hb = w.forward_handoff(), w.backward_handoff()
+            assert hf.epoch == epoch and hb.epoch == epoch
+            assert not any((hf.recv_state, hf.send_state, hb.recv_state, hb.send_state))
+            f = HO.lif_forward_handoff(X, PAPER, hf)
+            gx, gvi = HO.lif_backward_handoff(G, f, hb)
+            ref = snn.lif_forward(X, PAPER)
+            gref, gviref = snn.lif_backward(G, ref)
+            torch.cuda.synchronize()
+            assert torch.equal(f.spikes, ref.spikes) and torch.equal(f.v_final, ref.v_final)
+            assert torch.equal(gx, gref) and torch.equal(gvi, gviref)
+        rep = oracle_check(PAPER, X.cpu(), G.cpu(), f.spikes.cpu(), gx.cpu(), vf_gpu=f.v_final.cpu(),
+                           gvi_gpu=gvi.cpu())
+        assert rep.ok, str(rep)
+    finally:
+        w.close()
+
+
 # ------------------------------------------------------------------ two ranks, one GPU
 
 def _rendezvous_file():
@@ -90,6 +120,14 @@ def _worker(rank, world, path, T, N, n_chunks, out):
     except RuntimeError as e:                  # report (the parent kills a peer left waiting)
         out.put(("error", f"rank {rank}: {e}"))
         return
+    # the window handoff needs load/store peers: two "hosts" (one per NCCL_HOSTID) are not an
+    # LSA team, so creation must refuse cleanly (SNN_ERR_UNSUPPORTED), not hang or fault
+    from paper_2408_00280_b200 import handoff as HO
+    try:
+        HO.WindowHandoff(comm, N).close()
+        refusal = "created"
+    except RuntimeError as e:
+        refusal = str(e)
     p = snn.LIFParams.paper()
     a, b = D.partition_time(T, world)[rank]
     X = snn_synth.normal_tensor(1234, b - a, N, t_offset=a, device="cuda")
@@ -104,7 +142,7 @@ def _worker(rank, world, path, T, N, n_chunks, out):
                     None if gvi is None else gvi.cpu().numpy(), ts.messages_sent))
     comm.close()
     objs = [None] * world
-    dist.all_gather_object(objs, (a, b, res))
+    dist.all_gather_object(objs, (a, b, res, refusal))
     if rank == 0:
         out.put(("ok", objs))
     dist.barrier()
@@ -148,6 +186,8 @@ def test_two_rank_nccl_tsplit_on_one_gpu(world, n_chunks):
     rep = oracle_check(PAPER, X.cpu(), G.cpu(), torch.from_numpy(S), torch.from_numpy(GX),
                        vf_gpu=torch.from_numpy(objs[-1][2][1][2]), gvi_gpu=torch.from_numpy(objs[0][2][1][3]))
     assert rep.ok, str(rep)
+    for o in objs:
+        assert "UNSUPPORTED" in o[3] and "load/store peer" in o[3], o[3]
     # one message per chunk per boundary per direction
     n_eff = len(D.neuron_chunks(N, n_chunks, 512))
     assert objs[0][2][0][4] == n_eff and objs[-1][2][0][4] == n_eff
