@@ -122,6 +122,7 @@ __device__ __forceinline__ void produce(unsigned char* smem, Barriers<S>* bar, i
             }
             if constexpr (WARP) __syncwarp();
             issue(smem + s * STAGE_BYTES, tile, j, &bar->full[s]);
+            trace_issue();
         }
         tile = -1;
         while (consumed < issued) {

@@ -18,12 +18,8 @@ struct TraceRec {
     int64_t T, N;
     uint64_t t_entry, t_wait, t_first, t_end;
     int32_t first_stolen, last_tile;   // tile indices: the first taken over from a pending CTA, the last run
+    uint64_t t_issue;                  // the producer issued the first stage's loads
 };
-struct TraceBuf {   // device memory, allocated by snn_trace_read's first call
-    unsigned int count, pad[15];
-    TraceRec rec[kTraceRecords];
-};
-
 __device__ __forceinline__ uint64_t gtimer() {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -34,11 +30,28 @@ __device__ __forceinline__ uint32_t smid() {
     asm volatile("mov.u32 %0, %%smid;" : "=r"(s));
     return s;
 }
+__device__ __forceinline__ uint64_t* trace_issue_slot() {
+    __shared__ uint64_t slot;
+    return &slot;
+}
+// producer: stamp the first issue (the slot is zeroed by thread 0 before the CTA's first barrier)
+__device__ __forceinline__ void trace_issue() {
+    uint64_t* p = trace_issue_slot();
+    if (*p == 0) *p = gtimer();
+}
+struct TraceBuf {   // device memory, allocated by snn_trace_read's first call
+    unsigned int count, pad[15];
+    TraceRec rec[kTraceRecords];
+};
+
 struct TraceCta {
     uint64_t t_entry = 0, t_wait = 0, t_first = 0;
     uint32_t tiles = 0;
     int32_t first_stolen = -1, last_tile = -1;
-    __device__ __forceinline__ void entry() { t_entry = gtimer(); }
+    __device__ __forceinline__ void entry() {
+        t_entry = gtimer();
+        if (threadIdx.x == 0) *trace_issue_slot() = 0;
+    }
     __device__ __forceinline__ void waited() { t_wait = gtimer(); }
     __device__ __forceinline__ void stage() {
         if (t_first == 0) t_first = gtimer();
@@ -59,10 +72,12 @@ struct TraceCta {
         r.T = T; r.N = N;
         r.t_entry = t_entry; r.t_wait = t_wait; r.t_first = t_first; r.t_end = gtimer();
         r.first_stolen = first_stolen; r.last_tile = last_tile;
+        r.t_issue = *trace_issue_slot();
         b->rec[i] = r;
     }
 };
 #else
+__device__ __forceinline__ void trace_issue() {}
 struct TraceCta {
     __device__ __forceinline__ void entry() {}
     __device__ __forceinline__ void waited() {}

@@ -24,7 +24,7 @@ import snn_synth  # noqa: E402
 
 REC = np.dtype([("kind", "<u4"), ("grid", "<u4"), ("smid", "<u4"), ("tiles", "<u4"), ("T", "<i8"), ("N", "<i8"),
                 ("t_entry", "<u8"), ("t_wait", "<u8"), ("t_first", "<u8"), ("t_end", "<u8"),
-                ("first_stolen", "<i4"), ("last_tile", "<i4")])
+                ("first_stolen", "<i4"), ("last_tile", "<i4"), ("t_issue", "<u8")])
 KIND = {1: "fwd", 2: "bwd", 3: "bwdH"}
 ORDER = False
 
@@ -58,7 +58,8 @@ def report(recs, title):
     t0 = int(recs["t_entry"].min())
     prev_end = None
     print(f"{'launch':>22} {'ctas':>5} {'tiles':>6} {'entry':>8} {'wait0':>8} {'wait1':>8} {'first0':>8} "
-          f"{'first_med':>9} {'end_med':>8} {'end':>8} {'dur':>7} {'gap':>6} {'GB/s':>6} [us, from the first entry; GB/s = alg. bytes / (end - wait0)]")
+          f"{'first_med':>9} {'end_med':>8} {'end':>8} {'dur':>7} {'gap':>6} {'GB/s':>6} {'issue_med':>9} "
+          f"[us, from the first entry; GB/s = alg. bytes / (end - wait0); issue = producer's first loads]")
     for L in launches:
         a = np.array(L["rows"], dtype=REC)
         k, grid, T, N = L["key"]
@@ -71,7 +72,7 @@ def report(recs, title):
         print(f"{KIND.get(k, k):>5} T={T:<4d} N={N:<9d} {len(a):5d} {int(a['tiles'].sum()):6d} {us(ent):8.2f} "
               f"{us(a['t_wait'].min()):8.2f} {us(a['t_wait'].max()):8.2f} {us(a['t_first'].min()):8.2f} "
               f"{us(np.median(a['t_first'])):9.2f} {us(np.median(a['t_end'])):8.2f} {us(end):8.2f} "
-              f"{(int(end) - int(ent)) / 1e3:7.2f} {gap} {gbs:6.0f}")
+              f"{(int(end) - int(ent)) / 1e3:7.2f} {gap} {gbs:6.0f} {us(np.median(a['t_issue'])):9.2f}")
         prev_end = int(end)
         if ORDER and grid > len(a):
             # steal order: first stolen tile of each CTA (sorted by time it was taken ~ entry order),
