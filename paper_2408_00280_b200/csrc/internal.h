@@ -128,16 +128,15 @@ int cached_occupancy(const void* k, int threads, int smem, int (*prep)(const voi
 // an evict-first hint on the prefetch does not change that).
 // Environment overrides (A/B timing, tools/trace_timeline.py): SNN_LIF_CLC_DEPTH (requests
 // in flight, 1..4), SNN_LIF_PREFETCH (0: never prefetch; >0: prefetch tiles of up to that
-// many stages), SNN_LIF_RUNAHEAD_MB (L2 budget of the final-phase run-ahead; 0: off).
+// many stages).
 struct SchedKnobs {
     int max_depth = 1;
     int prefetch_max_stages = 4;
-    int runahead_mb = 48;   // L2 budget of the final-phase run-ahead over all resident CTAs
 };
 const SchedKnobs& sched_knobs();
 
 template <typename Kernel, typename... Args>
-snn_status launch_tiles(Kernel k, int threads, int smem, int stage_bytes, int64_t ntiles, int64_t stages_per_tile,
+snn_status launch_tiles(Kernel k, int threads, int smem, int64_t ntiles, int64_t stages_per_tile,
                         cudaStream_t st, const char* what, const Args&... args) {
     const int occ = cached_occupancy(reinterpret_cast<const void*>(k), threads, smem, [](const void* kk, int t, int sm) {
         return prepare(reinterpret_cast<Kernel>(const_cast<void*>(kk)), t, sm);
@@ -152,8 +151,6 @@ snn_status launch_tiles(Kernel k, int threads, int smem, int stage_bytes, int64_
                    ? 0
                    : (int)std::max<int64_t>(1, std::min<int64_t>(kn.max_depth, (8 + stages_per_tile - 1) / stages_per_tile));
     sc.prefetch = stages_per_tile <= kn.prefetch_max_stages ? 1 << 20 : 0;
-    sc.runahead = (int)std::min<int64_t>(
-        16, ((int64_t)kn.runahead_mb << 20) / std::max<int64_t>(1, std::min(ntiles, resident) * (int64_t)stage_bytes));
     return launch_kernel(k, dim3((unsigned)ntiles), dim3(threads), (size_t)smem, st, true, what, args..., sc);
 }
 

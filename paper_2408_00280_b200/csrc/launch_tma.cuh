@@ -96,7 +96,7 @@ snn_status launch_forward_tma(const snn_lif_shape* s, const snn::FwdArgs& a0, bo
         auto k = snn::lif_forward_tma_kernel<IO, C::FV, decltype(sfmt)::value, decltype(save)::value,
                                              (bool)decltype(sft)::value, P >= 1, P == 2, NC, C::FR, NS, UNAL,
                                              (bool)decltype(pz)::value>;
-        return launch_tiles(k, K::THREADS, K::SMEM, K::STAGE_BYTES, (s->N + K::W - 1) / K::W, (s->T + C::FR - 1) / C::FR,
+        return launch_tiles(k, K::THREADS, K::SMEM, (s->N + K::W - 1) / K::W, (s->T + C::FR - 1) / C::FR,
                             st, "lif_forward_tma_kernel", tmx, tmr, a);
     };
     auto by_aff = [&](auto sfmt, auto save, auto sft) {
@@ -137,7 +137,7 @@ snn_status launch_backward_tma_mode(const snn_lif_shape* s, const snn::BwdArgs& 
             !encode_io<IO, UNAL>(&tmg, a.gS, s, Cfg::BW, C::HR, &a.g_off))
             return fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled failed (SAVE_H backward)%s", encode_detail());
         auto k = snn::lif_backward_saveh_tma_kernel<IO, C::HV, MODE, C::HN, C::HR, C::HS, UNAL>;
-        return launch_tiles(k, Cfg::THREADS, Cfg::SMEM, Cfg::STAGE_BYTES, (s->N + Cfg::W - 1) / Cfg::W,
+        return launch_tiles(k, Cfg::THREADS, Cfg::SMEM, (s->N + Cfg::W - 1) / Cfg::W,
                             (s->T + C::HR - 1) / C::HR, st, "lif_backward_saveh_tma_kernel", tmh, tmg, a);
     }
     }
@@ -154,7 +154,7 @@ snn_status launch_backward_tma_mode(const snn_lif_shape* s, const snn::BwdArgs& 
     if (RES && !encode_io<IO, UNAL>(&tmr, a.af.residual, s, Cfg::BW, snn::kCkpt, &a.r_off))
         return fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled failed for the residual%s", encode_detail());
     auto k = snn::lif_backward_recompute_tma_kernel<IO, C::RV, MODE, C::RN, NS, UNAL>;
-    return launch_tiles(k, Cfg::THREADS, Cfg::SMEM, Cfg::STAGE_BYTES, (s->N + Cfg::W - 1) / Cfg::W, nch, st,
+    return launch_tiles(k, Cfg::THREADS, Cfg::SMEM, (s->N + Cfg::W - 1) / Cfg::W, nch, st,
                         "lif_backward_recompute_tma_kernel", tmx, tmg, tmck, tmr, a);
 }
 

@@ -149,21 +149,4 @@ __device__ __forceinline__ int clc_next_tile(ClcSlot* c, uint32_t& phase) {
     return ok ? (int)x : -1;
 }
 
-// Non-blocking look at an outstanding steal request (producer): true once its answer has
-// arrived and says no CTA was pending -- the tile being issued is this CTA's last.  Consumes
-// nothing (clc_next_tile still reads the same answer later).
-__device__ __forceinline__ bool clc_peek_failed(ClcSlot* c, uint32_t phase) {
-    if (!mbar_try_wait(&c->bar, phase)) return false;
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .b128 r;\n\t.reg .pred p;\n\t"
-        "ld.shared.b128 r, [%1];\n\t"
-        "clusterlaunchcontrol.query_cancel.is_canceled.pred.b128 p, r;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(smem_u32(&c->resp))
-        : "memory");
-    return ok == 0;
-}
-
 }  // namespace snn

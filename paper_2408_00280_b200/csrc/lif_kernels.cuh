@@ -94,7 +94,6 @@ __device__ __forceinline__ AffCoef<VEC> load_affine(const Affine& af, int64_t n0
 struct Sched {
     int depth;      // steal requests kept in flight, 1..kMaxClc (0: the whole grid is resident)
     int prefetch;   // ring stages of the CTA's own tile to L2-prefetch before griddepcontrol.wait
-    int runahead;   // final phase: stages to L2-prefetch beyond the ring (lif_tma.cuh produce)
 };
 
 struct FwdArgs {

@@ -100,29 +100,19 @@ __device__ __forceinline__ void init_barriers(Barriers<S>* b, uint32_t consumer_
 // barriers and sends the steal requests, and `issue` is called on every lane (the unaligned
 // kernels spread their per-row TMA loads over the lanes: one thread issues ~one UTMALDG per
 // 50 ns, too few for rows that each need their own loads).
-//
-// Final-phase run-ahead (sc.runahead > 0): once the outstanding steal request has come back
-// empty, the tile being issued is the CTA's last, and the CTAs drop out one by one while the
-// survivors are limited by their ring (S stages in flight at the then unloaded latency: the
-// end-of-grid tail, ~15-35 us at T = 512).  From then on the producer also L2-prefetches
-// (`prefetch(tile, j)`) up to sc.runahead stages beyond the ring, so the last tiles stream from
-// L2 with more bytes in flight; sc.runahead is sized on the host so every CTA's run-ahead fits
-// in a share of L2.
-template <int S, int STAGE_BYTES, bool WARP = false, typename Bytes, typename Issue, typename Prefetch>
+template <int S, int STAGE_BYTES, bool WARP = false, typename Bytes, typename Issue>
 __device__ __forceinline__ void produce(unsigned char* smem, Barriers<S>* bar, int64_t nstages,
-                                        const Sched& sc, Bytes bytes, Issue issue, Prefetch prefetch) {
+                                        const Sched& sc, Bytes bytes, Issue issue) {
     const bool leader = !WARP || (threadIdx.x & 31) == 0;
     const int depth = sc.depth;
     uint32_t k = 0;
     uint32_t phases = 0;   // bit i = parity of CLC slot i (a bit set, not an array: no local memory)
     int issued = 0, consumed = 0;
     bool stop = false;
-    bool last = depth == 0;   // the whole grid is resident: every CTA's tile is its last
     for (int i = 0; i < depth; ++i, ++issued)
         if (leader) clc_request(&bar->clc[i]);
     int tile = (int)blockIdx.x;
     while (true) {
-        int64_t pf_next = S;   // next stage of this tile to run ahead on (the ring covers [j, j + S))
         for (int64_t j = 0; j < nstages; ++j, ++k) {
             const int s = k % S;
             mbar_wait(&bar->empty[s], ((k / S) & 1) ^ 1);
@@ -133,19 +123,6 @@ __device__ __forceinline__ void produce(unsigned char* smem, Barriers<S>* bar, i
             if constexpr (WARP) __syncwarp();
             issue(smem + s * STAGE_BYTES, tile, j, &bar->full[s]);
             trace_issue();
-            if (sc.runahead > 0 && nstages > S) {
-                if (!last && consumed < issued) {
-                    const int i = consumed % depth;
-                    bool f = clc_peek_failed(&bar->clc[i], (phases >> i) & 1u);
-                    if constexpr (WARP) f = __shfl_sync(0xffffffffu, f, 0);
-                    last = f;
-                }
-                if (last && leader) {
-                    if (pf_next < j + S) pf_next = j + S;
-                    const int64_t lim = min(nstages, j + S + sc.runahead);
-                    for (; pf_next < lim; ++pf_next) prefetch(tile, pf_next);
-                }
-            }
         }
         tile = -1;
         while (consumed < issued) {
@@ -419,15 +396,6 @@ lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_con
                     Reg::load(stg, &tmx, fx, (int64_t)tile * W, rb * R, rows_of(rb), a.ld, fb, pol);
                     if constexpr (RES)
                         Reg::load(stg + Cfg::R_OFF, &tmr, fr, (int64_t)tile * W, rb * R, rows_of(rb), a.ld, fb, pol, R);
-                },
-                [&](int tile, int64_t rb) {
-                    if constexpr (!UNAL) {
-#pragma unroll
-                        for (int b = 0; b < NB; ++b) {
-                            tma_prefetch_2d(&tmx, tile * W + b * BW, (int)(rb * R));
-                            if constexpr (RES) tma_prefetch_2d(&tmr, tile * W + b * BW, (int)(rb * R));
-                        }
-                    }
                 });
         }
         return;
@@ -696,18 +664,6 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
                     Reg::load(stg + Cfg::X_OFF, &tmx, fx, c0, ch * kCkpt, rows, ld, fb, pol);
                     Reg::load(stg + Cfg::G_OFF, &tmg, fg, c0, ch * kCkpt, rows, ld, fb, pol, kCkpt);
                     if constexpr (RES) Reg::load(stg + Cfg::R_OFF, &tmr, fr, c0, ch * kCkpt, rows, ld, fb, pol, 2 * kCkpt);
-                },
-                [&](int tile, int64_t j) {
-                    const int ch = (int)(nch - 1 - j);
-#pragma unroll
-                    for (int b = 0; b < NB; ++b) {
-                        tma_prefetch_2d(&tmck, tile * W + b * BW, ch);
-                        if constexpr (!UNAL) {
-                            tma_prefetch_2d(&tmx, tile * W + b * BW, ch * kCkpt);
-                            tma_prefetch_2d(&tmg, tile * W + b * BW, ch * kCkpt);
-                            if constexpr (RES) tma_prefetch_2d(&tmr, tile * W + b * BW, ch * kCkpt);
-                        }
-                    }
                 });
         }
         return;
@@ -878,14 +834,6 @@ lif_backward_saveh_tma_kernel(const __grid_constant__ CUtensorMap tmh,
                             tma_load_2d(stg + b * Cfg::HBOX, &tmh, (int)(c0 + b * BW), (int)(rb * R), fb, pol);
                     }
                     Reg::load(stg + Cfg::G_OFF, &tmg, fg, c0, rb * R, rows_of(j), ld, fb, pol);
-                },
-                [&](int tile, int64_t j) {
-                    const int rb = (int)(nrb - 1 - j);
-#pragma unroll
-                    for (int b = 0; b < NB; ++b) {
-                        tma_prefetch_2d(&tmh, tile * W + b * BW, rb * R);
-                        if constexpr (!UNAL) tma_prefetch_2d(&tmg, tile * W + b * BW, rb * R);
-                    }
                 });
         }
         return;

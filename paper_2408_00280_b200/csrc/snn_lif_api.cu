@@ -66,7 +66,6 @@ const SchedKnobs& sched_knobs() {
         };
         env("SNN_LIF_CLC_DEPTH", &r.max_depth);
         env("SNN_LIF_PREFETCH", &r.prefetch_max_stages);
-        env("SNN_LIF_RUNAHEAD_MB", &r.runahead_mb);
         r.max_depth = std::max(1, std::min(r.max_depth, 4));
         return r;
     }();
