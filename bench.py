@@ -629,6 +629,40 @@ def run_affine(args, params, dev):
     return res
 
 
+def torch_serial_lif(X, G, params, out=None):
+    """Fig. 5's "Serial (PyTorch)" baseline: the LIF forward and its BPTT
+    backward written step by step with eager torch ops -- every time step round-trips V / dL/dV
+    through memory, one kernel per op.  Paper mode only (hard reset, sigmoid surrogate, the
+    charge H = k V + X + V_reset / tau of Eq. 1; dV/dH = (1 - S) + (V_reset - H) d,
+    DESIGN.md R7).  Returns (S [T, N], dL/dX [T, N]) in X's dtype (`out`: preallocated pair).
+    Checked against the oracle in tests/test_bench_reference.py."""
+    import torch
+    assert params.reset == "hard" and params.surrogate == "sigmoid" and not params.decay_input \
+        and not params.detach_reset, "the serial PyTorch baseline is written for the paper's mode"
+    T, N = X.shape
+    k = 1.0 - 1.0 / params.tau
+    vth, vr = params.v_th, params.v_reset
+    S_out, gX = out if out is not None else (torch.empty_like(X), torch.empty_like(X))
+    V = torch.full((N,), vr, device=X.device, dtype=torch.float32)
+    Hs = []
+    for t in range(T):
+        H = k * V + X[t] + vr / params.tau
+        S = (H >= vth).to(torch.float32)
+        V = torch.where(S > 0, torch.full_like(H, vr), H)
+        S_out[t] = S
+        Hs.append(H)
+    gV = torch.zeros(N, device=X.device, dtype=torch.float32)
+    for t in range(T - 1, -1, -1):
+        H = Hs[t]
+        e = torch.exp(-params.alpha * (H - vth).abs())
+        d = params.alpha * e / (1 + e) ** 2
+        S = (H >= vth).to(H.dtype)
+        gH = G[t] * d + gV * ((1 - S) + (vr - H) * d)
+        gX[t] = gH
+        gV = k * gH
+    return S_out, gX
+
+
 def time_serial_baselines(params, X, G, dev, flush, reps=5):
     """The paper's self-built baselines of Fig. 5: "Serial (CUDA)" -- one
     launch per time step through the C ABI (snn_lif_serial_*_step), state through HBM --
@@ -636,26 +670,10 @@ def time_serial_baselines(params, X, G, dev, flush, reps=5):
     fwd+bwd over the same inputs; median of `reps`, L2 flushed before each."""
     import torch
     from paper_2408_00280_b200.lif import lif_serial
-    T, N = X.shape
-    k = 1.0 - 1.0 / params.tau
-    vth, vr = params.v_th, params.v_reset
+    outs = (torch.empty_like(X), torch.empty_like(X))
 
     def torch_serial():
-        V = torch.full((N,), vr, device=dev)
-        Hs = []
-        for t in range(T):
-            H = k * V + X[t] + vr / params.tau
-            S = (H >= vth).to(X.dtype)
-            V = torch.where(S > 0, torch.full_like(H, vr), H)
-            Hs.append(H)
-        gV = torch.zeros(N, device=dev)
-        for t in range(T - 1, -1, -1):
-            H = Hs[t]
-            e = torch.exp(-params.alpha * (H - vth).abs())
-            d = params.alpha * e / (1 + e) ** 2
-            S = (H >= vth).to(H.dtype)
-            gH = G[t] * d + gV * ((1 - S) + (vr - H) * d)
-            gV = k * gH
+        torch_serial_lif(X, G, params, outs)
 
     out = {}
     for name, fn in (("cuda_ms", lambda: lif_serial(X, G, params)), ("torch_ms", torch_serial)):

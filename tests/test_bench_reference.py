@@ -64,3 +64,22 @@ def test_gpus_flag_relaunches_under_torchrun(monkeypatch):
     import pytest
     with pytest.raises(SystemExit):
         bench.main()
+
+
+def test_serial_pytorch_baseline_matches_oracle():
+    """Fig. 5's "Serial (PyTorch)" baseline that bench.py --sweep --serial times computes the same
+    layer as the method: spikes and dL/dX against the fp64 oracle (CPU, paper parameters)."""
+    import torch
+    sys.path.insert(0, ROOT)
+    import bench
+    import paper_2408_00280_b200 as snn
+    import snn_synth
+    from parity import oracle_check
+    p = snn.LIFParams.paper()
+    T, N = 24, 700
+    X = snn_synth.normal_tensor(1234, T, N)
+    G = snn_synth.normal_tensor(4321, T, N)
+    S, gX = bench.torch_serial_lif(X, G, p)
+    rep = oracle_check(p, X, G, S.to(torch.uint8), gX)
+    assert rep.ok, str(rep)
+    assert 0.05 < S.float().mean() < 0.95   # non-degenerate firing
