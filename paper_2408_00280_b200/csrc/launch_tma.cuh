@@ -12,7 +12,7 @@ namespace snn_host {
 
 // Tile configurations: VEC neurons per consumer lane x NCONS
 // consumer threads = W-neuron tile; R rows per stage; S stages in the smem ring.
-// The SNN_{F32,BF16}_{FN,FS,RN,RS} macros exist for A/B builds of other tile geometries
+// The SNN_{F32,BF16}_{FN,FS,RN,RS} and SNN_BF16_FV macros exist for A/B builds of other tile geometries
 // (tools/variant_build.py); the product build takes the defaults.
 #ifndef SNN_F32_FN
 #define SNN_F32_FN 256
@@ -28,6 +28,9 @@ namespace snn_host {
 #endif
 #ifndef SNN_BF16_FN
 #define SNN_BF16_FN 128
+#endif
+#ifndef SNN_BF16_FV
+#define SNN_BF16_FV 8
 #endif
 #ifndef SNN_BF16_FS
 #define SNN_BF16_FS 6
@@ -49,7 +52,7 @@ template <> struct TmaCfg<float> {
     static constexpr int HV = 2, HN = 256, HR = 8, HS = 6;   // backward SAVE_H: 32 KB stages
 };
 template <> struct TmaCfg<__nv_bfloat16> {
-    static constexpr int FV = 8, FN = SNN_BF16_FN, FR = 8, FS = SNN_BF16_FS;   // (8 warps x 2048-neuron tiles: slower on mid layers)
+    static constexpr int FV = SNN_BF16_FV, FN = SNN_BF16_FN, FR = 8, FS = SNN_BF16_FS;   // (8 warps x 2048-neuron tiles: slower on mid layers)
     static constexpr int FN_RES = 128, FS_RES = 3;
     static constexpr int RV = 2, RN = SNN_BF16_RN, RS = SNN_BF16_RS;   // 34 KB chunks, 2 CTAs/SM (VEC 4 x 128 lanes measured 6% slower at T=16)
     static constexpr int RS_RES = 2;                         // + residual rows: 51 KB chunks
