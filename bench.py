@@ -779,7 +779,13 @@ def tsplit_measure(args, world, rank, dev, N, T, steps, warmup, transport="nccl"
         from paper_2408_00280_b200 import handoff as HO
         if transport == "handoff-nccl":
             comm = D.NcclComm()
-            ph = HO.WindowHandoff(comm, N)
+            try:
+                ph = HO.WindowHandoff(comm, N)
+            except RuntimeError as e:   # a time neighbour is not a load/store peer: CUDA IPC peers
+                out["window_refused"] = str(e).splitlines()[0][:300]
+                comm.close()
+                comm = None
+                ph = HO.PeerHandoff(N)
         else:
             ph = HO.PeerHandoff(N)
 

@@ -44,7 +44,8 @@ def test_default_line_contract_keys():
 
 
 @pytest.mark.parametrize("workload,extra", [("cfg1", ["--T", "32"]), ("cfg3", ["--T", "64"]),
-                                            ("cfg3", ["--T", "64", "--transport", "handoff"])])
+                                            ("cfg3", ["--T", "64", "--transport", "handoff"]),
+                                            ("cfg3", ["--T", "64", "--transport", "handoff-nccl"])])
 def test_multirank_paths_under_torchrun(workload, extra):
     d = _run(["--gpus", "2", "--workload", workload, "--steps", "2", "--warmup", "3", "--no-e2e",
               "--debug-single-gpu", *extra], nproc=2, port=29532 if workload == "cfg1" else 29533)
@@ -52,6 +53,8 @@ def test_multirank_paths_under_torchrun(workload, extra):
     assert d["scaling"] == ("weak" if workload == "cfg1" else "strong")
     ts = d["tsplit"]
     assert ts["k"] == 2 and ts["Tk_ms"] > 0 and ts["T1_ms"] > 0 and ts["mu_measured"] > 0
+    if "handoff-nccl" in extra:   # two NCCL "hosts" on one GPU are no LSA team: refused, IPC peers used
+        assert "load/store peer" in ts["window_refused"]
 
 
 def test_gpus_flag_self_launches_ranks():
