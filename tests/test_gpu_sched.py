@@ -72,3 +72,25 @@ def test_many_tile_grid_matches_oracle_on_sampled_columns():
     rep = oracle_check(p, X.cpu()[:, c], G.cpu()[:, c], f.spikes.cpu()[:, c], gx.cpu()[:, c],
                        vf_gpu=f.v_final.cpu()[c], gvi_gpu=gv.cpu()[c])
     assert rep.ok, str(rep)
+
+
+@pytest.mark.parametrize("tiles_fwd", [295, 296, 297, 593])
+def test_grid_sizes_around_the_resident_count_equal_generic(monkeypatch, tiles_fwd):
+    """Grids just below / at / just above the resident CTA count (148 SMs x 2 forward CTAs of
+    1024 neurons; the backward's 512-neuron tiles give twice the count at 1 CTA/SM): no steal,
+    exactly one steal, and a second wave -- the TMA kernels equal the generic kernels bitwise."""
+    import paper_2408_00280_b200 as snn
+    import snn_synth
+    p = snn.LIFParams.paper()
+    T, N = 20, tiles_fwd * 1024
+    X = snn_synth.normal_tensor(1234, T, N, device="cuda")
+    G = snn_synth.normal_tensor(4321, T, N, device="cuda")
+    outs = []
+    for no_tma in ("0", "1"):
+        monkeypatch.setenv("SNN_LIF_NO_TMA", no_tma)
+        f = snn.lif_forward(X, p)
+        gx, gv = snn.lif_backward(G, f)
+        torch.cuda.synchronize()
+        outs.append((f.spikes, f.v_final, gx, gv))
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
