@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--workload", choices=["cfg1", "cfg2", "cfg3", "cfg4"], default="cfg1")
     ap.add_argument("--T", type=int, default=None, help="time steps (cfg1: 512, cfg3: 1024)")
     ap.add_argument("--sweep", action="store_true",
-                    help="cfg1: also time T in {8,32,128,512} (L2 flushed before every launch)")
+                    help="cfg1: also time T in {8,32,128,512} (a clean L2 flush before every launch)")
     ap.add_argument("--chunks", type=int, default=32, help="cfg3 neuron chunks of the wavefront")
     ap.add_argument("--transport", choices=["handoff", "handoff-nccl", "nccl"], default="nccl",
                     help="cfg3 boundary exchange: NCCL send/recv between per-chunk launches inside the "
@@ -110,11 +110,18 @@ def layer_list(args, world):
             for i, (c, h, w) in enumerate(RESNET18_DVS_LAYERS)]
 
 
+def ckpt_bytes(T, ck0=False):
+    """RECOMPUTE checkpoint bytes per neuron-step: one fp32 V entering every 16-step chunk
+    except the first (V[-1] is v_init / V_reset, which the backward re-reads itself; r2c),
+    unless ck0 (the affine / handoff entry points store it)."""
+    return 4.0 * (math.ceil(T / 16) - (0 if ck0 else 1)) / T
+
+
 def bytes_per_neuron_step(dtype_bytes, spike_fmt, save_mode, T):
     """Algorithmic HBM bytes per neuron-step."""
     spk = {"u8": 1.0, "bits": 1.0 / 8.0, "io": float(dtype_bytes)}[spike_fmt]
     if save_mode == "recompute":
-        ck = 4.0 * math.ceil(T / 16) / T          # fp32 V checkpoint every 16 steps
+        ck = ckpt_bytes(T)                         # fp32 V checkpoint every 16 steps
         fwd = dtype_bytes + spk + ck               # read X, write S, write ckpt
         bwd = 3 * dtype_bytes + ck                 # read gS, read X, write gX, read ckpt
     else:
@@ -339,15 +346,69 @@ class OracleSample:
 
 # ----------------------------------------------------------------------------- cfg1 sweep
 
+class L2Flush:
+    """Cold-L2 preparation before an isolated launch (outside its events).  `dirty`: a 512 MiB
+    memset -- it leaves L2 full of the memset's own dirty lines, so the timed launch pays for
+    writing them back as it evicts them (measured: +2-9 us per launch at T = 8-128,
+    profiles/r02c_small_t_probe.log).  `clean` (the sweep's default since r2c): the same memset,
+    then a 256 MiB read pass (a sum), so the write-backs finish before the events and the
+    launch meets an L2 holding only clean, unrelated lines -- what ncu's --cache-control all
+    gives a profiled launch."""
+
+    def __init__(self, dev, clean=True):
+        import torch
+        self.buf = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+        self.rd = torch.empty(64 << 20, dtype=torch.float32, device=dev)
+        self.acc = torch.zeros((), dtype=torch.float32, device=dev)
+        self.clean = clean
+
+    def __call__(self):
+        import torch
+        self.buf.zero_()
+        if self.clean:
+            torch.sum(self.rd, 0, out=self.acc)
+
+
+def time_isolated(fwd, bwd, flush, warmup, reps=20):
+    """Median CUDA-event durations of fwd() and bwd(), each launched alone after flush();
+    the reps are captured as one graph (no host gaps inside the events).  Also times an
+    empty kernel the same way (`floor_ms`: what the events and the launch cost with no work)."""
+    import torch
+    evs, nul = [], []
+
+    def one(record):
+        e = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(6)] if record else None
+        for i, fn in enumerate((fwd, bwd, lambda: torch.cuda._sleep(1))):
+            flush()
+            if record: e[2 * i].record()
+            fn()
+            if record: e[2 * i + 1].record()
+        if record: evs.append(e)
+
+    for _ in range(max(3, warmup)):
+        one(False)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(reps):
+            one(True)
+    g.replay()
+    torch.cuda.synchronize()
+    med = [sorted(e[2 * i].elapsed_time(e[2 * i + 1]) for e in evs)[reps // 2] for i in range(3)]
+    del g
+    return med
+
+
 def run_sweep(args, params, dev, stream):
     """BASELINE configs[1]: N = 2^20, T in {8, 32, 128, 512}.  Each fwd / bwd launch is
-    timed alone with CUDA events; an L2 flush (a 512 MiB memset, outside the events)
-    precedes every launch so small-T working sets are not served from the 126 MB L2.
-    `stream`: the same layer timed like the main line (sweep_stream)."""
+    timed alone with CUDA events after a clean L2 flush (L2Flush: memset + read pass, outside
+    the events) so small-T working sets are not served from the 126 MB L2; `dirty_flush` repeats
+    the timing after the memset alone (round-1/2b methodology).  `stream`: the same layer timed
+    like the main line (sweep_stream)."""
     import torch
     import paper_2408_00280_b200 as snn
     import snn_synth
-    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    flushes = {"clean": L2Flush(dev, clean=True), "dirty": L2Flush(dev, clean=False)}
     out = []
     for T in (8, 32, 128, 512):
         N = 1 << 20
@@ -356,49 +417,36 @@ def run_sweep(args, params, dev, stream):
         f = snn.lif_forward(X, params, spike_fmt=args.spike_fmt, save_mode=args.save_mode,
                             return_v_final=False)
         gx, _ = snn.lif_backward(G, f, return_grad_v_init=False)
-        evs = []
 
-        def one(record):
-            flush.zero_()
-            e = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(4)] if record else None
-            if record: e[0].record()
+        def fwd():
             snn.lif_forward(X, params, spike_fmt=args.spike_fmt, save_mode=args.save_mode,
                             spikes=f.spikes, saved=f.saved, return_v_final=False)
-            if record: e[1].record()
-            flush.zero_()
-            if record: e[2].record()
-            snn.lif_backward(G, f, grad_x=gx, return_grad_v_init=False)
-            if record:
-                e[3].record(); evs.append(e)
 
-        for _ in range(max(3, args.warmup)):
-            one(False)
-        torch.cuda.synchronize(dev)
-        g = torch.cuda.CUDAGraph()      # launched as one graph: no host gaps inside the events
-        with torch.cuda.graph(g):
-            for _ in range(20):
-                one(True)
-        g.replay()
-        torch.cuda.synchronize(dev)
-        tf = [e[0].elapsed_time(e[1]) for e in evs]
-        tb = [e[2].elapsed_time(e[3]) for e in evs]
-        tf.sort(); tb.sort()
-        mf, mb = tf[len(tf) // 2], tb[len(tb) // 2]
-        serial = None
-        if args.serial:
-            serial = time_serial_baselines(params, X, G, dev, flush)
+        def bwd():
+            snn.lif_backward(G, f, grad_x=gx, return_grad_v_init=False)
+
         bf, bb = bytes_per_neuron_step(4, args.spike_fmt, args.save_mode, T)
         ns = N * T
-        out.append({"T": T, "fwd_ms": round(mf, 4), "bwd_ms": round(mb, 4),
+
+        def rec(mf, mb, floor):
+            return {"fwd_ms": round(mf, 4), "bwd_ms": round(mb, 4),
                     "neuron_steps_per_s": ns / ((mf + mb) / 1e3),
                     "fwd_GBps": round(bf * ns / (mf / 1e3) / 1e9, 1),
                     "bwd_GBps": round(bb * ns / (mb / 1e3) / 1e9, 1),
-                    "fwdbwd_GBps": round((bf + bb) * ns / ((mf + mb) / 1e3) / 1e9, 1)})
+                    "fwdbwd_GBps": round((bf + bb) * ns / ((mf + mb) / 1e3) / 1e9, 1),
+                    "floor_ms": round(floor, 4)}
+
+        mf, mb, fl = time_isolated(fwd, bwd, flushes["clean"], args.warmup)
+        out.append({"T": T, **rec(mf, mb, fl)})
+        out[-1]["dirty_flush"] = rec(*time_isolated(fwd, bwd, flushes["dirty"], args.warmup))
+        serial = None
+        if args.serial:
+            serial = time_serial_baselines(params, X, G, dev, flushes["clean"])
         if serial is not None:
             out[-1]["serial"] = serial
             out[-1]["speedup_vs_serial_cuda"] = round(serial["cuda_ms"] / (mf + mb), 2)
             out[-1]["speedup_vs_serial_torch"] = round(serial["torch_ms"] / (mf + mb), 2)
-        del X, G, f, gx, g
+        del X, G, f, gx
         out[-1]["stream"] = sweep_stream(args, params, dev, T, N)
     return out
 
@@ -514,10 +562,9 @@ def run_resnet_prologue(args, params, dev):
                               0.2 * torch.randn(c, device=dev, generator=gen), c, HW)
         plans_p.append(snn.LIFPlan(X, params, grad_spikes=G, affine=spec, residual=R))
         plans_0.append(snn.LIFPlan(X, params, grad_spikes=G))
-        ck = 4.0 * math.ceil(T / 16) / T
-        base = (4 + 1 + ck) + (12 + ck)
-        nbytes_0 += base * T * N
-        nbytes_p += (base + 8.0 / T + (12.0 if res else 0.0)) * T * N   # partials; R in x2, dL/dR out
+        ck, ckp = ckpt_bytes(T), ckpt_bytes(T, ck0=True)   # the affine pair stores V[-1]
+        nbytes_0 += ((4 + 1 + ck) + (12 + ck)) * T * N
+        nbytes_p += ((4 + 1 + ckp) + (12 + ckp) + 8.0 / T + (12.0 if res else 0.0)) * T * N   # partials; R in x2, dL/dR out
         ns += T * N
     out = {"layers": len(plans_p), "B": B, "T": T, "neurons": ns // T,
            "residual_layers": sum(1 for p_ in plans_p if getattr(p_, "residual", None) is not None)}
@@ -680,7 +727,7 @@ def time_serial_baselines(params, X, G, dev, flush, reps=5):
         fn()
         ts = []
         for _ in range(reps):
-            flush.zero_()
+            flush()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             fn()

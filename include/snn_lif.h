@@ -148,7 +148,10 @@ snn_status snn_lif_forward(const snn_lif_params* params, const snn_lif_shape* sh
  * (the delta term dropped when detach_reset).
  *   grad_spikes  [T, ld] io dtype   dL/dS[t] from the next layer (the paper's grad y)  (read)
  *   x            [T, ld] io dtype   required iff SAVE_RECOMPUTE, else ignored (may be NULL)
- *   v_init       [N] fp32 or NULL   the value given to the forward (RECOMPUTE only)
+ *   v_init       [N] fp32 or NULL   RECOMPUTE: the SAME pointer and contents given to the forward
+ *                                   (NULL iff the forward's was NULL): V[-1] is not checkpointed,
+ *                                   the backward re-reads it here (for T <= 16 the forward
+ *                                   stores no checkpoint at all).  Ignored for SAVE_H.   (read)
  *   saved        the forward's saved buffer (same params/shape)                   (read)
  *   grad_v_final [N] fp32 or NULL -> 0   dL/dV[T-1] from a later time segment      (read)
  *   grad_x       [T, ld] io dtype   dL/dX[t]; must not alias any input            (write)
@@ -174,6 +177,9 @@ snn_status snn_lif_backward(const snn_lif_params* params, const snn_lif_shape* s
  *          v_init.  Backward: recv_* carry dL/dV from the LATER segment, send_* go to the
  *          earlier one.  NULL recv_state = first segment (v_init / grad_v_final apply);
  *          NULL send_state = last segment.
+ * SAVE_RECOMPUTE state written by snn_lif_forward_handoff holds V[-1] (it arrives inside the
+ * kernel), so it pairs with snn_lif_backward_handoff only -- and snn_lif_forward's with
+ * snn_lif_backward (which re-reads V[-1] from its v_init); likewise the affine pair below.
  * Requires the TMA path (16-byte-aligned pointers, ld a multiple of 16 bytes, N a
  * multiple of 8 for bf16 / 4 for fp32), else SNN_ERR_UNSUPPORTED. */
 #define SNN_LIF_HANDOFF_BLOCK 256
@@ -231,7 +237,8 @@ snn_status snn_lif_backward_handoff(const snn_lif_params* params, const snn_lif_
  * snn_lif_backward_tsplit: the mirror image -- per chunk receive dL/dV from rank+1 into
  * g_in_ws, run the fused backward, send grad_v_init (g_out_ws) to rank-1.
  *   grad_spikes, x, saved, grad_x  as snn_lif_backward over the local segment
- *   v_in_ws            ignored (the RECOMPUTE checkpoints hold each segment's V[-1]); may be NULL
+ *   v_in_ws  [N] fp32  the forward's v_in_ws, unchanged since (each chunk's V[-1]); NULL iff
+ *                      the forward's was NULL (rank 0 without v_init)
  *   g_in_ws  [N] fp32  rank < nranks-1: receive buffer (required); last rank: the layer's
  *                      grad_v_final, or NULL (0)
  *   g_out_ws [N] fp32  rank > 0: send buffer (required); rank 0: the layer's grad_v_init, or NULL

@@ -394,7 +394,6 @@ snn_status snn_lif_backward_tsplit(snn_comm* c, const snn_lif_params* p, const s
                                    int n_chunks, const void* grad_spikes, const void* x,
                                    const float* v_in_ws, const void* saved, void* grad_x,
                                    float* g_in_ws, float* g_out_ws, void* stream) {
-    (void)v_in_ws;   // the RECOMPUTE checkpoints already hold each segment's V[-1]
     NvtxRange range("snn_lif_backward_tsplit");
     snn_status st;
     if ((st = tsplit_common_checks(c, s, n_chunks)) != SNN_OK) return st;
@@ -402,7 +401,7 @@ snn_status snn_lif_backward_tsplit(snn_comm* c, const snn_lif_params* p, const s
     if (!last && !g_in_ws) return fail(SNN_ERR_NULL_POINTER, "g_in_ws is required on ranks < nranks-1 (receive buffer)");
     if (!first && !g_out_ws) return fail(SNN_ERR_NULL_POINTER, "g_out_ws is required on ranks > 0 (send buffer)");
     if ((st = dry_run([&] {
-             return backward_impl(p, s, grad_spikes, x, saved, g_in_ws, nullptr, grad_x, g_out_ws, stream);
+             return backward_impl(p, s, grad_spikes, x, v_in_ws, saved, g_in_ws, nullptr, grad_x, g_out_ws, stream);
          })) != SNN_OK)
         return st;
     const int M = effective_chunks(s->N, n_chunks);
@@ -414,7 +413,10 @@ snn_status snn_lif_backward_tsplit(snn_comm* c, const snn_lif_params* p, const s
         sc.N = b - a;
         // the last rank starts from g_in_ws (the layer's grad_v_final) when given, else 0
         const float* gin = g_in_ws ? g_in_ws + a : nullptr;
-        return backward_impl(p, &sc, col(grad_spikes, a, esz), col(x, a, esz), col(saved, a, 4), gin, nullptr,
+        // chunk 0's V[-1]: the slice of v_in_ws the forward started from (received from d-1, or
+        // rank 0's v_init), else V_reset
+        const float* vin = v_in_ws ? v_in_ws + a : nullptr;
+        return backward_impl(p, &sc, col(grad_spikes, a, esz), col(x, a, esz), vin, col(saved, a, 4), gin, nullptr,
                              col(grad_x, a, esz), g_out_ws ? g_out_ws + a : nullptr, stream, nullptr, nullptr,
                              nullptr, &cv);
     });

@@ -175,7 +175,7 @@ snn_status forward_impl(const snn_lif_params* p, const snn_lif_shape* s, const v
                         float* v_final, void* stream, const snn_lif_affine* affine = nullptr,
                         const ChunkView* cv = nullptr);
 snn_status backward_impl(const snn_lif_params* p, const snn_lif_shape* s, const void* grad_spikes,
-                         const void* x, const void* saved, const float* grad_v_final,
+                         const void* x, const float* v_init, const void* saved, const float* grad_v_final,
                          const snn_lif_handoff* handoff, void* grad_x, float* grad_v_init, void* stream,
                          const snn_lif_affine* affine = nullptr, float* part_a = nullptr,
                          float* part_b = nullptr, const ChunkView* cv = nullptr, int* seg_out = nullptr);

@@ -107,6 +107,8 @@ struct FwdArgs {
                           // layer's when this launch covers a neuron chunk of it (time split)
     int x_off, r_off;     // unaligned TMA path: element offset of x / residual from their 1-D
                           // tensor maps' (16-byte aligned) base
+    int ck0;              // RECOMPUTE: 1 = store checkpoint row 0 (V[-1]); 0 = skip it -- it would
+                          // equal v_init / V_reset, which the backward reads instead (BwdArgs::ck0)
     LifConsts c;
     Handoff h;            // boundary V from / to the neighbour time segment (TMA path only)
     Affine af;            // input prologue (identity when af.scale == null)
@@ -124,6 +126,8 @@ struct BwdArgs {
     float* grad_v_init;         // [N] or null
     int64_t T, N, ld, ldh;
     int x_off, g_off, r_off;    // unaligned TMA path: element offsets of x / gS / residual
+    const float* v_init;        // RECOMPUTE with ck0 == 0: V[-1] of chunk 0 ([N], or null -> V_reset)
+    int ck0;                    // 1: chunk 0's entry V is checkpoint row 0 (the forward stored it)
     LifConsts c;
     Handoff h;                  // boundary dL/dV from / to the neighbour segment (TMA path only)
     Affine af;                  // input prologue + its per-neuron gradient partials
@@ -397,7 +401,7 @@ lif_forward_kernel(const FwdArgs a) {
                 const Pack<IO, VEC> xv = buf[j];
                 if (t + PF < T) buf[j] = ld_group<IO, VEC>(x + (t + PF) * ld, nvalid);
                 if constexpr (SAVE == SAVE_RECOMPUTE) {
-                    if ((t % kCkpt) == 0 && nvalid > 0) {
+                    if ((t % kCkpt) == 0 && nvalid > 0 && (t > 0 || a.ck0)) {
                         Pack<float, VEC> ck;
 #pragma unroll
                         for (int i = 0; i < VEC; ++i) ck.v[i] = V[i];
@@ -482,6 +486,17 @@ lif_backward_saveh_kernel(const BwdArgs a) {
 }
 
 // ------------------------------------------------------------------------------------
+// V[-1] of the RECOMPUTE backward's chunk 0 when the forward did not store checkpoint row 0
+// (ck0 == 0): the caller's v_init (the value the forward started from; any alignment), else
+// V_reset.  Elements past nvalid are V_reset (never stored).
+template <int VEC>
+__device__ __forceinline__ Pack<float, VEC> entry_v0(const float* v_init, int64_t n0, int nvalid, float v_reset) {
+    Pack<float, VEC> v;
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) v.v[i] = (v_init != nullptr && i < nvalid) ? v_init[n0 + i] : v_reset;
+    return v;
+}
+
 // Generic backward, SAVE_RECOMPUTE: per kCkpt-step chunk (last chunk first) reload the
 // chunk's entry V checkpoint, re-run the forward charge over the chunk from x (identical
 // instruction sequence -> bitwise-identical H), then walk the chunk backwards.
@@ -522,7 +537,8 @@ lif_backward_recompute_kernel(const BwdArgs a) {
         constexpr bool FULL = decltype(full)::value;
         const int64_t t0 = ch * kCkpt;
         const int len = FULL ? kCkpt : (int)min((int64_t)kCkpt, T - t0);
-        const Pack<float, VEC> v0 = ld_group<float, VEC>(ck + ch * ldh, nvalid);
+        const Pack<float, VEC> v0 = (ch > 0 || a.ck0) ? ld_group<float, VEC>(ck + ch * ldh, nvalid)
+                                                      : entry_v0<VEC>(a.v_init, n0, nvalid, c.v_reset);
         Pack<IO, VEC> xb[kCkpt];
         Pack<IO, VEC> gb[kCkpt];
 #pragma unroll

@@ -454,7 +454,7 @@ lif_forward_tma_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_con
                         // checkpoint the V entering step t when t % kCkpt == 0 (the saved rows are
                         // padded to 16 floats: a ragged group's pack store stays inside its row)
                         const int64_t t = rb * R + r;
-                        if ((t % kCkpt) == 0 && nv > 0) {
+                        if ((t % kCkpt) == 0 && nv > 0 && (t > 0 || a.ck0)) {
                             Pack<float, VEC> ck;
 #pragma unroll
                             for (int i = 0; i < VEC; ++i) ck.v[i] = V[i];
@@ -620,7 +620,7 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
             const int ch = (int)nch - 1 - j;
 #pragma unroll
             for (int b = 0; b < NB; ++b) {
-                tma_prefetch_2d(&tmck, c0 + b * BW, ch);
+                if (ch > 0 || a.ck0) tma_prefetch_2d(&tmck, c0 + b * BW, ch);
                 if constexpr (!UNAL) {
                     tma_prefetch_2d(&tmx, c0 + b * BW, ch * kCkpt);
                     tma_prefetch_2d(&tmg, c0 + b * BW, ch * kCkpt);
@@ -646,7 +646,8 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
                 smem, bar, nch, sc,
                 [&](int tile, int64_t j) {
                     const int64_t t0 = (nch - 1 - j) * kCkpt, c0 = (int64_t)tile * W;
-                    uint32_t b = (uint32_t)(NB * Cfg::CK_BOX_BYTES) + Reg::tx_bytes(fx, t0, rows_of(j), c0, ld) +
+                    const bool ck = t0 > 0 || a.ck0;   // chunk 0 without a stored V[-1]: no checkpoint box
+                    uint32_t b = (ck ? (uint32_t)(NB * Cfg::CK_BOX_BYTES) : 0u) + Reg::tx_bytes(fx, t0, rows_of(j), c0, ld) +
                                  Reg::tx_bytes(fg, t0, rows_of(j), c0, ld);
                     if constexpr (RES) b += Reg::tx_bytes(fr, t0, rows_of(j), c0, ld);
                     return b;
@@ -655,7 +656,7 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
                     const int64_t ch = nch - 1 - j;
                     const int rows = rows_of(j);
                     const int64_t c0 = (int64_t)tile * W;
-                    if (lane == 0) {
+                    if (lane == 0 && (ch > 0 || a.ck0)) {
 #pragma unroll
                         for (int b = 0; b < NB; ++b)   // checkpoints: the saved rows are always 16-B aligned
                             tma_load_2d(stg + Cfg::CK_OFF + b * Cfg::CK_BOX_BYTES, &tmck, (int)(c0 + b * BW), (int)ch,
@@ -712,7 +713,9 @@ lif_backward_recompute_tma_kernel(const __grid_constant__ CUtensorMap tmx,
             const auto gsm = row_src<IO, VEC, BW, kCkpt, NB, UNAL>(stg + Cfg::G_OFF, nt, t0, ld, a.g_off);
             const auto rs = row_src<IO, VEC, BW, kCkpt, NB, UNAL>(stg + Cfg::R_OFF, nt, t0, ld, a.r_off);
             const Pack<float, VEC> v0 =
-                *reinterpret_cast<const Pack<float, VEC>*>(reinterpret_cast<const float*>(stg + Cfg::CK_OFF) + ckoff);
+                (ch > 0 || a.ck0)
+                    ? *reinterpret_cast<const Pack<float, VEC>*>(reinterpret_cast<const float*>(stg + Cfg::CK_OFF) + ckoff)
+                    : entry_v0<VEC>(a.v_init, n0, nvalid, c.v_reset);
             float V[VEC];
 #pragma unroll
             for (int i = 0; i < VEC; ++i) V[i] = v0.v[i];

@@ -358,6 +358,11 @@ snn_status forward_impl(const snn_lif_params* p, const snn_lif_shape* s, const v
     snn::FwdArgs a{};
     a.x = x; a.v_init = v_init; a.spikes = spikes;
     a.saved = s->save_mode == SNN_SAVE_NONE ? nullptr : static_cast<float*>(saved);
+    // RECOMPUTE checkpoint row 0 (V[-1]) is stored only where the matching backward entry point
+    // cannot be handed v_init: the fused handoff (V[-1] arrives from the neighbour inside the
+    // kernel) and the affine prologue (its backward takes no v_init).  Elsewhere V[-1] is v_init
+    // or V_reset, which snn_lif_backward receives itself: T <= 16 saves the whole checkpoint.
+    a.ck0 = (handoff != nullptr || affine != nullptr) ? 1 : 0;
     a.v_final = v_final;
     a.T = s->T; a.N = s->N; a.ld = s->ld; a.ldh = saved_ld(s); a.nwords = (s->N + 31) / 32;
     a.spk_words_ld = a.nwords;
@@ -399,7 +404,7 @@ snn_status forward_impl(const snn_lif_params* p, const snn_lif_shape* s, const v
 }
 
 snn_status backward_impl(const snn_lif_params* p, const snn_lif_shape* s,
-                         const void* grad_spikes, const void* x, const void* saved,
+                         const void* grad_spikes, const void* x, const float* v_init, const void* saved,
                          const float* grad_v_final, const snn_lif_handoff* handoff, void* grad_x,
                          float* grad_v_init, void* stream, const snn_lif_affine* affine,
                          float* part_a, float* part_b, const ChunkView* cv, int* seg_out) {
@@ -424,6 +429,9 @@ snn_status backward_impl(const snn_lif_params* p, const snn_lif_shape* s,
     a.gS = grad_spikes; a.x = x; a.saved = static_cast<const float*>(saved);
     a.grad_v_final = grad_v_final; a.gX = grad_x; a.grad_v_init = grad_v_init;
     a.T = s->T; a.N = s->N; a.ld = s->ld; a.ldh = cv ? cv->ldh : saved_ld(s);
+    a.v_init = v_init;
+    a.ck0 = (handoff != nullptr || affine != nullptr) ? 1 : 0;   // as forward_impl stored it
+    if (v_init && !aligned(v_init, 4)) return fail(SNN_ERR_MISALIGNED, "v_init is not 4-byte aligned");
 #ifdef SNN_TRACE
     a.trace = trace_buf();
 #endif
@@ -506,9 +514,8 @@ snn_status snn_lif_backward(const snn_lif_params* p, const snn_lif_shape* s,
                             const void* grad_spikes, const void* x, const float* v_init,
                             const void* saved, const float* grad_v_final, void* grad_x,
                             float* grad_v_init, void* stream) {
-    (void)v_init;  // the RECOMPUTE checkpoints already hold V[-1]
     NvtxRange r("snn_lif_backward");
-    return backward_impl(p, s, grad_spikes, x, saved, grad_v_final, nullptr, grad_x, grad_v_init, stream);
+    return backward_impl(p, s, grad_spikes, x, v_init, saved, grad_v_final, nullptr, grad_x, grad_v_init, stream);
 }
 
 snn_status snn_lif_forward_affine(const snn_lif_params* p, const snn_lif_shape* s, const void* x,
@@ -528,7 +535,7 @@ snn_status snn_lif_backward_affine(const snn_lif_params* p, const snn_lif_shape*
     if (!grad_scale || !grad_shift) return fail(SNN_ERR_NULL_POINTER, "grad_scale / grad_shift is NULL");
     NvtxRange r("snn_lif_backward_affine");
     int seg = 0;
-    snn_status st = backward_impl(p, s, grad_spikes, x, saved, grad_v_final, nullptr, grad_x, grad_v_init,
+    snn_status st = backward_impl(p, s, grad_spikes, x, nullptr, saved, grad_v_final, nullptr, grad_x, grad_v_init,
                                   stream, af, part_a, part_b, nullptr, &seg);
     if (st != SNN_OK) return st;
     if (seg > 0)   // the backward already reduced each tile into channel segments: one tiny finish
@@ -556,7 +563,7 @@ snn_status snn_lif_backward_handoff(const snn_lif_params* p, const snn_lif_shape
                                     float* grad_v_init, void* stream) {
     if (!h) return fail(SNN_ERR_NULL_POINTER, "handoff is NULL");
     NvtxRange r("snn_lif_backward_handoff");
-    return backward_impl(p, s, grad_spikes, x, saved, grad_v_final, h, grad_x, grad_v_init, stream);
+    return backward_impl(p, s, grad_spikes, x, nullptr, saved, grad_v_final, h, grad_x, grad_v_init, stream);
 }
 
 snn_status snn_lif_serial_forward_step(const snn_lif_params* p, int io_dtype, int64_t N,
@@ -647,7 +654,8 @@ snn_status snn_lif_plan_create(snn_lif_plan** out, const snn_lif_params* p, cons
     if (st != SNN_OK) return st;
     if (grad_spikes) {
         st = record_into(plan->bwd, [&] {
-            return backward_impl(p, s, grad_spikes, x, saved, grad_v_final, nullptr, grad_x, grad_v_init, nullptr);
+            return backward_impl(p, s, grad_spikes, x, v_init, saved, grad_v_final, nullptr, grad_x, grad_v_init,
+                                 nullptr);
         });
         if (st != SNN_OK) return st;
         plan->has_backward = true;

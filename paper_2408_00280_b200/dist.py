@@ -180,7 +180,8 @@ def lif_backward_tsplit(comm: NcclComm, grad_local: torch.Tensor, fwd, *, n_chun
     g_in = _vec("grad_v_final", grad_v_final, N, dev) if last else torch.empty(N, dtype=torch.float32, device=dev)
     g_out = torch.empty(N, dtype=torch.float32, device=dev)
     _lib.snn_lif_backward_tsplit(comm.handle, fwd.params.to_c(), fwd.shape, int(n_chunks), _ptr(grad_local),
-                                 _ptr(x), None, _ptr(fwd.saved), _ptr(grad_x), _ptr(g_in), _ptr(g_out),
+                                 _ptr(x), _ptr(getattr(fwd, "v_in_ws", fwd.v_init)), _ptr(fwd.saved),
+                                 _ptr(grad_x), _ptr(g_in), _ptr(g_out),
                                  _stream(dev))
     return grad_x, (g_out if first else None)
 

@@ -54,7 +54,7 @@ def time_null(reps):
 
 def alg_bytes(dt, T, N, save_mode="recompute"):
     e = 4 if dt == "f32" else 2
-    ck = 4.0 / 16
+    ck = 4.0 * (-(-T // 16) - 1) / T   # checkpoint rows after the first (V[-1] is not stored)
     return (e + 1 + ck) * T * N, (3 * e + ck) * T * N
 
 

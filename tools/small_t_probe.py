@@ -42,7 +42,7 @@ def run(T, N, prep, family, reps, dev):
         if prep in ("dirty", "clean"):
             flush.zero_()
         if prep == "clean":
-            torch.sum(rd, out=acc)
+            torch.sum(rd, 0, out=acc)
 
     def one(i, record):
         b = i % 2
@@ -69,7 +69,8 @@ def run(T, N, prep, family, reps, dev):
     torch.cuda.synchronize(dev)
     tf = sorted(e[0].elapsed_time(e[1]) for e in evs)[reps // 2]
     tb = sorted(e[2].elapsed_time(e[3]) for e in evs)[reps // 2]
-    bf, bb = (4 + 1 + 0.25) * T * N, (12 + 0.25) * T * N
+    ck = 4.0 * (-(-T // 16) - 1) / T   # checkpoint rows after the first (V[-1] is not stored)
+    bf, bb = (4 + 1 + ck) * T * N, (12 + ck) * T * N
     print(f"T={T:4d} N={N} {prep:5s} {family:7s} fwd {tf * 1e3:7.2f} us {bf / tf / 1e6:6.0f} GB/s  "
           f"bwd {tb * 1e3:7.2f} us {bb / tb / 1e6:6.0f} GB/s  fwd+bwd {(bf + bb) / (tf + tb) / 1e6:6.0f} GB/s "
           f"{T * N / ((tf + tb) / 1e3):.3e} ns/s", flush=True)

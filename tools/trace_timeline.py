@@ -67,7 +67,8 @@ def report(recs, title):
         ent = a["t_entry"].min(); end = a["t_end"].max()
         gap = "  --  " if prev_end is None else f"{(int(ent) - prev_end) / 1e3:6.2f}"
         esz = 2 if k_is_bf16(T, N) else 4
-        nbytes = ((esz + 1.25) if k == 1 else (3 * esz + 0.25)) * T * N
+        ck = 4.0 * (-(-T // 16) - 1) / T   # checkpoint rows after the first (V[-1] is not stored)
+        nbytes = ((esz + 1 + ck) if k == 1 else (3 * esz + ck)) * T * N
         gbs = nbytes / max(1, int(end) - int(a["t_wait"].min()))
         print(f"{KIND.get(k, k):>5} T={T:<4d} N={N:<9d} {len(a):5d} {int(a['tiles'].sum()):6d} {us(ent):8.2f} "
               f"{us(a['t_wait'].min()):8.2f} {us(a['t_wait'].max()):8.2f} {us(a['t_first'].min()):8.2f} "
