@@ -113,7 +113,7 @@ def layer_list(args, world):
 def ckpt_bytes(T, ck0=False):
     """RECOMPUTE checkpoint bytes per neuron-step: one fp32 V entering every 16-step chunk
     except the first (V[-1] is v_init / V_reset, which the backward re-reads itself; r2c),
-    unless ck0 (the affine / handoff entry points store it)."""
+    unless ck0 (the handoff entry points store it)."""
     return 4.0 * (math.ceil(T / 16) - (0 if ck0 else 1)) / T
 
 
@@ -562,9 +562,10 @@ def run_resnet_prologue(args, params, dev):
                               0.2 * torch.randn(c, device=dev, generator=gen), c, HW)
         plans_p.append(snn.LIFPlan(X, params, grad_spikes=G, affine=spec, residual=R))
         plans_0.append(snn.LIFPlan(X, params, grad_spikes=G))
-        ck, ckp = ckpt_bytes(T), ckpt_bytes(T, ck0=True)   # the affine pair stores V[-1]
-        nbytes_0 += ((4 + 1 + ck) + (12 + ck)) * T * N
-        nbytes_p += ((4 + 1 + ckp) + (12 + ckp) + 8.0 / T + (12.0 if res else 0.0)) * T * N   # partials; R in x2, dL/dR out
+        ck = ckpt_bytes(T)
+        base = (4 + 1 + ck) + (12 + ck)
+        nbytes_0 += base * T * N
+        nbytes_p += (base + 8.0 / T + (12.0 if res else 0.0)) * T * N   # partials; R in x2, dL/dR out
         ns += T * N
     out = {"layers": len(plans_p), "B": B, "T": T, "neurons": ns // T,
            "residual_layers": sum(1 for p_ in plans_p if getattr(p_, "residual", None) is not None)}

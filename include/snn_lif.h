@@ -179,7 +179,8 @@ snn_status snn_lif_backward(const snn_lif_params* params, const snn_lif_shape* s
  *          NULL send_state = last segment.
  * SAVE_RECOMPUTE state written by snn_lif_forward_handoff holds V[-1] (it arrives inside the
  * kernel), so it pairs with snn_lif_backward_handoff only -- and snn_lif_forward's with
- * snn_lif_backward (which re-reads V[-1] from its v_init); likewise the affine pair below.
+ * snn_lif_backward (which re-reads V[-1] from its v_init); likewise the affine pair below
+ * (v_init: the forward's, as for snn_lif_backward).
  * Requires the TMA path (16-byte-aligned pointers, ld a multiple of 16 bytes, N a
  * multiple of 8 for bf16 / 4 for fp32), else SNN_ERR_UNSUPPORTED. */
 #define SNN_LIF_HANDOFF_BLOCK 256
@@ -325,7 +326,7 @@ snn_status snn_lif_forward_affine(const snn_lif_params* params, const snn_lif_sh
 /* part_a, part_b: [N] fp32 caller scratch (16-B aligned; contents undefined on return);
  * grad_scale, grad_shift: [C] fp32 outputs, bitwise deterministic run to run. */
 snn_status snn_lif_backward_affine(const snn_lif_params* params, const snn_lif_shape* shape,
-                                   const void* grad_spikes, const void* x, const void* saved,
+                                   const void* grad_spikes, const void* x, const float* v_init, const void* saved,
                                    const float* grad_v_final, const snn_lif_affine* affine,
                                    void* grad_x, float* grad_v_init, float* part_a, float* part_b,
                                    float* grad_scale, float* grad_shift, void* stream);

@@ -109,7 +109,7 @@ def _load() -> ctypes.CDLL:
     Ap = ctypes.POINTER(snn_lif_affine)
     lib.snn_lif_forward_affine.argtypes = [P, S, vp, fp, Ap, vp, vp, fp, vp]
     lib.snn_lif_forward_affine.restype = ctypes.c_int
-    lib.snn_lif_backward_affine.argtypes = [P, S, vp, vp, vp, fp, Ap, vp, fp, fp, fp, fp, fp, vp]
+    lib.snn_lif_backward_affine.argtypes = [P, S, vp, vp, fp, vp, fp, Ap, vp, fp, fp, fp, fp, fp, vp]
     lib.snn_lif_backward_affine.restype = ctypes.c_int
     lib.snn_lif_host_workspace_bytes.argtypes = [P, S, ctypes.c_int64, ctypes.c_int]
     lib.snn_lif_host_workspace_bytes.restype = ctypes.c_size_t
@@ -211,9 +211,9 @@ def snn_lif_forward_affine(params, shape, x, v_init, affine, spikes, saved, v_fi
                                      ctypes.byref(affine), spikes, saved, v_final, stream))
 
 
-def snn_lif_backward_affine(params, shape, grad_spikes, x, saved, grad_v_final, affine, grad_x,
+def snn_lif_backward_affine(params, shape, grad_spikes, x, v_init, saved, grad_v_final, affine, grad_x,
                             grad_v_init, part_a, part_b, grad_scale, grad_shift, stream) -> None:
-    check(lib.snn_lif_backward_affine(ctypes.byref(params), ctypes.byref(shape), grad_spikes, x, saved,
+    check(lib.snn_lif_backward_affine(ctypes.byref(params), ctypes.byref(shape), grad_spikes, x, v_init, saved,
                                       grad_v_final, ctypes.byref(affine), grad_x, grad_v_init, part_a,
                                       part_b, grad_scale, grad_shift, stream))
 

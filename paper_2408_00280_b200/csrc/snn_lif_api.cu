@@ -358,11 +358,10 @@ snn_status forward_impl(const snn_lif_params* p, const snn_lif_shape* s, const v
     snn::FwdArgs a{};
     a.x = x; a.v_init = v_init; a.spikes = spikes;
     a.saved = s->save_mode == SNN_SAVE_NONE ? nullptr : static_cast<float*>(saved);
-    // RECOMPUTE checkpoint row 0 (V[-1]) is stored only where the matching backward entry point
-    // cannot be handed v_init: the fused handoff (V[-1] arrives from the neighbour inside the
-    // kernel) and the affine prologue (its backward takes no v_init).  Elsewhere V[-1] is v_init
-    // or V_reset, which snn_lif_backward receives itself: T <= 16 saves the whole checkpoint.
-    a.ck0 = (handoff != nullptr || affine != nullptr) ? 1 : 0;
+    // RECOMPUTE checkpoint row 0 (V[-1]) is stored only for the fused handoff, where V[-1]
+    // arrives from the neighbour inside the kernel.  Elsewhere it is v_init or V_reset, which
+    // the backward entry points receive themselves: a layer with T <= 16 stores no checkpoint.
+    a.ck0 = handoff != nullptr ? 1 : 0;
     a.v_final = v_final;
     a.T = s->T; a.N = s->N; a.ld = s->ld; a.ldh = saved_ld(s); a.nwords = (s->N + 31) / 32;
     a.spk_words_ld = a.nwords;
@@ -430,7 +429,7 @@ snn_status backward_impl(const snn_lif_params* p, const snn_lif_shape* s,
     a.grad_v_final = grad_v_final; a.gX = grad_x; a.grad_v_init = grad_v_init;
     a.T = s->T; a.N = s->N; a.ld = s->ld; a.ldh = cv ? cv->ldh : saved_ld(s);
     a.v_init = v_init;
-    a.ck0 = (handoff != nullptr || affine != nullptr) ? 1 : 0;   // as forward_impl stored it
+    a.ck0 = handoff != nullptr ? 1 : 0;   // as forward_impl stored it
     if (v_init && !aligned(v_init, 4)) return fail(SNN_ERR_MISALIGNED, "v_init is not 4-byte aligned");
 #ifdef SNN_TRACE
     a.trace = trace_buf();
@@ -527,7 +526,7 @@ snn_status snn_lif_forward_affine(const snn_lif_params* p, const snn_lif_shape* 
 }
 
 snn_status snn_lif_backward_affine(const snn_lif_params* p, const snn_lif_shape* s,
-                                   const void* grad_spikes, const void* x, const void* saved,
+                                   const void* grad_spikes, const void* x, const float* v_init, const void* saved,
                                    const float* grad_v_final, const snn_lif_affine* af, void* grad_x,
                                    float* grad_v_init, float* part_a, float* part_b,
                                    float* grad_scale, float* grad_shift, void* stream) {
@@ -535,7 +534,7 @@ snn_status snn_lif_backward_affine(const snn_lif_params* p, const snn_lif_shape*
     if (!grad_scale || !grad_shift) return fail(SNN_ERR_NULL_POINTER, "grad_scale / grad_shift is NULL");
     NvtxRange r("snn_lif_backward_affine");
     int seg = 0;
-    snn_status st = backward_impl(p, s, grad_spikes, x, nullptr, saved, grad_v_final, nullptr, grad_x, grad_v_init,
+    snn_status st = backward_impl(p, s, grad_spikes, x, v_init, saved, grad_v_final, nullptr, grad_x, grad_v_init,
                                   stream, af, part_a, part_b, nullptr, &seg);
     if (st != SNN_OK) return st;
     if (seg > 0)   // the backward already reduced each tile into channel segments: one tiny finish
@@ -683,7 +682,7 @@ snn_status snn_lif_plan_create_affine(snn_lif_plan** out, const snn_lif_params* 
     if (st != SNN_OK) return st;
     if (grad_spikes) {
         st = record_into(plan->bwd, [&] {
-            return snn_lif_backward_affine(p, s, grad_spikes, x, saved, grad_v_final, af, grad_x, grad_v_init,
+            return snn_lif_backward_affine(p, s, grad_spikes, x, v_init, saved, grad_v_final, af, grad_x, grad_v_init,
                                            part_a, part_b, grad_scale, grad_shift, nullptr);
         });
         if (st != SNN_OK) return st;

@@ -322,7 +322,8 @@ def lif_backward_affine(grad_spikes: torch.Tensor, fwd: LIFForward, *,
     gsh = torch.empty(af.C, dtype=torch.float32, device=x.device)
     res = getattr(fwd, "residual", None)
     grad_res = None if res is None else torch.empty((T, ld), dtype=x.dtype, device=x.device)[:, :N]
-    _lib.snn_lif_backward_affine(fwd.params.to_c(), fwd.shape, _ptr(grad_spikes), _ptr(x), _ptr(fwd.saved),
+    _lib.snn_lif_backward_affine(fwd.params.to_c(), fwd.shape, _ptr(grad_spikes), _ptr(x), _ptr(fwd.v_init),
+                                 _ptr(fwd.saved),
                                  _ptr(_vec("grad_v_final", grad_v_final, N, x.device)),
                                  af.to_c(res, grad_res), _ptr(grad_x), _ptr(gvi), _ptr(part[0]),
                                  _ptr(part[1]), _ptr(gsc), _ptr(gsh), _stream())

@@ -5,8 +5,8 @@ v_init (or V_reset), which snn_lif_backward receives itself (include/snn_lif.h; 
 section 6).  For T <= 16 nothing is checkpointed at all.  These tests pre-fill the saved
 buffer with NaN, so a kernel that still reads (or forgets to write) a checkpoint row would
 poison the gradients, and compare with the oracle (Eq. 3) on both kernel
-families.  The affine and handoff entry points keep storing V[-1] (their backward takes no
-v_init): covered with a non-trivial v_init below and in test_gpu_handoff.py.
+families.  The affine pair re-reads V[-1] the same way (a non-trivial v_init below); only
+the handoff pair keeps storing it (it arrives inside the kernel; test_gpu_handoff.py).
 """
 import numpy as np
 import pytest
@@ -79,9 +79,9 @@ def test_backward_reads_v_init():
 
 @pytest.mark.parametrize("family", ["tma", "generic"])
 @pytest.mark.parametrize("T", [8, 40])
-def test_affine_pair_keeps_v_init_checkpoint(family, T, monkeypatch):
-    """snn_lif_backward_affine takes no v_init: the affine forward still stores V[-1], so a
-    non-trivial v_init reaches the gradients through the checkpoint."""
+def test_affine_pair_v_init(family, T, monkeypatch):
+    """snn_lif_backward_affine re-reads V[-1] from its v_init like snn_lif_backward: a
+    non-trivial v_init through the affine pair matches the oracle."""
     monkeypatch.setenv("SNN_LIF_NO_TMA", "1" if family == "generic" else "0")
     B, C, HW = 4, 8, 64
     N = B * C * HW
