@@ -83,3 +83,20 @@ def test_serial_pytorch_baseline_matches_oracle():
     rep = oracle_check(p, X, G, S.to(torch.uint8), gX)
     assert rep.ok, str(rep)
     assert 0.05 < S.float().mean() < 0.95   # non-degenerate firing
+
+
+def test_algorithmic_bytes_count_the_stored_checkpoints():
+    """bench.py's algorithmic bytes: fp32 io, u8 spikes, RECOMPUTE moves
+    X in + S out (+ checkpoints) forward and gS, X in + gX out (+ checkpoints) backward; the
+    V[-1] checkpoint is never stored (r2c), so T <= 16 moves exactly 5 + 12 bytes."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    b = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(b)
+    assert b.bytes_per_neuron_step(4, "u8", "recompute", 16) == (5.0, 12.0)
+    assert b.bytes_per_neuron_step(4, "u8", "recompute", 8) == (5.0, 12.0)
+    f, w = b.bytes_per_neuron_step(4, "u8", "recompute", 512)       # 31 stored rows of 4 B each
+    assert abs(f - (5 + 4 * 31 / 512)) < 1e-12 and abs(w - (12 + 4 * 31 / 512)) < 1e-12
+    assert b.bytes_per_neuron_step(2, "io", "recompute", 16) == (4.0, 6.0)   # cfg2 with bf16 spikes
+    assert b.bytes_per_neuron_step(4, "bits", "h", 64) == (4 + 1 / 8 + 4, 12.0)
+    assert b.ckpt_bytes(33, ck0=True) == 4.0 * 3 / 33
