@@ -55,7 +55,7 @@
 extern "C" {
 #endif
 
-#define SNN_LIF_ABI_VERSION 3
+#define SNN_LIF_ABI_VERSION 4
 
 typedef enum {
     SNN_OK = 0,

@@ -60,7 +60,7 @@ class snn_lif_affine(ctypes.Structure):
                 ("HW", ctypes.c_int64), ("residual", ctypes.c_void_p), ("grad_residual", ctypes.c_void_p)]
 
 
-ABI_VERSION = 3   # include/snn_lif.h SNN_LIF_ABI_VERSION these structs mirror
+ABI_VERSION = 4   # include/snn_lif.h SNN_LIF_ABI_VERSION these structs mirror
 
 
 class snn_lif_handoff(ctypes.Structure):

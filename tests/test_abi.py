@@ -35,7 +35,7 @@ def test_every_declared_symbol_is_exported(lib):
 
 
 def test_abi_version_and_status_strings(lib):
-    assert lib.lib.snn_lif_abi_version() == lib.ABI_VERSION == 3
+    assert lib.lib.snn_lif_abi_version() == lib.ABI_VERSION == 4
     assert lib.lib.snn_status_string(0) == b"SNN_OK"
     assert lib.lib.snn_status_string(3) == b"SNN_ERR_MISALIGNED"
 
@@ -148,3 +148,31 @@ def test_nccl_unique_id_from_the_process_nccl(lib):
     """snn_nccl_unique_id resolves NCCL at run time (no GPU needed) and returns 128 bytes."""
     uid = lib.snn_nccl_unique_id()
     assert len(uid) == 128 and any(uid)
+
+
+def test_affine_validation(lib):
+    """snn_lif_forward_affine / snn_lif_backward_affine (ABI 4: the backward takes the forward's
+    v_init) validate before any launch."""
+    P, S = ctypes.byref(_p(lib)), ctypes.byref(_s(lib))
+    ok = lib.snn_lif_affine(scale=16, shift=16, C=4, HW=256, residual=None, grad_residual=None)
+    bad_div = lib.snn_lif_affine(scale=16, shift=16, C=3, HW=256, residual=None, grad_residual=None)
+    no_scale = lib.snn_lif_affine(scale=None, shift=16, C=4, HW=256, residual=None, grad_residual=None)
+    f = lib.lib.snn_lif_forward_affine
+    assert f(P, S, 16, None, None, 16, 16, None, None) == 2                      # affine NULL
+    assert f(P, S, 16, None, ctypes.byref(bad_div), 16, 16, None, None) == 1     # N % (C HW) != 0
+    assert f(P, S, 16, None, ctypes.byref(no_scale), 16, 16, None, None) == 1
+    assert f(P, S, 16, 18, ctypes.byref(ok), 16, 16, None, None) == 3            # v_init misaligned
+    b = lib.lib.snn_lif_backward_affine
+    #       P  S  gS  x   v_init saved gvf  af            gx  gvi  pa  pb  gsc gsh  stream
+    assert b(P, S, 16, 16, None, 16, None, None, 16, None, 16, 16, 16, 16, None) == 2          # affine NULL
+    assert b(P, S, 16, 16, None, 16, None, ctypes.byref(ok), 16, None, 16, 16, None, 16, None) == 2  # grad_scale
+    assert b(P, S, 16, 16, None, 16, None, ctypes.byref(ok), 16, None, None, 16, 16, 16, None) == 2  # part_a
+    assert b(P, S, 16, 16, 18, 16, None, ctypes.byref(ok), 16, None, 16, 16, 16, 16, None) == 3     # v_init
+    assert b(P, S, 16, 16, None, 16, None, ctypes.byref(bad_div), 16, None, 16, 16, 16, 16, None) == 1
+    Sh = ctypes.byref(_s(lib, save_mode=0))
+    assert b(P, Sh, 16, 16, None, 16, None, ctypes.byref(ok), 16, None, 16, 16, 16, 16, None) == 4  # SAVE_H
+
+
+def test_backward_v_init_alignment(lib):
+    P, S = ctypes.byref(_p(lib)), ctypes.byref(_s(lib))
+    assert lib.lib.snn_lif_backward(P, S, 16, 16, 18, 16, None, 16, None, None) == 3
