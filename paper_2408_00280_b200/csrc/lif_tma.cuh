@@ -225,15 +225,50 @@ struct Region {
     }
 };
 
+// 16 bytes of shared memory at p, s = p's byte shift (1..15, warp-uniform) past the 16-B
+// aligned address b below it: the two aligned chunks at b and b + 16 (two conflict-free LDS.128 per
+// lane), realigned in registers -- a word select for s % 4 == 0 (fp32 rows), PRMT byte
+// permutes otherwise (bf16 rows at an odd element).  (r2c: per-word or per-element loads at a
+// 16-byte-lane stride hit the same bank 4-way, i.e. 4-8x the shared-memory cycles of an
+// aligned row.)  The caller's row has >= 16 readable bytes past its last element (RP).
+__device__ __forceinline__ uint4 lds_realign16(const void* p, uint32_t s) {
+    const uint4* b = reinterpret_cast<const uint4*>(reinterpret_cast<uintptr_t>(p) & ~uintptr_t(15));
+    const uint4 lo = b[0], hi = b[1];
+    const uint32_t w[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+    uint32_t o[4];
+    const uint32_t sel = (s & 3u) == 2u ? 0x5432u : ((s & 3u) == 1u ? 0x4321u : 0x6543u);
+    auto pick = [&](auto q) {
+        constexpr int Q = decltype(q)::value;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            o[k] = (s & 3u) == 0u ? w[k + Q] : __byte_perm(w[k + Q], w[k + Q + 1], sel);
+    };
+    switch (s >> 2) {   // warp-uniform
+        case 0: pick(std::integral_constant<int, 0>{}); break;
+        case 1: pick(std::integral_constant<int, 1>{}); break;
+        case 2: pick(std::integral_constant<int, 2>{}); break;
+        default: pick(std::integral_constant<int, 3>{}); break;
+    }
+    return make_uint4(o[0], o[1], o[2], o[3]);
+}
+
 // VEC elements from shared memory at q of any element alignment, with the widest loads the
-// address allows (16 / 8 / 4 bytes; element loads only for 2-byte-aligned bf16).  The choice
-// is warp-uniform: every lane's q has the same misalignment.
+// address allows (16 / 8 / 4 bytes; element loads only for 2-byte-aligned bf16); 16-byte
+// packs are realigned from two aligned chunks (lds_realign16).  The choice is warp-uniform:
+// every lane's q has the same misalignment.
 template <typename IO, int VEC>
 __device__ __forceinline__ Pack<IO, VEC> lds_widest(const IO* q) {
     constexpr int B = (int)sizeof(Pack<IO, VEC>);
     const uint32_t a = smem_u32(q);
     Pack<IO, VEC> r;
     if (a % B == 0) return *reinterpret_cast<const Pack<IO, VEC>*>(q);
+    if constexpr (B == 16) {   // (an 8-byte-aligned row keeps the two LDS.64: measured faster)
+        if (a % 8 != 0) {
+            const uint4 v = lds_realign16(q, a & 15u);
+            *reinterpret_cast<uint4*>(&r) = v;
+            return r;
+        }
+    }
     if constexpr (B >= 16) {
         if (a % 8 == 0) {
 #pragma unroll
