@@ -59,6 +59,7 @@ def alg_bytes(dt, T, N, save_mode="recompute"):
 
 
 SAVE_MODE = "recompute"
+SPIKE_FMT = "u8"
 
 
 def time_case(dt, T, N, reps, off=0):
@@ -70,14 +71,14 @@ def time_case(dt, T, N, reps, off=0):
     st = torch.cuda.current_stream()
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(reps)]
     for i in range(3):
-        f = snn.lif_forward(xs[i % 2], p, return_v_final=False, save_mode=SAVE_MODE)
+        f = snn.lif_forward(xs[i % 2], p, return_v_final=False, save_mode=SAVE_MODE, spike_fmt=SPIKE_FMT)
         snn.lif_backward(gs[i % 2], f, return_grad_v_init=False)
     torch.cuda.synchronize()
     torch.cuda._sleep(int(3e6 + 2.5e5 * reps))   # keep the GPU busy while the host enqueues
     for i in range(reps):
         e = ev[i]
         e[0].record(st)
-        f = snn.lif_forward(xs[i % 2], p, return_v_final=False, save_mode=SAVE_MODE)
+        f = snn.lif_forward(xs[i % 2], p, return_v_final=False, save_mode=SAVE_MODE, spike_fmt=SPIKE_FMT)
         e[1].record(st)
         e[2].record(st)
         snn.lif_backward(gs[i % 2], f, return_grad_v_init=False)
@@ -96,9 +97,11 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--cases", default="cfg1,cfg2,t16")
     ap.add_argument("--save-mode", default="recompute")
+    ap.add_argument("--spike-fmt", default="u8")
     a = ap.parse_args()
-    global SAVE_MODE
+    global SAVE_MODE, SPIKE_FMT
     SAVE_MODE = a.save_mode
+    SPIKE_FMT = a.spike_fmt
     torch.cuda.set_device(0)
     time_null(a.reps)
     for c in a.cases.split(","):
