@@ -268,6 +268,27 @@ __device__ __forceinline__ void store_spike_bits(uint32_t* row, int64_t g, unsig
     }
 }
 
+// Four u8 spikes (w: byte i = neuron i) at a global address of any alignment, branch-free
+// (r2c): every case is a predicated store -- one 32-bit store when 4-aligned, two 16-bit ones
+// when 2-aligned, byte / 16-bit / byte when odd -- so an unaligned row costs no per-row
+// branches (streaming, evict-first like st_stream).
+__device__ __forceinline__ void st_u8x4_any(uint8_t* p, uint32_t w) {
+    const uint32_t a = (uint32_t)reinterpret_cast<uintptr_t>(p) & 3u;
+    const uint32_t mid = (w >> 8) & 0xffffu;   // bytes 1..2 (the odd case's 16-bit store at p+1)
+    asm volatile(
+        "{\n\t.reg .pred q4, q2, q1;\n\t"
+        "setp.eq.u32 q4, %1, 0;\n\t"
+        "setp.eq.u32 q2, %1, 2;\n\t"
+        "setp.eq.u32 q1, %5, 1;\n\t"
+        "@q4 st.global.cs.u32 [%0], %2;\n\t"
+        "@q2 st.global.cs.u16 [%0], %2;\n\t"
+        "@q2 st.global.cs.u16 [%0+2], %3;\n\t"
+        "@q1 st.global.cs.u8 [%0], %2;\n\t"
+        "@q1 st.global.cs.u16 [%0+1], %4;\n\t"
+        "@q1 st.global.cs.u8 [%0+3], %6;\n\t}"
+        :: "l"(p), "r"(a), "r"(w), "r"(w >> 16), "r"(mid), "r"(a & 1u), "r"(w >> 24) : "memory");
+}
+
 // Store one time row's spikes.  `row` = spikes + t*ld (U8/IO) or words + t*nwords (BITS).
 // Every lane of the warp must call this (BITS uses warp shuffles).
 // UNAL: the row may not be pack-aligned (odd row stride / unaligned view): st_any.
@@ -280,8 +301,14 @@ __device__ __forceinline__ void store_spikes(void* row, int64_t g, int64_t n0, u
             Pack<uint8_t, VEC> sp;
 #pragma unroll
             for (int i = 0; i < VEC; ++i) sp.v[i] = (uint8_t)((bits >> i) & 1u);
-            if constexpr (UNAL) st_any<uint8_t, VEC>(reinterpret_cast<uint8_t*>(row) + n0, sp, nvalid);
-            else st_group<uint8_t, VEC>(reinterpret_cast<uint8_t*>(row) + n0, sp, nvalid);
+            if constexpr (UNAL && VEC == 4) {
+                if (nvalid >= 4) st_u8x4_any(reinterpret_cast<uint8_t*>(row) + n0, *reinterpret_cast<const uint32_t*>(&sp));
+                else st_any<uint8_t, VEC>(reinterpret_cast<uint8_t*>(row) + n0, sp, nvalid);
+            } else if constexpr (UNAL) {
+                st_any<uint8_t, VEC>(reinterpret_cast<uint8_t*>(row) + n0, sp, nvalid);
+            } else {
+                st_group<uint8_t, VEC>(reinterpret_cast<uint8_t*>(row) + n0, sp, nvalid);
+            }
         }
     } else if constexpr (SFMT == SPK_IO) {
         if (nvalid > 0) {
