@@ -301,9 +301,10 @@ __device__ __forceinline__ void store_spikes(void* row, int64_t g, int64_t n0, u
             Pack<uint8_t, VEC> sp;
 #pragma unroll
             for (int i = 0; i < VEC; ++i) sp.v[i] = (uint8_t)((bits >> i) & 1u);
-            if constexpr (UNAL && VEC == 4) {
-                if (nvalid >= 4) st_u8x4_any(reinterpret_cast<uint8_t*>(row) + n0, *reinterpret_cast<const uint32_t*>(&sp));
-                else st_any<uint8_t, VEC>(reinterpret_cast<uint8_t*>(row) + n0, sp, nvalid);
+            if constexpr (UNAL && VEC == 4) {   // (bf16's 8 bytes as two of these: 7% slower than st_any)
+                uint8_t* q = reinterpret_cast<uint8_t*>(row) + n0;
+                if (nvalid >= VEC) st_u8x4_any(q, *reinterpret_cast<const uint32_t*>(&sp));
+                else st_any<uint8_t, VEC>(q, sp, nvalid);
             } else if constexpr (UNAL) {
                 st_any<uint8_t, VEC>(reinterpret_cast<uint8_t*>(row) + n0, sp, nvalid);
             } else {
