@@ -753,3 +753,31 @@ def test_affine_reduction_folded_into_backward(HW, B, C, dtype):
     rtol = 1e-2 if dtype == torch.bfloat16 else 1e-5
     assert np.all(np.abs(gsc.cpu().numpy() - rgs) <= rtol * tol_s + 1e-30)
     assert np.all(np.abs(gsh.cpu().numpy() - rgb) <= rtol * tol_b + 1e-30)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_unaligned_every_base_and_stride_residue_equals_generic(dtype, monkeypatch):
+    """r2c: the unaligned-row kernels read 16-byte packs branch-free (two aligned chunks, a SEL
+    rotate, PRMT for bf16) and store fp32's u8 spikes with one predicated block.  Every
+    combination of the view's element offset (m0) and row stride residue (ld mod 16 B) -- so
+    every per-row shift the rotate / permute / store code can meet -- must equal the generic
+    kernels bitwise (u8 and io spikes, forward and backward)."""
+    Q = 16 // (4 if dtype == torch.float32 else 2)
+    T, N = 19, 2048
+    for off in range(Q):
+        for ldx in range(Q):
+            base = snn_synth.normal_tensor(300 + off * Q + ldx, T, N + off + ldx, dtype=dtype).cuda()
+            X = base[:, off:off + N]
+            G = snn_synth.normal_tensor(900 + off, T, N + off + ldx, dtype=dtype).cuda()[:, off:off + N]
+            outs = []
+            for no_tma in ("0", "1"):
+                monkeypatch.setenv("SNN_LIF_NO_TMA", no_tma)
+                for fmt in ("u8", "io"):
+                    f, g, v = _run(PAPER, X, G, fmt, "recompute")
+                    torch.cuda.synchronize()
+                    outs.append((f.spikes.clone(), f.v_final.clone(), g.clone(), v.clone()))
+            half = len(outs) // 2
+            for o_tma, o_gen in zip(outs[:half], outs[half:]):
+                for a_, b_ in zip(o_tma, o_gen):
+                    assert torch.equal(a_, b_), (off, ldx)
+    monkeypatch.delenv("SNN_LIF_NO_TMA")
