@@ -325,6 +325,25 @@ __device__ __forceinline__ Pack<IO, VEC> lds_rot16(uint32_t b, uint32_t s) {
     return r;
 }
 
+// The backward's narrower packs, branch-free likewise (r2c): 8 bytes (fp32 pairs; always
+// 4-byte aligned) from the two aligned 8-byte words around them and a SEL; 4 bytes (bf16
+// pairs; 2-byte aligned) from two aligned words and a PRMT.  a = the pack's shared address.
+__device__ __forceinline__ uint2 lds_rot8(uint32_t a) {
+    const uint32_t b = a & ~7u;
+    uint32_t w0, w1, w2, w3;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(w0), "=r"(w1) : "r"(b));
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2+8];" : "=r"(w2), "=r"(w3) : "r"(b));
+    const bool sh = (a & 4u) != 0u;
+    return make_uint2(sh ? w1 : w0, sh ? w2 : w1);
+}
+__device__ __forceinline__ uint32_t lds_rot4(uint32_t a) {
+    const uint32_t b = a & ~3u;
+    uint32_t w0, w1;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w0) : "r"(b));
+    asm volatile("ld.shared.u32 %0, [%1+4];" : "=r"(w1) : "r"(b));
+    return __byte_perm(w0, w1, 0x3210u + 0x1111u * (a & 3u));
+}
+
 // A consumer lane's view of one tensor's rows in a stage: src(j) = the lane's VEC elements of
 // row j.  Aligned: box layout, pack loads.  UNAL: row-major with the row's element shift
 // m_j = (m0 + j*dm) mod Q (m0 = the first row's, dm = ld mod Q); pack loads where the shift keeps
@@ -341,6 +360,12 @@ struct RowSrc {
             if constexpr (sizeof(Pack<IO, VEC>) == 16) {   // the lane's chunk is 16-B aligned
                 return lds_rot16<IO, VEC>(smem_u32(p) + (uint32_t)(j * RPE * (int)sizeof(IO)),
                                           (uint32_t)(((m0 + j * dm) & (Q - 1)) * (int)sizeof(IO)));
+            } else if constexpr (sizeof(Pack<IO, VEC>) == 8 || sizeof(Pack<IO, VEC>) == 4) {
+                const IO* q = p + j * RPE + ((m0 + j * dm) & (Q - 1));
+                Pack<IO, VEC> r;
+                if constexpr (sizeof(Pack<IO, VEC>) == 8) *reinterpret_cast<uint2*>(&r) = lds_rot8(smem_u32(q));
+                else *reinterpret_cast<uint32_t*>(&r) = lds_rot4(smem_u32(q));
+                return r;
             } else {
                 const IO* q = p + j * RPE + ((m0 + j * dm) & (Q - 1));
                 return lds_widest<IO, VEC>(q);
@@ -371,7 +396,33 @@ row_src(const unsigned char* base, int nt, int64_t t0, int64_t ld, int off) {
 // element by element either way (a pack store would spill into the neighbouring columns).
 template <bool UNAL, typename T, int VEC>
 __device__ __forceinline__ void st_out(T* p, const Pack<T, VEC>& r, int nvalid) {
-    if constexpr (UNAL) {
+    if constexpr (UNAL && sizeof(Pack<T, VEC>) == 8 && sizeof(T) == 4) {   // fp32 pairs: 4-B aligned
+        if (nvalid >= VEC) {
+            const uint2 v = *reinterpret_cast<const uint2*>(&r);
+            asm volatile(
+                "{\n\t.reg .pred q8;\n\t"
+                "setp.eq.u32 q8, %1, 0;\n\t"
+                "@q8 st.global.cs.v2.u32 [%0], {%2, %3};\n\t"
+                "@!q8 st.global.cs.u32 [%0], %2;\n\t"
+                "@!q8 st.global.cs.u32 [%0+4], %3;\n\t}"
+                :: "l"(p), "r"((uint32_t)reinterpret_cast<uintptr_t>(p) & 7u), "r"(v.x), "r"(v.y) : "memory");
+        } else {
+            st_any<T, VEC>(p, r, nvalid);
+        }
+    } else if constexpr (UNAL && sizeof(Pack<T, VEC>) == 4 && sizeof(T) == 2) {   // bf16 pairs: 2-B aligned
+        if (nvalid >= VEC) {
+            const uint32_t v = *reinterpret_cast<const uint32_t*>(&r);
+            asm volatile(
+                "{\n\t.reg .pred q4;\n\t"
+                "setp.eq.u32 q4, %1, 0;\n\t"
+                "@q4 st.global.cs.u32 [%0], %2;\n\t"
+                "@!q4 st.global.cs.u16 [%0], %2;\n\t"
+                "@!q4 st.global.cs.u16 [%0+2], %3;\n\t}"
+                :: "l"(p), "r"((uint32_t)reinterpret_cast<uintptr_t>(p) & 3u), "r"(v), "r"(v >> 16) : "memory");
+        } else {
+            st_any<T, VEC>(p, r, nvalid);
+        }
+    } else if constexpr (UNAL) {
         st_any<T, VEC>(p, r, nvalid);
     } else if (nvalid >= VEC) {
         st_stream<T, VEC>(p, r);
