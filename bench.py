@@ -1116,6 +1116,11 @@ def run_ours(args):
         ram_ok = psutil.virtual_memory().available > 1.5 * need * int(os.environ.get("LOCAL_WORLD_SIZE", world))
     except Exception:
         ram_ok = True
+    if world > 1 and not args.no_e2e:
+        # one decision for all ranks (each rank looked at the host's free RAM at its own moment,
+        # possibly after another rank pinned its buffers): a rank skipping the leg while the
+        # others enter its barrier would hang the job
+        ram_ok = -max_over_ranks([-1.0 if ram_ok else 0.0], dev, args.debug_single_gpu)[0] > 0.5
     if not args.no_e2e and not ram_ok:
         e2e = {"value": None, "unit": UNIT, "skipped": "not enough host RAM to pin every rank's buffers"}
     if not args.no_e2e and ram_ok:
