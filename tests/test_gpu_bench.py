@@ -31,6 +31,21 @@ def _run(args, nproc=1, port=29531):
     return json.loads(lines[0])
 
 
+def test_sweep_records_clean_and_dirty_flush_and_floor():
+    """bench.py --sweep (BASELINE configs[1]'s T sweep): per T, the isolated launches after a
+    clean flush, the dirty-memset repeat, the empty-launch floor and the back-to-back figure;
+    the clean-flush launch is never slower than the floor alone."""
+    d = _run(["--sweep", "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-e2e"])
+    sw = d["sweep"]
+    assert [s["T"] for s in sw] == [8, 32, 128, 512]
+    for s in sw:
+        for k in ("fwd_ms", "bwd_ms", "neuron_steps_per_s", "fwd_GBps", "bwd_GBps", "floor_ms",
+                  "dirty_flush", "stream"):
+            assert k in s, k
+        assert 0 < s["floor_ms"] < s["fwd_ms"] and s["floor_ms"] < s["bwd_ms"]
+        assert s["dirty_flush"]["fwd_ms"] > 0 and s["stream"]["neuron_steps_per_s"] > 0
+
+
 def test_default_line_contract_keys():
     d = _run(["--steps", "5", "--warmup", "3", "--T", "64", "--cpu-seconds", "1", "--e2e-steps", "1"])
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
